@@ -1,0 +1,114 @@
+/*
+ * ffg.h -- C ABI of the B200-native ffpluq hot path (libffg_b200.so).
+ *
+ * Drop-in boundary for the reference's tile-recursive PLUQ over GF(p) and the
+ * two kernels under it.  Plain pointers and sizes only.  Matrices are row-major
+ * uint32 canonical residues in [0, p) with an explicit leading dimension, the
+ * layout of the reference's MatView (proj/include/ffpluq/matrix.hpp:13-43).
+ *
+ * Every entry point exists in two forms:
+ *   ffg_X(...)      host buffers: the drop-in for the reference call on a
+ *                   host MatView (copies in, computes on the GPU, copies out)
+ *   ffg_X_dev(...)  device buffers, enqueued on the context's stream
+ *
+ * Permutations are returned as index arrays with the meaning of
+ * PermSeq::to_array() (perm.hpp:88-95): entry t = original index now at
+ * position t.  Status codes mirror the reference exception types
+ * (proj/include/ffpluq/errors.hpp:9-59).
+ */
+#ifndef FFG_H
+#define FFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:9-59) ----------------------------------- */
+#define FFG_OK 0
+#define FFG_ERR_ZERO_DIVISION 1     /* ZeroDivision      errors.hpp:9-11  */
+#define FFG_ERR_CAPACITY 2          /* CapacityError     errors.hpp:13-15 (bad modulus) */
+#define FFG_ERR_DIM_MISMATCH 3      /* DimMismatch       errors.hpp:17-19 */
+#define FFG_ERR_EMPTY_MATRIX 4      /* EmptyMatrix       errors.hpp:21-23 */
+#define FFG_ERR_ZERO_PIVOT 5        /* ZeroPivot         errors.hpp:27-31 */
+#define FFG_ERR_SINGULAR_DIAGONAL 6 /* SingularDiagonal  errors.hpp:33-38, index via ffg_last_error_index() */
+#define FFG_ERR_NOT_RANK_REVEALING 7
+#define FFG_ERR_INVALID_BLOCK 8
+#define FFG_ERR_INVALID_DIM 9
+#define FFG_ERR_INVALID_RANK 10
+#define FFG_ERR_NO_MEMORY 12
+#define FFG_ERR_CUDA 100            /* CUDA runtime failure (message via ffg_last_error()) */
+#define FFG_ERR_NO_DEVICE 101       /* no sm_100 device: there is no CPU fallback */
+#define FFG_ERR_INVALID_ARG 102     /* null context / pointer */
+#define FFG_ERR_INTERNAL 103
+
+typedef struct ffg_ctx ffg_ctx;
+
+/* Context: one CUDA device, one stream, device workspace.  Fails with
+ * FFG_ERR_NO_DEVICE when the device is not a compute-capability 10.x GPU. */
+int ffg_create(ffg_ctx **out, int device);
+void ffg_destroy(ffg_ctx *ctx);
+/* cudaStream_t passed as void* so the header stays CUDA-free; NULL = the context's own */
+int ffg_set_stream(ffg_ctx *ctx, void *stream);
+void *ffg_get_stream(ffg_ctx *ctx);
+int ffg_synchronize(ffg_ctx *ctx);
+
+const char *ffg_last_error(void);     /* thread-local message of the last failure */
+size_t ffg_last_error_index(void);    /* SingularDiagonal::index (errors.hpp:33-38) */
+const char *ffg_version(void);
+
+/* ---- modular GEMM ------------------------------------------------------
+ * C <- alpha*A*B + beta*C mod p, A m x k, B k x n, C m x n.
+ * Replaces fgemm / fgemm_classical / pfgemm (blas.hpp:31-103, 220-246, 250-271):
+ * same arguments and values, any alpha, beta in [0, p).  2 <= p < 2^26 prime
+ * (PrimeField, field.hpp:47-54), else FFG_ERR_CAPACITY. */
+int ffg_fgemm(ffg_ctx *ctx, uint64_t p, uint32_t alpha, const uint32_t *A, size_t lda, const uint32_t *B,
+              size_t ldb, uint32_t beta, uint32_t *C, size_t ldc, size_t m, size_t n, size_t k);
+int ffg_fgemm_dev(ffg_ctx *ctx, uint64_t p, uint32_t alpha, const uint32_t *A, size_t lda, const uint32_t *B,
+                  size_t ldb, uint32_t beta, uint32_t *C, size_t ldc, size_t m, size_t n, size_t k);
+
+/* ---- triangular solve --------------------------------------------------
+ * B (m x n) <- op(A)^-1 B (side 0 = left) or B op(A)^-1 (side 1 = right), in place.
+ * uplo 0 = lower, 1 = upper; diag 0 = unit, 1 = nonunit.  A is t x t with
+ * t = m (left) or n (right); only the selected triangle (and the diagonal if
+ * nonunit) is read, so A may be a packed L\U square like in tile_rec.
+ * Replaces ftrsm / pftrsm (blas.hpp:389-398, 402-419).  A zero diagonal entry
+ * with diag = nonunit gives FFG_ERR_SINGULAR_DIAGONAL with the smallest index. */
+int ffg_ftrsm(ffg_ctx *ctx, uint64_t p, int side, int uplo, int diag, const uint32_t *A, size_t lda,
+              uint32_t *B, size_t ldb, size_t m, size_t n);
+int ffg_ftrsm_dev(ffg_ctx *ctx, uint64_t p, int side, int uplo, int diag, const uint32_t *A, size_t lda,
+                  uint32_t *B, size_t ldb, size_t m, size_t n);
+
+/* ---- rank-profile revealing PLUQ ---------------------------------------
+ * In place: A (m x n) receives the packed L\U factors exactly as the reference
+ * leaves them; P (m entries) and Q (n entries) receive PermSeq::to_array() of
+ * the row / column permutations; *rank the rank.
+ * ffg_pluq_tile_recursive replaces pluq_tile_recursive (rankrev.hpp:229-233,
+ * recursion rankrev.hpp:85-183, threshold clamped to >= 1).
+ * ffg_rr_base replaces the base case rr_base (rankrev.hpp:29-78). */
+int ffg_pluq_tile_recursive(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_t lda,
+                            size_t threshold, uint32_t *P, uint32_t *Q, size_t *rank);
+int ffg_pluq_tile_recursive_dev(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_t lda,
+                                size_t threshold, uint32_t *P, uint32_t *Q, size_t *rank);
+int ffg_rr_base(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_t lda, uint32_t *P, uint32_t *Q,
+                size_t *rank);
+
+/* ---- permutations (perm.hpp:167-215) -----------------------------------
+ * Row (axis 0) or column (axis 1) gather of a device matrix by an index array
+ * perm (device pointer, dim entries): out position t <- in position perm[t]
+ * (forward, = apply_perm of a PermSeq whose to_array() is perm), or the
+ * inverse scatter when inverse != 0. */
+int ffg_apply_perm_dev(ffg_ctx *ctx, uint32_t *A, size_t m, size_t n, size_t lda, int axis, int inverse,
+                       const uint32_t *perm);
+
+/* ---- instrumentation ----------------------------------------------------
+ * Kernel launches issued by this context since creation (all kernels of this
+ * library; used for the bench's gpu_launches claim). */
+uint64_t ffg_launch_count(ffg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

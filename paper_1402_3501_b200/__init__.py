@@ -1,0 +1,21 @@
+"""B200-native tile-recursive PLUQ over GF(p) (drop-in for the ffpluq hot path).
+
+The product is libffg_b200.so (C ABI in include/ffg.h, CUDA sm_100a kernels in
+csrc/).  This package is its Python host mirror; see ffpluq.py.
+"""
+from .ffpluq import (  # noqa: F401
+    CapacityError,
+    Context,
+    CudaError,
+    DimMismatch,
+    FfgError,
+    NoDevice,
+    PluqResult,
+    SingularDiagonal,
+    default_context,
+    fgemm,
+    ftrsm,
+    lib,
+    pluq_tile_recursive,
+    rr_base,
+)

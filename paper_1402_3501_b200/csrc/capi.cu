@@ -1,0 +1,226 @@
+// capi.cu -- the extern "C" boundary (include/ffg.h): context, status codes, host/device entry points.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "pluq.cuh"
+
+struct ffg_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    ffg::Workspace ws;
+    uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local size_t g_err_index = 0;
+
+template <class Fn>
+int guarded(ffg_ctx* ctx, Fn&& fn) {
+    if (!ctx) {
+        g_err = "null context";
+        return FFG_ERR_INVALID_ARG;
+    }
+    try {
+        cudaSetDevice(ctx->device);
+        fn();
+        return FFG_OK;
+    } catch (const ffg::Error& e) {
+        g_err = e.what();
+        g_err_index = e.index;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return FFG_ERR_NO_MEMORY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FFG_ERR_INTERNAL;
+    }
+}
+
+// device copy of a strided host matrix (pinned staging is the caller's choice; cudaMemcpy2D handles pageable)
+struct DevMat {
+    uint32_t* d = nullptr;
+    size_t rows = 0, cols = 0;
+    DevMat(size_t r, size_t c, cudaStream_t st) : rows(r), cols(c) {
+        if (r && c) FFG_CUDA(cudaMallocAsync(&d, r * c * sizeof(uint32_t), st));
+        stream = st;
+    }
+    ~DevMat() {
+        if (d) cudaFreeAsync(d, stream);
+    }
+    ffg::DView view() { return ffg::DView{d, rows, cols, cols}; }
+    void upload(const uint32_t* h, size_t ld) {
+        if (d)
+            FFG_CUDA(cudaMemcpy2DAsync(d, cols * 4, h, ld * 4, cols * 4, rows, cudaMemcpyHostToDevice, stream));
+    }
+    void download(uint32_t* h, size_t ld) {
+        if (d)
+            FFG_CUDA(cudaMemcpy2DAsync(h, ld * 4, d, cols * 4, cols * 4, rows, cudaMemcpyDeviceToHost, stream));
+    }
+    cudaStream_t stream;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ffg_version(void) { return "ffg_b200 0.1 (sm_100a tcgen05 kind::i8 limb GEMM)"; }
+const char* ffg_last_error(void) { return g_err.c_str(); }
+size_t ffg_last_error_index(void) { return g_err_index; }
+
+int ffg_create(ffg_ctx** out, int device) {
+    if (!out) return FFG_ERR_INVALID_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) {
+        (void)cudaGetLastError();
+        g_err = "no CUDA device";
+        return FFG_ERR_NO_DEVICE;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) {
+        g_err = "device is not sm_100 (compute capability 10.x); this library has no other code path";
+        return FFG_ERR_NO_DEVICE;
+    }
+    ffg_ctx* c = new ffg_ctx;
+    c->device = device;
+    cudaSetDevice(device);
+    if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        g_err = "stream creation failed";
+        return FFG_ERR_CUDA;
+    }
+    c->stream = c->own_stream;
+    // keep freed stream-ordered allocations cached in the pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+    return FFG_OK;
+}
+
+void ffg_destroy(ffg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+int ffg_set_stream(ffg_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream; });
+}
+void* ffg_get_stream(ffg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+int ffg_synchronize(ffg_ctx* ctx) { return guarded(ctx, [&] { FFG_CUDA(cudaStreamSynchronize(ctx->stream)); }); }
+uint64_t ffg_launch_count(ffg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ffg_fgemm_dev(ffg_ctx* ctx, uint64_t p, uint32_t alpha, const uint32_t* A, size_t lda, const uint32_t* B,
+                  size_t ldb, uint32_t beta, uint32_t* C, size_t ldc, size_t m, size_t n, size_t k) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        ffg::fgemm_dev(F, alpha, ffg::DView{const_cast<uint32_t*>(A), m, k, lda},
+                       ffg::DView{const_cast<uint32_t*>(B), k, n, ldb}, beta, ffg::DView{C, m, n, ldc}, ctx->stream,
+                       ctx->ws, &ctx->launches);
+    });
+}
+
+int ffg_fgemm(ffg_ctx* ctx, uint64_t p, uint32_t alpha, const uint32_t* A, size_t lda, const uint32_t* B,
+              size_t ldb, uint32_t beta, uint32_t* C, size_t ldc, size_t m, size_t n, size_t k) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        cudaStream_t st = ctx->stream;
+        DevMat dA(m, k, st), dB(k, n, st), dC(m, n, st);
+        dA.upload(A, lda);
+        dB.upload(B, ldb);
+        dC.upload(C, ldc);
+        ffg::fgemm_dev(F, alpha, dA.view(), dB.view(), beta, dC.view(), st, ctx->ws, &ctx->launches);
+        dC.download(C, ldc);
+        FFG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ffg_ftrsm_dev(ffg_ctx* ctx, uint64_t p, int side, int uplo, int diag, const uint32_t* A, size_t lda, uint32_t* B,
+                  size_t ldb, size_t m, size_t n) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        const size_t t = side == 0 ? m : n;
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        ffg::ftrsm_dev(blas, side, uplo, diag, ffg::DView{const_cast<uint32_t*>(A), t, t, lda}, ffg::DView{B, m, n, ldb},
+                       /*check_diag=*/true);
+    });
+}
+
+int ffg_ftrsm(ffg_ctx* ctx, uint64_t p, int side, int uplo, int diag, const uint32_t* A, size_t lda, uint32_t* B,
+              size_t ldb, size_t m, size_t n) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        cudaStream_t st = ctx->stream;
+        const size_t t = side == 0 ? m : n;
+        DevMat dA(t, t, st), dB(m, n, st);
+        dA.upload(A, lda);
+        dB.upload(B, ldb);
+        ffg::Blas blas{F, ctx->ws, st, &ctx->launches};
+        ffg::ftrsm_dev(blas, side, uplo, diag, dA.view(), dB.view(), true);
+        dB.download(B, ldb);
+        FFG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ffg_pluq_tile_recursive_dev(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, size_t n, size_t lda,
+                                size_t threshold, uint32_t* P, uint32_t* Q, size_t* rank) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        size_t r = ffg::pluq_tile_recursive_dev(blas, ffg::DView{A, m, n, lda}, threshold, P, Q);
+        if (rank) *rank = r;
+    });
+}
+
+int ffg_pluq_tile_recursive(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, size_t n, size_t lda, size_t threshold,
+                            uint32_t* P, uint32_t* Q, size_t* rank) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        cudaStream_t st = ctx->stream;
+        DevMat dA(m, n, st);
+        dA.upload(A, lda);
+        ffg::Blas blas{F, ctx->ws, st, &ctx->launches};
+        size_t r = ffg::pluq_tile_recursive_dev(blas, dA.view(), threshold, P, Q);
+        dA.download(A, lda);
+        FFG_CUDA(cudaStreamSynchronize(st));
+        if (rank) *rank = r;
+    });
+}
+
+int ffg_rr_base(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, size_t n, size_t lda, uint32_t* P, uint32_t* Q,
+                size_t* rank) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        cudaStream_t st = ctx->stream;
+        DevMat dA(m, n, st);
+        dA.upload(A, lda);
+        ffg::Blas blas{F, ctx->ws, st, &ctx->launches};
+        size_t r = ffg::rr_base_dev(blas, dA.view(), P, Q);
+        dA.download(A, lda);
+        FFG_CUDA(cudaStreamSynchronize(st));
+        if (rank) *rank = r;
+    });
+}
+
+int ffg_apply_perm_dev(ffg_ctx* ctx, uint32_t* A, size_t m, size_t n, size_t lda, int axis, int inverse,
+                       const uint32_t* perm) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(2);
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        ffg::apply_perm_dev(blas, ffg::DView{A, m, n, lda}, axis, inverse, perm);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// common.cuh -- shared host/device definitions of the B200 ffpluq library.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ffg.h"
+
+namespace ffg {
+
+// A non-owning row-major window of u32 residues in device memory (the
+// device-side twin of MatView, matrix.hpp:13-43).
+struct DView {
+    uint32_t* d = nullptr;
+    size_t rows = 0, cols = 0, ld = 0;
+    bool empty() const { return rows == 0 || cols == 0; }
+    DView sub(size_t r0, size_t c0, size_t h, size_t w) const { return DView{d + r0 * ld + c0, h, w, ld}; }
+};
+
+// Library error carrying an ffg status code (include/ffg.h, mirrors errors.hpp).
+struct Error : std::runtime_error {
+    int code;
+    size_t index;
+    Error(int c, const std::string& what, size_t idx = 0) : std::runtime_error(what), code(c), index(idx) {}
+};
+
+#define FFG_CUDA(x)                                                                                       \
+    do {                                                                                                  \
+        cudaError_t e_ = (x);                                                                             \
+        if (e_ != cudaSuccess)                                                                            \
+            throw ::ffg::Error(FFG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+// Prime-field context shared by every kernel (field.hpp:39-54 semantics plus the
+// tensor-core embedding parameters).
+struct Field {
+    uint32_t p = 2;
+    uint64_t mu = 0;      // floor(2^64 / p), Barrett constant
+    int limbs = 1;        // 8-bit limbs per residue
+    uint64_t kmax = 0;    // inner-dimension chunk that keeps every s32 limb accumulator exact
+    uint32_t w[8] = {};   // w[s] = 2^(8s) mod p, weights of the limb-product diagonals
+};
+
+Field make_field(uint64_t p);  // throws Error(FFG_ERR_CAPACITY) like PrimeField (field.hpp:47-54)
+
+// ---------------------------------------------------------------- device arithmetic
+__host__ __device__ __forceinline__ uint32_t mod_u64(uint64_t x, uint32_t p, uint64_t mu) {
+#ifdef __CUDA_ARCH__
+    uint64_t q = __umul64hi(x, mu);
+#else
+    uint64_t q = (uint64_t)(((unsigned __int128)x * mu) >> 64);
+#endif
+    uint64_t r = x - q * p;
+    if (r >= p) r -= p;
+    if (r >= p) r -= p;
+    return (uint32_t)r;
+}
+
+__host__ __device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, uint32_t p, uint64_t mu) {
+    return mod_u64((uint64_t)a * b, p, mu);
+}
+
+// extended Euclid (field.hpp:91-107); a != 0
+__host__ __device__ __forceinline__ uint32_t inv_mod(uint32_t a, uint32_t p) {
+    int64_t t = 0, nt = 1, r = p, nr = a;
+    while (nr != 0) {
+        int64_t q = r / nr, tmp = t - q * nt;
+        t = nt;
+        nt = tmp;
+        tmp = r - q * nr;
+        r = nr;
+        nr = tmp;
+    }
+    if (t < 0) t += p;
+    return (uint32_t)t;
+}
+
+inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+inline size_t ceil_div(size_t x, size_t m) { return (x + m - 1) / m; }
+
+}  // namespace ffg

@@ -1,0 +1,442 @@
+// gemm.cu -- exact modular GEMM  C <- alpha*A*B + beta*C (mod p) on tcgen05 tensor cores.
+//
+// Replaces fgemm_classical / fgemm / pfgemm (blas.hpp:31-103, 220-246, 250-271).
+//
+// Embedding (the paper's delayed reduction, PAPER.md "fgemm"): every residue
+// a < p < 2^26 is split into L = ceil(bits(p-1)/8) unsigned 8-bit limbs,
+// a = sum_i 2^(8i) a_i.  Then A*B = sum_s 2^(8s) D_s with the limb-product
+// diagonals D_s = sum_{i+j=s} A_i B_j, each computed EXACTLY by kind::i8
+// tcgen05.mma with s32 accumulation in TMEM.  The only reduction mod p is in
+// the epilogue (one per output entry), fused with alpha/beta and the C update;
+// the host splits K into chunks of Field::kmax only when the exact s32 bound
+// sum_{i+j=s} max(A_i)max(B_j) * K < 2^31 would be exceeded (never for the
+// BASELINE shapes: kmax = 16512 for p = 131071, 34359 for p = 251).
+//
+// Tile: M = 128 rows (one CTA, cta_group::1), NT output columns.  The B
+// operand tile holds the L limb planes of the NT columns stacked along N
+// (N' = L*NT <= 256), so one MMA  A_i x [B_0|..|B_{L-1}]  writes diagonals
+// i..i+L-1 at TMEM column offset i*NT: L MMAs per K-step cover all L^2 limb
+// products, accumulating into (2L-1)*NT <= 512 TMEM columns.
+//
+// Operands are staged by one conversion pass per call (split kernels below)
+// into K-major byte planes that TMA loads with 128-byte swizzle.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace ffg {
+
+// --------------------------------------------------------------------------- field
+Field make_field(uint64_t p) {
+    auto prime = [](uint64_t n) {
+        if (n < 2) return false;
+        for (uint64_t d = 2; d * d <= n; ++d)
+            if (n % d == 0) return false;
+        return true;
+    };
+    if (p < 2 || p >= (uint64_t(1) << 26) || !prime(p))
+        throw Error(FFG_ERR_CAPACITY, "modulus must be a prime with 2 <= p < 2^26");
+    Field F;
+    F.p = (uint32_t)p;
+    F.mu = ~uint64_t(0) / p;  // floor((2^64-1)/p) == floor(2^64/p) for p not a power of 2 (p=2: off by one, still < 3p)
+    uint64_t pm1 = p - 1;
+    int L = 1;
+    while (L < 4 && (pm1 >> (8 * L)) != 0) ++L;
+    F.limbs = L;
+    uint64_t ml[4] = {0, 0, 0, 0};
+    for (int i = 0; i < L; ++i) ml[i] = std::min<uint64_t>(255, pm1 >> (8 * i));
+    uint64_t worst = 1;
+    for (int s = 0; s <= 2 * (L - 1); ++s) {
+        uint64_t d = 0;
+        for (int i = 0; i < L; ++i) {
+            int j = s - i;
+            if (j >= 0 && j < L) d += ml[i] * ml[j];
+        }
+        worst = std::max(worst, d);
+    }
+    F.kmax = ((uint64_t(1) << 31) - 1) / worst;
+    uint64_t w = 1 % p;
+    for (int s = 0; s < 8; ++s) {
+        F.w[s] = (uint32_t)w;
+        w = (w << 8) % p;
+    }
+    return F;
+}
+
+// --------------------------------------------------------------------------- configs
+template <int L>
+struct TileCfg;
+template <>
+struct TileCfg<1> {
+    static constexpr int NT = 256, STAGES = 4;
+};
+template <>
+struct TileCfg<2> {
+    static constexpr int NT = 128, STAGES = 3;
+};
+template <>
+struct TileCfg<3> {
+    static constexpr int NT = 80, STAGES = 2;
+};
+template <>
+struct TileCfg<4> {
+    static constexpr int NT = 64, STAGES = 2;
+};
+
+constexpr int BM = 128;  // rows per CTA tile (UMMA M)
+constexpr int BK = 128;  // K bytes per stage (one 128-byte swizzle row)
+constexpr int GROUP_M = 16;
+
+int tile_n(int limbs) {
+    switch (limbs) {
+        case 1: return TileCfg<1>::NT;
+        case 2: return TileCfg<2>::NT;
+        case 3: return TileCfg<3>::NT;
+        default: return TileCfg<4>::NT;
+    }
+}
+
+template <int L>
+struct Smem {
+    static constexpr int NT = TileCfg<L>::NT, STAGES = TileCfg<L>::STAGES;
+    static constexpr int A_BYTES = L * BM * BK;       // L limb planes of 128 x 128 B
+    static constexpr int B_BYTES = L * NT * BK;       // L*NT rows of 128 B
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
+};
+
+struct EpiParams {
+    uint32_t* C;
+    uint64_t ldc;
+    uint32_t M, N;
+    uint32_t p;
+    uint64_t mu;
+    uint32_t alpha, beta;
+    uint32_t w[8];
+    uint32_t kblocks;
+    uint32_t m_tiles, n_tiles;
+};
+
+// --------------------------------------------------------------------------- the GEMM kernel
+template <int L>
+__global__ void __launch_bounds__(256, 1)
+    modgemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const EpiParams ep) {
+    using S = Smem<L>;
+    constexpr int NT = S::NT, STAGES = S::STAGES;
+    constexpr int D = 2 * L - 1;
+    constexpr uint32_t TMEM_COLS = 512;
+    static_assert(D * NT <= 512, "accumulator diagonals exceed TMEM");
+    static_assert(L * NT <= 256 && (L * NT) % 16 == 0 && NT % 16 == 0, "invalid UMMA N");
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+
+    // grouped rasterization: a wave covers GROUP_M row-blocks x a few column-blocks
+    const uint32_t pid = blockIdx.x;
+    const uint32_t in_group = GROUP_M * ep.n_tiles;
+    const uint32_t first_m = (pid / in_group) * GROUP_M;
+    const uint32_t gsize = min((uint32_t)GROUP_M, ep.m_tiles - first_m);
+    const uint32_t m_blk = first_m + (pid % in_group) % gsize;
+    const uint32_t n_blk = (pid % in_group) / gsize;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(tmem_full, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&mapA);
+        ptx::tma_prefetch(&mapB);
+    }
+    if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            const int32_t a_row0 = (int32_t)(m_blk * BM);
+            const int32_t b_row0 = (int32_t)(n_blk * L * NT);
+            for (uint32_t kb = 0; kb < ep.kblocks; ++kb) {
+                const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
+                ptx::mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * S::STAGE_BYTES;
+                ptx::mbar_expect_tx(&full[s], S::STAGE_BYTES);
+                for (int i = 0; i < L; ++i)
+                    ptx::tma_load_2d(st + i * BM * BK, &mapA, &full[s], (int32_t)(kb * BK),
+                                     a_row0 + i * (int32_t)(ep.m_tiles * BM));
+                ptx::tma_load_2d(st + S::A_BYTES, &mapB, &full[s], (int32_t)(kb * BK), b_row0);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (single thread)
+        if (lane == 0) {
+            constexpr uint32_t IDESC_FULL = ptx::idesc_u8(BM, L * NT);
+            constexpr uint32_t IDESC_HEAD = ptx::idesc_u8(BM, (L > 1 ? (L - 1) : 1) * NT);
+            constexpr uint32_t IDESC_TAIL = ptx::idesc_u8(BM, NT);
+            for (uint32_t kb = 0; kb < ep.kblocks; ++kb) {
+                const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
+                ptx::mbar_wait(&full[s], ph);
+                ptx::tc_fence_after();
+                const uint32_t a_base = ptx::smem_u32(smem + s * S::STAGE_BYTES);
+                const uint32_t b_base = a_base + S::A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BK / 32; ++kk) {
+                    const uint64_t bdesc = ptx::desc_kmajor_sw128(b_base + kk * 32);
+#pragma unroll
+                    for (int i = 0; i < L; ++i) {
+                        const uint64_t adesc = ptx::desc_kmajor_sw128(a_base + i * BM * BK + kk * 32);
+                        if (kb != 0 || kk != 0) {
+                            ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_FULL, 1);
+                        } else if (i == 0) {
+                            ptx::mma_i8(tmem, adesc, bdesc, IDESC_FULL, 0);
+                        } else {
+                            // first K-step: diagonals i..i+L-2 already hold data, i+L-1 is fresh
+                            ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_HEAD, 1);
+                            const uint64_t btail = ptx::desc_kmajor_sw128(b_base + (L - 1) * NT * BK + kk * 32);
+                            ptx::mma_i8(tmem + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
+                        }
+                    }
+                }
+                ptx::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
+            }
+            ptx::mma_commit(tmem_full);
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers -> mod p -> C
+        const uint32_t q = warp - 4;  // TMEM lane quarter
+        const uint32_t row = m_blk * BM + q * 32 + lane;
+        ptx::mbar_wait(tmem_full, 0);
+        ptx::tc_fence_after();
+        const uint32_t t_lane = tmem + ((q * 32) << 16);
+        uint32_t* crow = ep.C + (uint64_t)row * ep.ldc;
+        const uint32_t col0 = n_blk * NT;
+#pragma unroll 1
+        for (int c = 0; c < NT; c += 16) {
+            uint64_t acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0;
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                uint32_t r[16];
+                ptx::tmem_ld16(t_lane + s * NT + c, r);
+                ptx::tmem_ld_wait();
+                const uint64_t ws = ep.w[s];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += (uint64_t)r[j] * ws;
+            }
+            if (row < ep.M) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t col = col0 + c + j;
+                    if (col < ep.N) {
+                        const uint32_t prod = mod_u64(acc[j], ep.p, ep.mu);
+                        uint64_t v = (uint64_t)ep.alpha * prod;
+                        if (ep.beta) v += (uint64_t)ep.beta * crow[col];
+                        crow[col] = mod_u64(v, ep.p, ep.mu);
+                    }
+                }
+            }
+        }
+        ptx::tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// --------------------------------------------------------------------------- limb split kernels
+// A (M x K view, row-major) -> planes[l][Mp][Kp] bytes, K-major.  One thread = 4 consecutive k.
+__global__ void split_rows_kernel(const uint32_t* __restrict__ A, uint64_t lda, uint32_t M, uint32_t K,
+                                  uint8_t* __restrict__ out, uint32_t Mp, uint32_t Kp, int L) {
+    const uint32_t kq = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-byte group
+    const uint32_t m = blockIdx.y;
+    if (kq * 4 >= Kp) return;
+    uint32_t v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t k = kq * 4 + t;
+        v[t] = (m < M && k < K) ? A[(uint64_t)m * lda + k] : 0u;
+    }
+    for (int l = 0; l < L; ++l) {
+        const int sh = 8 * l;
+        const uint32_t packed = ((v[0] >> sh) & 0xFF) | (((v[1] >> sh) & 0xFF) << 8) | (((v[2] >> sh) & 0xFF) << 16) |
+                                (((v[3] >> sh) & 0xFF) << 24);
+        reinterpret_cast<uint32_t*>(out + ((uint64_t)l * Mp + m) * Kp)[kq] = packed;
+    }
+}
+
+// B (K x N view, row-major) -> rows (n/NT)*L*NT + l*NT + n%NT of Kp bytes (K-major), via a
+// 64(k) x 64(n) shared-memory transpose.
+__global__ void split_cols_kernel(const uint32_t* __restrict__ B, uint64_t ldb, uint32_t K, uint32_t N,
+                                  uint8_t* __restrict__ out, uint32_t Np, uint32_t Kp, int L, int NT) {
+    __shared__ uint32_t tile[64][65];
+    const uint32_t k0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+    const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 256 threads: 64 x 4
+    for (uint32_t r = ty; r < 64; r += 4) {
+        const uint32_t k = k0 + r, n = n0 + tx;
+        tile[r][tx] = (k < K && n < N) ? B[(uint64_t)k * ldb + n] : 0u;
+    }
+    __syncthreads();
+    // each output word = 4 consecutive k of one (n, limb): 64 n x 16 words x L
+    for (uint32_t idx = threadIdx.x; idx < 64u * 16u * (uint32_t)L; idx += blockDim.x) {
+        const uint32_t wq = idx & 15, nn = (idx >> 4) & 63, l = idx >> 10;
+        const uint32_t n = n0 + nn;
+        if (n >= Np) continue;
+        const int sh = 8 * l;
+        const uint32_t packed = ((tile[wq * 4 + 0][nn] >> sh) & 0xFF) | (((tile[wq * 4 + 1][nn] >> sh) & 0xFF) << 8) |
+                                (((tile[wq * 4 + 2][nn] >> sh) & 0xFF) << 16) |
+                                (((tile[wq * 4 + 3][nn] >> sh) & 0xFF) << 24);
+        const uint64_t orow = (uint64_t)(n / NT) * L * NT + (uint64_t)l * NT + (n % NT);
+        const uint32_t kw = (k0 >> 2) + wq;
+        if (kw * 4 < Kp) reinterpret_cast<uint32_t*>(out + orow * Kp)[kw] = packed;
+    }
+}
+
+// C <- beta*C (alpha == 0 or K == 0 path, blas.hpp:39-51)
+__global__ void scale_kernel(uint32_t* C, uint64_t ldc, uint32_t M, uint32_t N, uint32_t beta, uint32_t p,
+                             uint64_t mu) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+    if (i < M && j < N) {
+        uint32_t& c = C[(uint64_t)i * ldc + j];
+        c = beta == 0 ? 0u : (beta == 1 ? c : mul_mod(beta, c, p, mu));
+    }
+}
+
+// --------------------------------------------------------------------------- host side
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(f);
+    });
+    if (!fn) throw Error(FFG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap make_map(const uint8_t* base, uint64_t inner_bytes, uint64_t rows, uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner_bytes, rows};
+    cuuint64_t strides[1] = {inner_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(FFG_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+template <int L>
+void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t* Ap, const uint8_t* Bp, size_t Mp,
+                    size_t Np, size_t Kp, DView C, cudaStream_t st) {
+    using S = Smem<L>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        FFG_CUDA(cudaFuncSetAttribute(modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
+        attr_set = true;
+    }
+    CUtensorMap ma = make_map(Ap, Kp, (uint64_t)L * Mp, BM);
+    CUtensorMap mb = make_map(Bp, Kp, (uint64_t)(Np / S::NT) * L * S::NT, L * S::NT);
+    EpiParams ep;
+    ep.C = C.d;
+    ep.ldc = C.ld;
+    ep.M = (uint32_t)C.rows;
+    ep.N = (uint32_t)C.cols;
+    ep.p = F.p;
+    ep.mu = F.mu;
+    ep.alpha = alpha;
+    ep.beta = beta;
+    for (int s = 0; s < 8; ++s) ep.w[s] = F.w[s];
+    ep.kblocks = (uint32_t)(Kp / BK);
+    ep.m_tiles = (uint32_t)(Mp / BM);
+    ep.n_tiles = (uint32_t)(Np / S::NT);
+    dim3 grid(ep.m_tiles * ep.n_tiles);
+    modgemm_kernel<L><<<grid, 256, S::TOTAL, st>>>(ma, mb, ep);
+    FFG_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k) {
+    const int L = F.limbs, NT = tile_n(L);
+    const size_t kc = std::min<size_t>(k, F.kmax);
+    const size_t Kp = round_up(std::max<size_t>(kc, 1), BK);
+    return (size_t)L * round_up(m, BM) * Kp + (size_t)L * round_up(n, NT) * Kp + 2048;
+}
+
+void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, DView C, cudaStream_t st,
+               Workspace& ws, uint64_t* launches) {
+    if (A.cols != B.rows || C.rows != A.rows || C.cols != B.cols)
+        throw Error(FFG_ERR_DIM_MISMATCH, "gemm: non-conforming shapes");  // blas.hpp:21-24
+    const size_t M = C.rows, N = C.cols, K = A.cols;
+    if (M == 0 || N == 0) return;
+    alpha %= F.p;
+    beta %= F.p;
+    if (alpha == 0 || K == 0) {
+        if (beta != 1) {
+            dim3 g((unsigned)ceil_div(N, 256), (unsigned)M);
+            scale_kernel<<<g, 256, 0, st>>>(C.d, C.ld, (uint32_t)M, (uint32_t)N, beta, F.p, F.mu);
+            FFG_CUDA(cudaGetLastError());
+            if (launches) ++*launches;
+        }
+        return;
+    }
+    const int L = F.limbs, NT = tile_n(L);
+    const size_t Mp = round_up(M, BM), Np = round_up(N, NT);
+    for (size_t k0 = 0; k0 < K; k0 += F.kmax) {  // delayed reduction: one fold per kmax chunk
+        const size_t kc = std::min<size_t>(K - k0, F.kmax);
+        const size_t Kp = round_up(kc, BK);
+        uint8_t* Ap = ws.get(st, (size_t)L * Mp * Kp + (size_t)L * Np * Kp);
+        uint8_t* Bp = Ap + (size_t)L * Mp * Kp;
+        {
+            dim3 g((unsigned)ceil_div(Kp / 4, 128), (unsigned)Mp);
+            split_rows_kernel<<<g, 128, 0, st>>>(A.d + k0, A.ld, (uint32_t)M, (uint32_t)kc, Ap, (uint32_t)Mp,
+                                                 (uint32_t)Kp, L);
+            FFG_CUDA(cudaGetLastError());
+        }
+        {
+            dim3 g((unsigned)ceil_div(Kp, 64), (unsigned)ceil_div(Np, 64));
+            split_cols_kernel<<<g, 256, 0, st>>>(B.d + k0 * B.ld, B.ld, (uint32_t)kc, (uint32_t)N, Bp, (uint32_t)Np,
+                                                 (uint32_t)Kp, L, NT);
+            FFG_CUDA(cudaGetLastError());
+        }
+        const uint32_t b = (k0 == 0) ? beta : 1u;
+        switch (L) {
+            case 1: launch_modgemm<1>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
+            case 2: launch_modgemm<2>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
+            case 3: launch_modgemm<3>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
+            default: launch_modgemm<4>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
+        }
+        if (launches) *launches += 3;
+    }
+}
+
+}  // namespace ffg

@@ -1,0 +1,41 @@
+// pluq.cuh -- internal API of the triangular solves, base case, permutations and the
+// tile-recursive driver.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace ffg {
+
+// Everything a BLAS-level call needs: field, scratch, stream, launch counter.
+struct Blas {
+    const Field& F;
+    Workspace& ws;
+    cudaStream_t st;
+    uint64_t* launches;
+    void gemm(uint32_t alpha, DView A, DView B, uint32_t beta, DView C) const {
+        fgemm_dev(F, alpha, A, B, beta, C, st, ws, launches);
+    }
+    void count(uint64_t n = 1) const {
+        if (launches) *launches += n;
+    }
+};
+
+// B <- op(A)^-1 B (side 0) or B op(A)^-1 (side 1); blas.hpp:389-398.  check_diag
+// scans the diagonal first (nonunit) and throws SingularDiagonal(i) like blas.hpp:291-297.
+void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bool check_diag);
+
+// rr_base (rankrev.hpp:29-78) on a device block; P/Q host arrays (to_array semantics).
+size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q);
+
+// pluq_tile_recursive (rankrev.hpp:229-233); P/Q host arrays.
+size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q);
+
+// row (axis 0) / column (axis 1) gather by a device index array
+void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_t* perm);
+
+}  // namespace ffg

@@ -1,0 +1,265 @@
+"""Python host mirror of the reference ffpluq API over the C ABI (include/ffg.h).
+
+Names and argument meaning follow the reference (proj/include/ffpluq/*.hpp):
+
+    fgemm(p, alpha, A, B, beta, C)                 blas.hpp:220-246 (C updated, returned)
+    ftrsm(p, side, uplo, diag, A, B)               blas.hpp:389-398 (B solved, returned)
+    pluq_tile_recursive(p, A, threshold=8)         rankrev.hpp:229-233 -> PluqResult
+    rr_base(p, A)                                  rankrev.hpp:29-78   -> PluqResult
+
+Inputs are numpy uint32 arrays (host: the drop-in path, copies included) or
+torch.uint32/int32 CUDA tensors (device path, no copies).  Errors raise the
+reference's exception names (errors.hpp:9-59).  There is no CPU fallback: if
+libffg_b200.so is missing or no sm_100 GPU is present, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libffg_b200.so")
+
+
+class FfgError(RuntimeError):
+    code = -1
+
+
+class ZeroDivision(FfgError):
+    code = 1
+
+
+class CapacityError(FfgError):
+    code = 2
+
+
+class DimMismatch(FfgError):
+    code = 3
+
+
+class EmptyMatrix(FfgError):
+    code = 4
+
+
+class ZeroPivot(FfgError):
+    code = 5
+
+
+class SingularDiagonal(FfgError):
+    code = 6
+
+    def __init__(self, msg: str, index: int):
+        super().__init__(msg)
+        self.index = index
+
+
+class InvalidBlock(FfgError):
+    code = 8
+
+
+class CudaError(FfgError):
+    code = 100
+
+
+class NoDevice(FfgError):
+    code = 101
+
+
+_BY_CODE = {c.code: c for c in (ZeroDivision, CapacityError, DimMismatch, EmptyMatrix, ZeroPivot, InvalidBlock,
+                                CudaError, NoDevice)}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libffg_b200.so (built in-tree by paper_1402_3501_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1402_3501_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        sz, u32, u64, vp = C.c_size_t, C.c_uint32, C.c_uint64, C.c_void_p
+        L.ffg_create.argtypes = [C.POINTER(vp), C.c_int]
+        L.ffg_destroy.argtypes = [vp]
+        L.ffg_destroy.restype = None
+        L.ffg_last_error.restype = C.c_char_p
+        L.ffg_last_error_index.restype = sz
+        L.ffg_version.restype = C.c_char_p
+        L.ffg_set_stream.argtypes = [vp, vp]
+        L.ffg_get_stream.argtypes = [vp]
+        L.ffg_get_stream.restype = vp
+        L.ffg_synchronize.argtypes = [vp]
+        L.ffg_launch_count.argtypes = [vp]
+        L.ffg_launch_count.restype = u64
+        gemm_args = [vp, u64, u32, vp, sz, vp, sz, u32, vp, sz, sz, sz, sz]
+        L.ffg_fgemm.argtypes = gemm_args
+        L.ffg_fgemm_dev.argtypes = gemm_args
+        trsm_args = [vp, u64, C.c_int, C.c_int, C.c_int, vp, sz, vp, sz, sz, sz]
+        L.ffg_ftrsm.argtypes = trsm_args
+        L.ffg_ftrsm_dev.argtypes = trsm_args
+        pluq_args = [vp, u64, vp, sz, sz, sz, sz, vp, vp, C.POINTER(sz)]
+        L.ffg_pluq_tile_recursive.argtypes = pluq_args
+        L.ffg_pluq_tile_recursive_dev.argtypes = pluq_args
+        L.ffg_rr_base.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
+        L.ffg_apply_perm_dev.argtypes = [vp, vp, sz, sz, sz, C.c_int, C.c_int, vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    L = lib()
+    msg = (L.ffg_last_error() or b"").decode()
+    if rc == SingularDiagonal.code:
+        raise SingularDiagonal(msg, int(L.ffg_last_error_index()))
+    raise _BY_CODE.get(rc, FfgError)(f"[{rc}] {msg}")
+
+
+class Context:
+    """One GPU, one stream, device workspace (ffg_ctx)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self._h = C.c_void_p()
+        _check(lib().ffg_create(C.byref(self._h), device))
+        if stream is not None:
+            _check(lib().ffg_set_stream(self._h, C.c_void_p(stream)))
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def set_stream(self, stream: int | None) -> None:
+        _check(lib().ffg_set_stream(self._h, C.c_void_p(stream) if stream else None))
+
+    def synchronize(self) -> None:
+        _check(lib().ffg_synchronize(self._h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().ffg_launch_count(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            lib().ffg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default: Context | None = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+@dataclass
+class PluqResult:
+    """rankrev.hpp / pluq.hpp:12-19: packed factors stay in A; P, Q as PermSeq::to_array()."""
+    P: np.ndarray
+    Q: np.ndarray
+    rank: int
+    rank_revealing: bool = True
+
+    def profiles(self):
+        """extract_profiles (pluq.hpp:33-44): sorted first-r entries of P and Q."""
+        return np.sort(self.P[: self.rank]), np.sort(self.Q[: self.rank])
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _host(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.dtype != np.uint32:
+        raise TypeError("matrices are uint32 canonical residues")
+    if a.ndim != 2 or a.strides[1] != 4:
+        raise ValueError("row-major 2-D uint32 array with unit column stride required")
+    return a
+
+
+def _ld(a) -> int:
+    if _is_torch(a):
+        return int(a.stride(0)) if a.dim() == 2 and a.shape[0] > 0 else max(int(a.shape[-1]), 1)
+    return int(a.strides[0] // 4) if a.shape[0] > 0 else max(int(a.shape[1]), 1)
+
+
+def _ptr(a) -> int:
+    if _is_torch(a):
+        return int(a.data_ptr())
+    return int(a.ctypes.data)
+
+
+def fgemm(p: int, alpha: int, A, B, beta: int, Cm, ctx: Context | None = None):
+    """C <- alpha*A*B + beta*C mod p (blas.hpp:220-246).  Host arrays: C updated in place."""
+    ctx = ctx or default_context()
+    m, k = A.shape
+    n = B.shape[1]
+    dev = _is_torch(Cm)
+    if not dev:
+        A, B = _host(A), _host(B)
+        if not Cm.flags.writeable:
+            raise ValueError("C must be writeable")
+        _host(Cm)
+    if B.shape[0] != k or tuple(Cm.shape) != (m, n):
+        raise DimMismatch("gemm: non-conforming shapes")
+    fn = lib().ffg_fgemm_dev if dev else lib().ffg_fgemm
+    _check(fn(ctx.handle, p, alpha % p, _ptr(A), _ld(A), _ptr(B), _ld(B), beta % p, _ptr(Cm), _ld(Cm), m, n, k))
+    return Cm
+
+
+def ftrsm(p: int, side: int, uplo: int, diag: int, A, B, ctx: Context | None = None):
+    """B <- op(A)^-1 B (side 0) / B op(A)^-1 (side 1), in place (blas.hpp:389-398)."""
+    ctx = ctx or default_context()
+    m, n = B.shape
+    t = m if side == 0 else n
+    if A.shape[0] != A.shape[1]:
+        raise DimMismatch("trsm: triangle must be square")
+    if A.shape[0] != t:
+        raise DimMismatch("trsm: triangle does not match B")
+    dev = _is_torch(B)
+    if not dev:
+        A, B = _host(A), _host(B)
+    fn = lib().ffg_ftrsm_dev if dev else lib().ffg_ftrsm
+    _check(fn(ctx.handle, p, side, uplo, diag, _ptr(A), _ld(A), _ptr(B), _ld(B), m, n))
+    return B
+
+
+def pluq_tile_recursive(p: int, A, threshold: int = 8, ctx: Context | None = None) -> PluqResult:
+    """In-place tile-recursive PLUQ (rankrev.hpp:229-233)."""
+    ctx = ctx or default_context()
+    m, n = A.shape
+    P = np.zeros(max(m, 1), np.uint32)
+    Q = np.zeros(max(n, 1), np.uint32)
+    r = C.c_size_t(0)
+    dev = _is_torch(A)
+    if not dev:
+        A = _host(A)
+    fn = lib().ffg_pluq_tile_recursive_dev if dev else lib().ffg_pluq_tile_recursive
+    _check(fn(ctx.handle, p, _ptr(A), m, n, _ld(A), threshold, P.ctypes.data, Q.ctypes.data, C.byref(r)))
+    return PluqResult(P[:m], Q[:n], int(r.value))
+
+
+def rr_base(p: int, A, ctx: Context | None = None) -> PluqResult:
+    """Rank-revealing base case (rankrev.hpp:29-78) on a host array, in place."""
+    ctx = ctx or default_context()
+    A = _host(A)
+    m, n = A.shape
+    P = np.zeros(max(m, 1), np.uint32)
+    Q = np.zeros(max(n, 1), np.uint32)
+    r = C.c_size_t(0)
+    _check(lib().ffg_rr_base(ctx.handle, p, _ptr(A), m, n, _ld(A), P.ctypes.data, Q.ctypes.data, C.byref(r)))
+    return PluqResult(P[:m], Q[:n], int(r.value))
