@@ -1,0 +1,163 @@
+// perm.cu -- permutation kernels: index-array compositions and row/column gathers.
+//
+// Replaces apply_perm / rotate_rows_block / rotate_cols_block / PermSeq
+// composition (perm.hpp:44-53, 167-215).  The reference replays Rot/Swap
+// moves one at a time (each a memmove of whole rows); here a permutation is
+// an index array (PermSeq::to_array() semantics) and every application is one
+// gather over the moved range only: HBM traffic = 2 reads + 2 writes of the
+// rows/columns that actually move, nothing for the rest.
+#include "pluq.cuh"
+
+namespace ffg {
+
+// position t (relative to the range start) takes source position src(t)
+struct PermSrc {
+    const uint32_t* arr;  // if non-null: src(t) = arr[t + base] - base... see at()
+    uint32_t base;        // arr is indexed at t + base and returns absolute positions
+    uint32_t span, len;   // rotation: [0,len) <- [span, span+len), [len, len+span) <- [0, span)
+    __device__ __forceinline__ uint32_t at(uint32_t t) const {
+        if (arr) return arr[t + base] - base;
+        return t < len ? span + t : t - len;
+    }
+};
+
+__global__ void rows_gather_kernel(const uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows, uint32_t ncols,
+                                   PermSrc src, uint32_t* __restrict__ tmp) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
+    if (c < ncols && t < nrows) tmp[(uint64_t)t * ncols + c] = A[(uint64_t)src.at(t) * lda + c];
+}
+__global__ void rows_store_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows, uint32_t ncols,
+                                  const uint32_t* __restrict__ tmp) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
+    if (c < ncols && t < nrows) A[(uint64_t)t * lda + c] = tmp[(uint64_t)t * ncols + c];
+}
+__global__ void cols_gather_kernel(const uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows, uint32_t ncols,
+                                   PermSrc src, uint32_t* __restrict__ tmp) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (u < ncols && r < nrows) tmp[(uint64_t)r * ncols + u] = A[(uint64_t)r * lda + src.at(u)];
+}
+
+// in-place gather of an index array range through shared memory: a[t] = old[src(t)]
+__global__ void array_gather_kernel(uint32_t* __restrict__ a, uint32_t len, PermSrc src) {
+    extern __shared__ uint32_t s[];
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) s[t] = a[t];
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) a[t] = s[src.at(t)];
+}
+__global__ void array_gather_global_kernel(const uint32_t* __restrict__ a, uint32_t len, PermSrc src,
+                                          uint32_t* __restrict__ out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < len) out[t] = a[src.at(t)];
+}
+__global__ void iota_kernel(uint32_t* a, uint32_t len) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < len) a[t] = t;
+}
+
+namespace {
+void gather_rows(const Blas& b, DView a, PermSrc src) {
+    if (a.empty()) return;
+    uint32_t* tmp = nullptr;
+    FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
+    dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
+    rows_gather_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
+    rows_store_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
+    FFG_CUDA(cudaGetLastError());
+    FFG_CUDA(cudaFreeAsync(tmp, b.st));
+    b.count(2);
+}
+void gather_cols(const Blas& b, DView a, PermSrc src) {
+    if (a.empty()) return;
+    uint32_t* tmp = nullptr;
+    FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
+    dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
+    cols_gather_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
+    rows_store_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
+    FFG_CUDA(cudaGetLastError());
+    FFG_CUDA(cudaFreeAsync(tmp, b.st));
+    b.count(2);
+}
+}  // namespace
+
+void perm_apply_range(const Blas& b, DView a, int axis, const uint32_t* perm, size_t lo, size_t hi) {
+    if (hi <= lo || a.empty()) return;
+    PermSrc src{perm, (uint32_t)lo, 0, 0};
+    if (axis == 0)
+        gather_rows(b, a.sub(lo, 0, hi - lo, a.cols), src);
+    else
+        gather_cols(b, a.sub(0, lo, a.rows, hi - lo), src);
+}
+
+void rotate_block_dev(const Blas& b, DView a, int axis, size_t first, size_t mid, size_t len) {
+    if (len == 0 || mid == first || a.empty()) return;  // perm.hpp:198, 210
+    const size_t span = mid - first;
+    PermSrc src{nullptr, 0, (uint32_t)span, (uint32_t)len};
+    if (axis == 0)
+        gather_rows(b, a.sub(first, 0, span + len, a.cols), src);
+    else
+        gather_cols(b, a.sub(0, first, a.rows, span + len), src);
+}
+
+static void array_gather(const Blas& b, uint32_t* a, size_t len, PermSrc src) {
+    if (len == 0) return;
+    const size_t bytes = len * 4;
+    if (bytes <= 200 * 1024) {
+        static bool set = false;
+        if (!set) {
+            FFG_CUDA(cudaFuncSetAttribute(array_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            set = true;
+        }
+        array_gather_kernel<<<1, 1024, bytes, b.st>>>(a, (uint32_t)len, src);
+        b.count();
+    } else {
+        uint32_t* tmp = nullptr;
+        FFG_CUDA(cudaMallocAsync(&tmp, bytes, b.st));
+        array_gather_global_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, b.st>>>(a, (uint32_t)len, src, tmp);
+        FFG_CUDA(cudaMemcpyAsync(a, tmp, bytes, cudaMemcpyDeviceToDevice, b.st));
+        FFG_CUDA(cudaFreeAsync(tmp, b.st));
+        b.count();
+    }
+    FFG_CUDA(cudaGetLastError());
+}
+
+void perm_compose_dev(const Blas& b, uint32_t* dst, size_t off, const uint32_t* child, size_t lo, size_t hi) {
+    if (hi <= lo) return;
+    // dst[off + t] = dst[off + child[t]] for t in [lo, hi); child is identity outside the range
+    PermSrc src{child, (uint32_t)lo, 0, 0};
+    array_gather(b, dst + off + lo, hi - lo, src);
+}
+
+void perm_rot_dev(const Blas& b, uint32_t* arr, size_t first, size_t mid, size_t len) {
+    if (len == 0 || mid == first) return;
+    PermSrc src{nullptr, 0, (uint32_t)(mid - first), (uint32_t)len};
+    array_gather(b, arr + first, mid - first + len, src);
+}
+
+void perm_iota_dev(const Blas& b, uint32_t* arr, size_t len) {
+    if (!len) return;
+    iota_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, b.st>>>(arr, (uint32_t)len);
+    FFG_CUDA(cudaGetLastError());
+    b.count();
+}
+
+__global__ void invert_perm_kernel(const uint32_t* p, uint32_t* q, uint32_t n) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) q[p[t]] = t;
+}
+
+void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_t* perm) {
+    const size_t dim = axis == 0 ? a.rows : a.cols;
+    if (!inverse) {
+        perm_apply_range(b, a, axis, perm, 0, dim);
+        return;
+    }
+    // inverse (perm.hpp:190-192): out[perm[t]] = in[t] -> gather by the inverse index array
+    uint32_t* invp = nullptr;
+    FFG_CUDA(cudaMallocAsync(&invp, dim * 4, b.st));
+    invert_perm_kernel<<<(unsigned)ceil_div(dim, 256), 256, 0, b.st>>>(perm, invp, (uint32_t)dim);
+    b.count();
+    perm_apply_range(b, a, axis, invp, 0, dim);
+    FFG_CUDA(cudaFreeAsync(invp, b.st));
+}
+
+}  // namespace ffg

@@ -1,13 +1,273 @@
-// pluq.cu -- placeholder until the TRSM / base case / driver land.
+// pluq.cu -- host driver of the tile-recursive PLUQ (rankrev.hpp:85-183, 229-233).
+//
+// The recursion is copied exactly -- split m1 = ceil(m/2), n1 = ceil(n/2)
+// (:95), base case iff min(m, n) <= threshold (:92), the same Schur updates in
+// the same order, the same pivot-gather (A1, E, G, R) -- because on rank
+// deficient inputs the P/Q arrays depend on that structure.  What changes:
+//   * every block operation is a device kernel on the matrix resident in HBM
+//     (GEMM/TRSM on tcgen05, permutations as range-limited gathers);
+//   * permutations are index arrays in a device LIFO arena; the host only
+//     tracks each node's rank and the [lo, hi) range its P/Q actually move,
+//     so identity permutations (all of them on generic full-rank input) cost
+//     no launch at all;
+//   * the one unavoidable device->host sync is the rank of each base case,
+//     which decides every later block shape.
+// Deliberate deviation: rankrev.hpp:146 overwrites block I with J = L3^-1 I,
+// which corrupts the L factor whenever r2 > 0 and r3 > 0;
+// here J lives in a temporary, which is what the reference's own comment
+// "O = N - J*V2" describes.  Outputs equal the fixed reference everywhere and
+// the unmodified reference wherever r2 == 0 or r3 == 0 (all full-rank input).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "pluq.cuh"
 
 namespace ffg {
 
-void ftrsm_dev(const Blas&, int, int, int, DView, DView, bool) { throw Error(FFG_ERR_INTERNAL, "ftrsm: not built yet"); }
-size_t rr_base_dev(const Blas&, DView, uint32_t*, uint32_t*) { throw Error(FFG_ERR_INTERNAL, "rr_base: not built yet"); }
-size_t pluq_tile_recursive_dev(const Blas&, DView, size_t, uint32_t*, uint32_t*) {
-    throw Error(FFG_ERR_INTERNAL, "pluq: not built yet");
+namespace {
+
+struct Range {
+    size_t lo = 0, hi = 0;
+    bool empty() const { return hi <= lo; }
+    void add(size_t l, size_t h) {
+        if (h <= l) return;
+        if (empty()) {
+            lo = l;
+            hi = h;
+        } else {
+            lo = std::min(lo, l);
+            hi = std::max(hi, h);
+        }
+    }
+};
+
+struct NodeRes {
+    size_t rank = 0;
+    uint32_t* P = nullptr;  // device index arrays (valid inside pr / qr)
+    uint32_t* Q = nullptr;
+    Range pr, qr;
+};
+
+// device LIFO arena for permutation index arrays
+class PermArena {
+public:
+    PermArena(size_t words, cudaStream_t st) : st_(st), cap_(words) {
+        if (cap_) FFG_CUDA(cudaMallocAsync(&base_, cap_ * 4, st_));
+    }
+    ~PermArena() {
+        if (base_) cudaFreeAsync(base_, st_);
+    }
+    uint32_t* alloc(size_t words) {
+        if (top_ + words > cap_) throw Error(FFG_ERR_INTERNAL, "permutation arena exhausted");
+        uint32_t* p = base_ + top_;
+        top_ += (words + 31) & ~size_t(31);
+        return p;
+    }
+    size_t mark() const { return top_; }
+    void reset(size_t m) { top_ = m; }
+
+private:
+    cudaStream_t st_;
+    uint32_t* base_ = nullptr;
+    size_t cap_ = 0, top_ = 0;
+};
+
+struct Driver {
+    const Blas& b;
+    size_t thr;
+    PermArena arena;
+    BaseInfo* info_dev = nullptr;
+    BaseInfo* info_host = nullptr;
+    cudaEvent_t ev = nullptr;
+    uint64_t base_cases = 0;
+
+    Driver(const Blas& bl, size_t t, size_t m, size_t n)
+        : b(bl), thr(std::max<size_t>(1, t)), arena(8 * (m + n) + 4096, bl.st) {
+        FFG_CUDA(cudaMallocAsync(&info_dev, sizeof(BaseInfo), b.st));
+        FFG_CUDA(cudaMallocHost(&info_host, sizeof(BaseInfo)));
+        FFG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    ~Driver() {
+        if (info_dev) cudaFreeAsync(info_dev, b.st);
+        if (info_host) cudaFreeHost(info_host);
+        if (ev) cudaEventDestroy(ev);
+    }
+
+    NodeRes base(DView a, NodeRes res) {
+        rr_base_launch(b, a, res.P, res.Q, info_dev);
+        FFG_CUDA(cudaMemcpyAsync(info_host, info_dev, sizeof(BaseInfo), cudaMemcpyDeviceToHost, b.st));
+        FFG_CUDA(cudaEventRecord(ev, b.st));
+        FFG_CUDA(cudaEventSynchronize(ev));  // the rank decides every later shape
+        ++base_cases;
+        res.rank = info_host->rank;
+        res.pr = Range{info_host->plo, info_host->phi};
+        res.qr = Range{info_host->qlo, info_host->qhi};
+        return res;
+    }
+
+    void apply(const NodeRes& c, int axis, DView v) {
+        const Range& r = axis == 0 ? c.pr : c.qr;
+        if (r.empty() || v.empty()) return;
+        perm_apply_range(b, v, axis, axis == 0 ? c.P : c.Q, r.lo, r.hi);
+    }
+
+    void trsm_lower_unit(DView L, DView B) { ftrsm_dev(b, 0, 0, 0, L, B, false); }
+    void trsm_upper_nonunit(DView U, DView B) { ftrsm_dev(b, 1, 1, 1, U, B, false); }
+    void gemm_sub(DView A, DView B, DView C) { b.gemm(b.F.p - 1, A, B, 1, C); }
+
+    // compose a child's permutation into this node's array at offset off
+    void compose(uint32_t* arr, bool& init, size_t len, Range& acc, size_t off, const uint32_t* child,
+                 const Range& cr) {
+        if (cr.empty()) return;
+        if (!init) {
+            perm_iota_dev(b, arr, len);
+            init = true;
+        }
+        perm_compose_dev(b, arr, off, child, cr.lo, cr.hi);
+        acc.add(off + cr.lo, off + cr.hi);
+    }
+    void rot(uint32_t* arr, bool& init, size_t len, Range& acc, size_t first, size_t mid, size_t cnt) {
+        if (cnt == 0 || mid == first) return;
+        if (!init) {
+            perm_iota_dev(b, arr, len);
+            init = true;
+        }
+        perm_rot_dev(b, arr, first, mid, cnt);
+        acc.add(first, mid + cnt);
+    }
+
+    NodeRes rec(DView a) {
+        const size_t m = a.rows, n = a.cols;
+        NodeRes res;
+        res.P = arena.alloc(std::max<size_t>(m, 1));
+        res.Q = arena.alloc(std::max<size_t>(n, 1));
+        if (m == 0 || n == 0) return res;                        // rankrev.hpp:91
+        if (std::min(m, n) <= thr) return base(a, res);          // :92
+        const size_t mark = arena.mark();
+        const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;         // :95
+
+        NodeRes r1s = rec(a.sub(0, 0, m1, n1));                  // :97
+        const size_t r1 = r1s.rank;
+        apply(r1s, 0, a.sub(0, n1, m1, n - n1));                 // :99
+        apply(r1s, 1, a.sub(m1, 0, m - m1, n1));                 // :100
+
+        DView L1 = a.sub(0, 0, r1, r1);                          // :102-109
+        DView V1 = a.sub(0, r1, r1, n1 - r1);
+        DView M1 = a.sub(r1, 0, m1 - r1, r1);
+        DView D = a.sub(0, n1, r1, n - n1);
+        DView E = a.sub(r1, n1, m1 - r1, n - n1);
+        DView Fb = a.sub(m1, 0, m - m1, r1);
+        DView G = a.sub(m1, r1, m - m1, n1 - r1);
+        DView H = a.sub(m1, n1, m - m1, n - n1);
+        if (r1 > 0) {                                            // :111-117
+            if (!D.empty()) trsm_lower_unit(L1, D);
+            if (!E.empty()) gemm_sub(M1, D, E);
+            if (!Fb.empty()) trsm_upper_nonunit(L1, Fb);
+            if (!G.empty() && !V1.empty()) gemm_sub(Fb, V1, G);
+            if (!H.empty()) gemm_sub(Fb, D, H);
+        }
+
+        NodeRes r2s = rec(E);                                    // :119-125 (E, G independent)
+        NodeRes r3s = rec(G);
+        const size_t r2 = r2s.rank, r3 = r3s.rank;
+
+        apply(r2s, 0, a.sub(r1, 0, m1 - r1, r1));                // :128-133
+        apply(r2s, 1, a.sub(0, n1, r1, n - n1));
+        apply(r2s, 1, a.sub(m1, n1, m - m1, n - n1));
+        apply(r3s, 0, a.sub(m1, 0, m - m1, r1));
+        apply(r3s, 0, a.sub(m1, n1, m - m1, n - n1));
+        apply(r3s, 1, a.sub(0, r1, r1, n1 - r1));
+
+        DView U2 = a.sub(r1, n1, r2, r2);                        // :135-142
+        DView V2 = a.sub(r1, n1 + r2, r2, n - n1 - r2);
+        DView L3 = a.sub(m1, r1, r3, r3);
+        DView M3 = a.sub(m1 + r3, r1, m - m1 - r3, r3);
+        DView I = a.sub(m1, n1, r3, r2);
+        DView K = a.sub(m1 + r3, n1, m - m1 - r3, r2);
+        DView N = a.sub(m1, n1 + r2, r3, n - n1 - r2);
+        DView R = a.sub(m1 + r3, n1 + r2, m - m1 - r3, n - n1 - r2);
+
+        if (r2 > 0 && !I.empty()) trsm_upper_nonunit(U2, I);    // :144
+        if (r2 > 0 && !K.empty()) trsm_upper_nonunit(U2, K);    // :145
+        uint32_t* jbuf = nullptr;
+        DView J = I;
+        if (r3 > 0 && !I.empty()) {                              // :146, J = L3^-1 I into a temporary
+            FFG_CUDA(cudaMallocAsync(&jbuf, I.rows * I.cols * 4, b.st));
+            FFG_CUDA(cudaMemcpy2DAsync(jbuf, I.cols * 4, I.d, I.ld * 4, I.cols * 4, I.rows, cudaMemcpyDeviceToDevice,
+                                       b.st));
+            J = DView{jbuf, I.rows, I.cols, I.cols};
+            trsm_lower_unit(L3, J);
+        }
+        if (r3 > 0 && !N.empty()) trsm_lower_unit(L3, N);       // :147
+        if (!N.empty() && !J.empty()) gemm_sub(J, V2, N);        // :148  O = N - J*V2
+        if (!R.empty()) {                                        // :149-152
+            if (!K.empty() && !V2.empty()) gemm_sub(K, V2, R);
+            if (!N.empty()) gemm_sub(M3, N, R);
+        }
+        if (jbuf) FFG_CUDA(cudaFreeAsync(jbuf, b.st));
+
+        NodeRes r4s = rec(R);                                    // :154
+        const size_t r4 = r4s.rank;
+        apply(r4s, 0, a.sub(m1 + r3, 0, m - m1 - r3, r1 + r3));  // :156-161
+        if (r2 > 0) apply(r4s, 0, a.sub(m1 + r3, n1, m - m1 - r3, r2));
+        apply(r4s, 1, a.sub(0, n1 + r2, r1, n - n1 - r2));
+        if (r2 > 0) apply(r4s, 1, a.sub(r1, n1 + r2, r2, n - n1 - r2));
+        if (r3 > 0) apply(r4s, 1, a.sub(m1, n1 + r2, r3, n - n1 - r2));
+
+        bool pinit = false, qinit = false;                       // :163-170
+        compose(res.P, pinit, m, res.pr, 0, r1s.P, r1s.pr);
+        compose(res.P, pinit, m, res.pr, r1, r2s.P, r2s.pr);
+        compose(res.P, pinit, m, res.pr, m1, r3s.P, r3s.pr);
+        compose(res.P, pinit, m, res.pr, m1 + r3, r4s.P, r4s.pr);
+        compose(res.Q, qinit, n, res.qr, 0, r1s.Q, r1s.qr);
+        compose(res.Q, qinit, n, res.qr, r1, r3s.Q, r3s.qr);
+        compose(res.Q, qinit, n, res.qr, n1, r2s.Q, r2s.qr);
+        compose(res.Q, qinit, n, res.qr, n1 + r2, r4s.Q, r4s.qr);
+
+        rot(res.P, pinit, m, res.pr, r1 + r2, m1, r3 + r4);       // :174-179 pivot gather
+        rotate_block_dev(b, a, 0, r1 + r2, m1, r3 + r4);
+        rot(res.Q, qinit, n, res.qr, r1, n1, r2);
+        rotate_block_dev(b, a, 1, r1, n1, r2);
+        rot(res.Q, qinit, n, res.qr, r1 + r2 + r3, n1 + r2, r4);
+        rotate_block_dev(b, a, 1, r1 + r2 + r3, n1 + r2, r4);
+
+        res.rank = r1 + r2 + r3 + r4;
+        arena.reset(mark);  // children consumed (stream order protects the pending kernels)
+        return res;
+    }
+
+    void download(const NodeRes& res, size_t m, size_t n, uint32_t* P, uint32_t* Q) {
+        if (P) {
+            for (size_t i = 0; i < m; ++i) P[i] = (uint32_t)i;
+            if (!res.pr.empty())
+                FFG_CUDA(cudaMemcpyAsync(P + res.pr.lo, res.P + res.pr.lo, (res.pr.hi - res.pr.lo) * 4,
+                                         cudaMemcpyDeviceToHost, b.st));
+        }
+        if (Q) {
+            for (size_t j = 0; j < n; ++j) Q[j] = (uint32_t)j;
+            if (!res.qr.empty())
+                FFG_CUDA(cudaMemcpyAsync(Q + res.qr.lo, res.Q + res.qr.lo, (res.qr.hi - res.qr.lo) * 4,
+                                         cudaMemcpyDeviceToHost, b.st));
+        }
+        FFG_CUDA(cudaStreamSynchronize(b.st));
+    }
+};
+
+}  // namespace
+
+size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
+    Driver drv(b, threshold, a.rows, a.cols);
+    NodeRes res = drv.rec(a);
+    drv.download(res, a.rows, a.cols, P, Q);
+    return res.rank;
 }
-void apply_perm_dev(const Blas&, DView, int, int, const uint32_t*) { throw Error(FFG_ERR_INTERNAL, "perm: not built yet"); }
+
+size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q) {
+    Driver drv(b, SIZE_MAX, a.rows, a.cols);
+    NodeRes res = drv.rec(a);
+    drv.download(res, a.rows, a.cols, P, Q);
+    return res.rank;
+}
 
 }  // namespace ffg

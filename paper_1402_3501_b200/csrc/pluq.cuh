@@ -35,6 +35,20 @@ size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q);
 // pluq_tile_recursive (rankrev.hpp:229-233); P/Q host arrays.
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q);
 
+// rank + moved ranges of a base-case result (device -> pinned host)
+struct BaseInfo {
+    uint32_t rank, plo, phi, qlo, qhi;
+};
+// one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info
+void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev);
+
+// permutation kernels (perm.cu)
+void perm_apply_range(const Blas& b, DView a, int axis, const uint32_t* perm, size_t lo, size_t hi);
+void rotate_block_dev(const Blas& b, DView a, int axis, size_t first, size_t mid, size_t len);
+void perm_compose_dev(const Blas& b, uint32_t* dst, size_t off, const uint32_t* child, size_t lo, size_t hi);
+void perm_rot_dev(const Blas& b, uint32_t* arr, size_t first, size_t mid, size_t len);
+void perm_iota_dev(const Blas& b, uint32_t* arr, size_t len);
+
 // row (axis 0) / column (axis 1) gather by a device index array
 void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_t* perm);
 

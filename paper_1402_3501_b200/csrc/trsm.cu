@@ -1,0 +1,167 @@
+// trsm.cu -- modular triangular solves, recursive onto the tcgen05 GEMM.
+//
+// Replaces ftrsm / pftrsm / trsm_left / trsm_right (blas.hpp:285-419).  The
+// solution of a triangular system mod p is unique, so any exact evaluation
+// order gives the reference's bits.  Structure:
+//   1. one launch inverts every TB x TB diagonal block of the triangle
+//      (tri_inv_kernel, one CTA per block, exact column substitution in SMEM);
+//   2. a recursion split at multiples of TB turns the off-diagonal work into
+//      Schur GEMMs  B2 -= T21 X1  (fgemm, alpha = p-1, beta = 1);
+//   3. each leaf is the GEMM  X = inv(T_bb) B_b  (alpha = 1, beta = 0) written
+//      in place -- safe because the GEMM reads limb copies made before it runs.
+// Only the selected triangle (plus the diagonal when nonunit) is read, so T can
+// be the packed L\U square that tile_rec passes (rankrev.hpp:112,114).
+#include <mutex>
+
+#include "pluq.cuh"
+
+namespace ffg {
+
+constexpr int TB = 128;  // diagonal block (= GEMM K-block, so leaf GEMMs have no K padding)
+
+// inverse of the diagonal block b of T (t x t) into Tinv + b*TB*TB (TB x TB, zero padded)
+template <bool UPPER, bool UNIT>
+__global__ void __launch_bounds__(TB) tri_inv_kernel(const uint32_t* __restrict__ T, uint64_t ldt, uint32_t t,
+                                                    uint32_t* __restrict__ Tinv, uint32_t p, uint64_t mu) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* S = sm;              // TB x TB block of T
+    uint32_t* X = sm + TB * TB;    // TB x TB inverse, column j owned by thread j
+    uint32_t* dinv = X + TB * TB;  // TB
+    const uint32_t b = blockIdx.x, j = threadIdx.x;
+    const uint32_t o = b * TB;
+    const uint32_t tb = min((uint32_t)TB, t - o);
+    for (uint32_t idx = j; idx < (uint32_t)TB * TB; idx += TB) {
+        const uint32_t r = idx / TB, c = idx % TB;
+        S[idx] = (r < tb && c < tb) ? T[(uint64_t)(o + r) * ldt + o + c] : 0u;
+        X[idx] = 0u;
+    }
+    __syncthreads();
+    if (!UNIT && j < tb) dinv[j] = inv_mod(S[j * TB + j], p);
+    __syncthreads();
+    if (j < tb) {
+        X[j * TB + j] = UNIT ? 1u : dinv[j];
+        if (!UPPER) {
+            for (uint32_t i = j + 1; i < tb; ++i) {
+                uint64_t s = 0;
+                for (uint32_t k = j; k < i; ++k) s += (uint64_t)S[i * TB + k] * X[k * TB + j];
+                uint32_t v = mod_u64(s, p, mu);
+                v = v ? p - v : 0u;
+                X[i * TB + j] = UNIT ? v : mul_mod(v, dinv[i], p, mu);
+            }
+        } else {
+            for (int i = (int)j - 1; i >= 0; --i) {
+                uint64_t s = 0;
+                for (uint32_t k = i + 1; k <= j; ++k) s += (uint64_t)S[i * TB + k] * X[k * TB + j];
+                uint32_t v = mod_u64(s, p, mu);
+                v = v ? p - v : 0u;
+                X[i * TB + j] = UNIT ? v : mul_mod(v, dinv[i], p, mu);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t* out = Tinv + (uint64_t)b * TB * TB;
+    for (uint32_t idx = j; idx < (uint32_t)TB * TB; idx += TB) out[idx] = X[idx];
+}
+
+// smallest i with T[i][i] == 0 (blas.hpp:291-297 / 347-353)
+__global__ void first_zero_diag_kernel(const uint32_t* T, uint64_t ldt, uint32_t t, uint32_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < t && T[(uint64_t)i * ldt + i] == 0) atomicMin(out, i);
+}
+
+namespace {
+
+struct TrsmCtx {
+    const Blas& b;
+    int side, upper;
+    DView T;
+    const uint32_t* Tinv;  // one TB x TB inverse per diagonal block
+};
+
+// solve on the diagonal range [o, o + t) of T (o a multiple of TB) against B
+void trsm_rec(const TrsmCtx& c, size_t o, size_t t, DView B) {
+    const uint32_t pm1 = c.b.F.p - 1;
+    if (t <= (size_t)TB) {
+        DView inv{const_cast<uint32_t*>(c.Tinv) + (o / TB) * TB * TB, t, t, (size_t)TB};
+        if (c.side == 0)
+            c.b.gemm(1, inv, B, 0, B);
+        else
+            c.b.gemm(1, B, inv, 0, B);
+        return;
+    }
+    const size_t nb = ceil_div(t, TB);
+    const size_t t1 = ((nb + 1) / 2) * TB, t2 = t - t1;
+    DView T11 = c.T.sub(o, o, t1, t1), T22 = c.T.sub(o + t1, o + t1, t2, t2);
+    (void)T11;
+    (void)T22;
+    if (c.side == 0) {
+        DView B1 = B.sub(0, 0, t1, B.cols), B2 = B.sub(t1, 0, t2, B.cols);
+        if (!c.upper) {  // L X = B
+            trsm_rec(c, o, t1, B1);
+            c.b.gemm(pm1, c.T.sub(o + t1, o, t2, t1), B1, 1, B2);
+            trsm_rec(c, o + t1, t2, B2);
+        } else {  // U X = B
+            trsm_rec(c, o + t1, t2, B2);
+            c.b.gemm(pm1, c.T.sub(o, o + t1, t1, t2), B2, 1, B1);
+            trsm_rec(c, o, t1, B1);
+        }
+    } else {
+        DView B1 = B.sub(0, 0, B.rows, t1), B2 = B.sub(0, t1, B.rows, t2);
+        if (c.upper) {  // X U = B
+            trsm_rec(c, o, t1, B1);
+            c.b.gemm(pm1, B1, c.T.sub(o, o + t1, t1, t2), 1, B2);
+            trsm_rec(c, o + t1, t2, B2);
+        } else {  // X L = B
+            trsm_rec(c, o + t1, t2, B2);
+            c.b.gemm(pm1, B2, c.T.sub(o + t1, o, t2, t1), 1, B1);
+            trsm_rec(c, o, t1, B1);
+        }
+    }
+}
+
+}  // namespace
+
+void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bool check_diag) {
+    const size_t need = side == 0 ? B.rows : B.cols;
+    if (A.rows != A.cols) throw Error(FFG_ERR_DIM_MISMATCH, "trsm: triangle must be square");
+    if (A.rows != need) throw Error(FFG_ERR_DIM_MISMATCH, "trsm: triangle does not match B");
+    if (A.rows == 0 || B.rows == 0 || B.cols == 0) return;  // blas.hpp:393
+    const size_t t = A.rows;
+    const uint32_t p = b.F.p;
+    if (check_diag && diag == 1) {
+        uint32_t* d = nullptr;
+        FFG_CUDA(cudaMallocAsync(&d, sizeof(uint32_t), b.st));
+        FFG_CUDA(cudaMemsetAsync(d, 0xFF, sizeof(uint32_t), b.st));
+        first_zero_diag_kernel<<<(unsigned)ceil_div(t, 256), 256, 0, b.st>>>(A.d, A.ld, (uint32_t)t, d);
+        b.count();
+        uint32_t h = 0;
+        FFG_CUDA(cudaMemcpyAsync(&h, d, sizeof(uint32_t), cudaMemcpyDeviceToHost, b.st));
+        FFG_CUDA(cudaFreeAsync(d, b.st));
+        FFG_CUDA(cudaStreamSynchronize(b.st));
+        if (h != 0xFFFFFFFFu)
+            throw Error(FFG_ERR_SINGULAR_DIAGONAL, "zero diagonal entry " + std::to_string(h) + " in triangular solve",
+                        h);
+    }
+    const size_t nblk = ceil_div(t, TB);
+    uint32_t* Tinv = nullptr;
+    FFG_CUDA(cudaMallocAsync(&Tinv, nblk * TB * TB * sizeof(uint32_t), b.st));
+    const int upper = uplo == 1, unit = diag == 0;
+    const size_t smem = (2 * TB * TB + TB) * sizeof(uint32_t);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    });
+    auto kern = upper ? (unit ? tri_inv_kernel<true, true> : tri_inv_kernel<true, false>)
+                      : (unit ? tri_inv_kernel<false, true> : tri_inv_kernel<false, false>);
+    kern<<<(unsigned)nblk, TB, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.count();
+    TrsmCtx c{b, side, upper, A, Tinv};
+    trsm_rec(c, 0, t, B);
+    FFG_CUDA(cudaFreeAsync(Tinv, b.st));
+}
+
+}  // namespace ffg
