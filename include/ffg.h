@@ -103,6 +103,24 @@ int ffg_rr_base(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_
 int ffg_apply_perm_dev(ffg_ctx *ctx, uint32_t *A, size_t m, size_t n, size_t lda, int axis, int inverse,
                        const uint32_t *perm);
 
+/* ---- field embedding (introspection) ----------------------------------
+ * For modulus p: *limbs = 8-bit limbs per residue on the tensor cores,
+ * *kmax = inner-dimension chunk of one exact s32 accumulation (the GEMM reduces
+ * mod p once per kmax products -- the delayed-reduction bound, field.hpp:26-35
+ * restated for the limb embedding), *nt = output columns per GEMM tile.
+ * Pure host function (no device needed). */
+int ffg_field_info(uint64_t p, int *limbs, uint64_t *kmax, int *nt);
+
+/* ---- seeded inputs on the device (generate.hpp / test_util.hpp) --------
+ * ffg_random_mat_dev: A[i][j] = output i*n+j of SplitMix64(seed) mod p -- the
+ *   reference's random_mat (test_util.hpp:22-28), bit for bit.
+ * ffg_lru_matrix_dev: the BASELINE config-4 input M = L*R*U (n x n, rank r;
+ *   definition in DESIGN.md); rows/cols (host, r entries each, may be NULL)
+ *   receive the positions of R's ones, i.e. the rank profile matrix. */
+int ffg_random_mat_dev(ffg_ctx *ctx, uint64_t p, uint64_t seed, uint32_t *A, size_t m, size_t n, size_t lda);
+int ffg_lru_matrix_dev(ffg_ctx *ctx, uint64_t p, uint64_t seed, uint32_t *M, size_t n, size_t ldm, size_t r,
+                       uint32_t *rows, uint32_t *cols);
+
 /* ---- instrumentation ----------------------------------------------------
  * Kernel launches issued by this context since creation (all kernels of this
  * library; used for the bench's gpu_launches claim). */

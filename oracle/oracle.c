@@ -805,3 +805,72 @@ int orc_lru_matrix(size_t n, size_t r, u64 p, u64 seed, u32 *M, u32 *rows, u32 *
     free(U);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* generate.hpp:33-96 generate_matrix (restated; rows/cols get the intended  */
+/* profiles).  n x m output, ld m.                                           */
+
+static void sorted_subset(u64 seed, u64 *k, size_t dim, size_t count, u32 *out) /* generate.hpp:33-40 */
+{
+    u32 *all = (u32 *)malloc((dim ? dim : 1) * sizeof(u32));
+    for (size_t i = 0; i < dim; ++i) all[i] = (u32)i;
+    for (size_t i = dim; i > 1; --i) {
+        size_t s = (size_t)(orc_splitmix_at(seed, (*k)++) % i);
+        u32 t = all[i - 1];
+        all[i - 1] = all[s];
+        all[s] = t;
+    }
+    /* sort the first count entries (insertion sort; small) */
+    for (size_t i = 1; i < count; ++i) {
+        u32 v = all[i];
+        size_t j = i;
+        while (j > 0 && all[j - 1] > v) {
+            all[j] = all[j - 1];
+            --j;
+        }
+        all[j] = v;
+    }
+    memcpy(out, all, count * sizeof(u32));
+    free(all);
+}
+
+int orc_generate_matrix(size_t n, size_t m, size_t rank, u64 p, u64 seed, u32 *out, u32 *rows, u32 *cols)
+{
+    if (rank > (n < m ? n : m)) return ORC_INVALID_RANK;
+    u64 k = 0; /* position in the SplitMix64(seed) stream */
+    u32 *R = (u32 *)malloc((rank ? rank : 1) * sizeof(u32)), *Cc = (u32 *)malloc((rank ? rank : 1) * sizeof(u32));
+    sorted_subset(seed, &k, n, rank, R);
+    sorted_subset(seed, &k, m, rank, Cc);
+    u32 *X = (u32 *)calloc(n * (rank ? rank : 1), sizeof(u32)), *Y = (u32 *)calloc((rank ? rank : 1) * m, sizeof(u32));
+    size_t t = 0;
+    for (size_t i = 0; i < n; ++i) { /* :61-71 */
+        const int is_pivot = t < rank && R[t] == i;
+        for (size_t u = 0; u < t; ++u) X[i * rank + u] = (u32)(orc_splitmix_at(seed, k++) % p);
+        if (is_pivot) {
+            X[i * rank + t] = 1;
+            ++t;
+        }
+    }
+    t = 0;
+    for (size_t j = 0; j < m; ++j) { /* :72-82 */
+        const int is_pivot = t < rank && Cc[t] == j;
+        for (size_t u = 0; u < t; ++u) Y[u * m + j] = (u32)(orc_splitmix_at(seed, k++) % p);
+        if (is_pivot) {
+            Y[t * m + j] = (u32)(1 + orc_splitmix_at(seed, k++) % (p - 1));
+            ++t;
+        }
+    }
+    for (size_t i = 0; i < n; ++i) /* :85-91 */
+        for (size_t j = 0; j < m; ++j) {
+            u64 v = 0;
+            for (size_t u = 0; u < rank; ++u) v = (v + (u64)X[i * rank + u] * Y[u * m + j]) % p;
+            out[i * m + j] = (u32)v;
+        }
+    if (rows) memcpy(rows, R, rank * sizeof(u32));
+    if (cols) memcpy(cols, Cc, rank * sizeof(u32));
+    free(R);
+    free(Cc);
+    free(X);
+    free(Y);
+    return ORC_OK;
+}

@@ -95,6 +95,10 @@ uint64_t orc_checksum(const uint32_t *a, size_t m, size_t n, size_t lda, uint64_
 int orc_reconstruct(const orc_field *F, const uint32_t *packed, size_t m, size_t n, size_t lda,
                     const uint32_t *P, const uint32_t *Q, size_t rank, uint32_t *out);
 
+/* generate.hpp:52-96: n x m matrix of the given rank with intended profiles */
+int orc_generate_matrix(size_t n, size_t m, size_t rank, uint64_t p, uint64_t seed, uint32_t *out,
+                        uint32_t *rows, uint32_t *cols);
+
 /* config-4 generator (this repo's definition):
  * M = L * R * U mod p, L unit lower / U unit upper with SplitMix64 entries,
  * R an n x n 0/1 matrix with r ones at seeded positions (no shared row/col).

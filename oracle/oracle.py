@@ -60,6 +60,7 @@ def lib():
         L.orc_lru_matrix.argtypes = [_sz, _sz, _u64, _u64, _u32p, _u32p, _u32p]
         L.orc_apply_moves.argtypes = [_u32p, _sz, _sz, _sz, C.c_int, C.c_int, _u32p, _u32p, _u32p, _sz]
         L.orc_moves_to_array.argtypes = [_sz, _u32p, _u32p, _u32p, _sz, _u32p]
+        L.orc_generate_matrix.argtypes = [_sz, _sz, _sz, _u64, _u64, _u32p, _u32p, _u32p]
         L.orc_inv.argtypes = [C.POINTER(_Field), C.c_uint32]
         L.orc_inv.restype = C.c_uint32
     return _lib
@@ -159,6 +160,17 @@ def reconstruct(p: int, packed: np.ndarray, P: np.ndarray, Q: np.ndarray, rank: 
     out = np.zeros((m, n), np.uint32)
     lib().orc_reconstruct(C.byref(F), packed, m, n, n, _c(P), _c(Q), rank, out)
     return out
+
+
+def generate_matrix(p: int, n: int, m: int, rank: int, seed: int):
+    """generate.hpp:52-96 restated: (A, intended rows, intended cols)."""
+    a = np.zeros((n, m), np.uint32)
+    rows = np.zeros(max(rank, 1), np.uint32)
+    cols = np.zeros(max(rank, 1), np.uint32)
+    rc = lib().orc_generate_matrix(n, m, rank, p, seed, a if a.size else np.zeros((1, 1), np.uint32), rows, cols)
+    if rc:
+        raise OracleError(rc)
+    return a, rows[:rank], cols[:rank]
 
 
 def lru_matrix(n: int, r: int, p: int, seed: int):

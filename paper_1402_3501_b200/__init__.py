@@ -14,8 +14,11 @@ from .ffpluq import (  # noqa: F401
     SingularDiagonal,
     default_context,
     fgemm,
+    field_info,
     ftrsm,
     lib,
+    lru_matrix_dev,
+    random_mat_dev,
     pluq_tile_recursive,
     rr_base,
 )

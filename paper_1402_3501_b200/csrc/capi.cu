@@ -122,6 +122,36 @@ void* ffg_get_stream(ffg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 int ffg_synchronize(ffg_ctx* ctx) { return guarded(ctx, [&] { FFG_CUDA(cudaStreamSynchronize(ctx->stream)); }); }
 uint64_t ffg_launch_count(ffg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int ffg_field_info(uint64_t p, int* limbs, uint64_t* kmax, int* nt) {
+    try {
+        ffg::Field F = ffg::make_field(p);
+        if (limbs) *limbs = F.limbs;
+        if (kmax) *kmax = F.kmax;
+        if (nt) *nt = ffg::tile_n(F.limbs);
+        return FFG_OK;
+    } catch (const ffg::Error& e) {
+        g_err = e.what();
+        return e.code;
+    }
+}
+
+int ffg_random_mat_dev(ffg_ctx* ctx, uint64_t p, uint64_t seed, uint32_t* A, size_t m, size_t n, size_t lda) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        ffg::random_mat_dev(blas, ffg::DView{A, m, n, lda}, seed);
+    });
+}
+
+int ffg_lru_matrix_dev(ffg_ctx* ctx, uint64_t p, uint64_t seed, uint32_t* M, size_t n, size_t ldm, size_t r,
+                       uint32_t* rows, uint32_t* cols) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        ffg::lru_matrix_dev(blas, ffg::DView{M, n, n, ldm}, r, seed, rows, cols);
+    });
+}
+
 int ffg_fgemm_dev(ffg_ctx* ctx, uint64_t p, uint32_t alpha, const uint32_t* A, size_t lda, const uint32_t* B,
                   size_t ldb, uint32_t beta, uint32_t* C, size_t ldc, size_t m, size_t n, size_t k) {
     return guarded(ctx, [&] {

@@ -49,6 +49,10 @@ void perm_compose_dev(const Blas& b, uint32_t* dst, size_t off, const uint32_t* 
 void perm_rot_dev(const Blas& b, uint32_t* arr, size_t first, size_t mid, size_t len);
 void perm_iota_dev(const Blas& b, uint32_t* arr, size_t len);
 
+// seeded generators (gen.cu)
+void random_mat_dev(const Blas& b, DView A, uint64_t seed);
+void lru_matrix_dev(const Blas& b, DView M, size_t r, uint64_t seed, uint32_t* rows_out, uint32_t* cols_out);
+
 // row (axis 0) / column (axis 1) gather by a device index array
 void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_t* perm);
 

@@ -105,7 +105,10 @@ def lib() -> C.CDLL:
         L.ffg_pluq_tile_recursive.argtypes = pluq_args
         L.ffg_pluq_tile_recursive_dev.argtypes = pluq_args
         L.ffg_rr_base.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
+        L.ffg_field_info.argtypes = [u64, C.POINTER(C.c_int), C.POINTER(u64), C.POINTER(C.c_int)]
         L.ffg_apply_perm_dev.argtypes = [vp, vp, sz, sz, sz, C.c_int, C.c_int, vp]
+        L.ffg_random_mat_dev.argtypes = [vp, u64, u64, vp, sz, sz, sz]
+        L.ffg_lru_matrix_dev.argtypes = [vp, u64, u64, vp, sz, sz, sz, vp, vp]
         _lib = L
     return _lib
 
@@ -163,6 +166,14 @@ def default_context() -> Context:
     if _default is None:
         _default = Context(0)
     return _default
+
+
+def field_info(p: int) -> dict:
+    """Tensor-core embedding of GF(p): limbs, exact-accumulation chunk kmax, GEMM tile width."""
+    limbs, nt = C.c_int(0), C.c_int(0)
+    kmax = C.c_uint64(0)
+    _check(lib().ffg_field_info(p, C.byref(limbs), C.byref(kmax), C.byref(nt)))
+    return {"limbs": limbs.value, "kmax": kmax.value, "nt": nt.value}
 
 
 @dataclass
@@ -263,3 +274,21 @@ def rr_base(p: int, A, ctx: Context | None = None) -> PluqResult:
     r = C.c_size_t(0)
     _check(lib().ffg_rr_base(ctx.handle, p, _ptr(A), m, n, _ld(A), P.ctypes.data, Q.ctypes.data, C.byref(r)))
     return PluqResult(P[:m], Q[:n], int(r.value))
+
+
+def random_mat_dev(p: int, A, seed: int, ctx: Context | None = None):
+    """Fill a device matrix with the reference's random_mat (test_util.hpp:22-28)."""
+    ctx = ctx or default_context()
+    m, n = A.shape
+    _check(lib().ffg_random_mat_dev(ctx.handle, p, seed, _ptr(A), m, n, _ld(A)))
+    return A
+
+
+def lru_matrix_dev(p: int, M, r: int, seed: int, ctx: Context | None = None):
+    """Fill a square device matrix with the config-4 input L*R*U; returns (rows, cols) of R's ones."""
+    ctx = ctx or default_context()
+    n = M.shape[0]
+    rows = np.zeros(max(r, 1), np.uint32)
+    cols = np.zeros(max(r, 1), np.uint32)
+    _check(lib().ffg_lru_matrix_dev(ctx.handle, p, seed, _ptr(M), n, _ld(M), r, rows.ctypes.data, cols.ctypes.data))
+    return rows[:r], cols[:r]

@@ -1,0 +1,251 @@
+"""GPU parity: the B200 library (through the C ABI) against the reference's
+golden outputs (tests/golden/golden.json, produced by the reference itself)
+and against the oracle, bit-exact, plus full-size property checks.
+"""
+import numpy as np
+import pytest
+
+from golden_util import fnv_u32, load, make_input
+from verify import gemm_ok, pluq_ok
+
+pytestmark = pytest.mark.gpu
+
+GOLD = load()
+CASES = [c for c in GOLD["cases"] if c.get("variant") != "as_written"]
+
+
+def _ids(c):
+    return f"{c['kind']}-p{c['p']}-{c.get('note', '')[:24]}"
+
+
+def run_gpu(G, ctx, c):
+    p = c["p"]
+    if c["kind"] == "fgemm":
+        A, B, C0 = make_input(c["A"]), make_input(c["B"]), make_input(c["C"])
+        out = C0.copy()
+        G.fgemm(p, c["alpha"], A, B, c["beta"], out, ctx=ctx)
+        return {"out": out}
+    if c["kind"] == "ftrsm":
+        A, B = make_input(c["A"]), make_input(c["B"])
+        out = B.copy()
+        try:
+            G.ftrsm(p, c["side"], c["uplo"], c["diag"], A, out, ctx=ctx)
+        except G.SingularDiagonal as e:
+            return {"error": "SingularDiagonal", "index": e.index}
+        return {"out": out}
+    A = make_input(c["A"]).copy()
+    res = G.rr_base(p, A, ctx=ctx) if c["kind"] == "rr_base" else G.pluq_tile_recursive(p, A, c["thr"], ctx=ctx)
+    return {"out": A, "P": res.P, "Q": res.Q, "rank": res.rank}
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
+def test_gpu_matches_reference_golden(gpu, oracle_lib, case):
+    G, ctx = gpu
+    got = run_gpu(G, ctx, case)
+    if "error" in case:
+        assert got.get("error") == case["error"] and got.get("index") == case["index"]
+        return
+    assert "error" not in got
+    assert oracle_lib.checksum(got["out"], case["p"]) == case["out_ck"]
+    if "out" in case:
+        assert np.array_equal(got["out"].ravel(), np.array(case["out"], dtype=np.uint32))
+    if case["kind"] in ("rr_base", "tile_rec"):
+        assert got["rank"] == case["rank"]
+        assert fnv_u32(got["P"]) == case["P_h"] and fnv_u32(got["Q"]) == case["Q_h"]
+
+
+# ------------------------------------------------------------------ random + edge cases vs oracle
+PRIMES = (2, 3, 5, 251, 65521, 131071, 16777213, 67108859)
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_fgemm_random_vs_oracle(gpu, oracle_lib, p):
+    G, ctx = gpu
+    O = oracle_lib
+    rng = np.random.default_rng(p)
+    for t in range(8):
+        m, k, n = (int(x) for x in rng.integers(1, 400, 3))
+        A, B, C0 = O.random_mat(p, m, k, t), O.random_mat(p, k, n, t + 1), O.random_mat(p, m, n, t + 2)
+        for alpha, beta in ((p - 1, 1), (1, 0), (3 % p, 2 % p), (0, 1), (0, 0)):
+            want = O.fgemm(p, alpha, A, B, beta, C0)
+            got = C0.copy()
+            G.fgemm(p, alpha, A, B, beta, got, ctx=ctx)
+            assert np.array_equal(want, got), (m, k, n, alpha, beta)
+
+
+def test_fgemm_strided_views(gpu, oracle_lib):
+    """Sub-views with lda > cols and unaligned offsets (tile_rec hands such views to fgemm)."""
+    G, ctx = gpu
+    O = oracle_lib
+    p = 131071
+    big = O.random_mat(p, 300, 301, 3)
+    A = big[1:130, 3:200]
+    B = big[5:202, 7:90]
+    C = O.random_mat(p, 130, 300, 4)[1:130, 11:94]
+    want = O.fgemm(p, p - 1, A, B, 1, C)
+    got = C.copy()
+    G.fgemm(p, p - 1, A, B, 1, got, ctx=ctx)
+    assert np.array_equal(want, got)
+
+
+def test_fgemm_empty_and_k0(gpu, oracle_lib):
+    G, ctx = gpu
+    O = oracle_lib
+    p = 65521
+    for (m, k, n) in ((0, 5, 3), (4, 0, 3), (4, 5, 0), (1, 1, 1)):
+        A, B, C0 = O.random_mat(p, m, k, 1), O.random_mat(p, k, n, 2), O.random_mat(p, m, n, 3)
+        for beta in (0, 1, 7):
+            got = C0.copy()
+            G.fgemm(p, 5, A, B, beta, got, ctx=ctx)
+            assert np.array_equal(got, O.fgemm(p, 5, A, B, beta, C0))
+
+
+def test_fgemm_kmax_chunking(gpu, oracle_lib):
+    """K beyond the exact s32 bound: the kernel folds mod p once per kmax chunk (blas.hpp:85-88)."""
+    G, ctx = gpu
+    O = oracle_lib
+    for p in (251, 131071):
+        kmax = G.field_info(p)["kmax"]
+        k = kmax + 300
+        A, B, C0 = O.random_mat(p, 3, k, 1), O.random_mat(p, k, 5, 2), O.random_mat(p, 3, 5, 3)
+        got = C0.copy()
+        G.fgemm(p, p - 1, A, B, 1, got, ctx=ctx)
+        assert np.array_equal(got, O.fgemm(p, p - 1, A, B, 1, C0))
+        # all-(p-1) operands: the worst case for the accumulator bound
+        A = np.full((2, k), p - 1, np.uint32)
+        B = np.full((k, 3), p - 1, np.uint32)
+        got = np.zeros((2, 3), np.uint32)
+        G.fgemm(p, 1, A, B, 0, got, ctx=ctx)
+        assert np.all(got == (k % p) * 1 % p)  # (p-1)^2 = 1 mod p
+
+
+def test_ftrsm_errors(gpu):
+    G, ctx = gpu
+    U = np.array([[2, 1, 0], [0, 3, 1], [0, 0, 0]], np.uint32)
+    B = np.ones((4, 3), np.uint32)
+    with pytest.raises(G.SingularDiagonal) as ei:
+        G.ftrsm(5, 1, 1, 1, U, B, ctx=ctx)
+    assert ei.value.index == 2
+    with pytest.raises(G.DimMismatch):
+        G.ftrsm(5, 0, 0, 0, U, B, ctx=ctx)
+    # empty B: no check, no error (blas.hpp:393)
+    G.ftrsm(5, 1, 1, 1, np.zeros((0, 0), np.uint32), np.zeros((4, 0), np.uint32), ctx=ctx)
+
+
+@pytest.mark.parametrize("p", (2, 5, 251, 131071))
+def test_pluq_random_vs_oracle(gpu, oracle_lib, p):
+    G, ctx = gpu
+    O = oracle_lib
+    rng = np.random.default_rng(p + 17)
+    for t in range(10):
+        m, n = int(rng.integers(1, 320)), int(rng.integers(1, 320))
+        kind = t % 3
+        if kind == 0:
+            A = O.random_mat(p, m, n, 100 + t)
+        else:
+            N = max(m, n)
+            M, _, _ = O.lru_matrix(N, N // (2 if kind == 1 else 3), p, t)
+            A = M[:m, :n].copy()
+        for thr in (1, 3, 8, 32, 100):
+            if thr == 1 and max(m, n) > 160:
+                continue
+            a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+            a_g = A.copy()
+            res = G.pluq_tile_recursive(p, a_g, thr, ctx=ctx)
+            assert r_o == res.rank
+            assert np.array_equal(P_o, res.P) and np.array_equal(Q_o, res.Q)
+            assert np.array_equal(a_o, a_g)
+
+
+def test_pluq_edge_shapes(gpu, oracle_lib):
+    G, ctx = gpu
+    O = oracle_lib
+    p = 131071
+    for (m, n) in ((0, 5), (5, 0), (1, 1), (1, 300), (300, 1), (2, 257), (257, 2)):
+        for fill in ("zero", "rand"):
+            A = np.zeros((m, n), np.uint32) if fill == "zero" else O.random_mat(p, m, n, m * 7 + n)
+            a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 8)
+            a_g = A.copy()
+            res = G.pluq_tile_recursive(p, a_g, 8, ctx=ctx)
+            assert (r_o, P_o.tolist(), Q_o.tolist()) == (res.rank, res.P.tolist(), res.Q.tolist())
+            assert np.array_equal(a_o, a_g)
+
+
+def test_rr_base_large_block_global_path(gpu, oracle_lib):
+    """Blocks larger than shared memory take the global-scratch path of the base kernel."""
+    G, ctx = gpu
+    O = oracle_lib
+    for p in (5, 131071):
+        M, _, _ = O.lru_matrix(400, 150, p, 3)
+        A = M[:, :300].copy()
+        a_o, P_o, Q_o, r_o = O.rr_base(p, A)
+        a_g = A.copy()
+        res = G.rr_base(p, a_g, ctx=ctx)
+        assert r_o == res.rank and np.array_equal(P_o, res.P) and np.array_equal(Q_o, res.Q)
+        assert np.array_equal(a_o, a_g)
+
+
+# ------------------------------------------------------------------ device generators
+def test_device_generators_match_cpu(gpu, oracle_lib):
+    import torch
+    G, ctx = gpu
+    O = oracle_lib
+    for p in (251, 131071):
+        d = torch.empty((37, 53), dtype=torch.int32, device="cuda")
+        G.random_mat_dev(p, d, 99, ctx=ctx)
+        ctx.synchronize()
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), O.random_mat(p, 37, 53, 99))
+        M = torch.empty((70, 70), dtype=torch.int32, device="cuda")
+        rows, cols = G.lru_matrix_dev(p, M, 30, 5, ctx=ctx)
+        ctx.synchronize()
+        Mo, ro, co = O.lru_matrix(70, 30, p, 5)
+        assert np.array_equal(M.cpu().numpy().view(np.uint32), Mo)
+        assert np.array_equal(rows, ro) and np.array_equal(cols, co)
+
+
+# ------------------------------------------------------------------ larger sizes: properties
+def test_fgemm_8192_config2_freivalds(gpu, oracle_lib):
+    """BASELINE config 2 shape (8192^3, GF(131071), C <- C - A*B) via random projections."""
+    import torch
+    G, ctx = gpu
+    p, N = 131071, 8192
+    dA = torch.empty((N, N), dtype=torch.int32, device="cuda")
+    dB = torch.empty_like(dA)
+    dC = torch.empty_like(dA)
+    G.random_mat_dev(p, dA, 11, ctx=ctx)
+    G.random_mat_dev(p, dB, 12, ctx=ctx)
+    G.random_mat_dev(p, dC, 13, ctx=ctx)
+    ctx.synchronize()
+    A, B, C0 = (t.cpu().numpy().view(np.uint32) for t in (dA, dB, dC))
+    G.fgemm(p, p - 1, dA, dB, 1, dC, ctx=ctx)
+    ctx.synchronize()
+    assert gemm_ok(p, p - 1, A, B, 1, C0, dC.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("p,n,thr,kind", [(131071, 2048, 64, "iid"), (131071, 4096, 64, "iid"),
+                                          (251, 4096, 64, "iid"), (131071, 2048, 64, "lru"),
+                                          (251, 1024, 8, "lru")])
+def test_pluq_properties(gpu, oracle_lib, p, n, thr, kind):
+    """Factorization identity P A Q = L U, rank, profiles; bit-exact vs the oracle where it is fast."""
+    import torch
+    G, ctx = gpu
+    O = oracle_lib
+    d = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    if kind == "iid":
+        G.random_mat_dev(p, d, 1, ctx=ctx)
+        rows = cols = None
+    else:
+        rows, cols = G.lru_matrix_dev(p, d, n // 2, 4, ctx=ctx)
+    ctx.synchronize()
+    A = d.cpu().numpy().view(np.uint32).copy()
+    res = G.pluq_tile_recursive(p, d, thr, ctx=ctx)
+    ctx.synchronize()
+    packed = d.cpu().numpy().view(np.uint32)
+    assert pluq_ok(p, A, packed, res.P, res.Q, res.rank)
+    if kind == "lru":
+        assert res.rank == n // 2
+        assert set(zip(res.P[:res.rank].tolist(), res.Q[:res.rank].tolist())) == set(zip(rows.tolist(), cols.tolist()))
+    if n <= 2048:
+        a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+        assert r_o == res.rank and np.array_equal(P_o, res.P) and np.array_equal(Q_o, res.Q)
+        assert np.array_equal(a_o, packed)
