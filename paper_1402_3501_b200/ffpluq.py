@@ -197,7 +197,7 @@ def _host(a) -> np.ndarray:
     a = np.asarray(a)
     if a.dtype != np.uint32:
         raise TypeError("matrices are uint32 canonical residues")
-    if a.ndim != 2 or a.strides[1] != 4:
+    if a.ndim != 2 or (a.size and a.strides[1] != 4):
         raise ValueError("row-major 2-D uint32 array with unit column stride required")
     return a
 

@@ -41,7 +41,7 @@ def pluq_ok(p, A, packed, P, Q, r, reps=2, seed=0):
         # U x (U = rows [0, r) of packed, upper incl. diagonal)
         ux = np.zeros(r, np.int64)
         for i in range(0, r, CH):
-            blk = packed[i:i + CH].astype(np.int64)
+            blk = packed[i:min(i + CH, r)].astype(np.int64)
             rows = np.arange(i, min(i + CH, r))
             mask = np.arange(n)[None, :] >= rows[:, None]
             ux[i:i + CH] = ((blk * mask) @ x) % p
