@@ -139,6 +139,7 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const size_t fixed = (((size_t)m + n + 3) / 4 + 2 * std::min(m, n)) * 4;
     const size_t blk = (size_t)m * n * 4;
     BaseInfo* info = static_cast<BaseInfo*>(info_dev);
+    b.ws.prof.begin(b.st);
     if (fixed + blk <= BASE_SMEM_LIMIT) {
         static bool set = false;
         if (!set) {
@@ -162,6 +163,7 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
         FFG_CUDA(cudaFreeAsync(scratch, b.st));
     }
     FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_BASE, 2.0 * blk, 2.0 * std::min(m, n) * (double)m * n);
     b.count();
 }
 

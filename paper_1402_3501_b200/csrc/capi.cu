@@ -122,6 +122,24 @@ void* ffg_get_stream(ffg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 int ffg_synchronize(ffg_ctx* ctx) { return guarded(ctx, [&] { FFG_CUDA(cudaStreamSynchronize(ctx->stream)); }); }
 uint64_t ffg_launch_count(ffg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int ffg_profile_enable(ffg_ctx* ctx, int on) {
+    return guarded(ctx, [&] { ctx->ws.prof.on = on != 0; });
+}
+
+int ffg_profile_read(ffg_ctx* ctx, double* out, int nclasses) {
+    return guarded(ctx, [&] {
+        double ms[ffg::PROF_NKINDS], n[ffg::PROF_NKINDS], w[ffg::PROF_NKINDS], f[ffg::PROF_NKINDS];
+        ctx->ws.prof.read(ms, n, w, f);
+        ctx->ws.prof.clear();
+        for (int c = 0; c < nclasses && c < ffg::PROF_NKINDS; ++c) {
+            out[4 * c + 0] = ms[c];
+            out[4 * c + 1] = n[c];
+            out[4 * c + 2] = w[c];
+            out[4 * c + 3] = f[c];
+        }
+    });
+}
+
 int ffg_field_info(uint64_t p, int* limbs, uint64_t* kmax, int* nt) {
     try {
         ffg::Field F = ffg::make_field(p);

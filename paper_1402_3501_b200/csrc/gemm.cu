@@ -416,6 +416,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         const size_t Kp = round_up(kc, BK);
         uint8_t* Ap = ws.get(st, (size_t)L * Mp * Kp + (size_t)L * Np * Kp);
         uint8_t* Bp = Ap + (size_t)L * Mp * Kp;
+        ws.prof.begin(st);
         {
             dim3 g((unsigned)ceil_div(Kp / 4, 128), (unsigned)Mp);
             split_rows_kernel<<<g, 128, 0, st>>>(A.d + k0, A.ld, (uint32_t)M, (uint32_t)kc, Ap, (uint32_t)Mp,
@@ -428,13 +429,18 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
                                                  (uint32_t)Kp, L, NT);
             FFG_CUDA(cudaGetLastError());
         }
+        // split traffic: read M*kc + kc*N residues (4 B), write the padded limb planes
+        ws.prof.end(st, PROF_SPLIT, 4.0 * ((double)M * kc + (double)kc * N) + (double)L * Kp * (Mp + Np));
         const uint32_t b = (k0 == 0) ? beta : 1u;
+        ws.prof.begin(st);
         switch (L) {
             case 1: launch_modgemm<1>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
             case 2: launch_modgemm<2>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
             case 3: launch_modgemm<3>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
             default: launch_modgemm<4>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
         }
+        // algorithmic work: L^2 u8 limb products per field MAC -> 2 L^2 M N kc int8 tensor ops
+        ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * kc, 2.0 * (double)M * N * kc);
         if (launches) *launches += 3;
     }
 }

@@ -6,10 +6,78 @@
 #include <cstdint>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 
 namespace ffg {
+
+// Optional per-kernel timing: CUDA events recorded on the launching stream
+// around each kernel of a class, summed on read.  Off unless a caller enables
+// it (bench.py's roofline), so the product path pays nothing by default.
+enum ProfKind { PROF_GEMM = 0, PROF_SPLIT = 1, PROF_BASE = 2, PROF_TRINV = 3, PROF_PERM = 4, PROF_NKINDS = 5 };
+
+class Profiler {
+public:
+    bool on = false;
+    ~Profiler() { clear(true); }
+    void begin(cudaStream_t st) {
+        if (!on) return;
+        cur_a_ = take();
+        cudaEventRecord(cur_a_, st);
+    }
+    // work = algorithmic units of this launch (int8 tensor ops for GEMM, bytes for others)
+    void end(cudaStream_t st, int kind, double work, double field_ops = 0) {
+        if (!on) return;
+        cudaEvent_t b = take();
+        cudaEventRecord(b, st);
+        recs_.push_back(Rec{cur_a_, b, kind, work, field_ops});
+    }
+    // totals per kind: ms, launches, work, field_ops (synchronizes the recorded events)
+    void read(double* ms, double* launches, double* work, double* field_ops) {
+        for (int k = 0; k < PROF_NKINDS; ++k) ms[k] = launches[k] = work[k] = field_ops[k] = 0;
+        for (auto& r : recs_) {
+            cudaEventSynchronize(r.b);
+            float t = 0;
+            cudaEventElapsedTime(&t, r.a, r.b);
+            ms[r.kind] += t;
+            launches[r.kind] += 1;
+            work[r.kind] += r.work;
+            field_ops[r.kind] += r.field_ops;
+        }
+    }
+    void clear(bool destroy = false) {
+        for (auto& r : recs_) {
+            free_.push_back(r.a);
+            free_.push_back(r.b);
+        }
+        recs_.clear();
+        if (destroy) {
+            for (auto e : free_) cudaEventDestroy(e);
+            free_.clear();
+        }
+    }
+
+private:
+    struct Rec {
+        cudaEvent_t a, b;
+        int kind;
+        double work, field_ops;
+    };
+    cudaEvent_t take() {
+        if (!free_.empty()) {
+            cudaEvent_t e = free_.back();
+            free_.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaEvent_t cur_a_ = nullptr;
+    std::vector<Rec> recs_;
+    std::vector<cudaEvent_t> free_;
+};
 
 // Per-stream scratch arena (the limb planes of the operands, temporaries of the
 // recursion).  Growth synchronizes the owning stream, so kernels already
@@ -17,6 +85,7 @@ namespace ffg {
 // reset by mark/release around each top-level call.
 class Workspace {
 public:
+    Profiler prof;
     ~Workspace() {
         for (auto& kv : bufs_)
             if (kv.second.ptr) cudaFree(kv.second.ptr);

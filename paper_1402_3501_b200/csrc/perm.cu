@@ -60,8 +60,10 @@ void gather_rows(const Blas& b, DView a, PermSrc src) {
     uint32_t* tmp = nullptr;
     FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
     dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
+    b.ws.prof.begin(b.st);
     rows_gather_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
     rows_store_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
+    b.ws.prof.end(b.st, PROF_PERM, 16.0 * a.rows * a.cols);
     FFG_CUDA(cudaGetLastError());
     FFG_CUDA(cudaFreeAsync(tmp, b.st));
     b.count(2);
@@ -71,8 +73,10 @@ void gather_cols(const Blas& b, DView a, PermSrc src) {
     uint32_t* tmp = nullptr;
     FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
     dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
+    b.ws.prof.begin(b.st);
     cols_gather_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
     rows_store_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
+    b.ws.prof.end(b.st, PROF_PERM, 16.0 * a.rows * a.cols);
     FFG_CUDA(cudaGetLastError());
     FFG_CUDA(cudaFreeAsync(tmp, b.st));
     b.count(2);

@@ -156,8 +156,10 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     });
     auto kern = upper ? (unit ? tri_inv_kernel<true, true> : tri_inv_kernel<true, false>)
                       : (unit ? tri_inv_kernel<false, true> : tri_inv_kernel<false, false>);
+    b.ws.prof.begin(b.st);
     kern<<<(unsigned)nblk, TB, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * nblk * TB * TB);
     b.count();
     TrsmCtx c{b, side, upper, A, Tinv};
     trsm_rec(c, 0, t, B);

@@ -107,6 +107,8 @@ def lib() -> C.CDLL:
         L.ffg_rr_base.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
         L.ffg_field_info.argtypes = [u64, C.POINTER(C.c_int), C.POINTER(u64), C.POINTER(C.c_int)]
         L.ffg_apply_perm_dev.argtypes = [vp, vp, sz, sz, sz, C.c_int, C.c_int, vp]
+        L.ffg_profile_enable.argtypes = [vp, C.c_int]
+        L.ffg_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.c_int]
         L.ffg_random_mat_dev.argtypes = [vp, u64, u64, vp, sz, sz, sz]
         L.ffg_lru_matrix_dev.argtypes = [vp, u64, u64, vp, sz, sz, sz, vp, vp]
         _lib = L
@@ -145,6 +147,19 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().ffg_launch_count(self._h))
+
+    PROFILE_CLASSES = ("gemm", "split", "base", "trinv", "perm")
+
+    def profile(self, on: bool) -> None:
+        _check(lib().ffg_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """{class: {ms, launches, work, field_ops}} since the last read (CUDA-event timed)."""
+        n = len(self.PROFILE_CLASSES)
+        buf = (C.c_double * (4 * n))()
+        _check(lib().ffg_profile_read(self._h, buf, n))
+        return {k: {"ms": buf[4 * i], "launches": int(buf[4 * i + 1]), "work": buf[4 * i + 2],
+                    "field_ops": buf[4 * i + 3]} for i, k in enumerate(self.PROFILE_CLASSES)}
 
     def close(self) -> None:
         if self._h:
