@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fgemm", action="store_true")
+    ap.add_argument("--no-prof", action="store_true", help="no per-kernel CUDA events in the timed region")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3) if a.impl == "ours" else a.warmup
     if a.n is None:
@@ -285,7 +286,7 @@ def our_arm(a, rank, world, local_rank):
 
     # ---- timed region: exactly K steps
     launches0 = ctx.launches
-    ctx.profile(True)
+    ctx.profile(not a.no_prof)
     with ClockSampler(local_rank) as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)

@@ -127,7 +127,7 @@ int ffg_lru_matrix_dev(ffg_ctx *ctx, uint64_t p, uint64_t seed, uint32_t *M, siz
 uint64_t ffg_launch_count(ffg_ctx *ctx);
 /* Per-kernel-class timing with CUDA events on the launching stream (off by
  * default).  Classes: 0 tensor-core GEMM, 1 limb split, 2 base case,
- * 3 triangle inverse, 4 permutation gathers.  ffg_profile_read fills
+ * 3 triangle inverse, 4 permutation gathers, 5 CUDA-core small GEMM.  ffg_profile_read fills
  * out[4*c + {0,1,2,3}] = {milliseconds, launches, work, field ops} per class c
  * (work = int8 tensor ops for class 0, bytes moved otherwise) and clears. */
 int ffg_profile_enable(ffg_ctx *ctx, int on);

@@ -6,91 +6,178 @@
 // row is nonzero, at the first nonzero non-pivot column (original order) --
 // rotations keep non-pivot rows/columns in original relative order
 // (perm.hpp:11-13).  Given the pivot sequence, P A Q = L U has unique packed
-// factors, so this kernel uses eager right-looking elimination on the block
-// held in shared memory, keeps rows/columns in place, and applies the final
-// permutations once when writing the block back:
+// factors, so this kernel eliminates eagerly on the block held in shared
+// memory with rows and columns left in place, and applies the permutations
+// once when writing the block back:
 //     P = [pivot rows in discovery order, non-pivot rows ascending]
 //     Q = [pivot cols in discovery order, non-pivot cols ascending]
-//     out[t][u] = S[P[t]][Q[u]]
-// Exhausted rows (no nonzero left, rankrev.hpp:54-57) keep their computed
-// zeros; their L entries for later pivots are those zeros, as in the
-// reference.  Values are exact residues, so the bits match rr_base.
+//
+// Phase 1 (pivot discovery) is fraction-free: at pivot k every later row becomes
+//     S_i <- piv_k * S_i - S_i[q_k] * S_{p_k}        (mod p),
+// the true Schur row times the common nonzero factor piv_0 ... piv_k.  Nonzero
+// scaling keeps the zero pattern, so the search sees exactly what rr_base sees,
+// and no modular inverse sits on the serial path.  Eliminating column q_k zeroes
+// it in every later row, so the update runs over whole rows without pivot-column
+// masks (the L numerator S_i[q_k] is saved to Lb first) and the row search is a
+// plain first-nonzero scan.  Phase 2 recovers the exact factors in parallel:
+//     L[i][k] = Lb[i][k] / piv_k,    U[k][:] = S_{p_k}[:] / (piv_0 ... piv_{k-1}).
+// Exhausted rows (rankrev.hpp:54-57) keep their zero Schur rows and zero L
+// entries for later pivots, as in the reference.
 #include "pluq.cuh"
 
 namespace ffg {
 
-constexpr int BASE_THREADS = 512;
+constexpr int BASE_THREADS = 256;
 constexpr size_t BASE_SMEM_LIMIT = 200 * 1024;
+constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
 
+// binary extended Euclid for odd p (no divisions); p == 2 -> the only unit is 1
+__device__ __forceinline__ uint32_t inv_mod_bin(uint32_t a, uint32_t p) {
+    if (p == 2) return 1;
+    uint32_t u = a, v = p, x1 = 1, x2 = 0;  // a*x1 = u, a*x2 = v (mod p)
+    while (u != 1 && v != 1) {
+        while ((u & 1) == 0) {
+            u >>= 1;
+            x1 = (x1 & 1) ? (x1 + p) >> 1 : x1 >> 1;
+        }
+        while ((v & 1) == 0) {
+            v >>= 1;
+            x2 = (x2 & 1) ? (x2 + p) >> 1 : x2 >> 1;
+        }
+        if (u >= v) {
+            u -= v;
+            x1 = x1 >= x2 ? x1 - x2 : x1 + p - x2;
+        } else {
+            v -= u;
+            x2 = x2 >= x1 ? x2 - x1 : x2 + p - x1;
+        }
+    }
+    return u == 1 ? x1 : x2;
+}
+
+struct BaseLayout {
+    uint32_t m, n, ns, rmax;  // ns = padded row stride of S (multiple of 8)
+};
+
 template <bool IN_SMEM>
 __global__ void __launch_bounds__(BASE_THREADS)
-    rr_base_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t m, uint32_t n, uint32_t* __restrict__ scratch,
+    rr_base_kernel(uint32_t* __restrict__ A, uint64_t lda, BaseLayout lay, uint32_t* __restrict__ scratch,
                    uint32_t* __restrict__ Pd, uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p,
                    uint64_t mu) {
-    extern __shared__ uint32_t sm[];
-    // shared layout: [flags: rowpiv m bytes | colpiv n bytes] [prow | pcol] [block if IN_SMEM]
-    uint8_t* rowpiv = reinterpret_cast<uint8_t*>(sm);
-    uint8_t* colpiv = rowpiv + m;
-    const uint32_t flag_words = (m + n + 3) / 4;
-    uint32_t* prow = sm + flag_words;
-    const uint32_t rmax = min(m, n);
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t m = lay.m, n = lay.n, ns = lay.ns, rmax = lay.rmax;
+    // shared: prow | pcol | pivv | invp | invD (rmax each) | Psh m | Qsh n | rowrank m | colrank n
+    uint32_t* prow = sm;
     uint32_t* pcol = prow + rmax;
-    uint32_t* S = IN_SMEM ? (pcol + rmax) : scratch;
-    __shared__ uint32_t s_pi, s_pj, s_inv;
+    uint32_t* pivv = pcol + rmax;
+    uint32_t* invp = pivv + rmax;
+    uint32_t* invD = invp + rmax;
+    uint32_t* Psh = invD + rmax;
+    uint32_t* Qsh = Psh + m;
+    uint32_t* rowrank = Qsh + n;
+    uint32_t* colrank = rowrank + m;
+    uint32_t* tail = colrank + n;
+    tail += (4 - (reinterpret_cast<uintptr_t>(tail) / 4) % 4) % 4;  // 16-byte align
+    uint32_t* S = IN_SMEM ? tail : scratch;             // m x ns
+    uint32_t* Lb = IN_SMEM ? tail + (size_t)m * ns : scratch + (size_t)m * ns;  // m x rmax numerators
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = BASE_THREADS / 32;
-    for (uint32_t i = tid; i < m + n; i += BASE_THREADS) rowpiv[i] = 0;
-    for (uint32_t idx = tid; idx < m * n; idx += BASE_THREADS) {
-        const uint32_t r = idx / n, c = idx % n;
-        S[idx] = A[(uint64_t)r * lda + c];
+    for (uint32_t t = warp; t < m; t += nwarps) {
+        for (uint32_t u = lane; u < ns; u += 32) S[(size_t)t * ns + u] = u < n ? A[(uint64_t)t * lda + u] : 0u;
+        for (uint32_t u = lane; u < rmax; u += 32) Lb[(size_t)t * rmax + u] = 0u;
     }
     __syncthreads();
 
+    const uint32_t ngroups = ns / 8;
+    uint32_t lg = 0;  // row segment = 2^lg lanes >= ngroups
+    while ((1u << lg) < ngroups) ++lg;
+    const uint32_t seg = 1u << lg;
     uint32_t r = 0, cur = 0;
     while (cur < m && r < n) {
-        if (warp == 0) {  // row-major pivot search (rankrev.hpp:40-57)
-            uint32_t pi = m, pj = n;
-            for (uint32_t i = cur; i < m && pi == m; ++i) {
-                const uint32_t* row = S + (uint64_t)i * n;
-                for (uint32_t jc = 0; jc < n; jc += 32) {
-                    const uint32_t j = jc + lane;
-                    const bool nz = j < n && !colpiv[j] && row[j] != 0;
-                    const uint32_t bal = __ballot_sync(0xffffffffu, nz);
-                    if (bal) {
-                        pi = i;
-                        pj = jc + __ffs(bal) - 1;
-                        break;
-                    }
-                }
-            }
-            if (lane == 0) {
-                s_pi = pi;
-                s_pj = pj;
-                if (pi < m) {
-                    s_inv = inv_mod(S[(uint64_t)pi * n + pj], p);
-                    prow[r] = pi;
-                    pcol[r] = pj;
-                    rowpiv[pi] = 1;
-                    colpiv[pj] = 1;
+        // row-major pivot search (rankrev.hpp:40-57), done redundantly by every warp so no
+        // barrier separates it from the update; pivot columns are already 0 in rows >= cur,
+        // and rows in [cur, pi] are never written during this step
+        uint32_t pi = m, pj = n;
+        for (uint32_t i = cur; i < m && pi == m; ++i) {
+            const uint32_t* row = S + (size_t)i * ns;
+            for (uint32_t jc = 0; jc < n; jc += 32) {
+                const uint32_t j = jc + lane;
+                const uint32_t bal = __ballot_sync(0xffffffffu, j < n && row[j] != 0);
+                if (bal) {
+                    pi = i;
+                    pj = jc + __ffs(bal) - 1;
+                    break;
                 }
             }
         }
-        __syncthreads();
-        const uint32_t pi = s_pi, pj = s_pj;
-        if (pi >= m) break;
-        const uint32_t inv = s_inv;
-        const uint32_t* prw = S + (uint64_t)pi * n;
-        // eager update of the rows after the pivot row; rows before it are pivots or exhausted
-        for (uint32_t i = pi + 1 + warp; i < m; i += nwarps) {
-            uint32_t* row = S + (uint64_t)i * n;
-            const uint32_t l = mul_mod(row[pj], inv, p, mu);
-            __syncwarp();
-            if (lane == 0) row[pj] = l;  // L entry (rankrev.hpp:68-72)
-            if (l) {
-                for (uint32_t j = lane; j < n; j += 32)
-                    if (!colpiv[j]) row[j] = sub_mod(row[j], mul_mod(l, prw[j], p, mu), p);
+        if (pi >= m) break;  // uniform: every warp found the same (pi, pj)
+        const uint32_t* prw = S + (size_t)pi * ns;
+        const uint32_t pv = prw[pj];
+        const uint32_t pvp = shoup_pre(pv, p, mu);
+        if (tid == 0) {
+            prow[r] = pi;
+            pcol[r] = pj;
+            pivv[r] = pv;
+        }
+        const uint32_t rows_below = m - pi - 1;
+        if (seg <= 32) {
+            // a row's column groups sit in one warp segment of `seg` lanes: the lane holding
+            // column pj broadcasts the numerator by shuffle before anyone overwrites it
+            const uint32_t lseg = lane & (seg - 1), sbase = lane - lseg, owner = sbase + (pj >> 3);
+            const uint32_t q = pj & 7;
+            for (uint32_t r0 = warp << (5 - lg); r0 < rows_below; r0 += nwarps << (5 - lg)) {
+                const uint32_t i = pi + 1 + r0 + (lane >> lg);
+                const bool live = i < m && lseg < ngroups;
+                const uint32_t g = live ? lseg : 0u;
+                uint32_t* row = S + (size_t)(live ? i : pi) * ns + g * 8;
+                const uint4 a0 = reinterpret_cast<const uint4*>(row)[0], a1 = reinterpret_cast<const uint4*>(row)[1];
+                const uint4 b0 = reinterpret_cast<const uint4*>(prw + g * 8)[0];
+                const uint4 b1 = reinterpret_cast<const uint4*>(prw + g * 8)[1];
+                const uint32_t lo = (q & 2) ? ((q & 1) ? a0.w : a0.z) : ((q & 1) ? a0.y : a0.x);
+                const uint32_t hi = (q & 2) ? ((q & 1) ? a1.w : a1.z) : ((q & 1) ? a1.y : a1.x);
+                const uint32_t numer = __shfl_sync(0xffffffffu, (q & 4) ? hi : lo, owner);
+                if (!live) continue;
+                const uint32_t nump = shoup_pre(numer, p, mu);
+                uint4 o0, o1;
+                o0.x = sub_mod(shoup_mul(a0.x, pv, pvp, p), shoup_mul(b0.x, numer, nump, p), p);
+                o0.y = sub_mod(shoup_mul(a0.y, pv, pvp, p), shoup_mul(b0.y, numer, nump, p), p);
+                o0.z = sub_mod(shoup_mul(a0.z, pv, pvp, p), shoup_mul(b0.z, numer, nump, p), p);
+                o0.w = sub_mod(shoup_mul(a0.w, pv, pvp, p), shoup_mul(b0.w, numer, nump, p), p);
+                o1.x = sub_mod(shoup_mul(a1.x, pv, pvp, p), shoup_mul(b1.x, numer, nump, p), p);
+                o1.y = sub_mod(shoup_mul(a1.y, pv, pvp, p), shoup_mul(b1.y, numer, nump, p), p);
+                o1.z = sub_mod(shoup_mul(a1.z, pv, pvp, p), shoup_mul(b1.z, numer, nump, p), p);
+                o1.w = sub_mod(shoup_mul(a1.w, pv, pvp, p), shoup_mul(b1.w, numer, nump, p), p);
+                if (lseg == (pj >> 3)) Lb[(size_t)i * rmax + r] = numer;
+                reinterpret_cast<uint4*>(row)[0] = o0;
+                reinterpret_cast<uint4*>(row)[1] = o1;
+            }
+        } else {
+            // wide rows: save the L numerators of column pj before the update zeroes it
+            __syncthreads();  // every warp has finished reading the pivot row / numerators
+            for (uint32_t i = pi + 1 + tid; i < m; i += BASE_THREADS)
+                Lb[(size_t)i * rmax + r] = S[(size_t)i * ns + pj];
+            __syncthreads();
+            for (uint32_t idx = tid; idx < rows_below * ngroups; idx += BASE_THREADS) {
+                const uint32_t i = pi + 1 + idx / ngroups, g = idx % ngroups;
+                uint32_t* row = S + (size_t)i * ns + g * 8;
+                const uint32_t numer = Lb[(size_t)i * rmax + r];
+                const uint32_t nump = shoup_pre(numer, p, mu);
+                const uint4 a0 = reinterpret_cast<const uint4*>(row)[0], a1 = reinterpret_cast<const uint4*>(row)[1];
+                const uint4 b0 = reinterpret_cast<const uint4*>(prw + g * 8)[0];
+                const uint4 b1 = reinterpret_cast<const uint4*>(prw + g * 8)[1];
+                uint4 o0, o1;
+                o0.x = sub_mod(shoup_mul(a0.x, pv, pvp, p), shoup_mul(b0.x, numer, nump, p), p);
+                o0.y = sub_mod(shoup_mul(a0.y, pv, pvp, p), shoup_mul(b0.y, numer, nump, p), p);
+                o0.z = sub_mod(shoup_mul(a0.z, pv, pvp, p), shoup_mul(b0.z, numer, nump, p), p);
+                o0.w = sub_mod(shoup_mul(a0.w, pv, pvp, p), shoup_mul(b0.w, numer, nump, p), p);
+                o1.x = sub_mod(shoup_mul(a1.x, pv, pvp, p), shoup_mul(b1.x, numer, nump, p), p);
+                o1.y = sub_mod(shoup_mul(a1.y, pv, pvp, p), shoup_mul(b1.y, numer, nump, p), p);
+                o1.z = sub_mod(shoup_mul(a1.z, pv, pvp, p), shoup_mul(b1.z, numer, nump, p), p);
+                o1.w = sub_mod(shoup_mul(a1.w, pv, pvp, p), shoup_mul(b1.w, numer, nump, p), p);
+                reinterpret_cast<uint4*>(row)[0] = o0;
+                reinterpret_cast<uint4*>(row)[1] = o1;
             }
         }
         ++r;
@@ -98,46 +185,104 @@ __global__ void __launch_bounds__(BASE_THREADS)
         __syncthreads();
     }
 
-    // permutations: pivots in discovery order, then the rest ascending
-    if (tid == 0) {
-        uint32_t t = r;
-        for (uint32_t i = 0; i < m; ++i)
-            if (!rowpiv[i]) Pd[t++] = i;
-        for (uint32_t k = 0; k < r; ++k) Pd[k] = prow[k];
-        t = r;
-        for (uint32_t j = 0; j < n; ++j)
-            if (!colpiv[j]) Qd[t++] = j;
-        for (uint32_t k = 0; k < r; ++k) Qd[k] = pcol[k];
-        uint32_t lo = m, hi = 0;
-        for (uint32_t i = 0; i < m; ++i)
-            if (Pd[i] != i) {
-                lo = min(lo, i);
-                hi = i + 1;
-            }
-        info->rank = r;
-        info->plo = lo < hi ? lo : 0;
-        info->phi = lo < hi ? hi : 0;
-        lo = n;
-        hi = 0;
-        for (uint32_t j = 0; j < n; ++j)
-            if (Qd[j] != j) {
-                lo = min(lo, j);
-                hi = j + 1;
-            }
-        info->qlo = lo < hi ? lo : 0;
-        info->qhi = lo < hi ? hi : 0;
+    // ---- phase 2: exact values (pivot inverses in parallel, prefix products, scaling)
+    for (uint32_t k = tid; k < r; k += BASE_THREADS) invp[k] = inv_mod_bin(pivv[k], p);
+    for (uint32_t i = tid; i < m; i += BASE_THREADS) rowrank[i] = NONE;
+    for (uint32_t j = tid; j < n; j += BASE_THREADS) colrank[j] = NONE;
+    __syncthreads();
+    for (uint32_t k = tid; k < r; k += BASE_THREADS) {
+        rowrank[prow[k]] = k;
+        colrank[pcol[k]] = k;
     }
     __syncthreads();
-    for (uint32_t idx = tid; idx < m * n; idx += BASE_THREADS) {
-        const uint32_t t = idx / n, u = idx % n;
-        A[(uint64_t)t * lda + u] = S[(uint64_t)Pd[t] * n + Qd[u]];
+    if (warp == 0) {  // invD[k] = 1 / (piv_0 ... piv_{k-1}): exclusive prefix product, 32 per round
+        uint32_t carry = 1 % p;
+        for (uint32_t c = 0; c < r; c += 32) {
+            const uint32_t k = c + lane;
+            uint32_t v = k < r ? invp[k] : 1u % p;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {  // inclusive scan (Hillis-Steele)
+                const uint32_t o = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= (uint32_t)off) v = mul_mod(v, o, p, mu);
+            }
+            uint32_t ex = __shfl_up_sync(0xffffffffu, v, 1);
+            if (lane == 0) ex = 1u % p;
+            if (k < r) invD[k] = mul_mod(carry, ex, p, mu);
+            carry = mul_mod(carry, __shfl_sync(0xffffffffu, v, 31), p, mu);
+        }
+    }
+    __syncthreads();
+
+    // ---- permutations: pivots in discovery order, then the rest ascending (warp 0: P, warp 1: Q),
+    // built in shared memory with ballot compaction, moved ranges by warp min/max reductions
+    if (warp < 2) {
+        const uint32_t dim = warp == 0 ? m : n;
+        const uint32_t* rank_of = warp == 0 ? rowrank : colrank;
+        const uint32_t* order = warp == 0 ? prow : pcol;
+        uint32_t* out = warp == 0 ? Psh : Qsh;
+        uint32_t base = 0;
+        for (uint32_t c = 0; c < dim; c += 32) {
+            const uint32_t i = c + lane;
+            const bool np = i < dim && rank_of[i] == NONE;
+            const uint32_t bal = __ballot_sync(0xffffffffu, np);
+            if (np) out[r + base + __popc(bal & ((1u << lane) - 1u))] = i;
+            base += __popc(bal);
+        }
+        for (uint32_t k = lane; k < r; k += 32) out[k] = order[k];
+        __syncwarp();
+        uint32_t lo = NONE, hi = 0;
+        for (uint32_t i = lane; i < dim; i += 32)
+            if (out[i] != i) {
+                lo = min(lo, i);
+                hi = max(hi, i + 1);
+            }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0) {
+            if (warp == 0) {
+                info->rank = r;
+                info->plo = lo < hi ? lo : 0;
+                info->phi = lo < hi ? hi : 0;
+            } else {
+                info->qlo = lo < hi ? lo : 0;
+                info->qhi = lo < hi ? hi : 0;
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < m; i += BASE_THREADS) Pd[i] = Psh[i];
+    for (uint32_t j = tid; j < n; j += BASE_THREADS) Qd[j] = Qsh[j];
+    // packed output: out[t][u] for original row i = P[t], column j = Q[u]
+    for (uint32_t t = warp; t < m; t += nwarps) {
+        const uint32_t i = Psh[t];
+        const uint32_t k = rowrank[i];
+        const uint32_t du = k < r ? invD[k] : 0u, dup = k < r ? shoup_pre(du, p, mu) : 0u;
+        const uint32_t* srow = S + (size_t)i * ns;
+        const uint32_t* lrow = Lb + (size_t)i * rmax;
+        uint32_t* dst = A + (uint64_t)t * lda;
+        for (uint32_t u = lane; u < n; u += 32) {
+            const uint32_t j = Qsh[u];
+            const uint32_t tc = colrank[j];
+            uint32_t v;
+            if (tc < r && tc < k)  // L entry for pivot tc (k == NONE for non-pivot rows)
+                v = mul_mod(lrow[tc], invp[tc], p, mu);
+            else if (k < r)  // U row k
+                v = shoup_mul(srow[j], du, dup, p);
+            else  // non-pivot row, non-pivot column: the zero Schur complement
+                v = srow[j];
+            dst[u] = v;
+        }
     }
 }
 
 void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev) {
-    const uint32_t m = (uint32_t)a.rows, n = (uint32_t)a.cols;
-    const size_t fixed = (((size_t)m + n + 3) / 4 + 2 * std::min(m, n)) * 4;
-    const size_t blk = (size_t)m * n * 4;
+    BaseLayout lay;
+    lay.m = (uint32_t)a.rows;
+    lay.n = (uint32_t)a.cols;
+    lay.ns = (uint32_t)round_up(a.cols, 8);
+    lay.rmax = (uint32_t)std::min(a.rows, a.cols);
+    const size_t fixed = ((size_t)5 * lay.rmax + 2 * ((size_t)lay.m + lay.n) + 4) * 4;
+    const size_t blk = ((size_t)lay.m * lay.ns + (size_t)lay.m * lay.rmax) * 4;
     BaseInfo* info = static_cast<BaseInfo*>(info_dev);
     b.ws.prof.begin(b.st);
     if (fixed + blk <= BASE_SMEM_LIMIT) {
@@ -147,7 +292,7 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
                                           (int)BASE_SMEM_LIMIT));
             set = true;
         }
-        rr_base_kernel<true><<<1, BASE_THREADS, fixed + blk, b.st>>>(a.d, a.ld, m, n, nullptr, Pd, Qd, info, b.F.p,
+        rr_base_kernel<true><<<1, BASE_THREADS, fixed + blk, b.st>>>(a.d, a.ld, lay, nullptr, Pd, Qd, info, b.F.p,
                                                                      b.F.mu);
     } else {
         if (fixed > BASE_SMEM_LIMIT) throw Error(FFG_ERR_INVALID_BLOCK, "base case block too large");
@@ -159,11 +304,11 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
         }
         uint32_t* scratch = nullptr;
         FFG_CUDA(cudaMallocAsync(&scratch, blk, b.st));
-        rr_base_kernel<false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, m, n, scratch, Pd, Qd, info, b.F.p, b.F.mu);
+        rr_base_kernel<false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, lay, scratch, Pd, Qd, info, b.F.p, b.F.mu);
         FFG_CUDA(cudaFreeAsync(scratch, b.st));
     }
     FFG_CUDA(cudaGetLastError());
-    b.ws.prof.end(b.st, PROF_BASE, 2.0 * blk, 2.0 * std::min(m, n) * (double)m * n);
+    b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
     b.count();
 }
 

@@ -78,6 +78,43 @@ __host__ __device__ __forceinline__ uint32_t inv_mod(uint32_t a, uint32_t p) {
     return (uint32_t)t;
 }
 
+// extended Euclid in 32-bit arithmetic (p < 2^26 keeps every quantity in range); a != 0
+__host__ __device__ __forceinline__ uint32_t inv_mod32(uint32_t a, uint32_t p) {
+    int32_t t = 0, nt = 1;
+    uint32_t r = p, nr = a;
+    while (nr != 0) {
+        const uint32_t q = r / nr;
+        const int32_t tmp = t - (int32_t)q * nt;
+        t = nt;
+        nt = tmp;
+        const uint32_t r2 = r - q * nr;
+        r = nr;
+        nr = r2;
+    }
+    return t < 0 ? (uint32_t)(t + (int32_t)p) : (uint32_t)t;
+}
+
+// Shoup multiplication by a fixed factor w: wp = floor(w * 2^32 / p); x*w mod p in 32-bit ops
+__host__ __device__ __forceinline__ uint32_t shoup_pre(uint32_t w, uint32_t p, uint64_t mu) {
+    const uint64_t x = (uint64_t)w << 32;
+#ifdef __CUDA_ARCH__
+    uint64_t q = __umul64hi(x, mu);
+#else
+    uint64_t q = (uint64_t)(((unsigned __int128)x * mu) >> 64);
+#endif
+    uint64_t r = x - q * p;
+    while (r >= p) {
+        r -= p;
+        ++q;
+    }
+    return (uint32_t)q;
+}
+__device__ __forceinline__ uint32_t shoup_mul(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
+    const uint32_t q = __umulhi(x, wp);
+    uint32_t t = x * w - q * p;  // exact in [0, 2p) modulo 2^32
+    return t >= p ? t - p : t;
+}
+
 inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 inline size_t ceil_div(size_t x, size_t m) { return (x + m - 1) / m; }
 

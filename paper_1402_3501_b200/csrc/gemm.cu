@@ -262,51 +262,132 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 2) ptx::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-// --------------------------------------------------------------------------- limb split kernels
-// A (M x K view, row-major) -> planes[l][Mp][Kp] bytes, K-major.  One thread = 4 consecutive k.
-__global__ void split_rows_kernel(const uint32_t* __restrict__ A, uint64_t lda, uint32_t M, uint32_t K,
-                                  uint8_t* __restrict__ out, uint32_t Mp, uint32_t Kp, int L) {
-    const uint32_t kq = blockIdx.x * blockDim.x + threadIdx.x;  // index of a 4-byte group
-    const uint32_t m = blockIdx.y;
-    if (kq * 4 >= Kp) return;
-    uint32_t v[4];
+// --------------------------------------------------------------------------- limb split (one launch)
+// Blocks [0, a_blocks): A (M x K view) -> planes[l][Mp][Kp] (K-major, no transpose), one
+//   thread = 4 consecutive k of one row, 1024 (row, k-quad) items per block.
+// Blocks [a_blocks, ...): B (K x N view) -> rows (n/NT)*L*NT + l*NT + n%NT of Kp bytes
+//   (K-major), through a 64(k) x 64(n) shared-memory transpose.
+struct SplitArgs {
+    const uint32_t* A;
+    uint64_t lda;
+    uint32_t M, K, Mp, Kp;
+    uint8_t* outA;
+    const uint32_t* B;
+    uint64_t ldb;
+    uint32_t N, Np;
+    uint8_t* outB;
+    int L, NT;
+    uint32_t a_blocks, b_kblocks;
+};
+
+__device__ __forceinline__ uint32_t pack_limb(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, int sh) {
+    return ((v0 >> sh) & 0xFF) | (((v1 >> sh) & 0xFF) << 8) | (((v2 >> sh) & 0xFF) << 16) | (((v3 >> sh) & 0xFF) << 24);
+}
+
+__global__ void __launch_bounds__(256) split_kernel(const SplitArgs a) {
+    __shared__ uint32_t tile[64][65];
+    if (blockIdx.x < a.a_blocks) {
+        const uint32_t kq_per_row = a.Kp >> 2;
+        for (uint32_t it = 0; it < 4; ++it) {
+            const uint64_t item = ((uint64_t)blockIdx.x * 4 + it) * 256 + threadIdx.x;
+            const uint32_t m = (uint32_t)(item / kq_per_row), kq = (uint32_t)(item % kq_per_row);
+            if (m >= a.Mp) return;
+            const uint32_t k = kq * 4;
+            uint32_t v[4];
+            const uint32_t* row = a.A + (uint64_t)m * a.lda;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        const uint32_t k = kq * 4 + t;
-        v[t] = (m < M && k < K) ? A[(uint64_t)m * lda + k] : 0u;
+            for (int t = 0; t < 4; ++t) v[t] = (m < a.M && k + t < a.K) ? row[k + t] : 0u;
+            for (int l = 0; l < a.L; ++l)
+                reinterpret_cast<uint32_t*>(a.outA + ((uint64_t)l * a.Mp + m) * a.Kp)[kq] =
+                    pack_limb(v[0], v[1], v[2], v[3], 8 * l);
+        }
+        return;
     }
-    for (int l = 0; l < L; ++l) {
-        const int sh = 8 * l;
-        const uint32_t packed = ((v[0] >> sh) & 0xFF) | (((v[1] >> sh) & 0xFF) << 8) | (((v[2] >> sh) & 0xFF) << 16) |
-                                (((v[3] >> sh) & 0xFF) << 24);
-        reinterpret_cast<uint32_t*>(out + ((uint64_t)l * Mp + m) * Kp)[kq] = packed;
+    const uint32_t bid = blockIdx.x - a.a_blocks;
+    const uint32_t k0 = (bid % a.b_kblocks) * 64, n0 = (bid / a.b_kblocks) * 64;
+    const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    for (uint32_t r = ty; r < 64; r += 4) {
+        const uint32_t k = k0 + r, n = n0 + tx;
+        tile[r][tx] = (k < a.K && n < a.N) ? a.B[(uint64_t)k * a.ldb + n] : 0u;
+    }
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < 64u * 16u * (uint32_t)a.L; idx += blockDim.x) {
+        const uint32_t wq = idx & 15, nn = (idx >> 4) & 63, l = idx >> 10;
+        const uint32_t n = n0 + nn;
+        const uint32_t kw = (k0 >> 2) + wq;
+        if (n >= a.Np || kw * 4 >= a.Kp) continue;
+        const uint32_t packed =
+            pack_limb(tile[wq * 4 + 0][nn], tile[wq * 4 + 1][nn], tile[wq * 4 + 2][nn], tile[wq * 4 + 3][nn], 8 * l);
+        const uint64_t orow = (uint64_t)(n / a.NT) * a.L * a.NT + (uint64_t)l * a.NT + (n % a.NT);
+        reinterpret_cast<uint32_t*>(a.outB + orow * a.Kp)[kw] = packed;
     }
 }
 
-// B (K x N view, row-major) -> rows (n/NT)*L*NT + l*NT + n%NT of Kp bytes (K-major), via a
-// 64(k) x 64(n) shared-memory transpose.
-__global__ void split_cols_kernel(const uint32_t* __restrict__ B, uint64_t ldb, uint32_t K, uint32_t N,
-                                  uint8_t* __restrict__ out, uint32_t Np, uint32_t Kp, int L, int NT) {
-    __shared__ uint32_t tile[64][65];
-    const uint32_t k0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
-    const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 256 threads: 64 x 4
-    for (uint32_t r = ty; r < 64; r += 4) {
-        const uint32_t k = k0 + r, n = n0 + tx;
-        tile[r][tx] = (k < K && n < N) ? B[(uint64_t)k * ldb + n] : 0u;
+// --------------------------------------------------------------------------- CUDA-core path for small GEMMs
+// C <- alpha*A*B + beta*C with 64x64 tiles, 256 threads x (4x4) outputs, exact u64
+// accumulation (products < 2^52; folded mod p every 2048 terms).  One launch, no limb
+// staging: used when the problem is too small to amortize split + tensor-core launches.
+constexpr int SG_T = 64, SG_K = 32;
+__global__ void __launch_bounds__(256) modgemm_simt_kernel(const uint32_t* __restrict__ A, uint64_t lda,
+                                                          const uint32_t* __restrict__ B, uint64_t ldb,
+                                                          uint32_t* __restrict__ C, uint64_t ldc, uint32_t M,
+                                                          uint32_t N, uint32_t K, uint32_t alpha, uint32_t beta,
+                                                          uint32_t p, uint64_t mu) {
+    __shared__ uint32_t As[SG_K][SG_T + 1];  // transposed: As[k][m]
+    __shared__ uint32_t Bs[SG_K][SG_T];
+    const uint32_t m0 = blockIdx.y * SG_T, n0 = blockIdx.x * SG_T;
+    const uint32_t tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 outputs each
+    uint64_t acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+    uint32_t since_fold = 0;
+    for (uint32_t k0 = 0; k0 < K; k0 += SG_K) {
+        for (uint32_t idx = threadIdx.x; idx < SG_T * SG_K; idx += 256) {
+            const uint32_t r = idx / SG_K, c = idx % SG_K;  // A tile: rows m, cols k
+            const uint32_t m = m0 + r, k = k0 + c;
+            As[c][r] = (m < M && k < K) ? A[(uint64_t)m * lda + k] : 0u;
+            const uint32_t rb = idx / SG_T, cb = idx % SG_T;  // B tile: rows k, cols n
+            const uint32_t kb = k0 + rb, n = n0 + cb;
+            Bs[rb][cb] = (kb < K && n < N) ? B[(uint64_t)kb * ldb + n] : 0u;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < SG_K; ++kk) {
+            uint32_t a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += (uint64_t)a[i] * b[j];
+        }
+        since_fold += SG_K;
+        if (since_fold >= 2048) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = mod_u64(acc[i][j], p, mu);
+            since_fold = 0;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    // each output word = 4 consecutive k of one (n, limb): 64 n x 16 words x L
-    for (uint32_t idx = threadIdx.x; idx < 64u * 16u * (uint32_t)L; idx += blockDim.x) {
-        const uint32_t wq = idx & 15, nn = (idx >> 4) & 63, l = idx >> 10;
-        const uint32_t n = n0 + nn;
-        if (n >= Np) continue;
-        const int sh = 8 * l;
-        const uint32_t packed = ((tile[wq * 4 + 0][nn] >> sh) & 0xFF) | (((tile[wq * 4 + 1][nn] >> sh) & 0xFF) << 8) |
-                                (((tile[wq * 4 + 2][nn] >> sh) & 0xFF) << 16) |
-                                (((tile[wq * 4 + 3][nn] >> sh) & 0xFF) << 24);
-        const uint64_t orow = (uint64_t)(n / NT) * L * NT + (uint64_t)l * NT + (n % NT);
-        const uint32_t kw = (k0 >> 2) + wq;
-        if (kw * 4 < Kp) reinterpret_cast<uint32_t*>(out + orow * Kp)[kw] = packed;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t m = m0 + ty * 4 + i;
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t n = n0 + tx * 4 + j;
+            if (n >= N) continue;
+            uint32_t& c = C[(uint64_t)m * ldc + n];
+            uint64_t v = (uint64_t)alpha * mod_u64(acc[i][j], p, mu);
+            if (beta) v += (uint64_t)beta * c;
+            c = mod_u64(v, p, mu);
+        }
     }
 }
 
@@ -385,6 +466,10 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
 
 }  // namespace
 
+// Small problems: one CUDA-core launch beats split + tensor-core launches (tuned on B200).
+size_t g_simt_macs = size_t(1) << 24;
+bool use_simt(size_t M, size_t N, size_t K) { return M * N * K <= g_simt_macs; }
+
 size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k) {
     const int L = F.limbs, NT = tile_n(L);
     const size_t kc = std::min<size_t>(k, F.kmax);
@@ -409,6 +494,40 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         }
         return;
     }
+    // element-exact overlap of two strided windows; windows of one parent (same ld) compare as
+    // rectangles, anything else conservatively by address span
+    auto overlap = [](const DView& x, const DView& y) {
+        if (x.empty() || y.empty()) return false;
+        if (x.ld == y.ld && x.ld > 0) {
+            const int64_t off = (int64_t)(y.d - x.d);  // y's origin relative to x's, in elements
+            const int64_t ld = (int64_t)x.ld;
+            int64_t r = off / ld, c = off % ld;
+            if (c < 0) {
+                c += ld;
+                --r;
+            }
+            // the column offset is c or c - ld (one row further down); test both placements
+            auto hit = [&](int64_t rr, int64_t cc) {
+                return rr < (int64_t)x.rows && rr + (int64_t)y.rows > 0 && cc < (int64_t)x.cols &&
+                       cc + (int64_t)y.cols > 0;
+            };
+            return hit(r, c) || hit(r + 1, c - ld);
+        }
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(x.d), a1 = reinterpret_cast<uintptr_t>(x.d + (x.rows - 1) * x.ld + x.cols);
+        const uintptr_t b0 = reinterpret_cast<uintptr_t>(y.d), b1 = reinterpret_cast<uintptr_t>(y.d + (y.rows - 1) * y.ld + y.cols);
+        return a0 < b1 && b0 < a1;
+    };
+    // the CUDA-core kernel reads operands while other CTAs write C: only when C aliases nothing
+    if (use_simt(M, N, K) && !overlap(C, A) && !overlap(C, B)) {
+        ws.prof.begin(st);
+        dim3 g((unsigned)ceil_div(N, SG_T), (unsigned)ceil_div(M, SG_T));
+        modgemm_simt_kernel<<<g, 256, 0, st>>>(A.d, A.ld, B.d, B.ld, C.d, C.ld, (uint32_t)M, (uint32_t)N, (uint32_t)K,
+                                               alpha, beta, F.p, F.mu);
+        FFG_CUDA(cudaGetLastError());
+        ws.prof.end(st, PROF_SIMT, 2.0 * (double)M * N * K, 2.0 * (double)M * N * K);
+        if (launches) ++*launches;
+        return;
+    }
     const int L = F.limbs, NT = tile_n(L);
     const size_t Mp = round_up(M, BM), Np = round_up(N, NT);
     for (size_t k0 = 0; k0 < K; k0 += F.kmax) {  // delayed reduction: one fold per kmax chunk
@@ -418,15 +537,25 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         uint8_t* Bp = Ap + (size_t)L * Mp * Kp;
         ws.prof.begin(st);
         {
-            dim3 g((unsigned)ceil_div(Kp / 4, 128), (unsigned)Mp);
-            split_rows_kernel<<<g, 128, 0, st>>>(A.d + k0, A.ld, (uint32_t)M, (uint32_t)kc, Ap, (uint32_t)Mp,
-                                                 (uint32_t)Kp, L);
-            FFG_CUDA(cudaGetLastError());
-        }
-        {
-            dim3 g((unsigned)ceil_div(Kp, 64), (unsigned)ceil_div(Np, 64));
-            split_cols_kernel<<<g, 256, 0, st>>>(B.d + k0 * B.ld, B.ld, (uint32_t)kc, (uint32_t)N, Bp, (uint32_t)Np,
-                                                 (uint32_t)Kp, L, NT);
+            SplitArgs sa;
+            sa.A = A.d + k0;
+            sa.lda = A.ld;
+            sa.M = (uint32_t)M;
+            sa.K = (uint32_t)kc;
+            sa.Mp = (uint32_t)Mp;
+            sa.Kp = (uint32_t)Kp;
+            sa.outA = Ap;
+            sa.B = B.d + k0 * B.ld;
+            sa.ldb = B.ld;
+            sa.N = (uint32_t)N;
+            sa.Np = (uint32_t)Np;
+            sa.outB = Bp;
+            sa.L = L;
+            sa.NT = NT;
+            sa.a_blocks = (uint32_t)ceil_div(Mp * (Kp / 4), 1024);
+            sa.b_kblocks = (uint32_t)ceil_div(Kp, 64);
+            const size_t nblk = sa.a_blocks + (size_t)sa.b_kblocks * ceil_div(Np, 64);
+            split_kernel<<<(unsigned)nblk, 256, 0, st>>>(sa);
             FFG_CUDA(cudaGetLastError());
         }
         // split traffic: read M*kc + kc*N residues (4 B), write the padded limb planes
@@ -441,7 +570,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         }
         // algorithmic work: L^2 u8 limb products per field MAC -> 2 L^2 M N kc int8 tensor ops
         ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * kc, 2.0 * (double)M * N * kc);
-        if (launches) *launches += 3;
+        if (launches) *launches += 2;
     }
 }
 

@@ -15,7 +15,15 @@ namespace ffg {
 // Optional per-kernel timing: CUDA events recorded on the launching stream
 // around each kernel of a class, summed on read.  Off unless a caller enables
 // it (bench.py's roofline), so the product path pays nothing by default.
-enum ProfKind { PROF_GEMM = 0, PROF_SPLIT = 1, PROF_BASE = 2, PROF_TRINV = 3, PROF_PERM = 4, PROF_NKINDS = 5 };
+enum ProfKind {
+    PROF_GEMM = 0,
+    PROF_SPLIT = 1,
+    PROF_BASE = 2,
+    PROF_TRINV = 3,
+    PROF_PERM = 4,
+    PROF_SIMT = 5,
+    PROF_NKINDS = 6
+};
 
 class Profiler {
 public:
@@ -127,5 +135,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
                Workspace& ws, uint64_t* launches);
 size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k);
 int tile_n(int limbs);
+extern size_t g_simt_macs;  // problems with M*N*K <= this use the CUDA-core kernel
+bool use_simt(size_t M, size_t N, size_t K);
 
 }  // namespace ffg

@@ -19,48 +19,87 @@ namespace ffg {
 
 constexpr int TB = 128;  // diagonal block (= GEMM K-block, so leaf GEMMs have no K padding)
 
-// inverse of the diagonal block b of T (t x t) into Tinv + b*TB*TB (TB x TB, zero padded)
+// Inverse of diagonal block b of T (t x t) into Tinv + b*TB*TB (TB x TB, zero padded).
+// One warp per column j of the inverse (32 columns per CTA, TB/32 CTAs per block), solving
+// T x = e_j by substitution in 32-row chunks with lane = row within the chunk:
+//   1. each lane accumulates its row's dot product with the x entries of earlier chunks
+//      (independent per lane: no reduction, x broadcast by shuffles);
+//   2. the 32 x 32 diagonal sub-block is solved with one shuffle + one MAC per step.
+// Sums stay exact in u64 (< 128 products of < 2^52); one Barrett fold per entry.
+constexpr int TRI_COLS = 32;
+constexpr int TSTR = TB + 1;  // padded row stride: lanes read different rows of one column
 template <bool UPPER, bool UNIT>
-__global__ void __launch_bounds__(TB) tri_inv_kernel(const uint32_t* __restrict__ T, uint64_t ldt, uint32_t t,
-                                                    uint32_t* __restrict__ Tinv, uint32_t p, uint64_t mu) {
+__global__ void __launch_bounds__(TRI_COLS * 32) tri_inv_kernel(const uint32_t* __restrict__ T, uint64_t ldt,
+                                                               uint32_t t, uint32_t* __restrict__ Tinv, uint32_t p,
+                                                               uint64_t mu) {
     extern __shared__ uint32_t sm[];
-    uint32_t* S = sm;              // TB x TB block of T
-    uint32_t* X = sm + TB * TB;    // TB x TB inverse, column j owned by thread j
-    uint32_t* dinv = X + TB * TB;  // TB
-    const uint32_t b = blockIdx.x, j = threadIdx.x;
+    uint32_t* S = sm;                 // TB x TSTR block of T
+    uint32_t* dinv = sm + TB * TSTR;  // TB inverses of the diagonal (nonunit)
+    uint32_t* dinvp = dinv + TB;      // their Shoup factors
+    const uint32_t b = blockIdx.x / (TB / TRI_COLS), cblk = blockIdx.x % (TB / TRI_COLS);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t o = b * TB;
     const uint32_t tb = min((uint32_t)TB, t - o);
-    for (uint32_t idx = j; idx < (uint32_t)TB * TB; idx += TB) {
-        const uint32_t r = idx / TB, c = idx % TB;
-        S[idx] = (r < tb && c < tb) ? T[(uint64_t)(o + r) * ldt + o + c] : 0u;
-        X[idx] = 0u;
-    }
+    for (uint32_t r = warp; r < (uint32_t)TB; r += TRI_COLS)
+        for (uint32_t c = lane; c < (uint32_t)TB; c += 32)
+            S[r * TSTR + c] = (r < tb && c < tb) ? T[(uint64_t)(o + r) * ldt + o + c] : 0u;
     __syncthreads();
-    if (!UNIT && j < tb) dinv[j] = inv_mod(S[j * TB + j], p);
+    if (!UNIT)
+        for (uint32_t i = threadIdx.x; i < tb; i += blockDim.x) {
+            dinv[i] = inv_mod32(S[i * TSTR + i], p);
+            dinvp[i] = shoup_pre(dinv[i], p, mu);
+        }
     __syncthreads();
+    const uint32_t j = cblk * TRI_COLS + warp;  // column of the inverse owned by this warp
+    uint32_t x[TB / 32];                         // x[q] = X[q*32 + lane][j]
+#pragma unroll
+    for (int q = 0; q < TB / 32; ++q) x[q] = 0;
     if (j < tb) {
-        X[j * TB + j] = UNIT ? 1u : dinv[j];
-        if (!UPPER) {
-            for (uint32_t i = j + 1; i < tb; ++i) {
-                uint64_t s = 0;
-                for (uint32_t k = j; k < i; ++k) s += (uint64_t)S[i * TB + k] * X[k * TB + j];
-                uint32_t v = mod_u64(s, p, mu);
-                v = v ? p - v : 0u;
-                X[i * TB + j] = UNIT ? v : mul_mod(v, dinv[i], p, mu);
+        const uint32_t xj = UNIT ? 1u : dinv[j];
+        const int cj = (int)(j >> 5);
+#pragma unroll
+        for (int cc = 0; cc < TB / 32; ++cc) {
+            const int c = UPPER ? (TB / 32 - 1 - cc) : cc;
+            if (UPPER ? (c > cj) : (c < cj)) continue;  // chunk entirely zero for this column
+            const uint32_t i = (uint32_t)c * 32 + lane;  // this lane's row
+            uint64_t s = 0;
+            // 1. contributions of the already-solved chunks
+#pragma unroll
+            for (int q = 0; q < TB / 32; ++q) {
+                if (UPPER ? (q <= c || q > cj) : (q >= c || q < cj)) continue;
+                for (int l2 = 0; l2 < 32; ++l2) {
+                    const uint32_t xk = __shfl_sync(0xffffffffu, x[q], l2);
+                    s += (uint64_t)S[i * TSTR + q * 32 + l2] * xk;
+                }
             }
-        } else {
-            for (int i = (int)j - 1; i >= 0; --i) {
-                uint64_t s = 0;
-                for (uint32_t k = i + 1; k <= j; ++k) s += (uint64_t)S[i * TB + k] * X[k * TB + j];
-                uint32_t v = mod_u64(s, p, mu);
-                v = v ? p - v : 0u;
-                X[i * TB + j] = UNIT ? v : mul_mod(v, dinv[i], p, mu);
+            // 2. the diagonal 32 x 32 sub-block, one row per step
+            uint32_t mine = 0;
+            for (int s2 = 0; s2 < 32; ++s2) {
+                const int kk = UPPER ? 31 - s2 : s2;
+                const uint32_t k = (uint32_t)c * 32 + kk;
+                uint32_t v = 0;
+                if (lane == (uint32_t)kk) {
+                    if (k == j) {
+                        v = xj;
+                    } else if (UPPER ? (k < j) : (k > j)) {
+                        v = mod_u64(s, p, mu);
+                        v = v ? p - v : 0u;
+                        if (!UNIT && k < tb) v = shoup_mul(v, dinv[k], dinvp[k], p);
+                        if (k >= tb) v = 0;
+                    }
+                    mine = v;
+                }
+                const uint32_t xk = __shfl_sync(0xffffffffu, v, kk);
+                if (UPPER ? (lane < (uint32_t)kk) : (lane > (uint32_t)kk)) s += (uint64_t)S[i * TSTR + k] * xk;
             }
+            x[c] = mine;
         }
     }
-    __syncthreads();
     uint32_t* out = Tinv + (uint64_t)b * TB * TB;
-    for (uint32_t idx = j; idx < (uint32_t)TB * TB; idx += TB) out[idx] = X[idx];
+    if (j < (uint32_t)TB) {
+#pragma unroll
+        for (int q = 0; q < TB / 32; ++q) out[(uint64_t)(q * 32 + lane) * TB + j] = x[q];
+    }
 }
 
 // smallest i with T[i][i] == 0 (blas.hpp:291-297 / 347-353)
@@ -146,7 +185,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     uint32_t* Tinv = nullptr;
     FFG_CUDA(cudaMallocAsync(&Tinv, nblk * TB * TB * sizeof(uint32_t), b.st));
     const int upper = uplo == 1, unit = diag == 0;
-    const size_t smem = (2 * TB * TB + TB) * sizeof(uint32_t);
+    const size_t smem = (TB * TSTR + 2 * TB) * sizeof(uint32_t);
     static std::once_flag once;
     std::call_once(once, [&] {
         FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -157,7 +196,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     auto kern = upper ? (unit ? tri_inv_kernel<true, true> : tri_inv_kernel<true, false>)
                       : (unit ? tri_inv_kernel<false, true> : tri_inv_kernel<false, false>);
     b.ws.prof.begin(b.st);
-    kern<<<(unsigned)nblk, TB, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
+    kern<<<(unsigned)(nblk * (TB / TRI_COLS)), TRI_COLS * 32, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * nblk * TB * TB);
     b.count();

@@ -148,7 +148,7 @@ class Context:
     def launches(self) -> int:
         return int(lib().ffg_launch_count(self._h))
 
-    PROFILE_CLASSES = ("gemm", "split", "base", "trinv", "perm")
+    PROFILE_CLASSES = ("gemm", "split", "base", "trinv", "perm", "simt")
 
     def profile(self, on: bool) -> None:
         _check(lib().ffg_profile_enable(self._h, 1 if on else 0))
