@@ -110,7 +110,11 @@ struct Smem {
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
 };
 
+enum EpiMode : uint32_t { EPI_GENERIC = 0, EPI_SUB = 1, EPI_PROD = 2, EPI_ADD = 3 };
+
 struct EpiParams {
+    uint32_t mode;     // EPI_SUB: C - AB (alpha = p-1, beta = 1); EPI_PROD: AB (alpha 1, beta 0); EPI_ADD: C + AB
+    uint32_t vec_ok;   // C rows 16-byte aligned (C and ldc multiples of 4 words)
     uint32_t* C;
     uint64_t ldc;
     uint32_t M, N;
@@ -124,7 +128,7 @@ struct EpiParams {
 
 // --------------------------------------------------------------------------- the GEMM kernel
 template <int L>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     modgemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const EpiParams ep) {
     using S = Smem<L>;
@@ -221,39 +225,87 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncwarp();
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers -> mod p -> C
-        const uint32_t q = warp - 4;  // TMEM lane quarter
+        // ---------------- epilogue (8 warps): TMEM -> registers -> mod p -> C
+        // warp (4 + e): TMEM lane quarter e & 3, column half e >> 2 (8-column chunks)
+        constexpr int PER = NT / 16;                 // chunks per half
+        constexpr bool PREFETCH = PER * 8 <= 64;     // keep this thread's C values in registers
+        const uint32_t e = warp - 4, q = e & 3, half = e >> 2;
         const uint32_t row = m_blk * BM + q * 32 + lane;
+        const uint32_t col_first = n_blk * NT + half * PER * 8;
+        const bool row_ok = row < ep.M;
+        uint32_t* crow = ep.C + (uint64_t)(row_ok ? row : 0) * ep.ldc;
+        const bool vec = ep.vec_ok && col_first + PER * 8 <= ep.N;
+        const bool need_c = ep.mode != EPI_PROD;
+        uint32_t cpre[PREFETCH ? PER * 8 : 1];
+        if (PREFETCH && need_c && row_ok) {  // overlap the C read with the mainloop
+#pragma unroll
+            for (int ch = 0; ch < (PREFETCH ? PER : 0); ++ch) {
+                const uint32_t col = col_first + ch * 8;
+                if (vec) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
+                    const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
+                    cpre[ch * 8 + 0] = a.x, cpre[ch * 8 + 1] = a.y, cpre[ch * 8 + 2] = a.z, cpre[ch * 8 + 3] = a.w;
+                    cpre[ch * 8 + 4] = b.x, cpre[ch * 8 + 5] = b.y, cpre[ch * 8 + 6] = b.z, cpre[ch * 8 + 7] = b.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) cpre[ch * 8 + j] = col + j < ep.N ? crow[col + j] : 0u;
+                }
+            }
+        }
         ptx::mbar_wait(tmem_full, 0);
         ptx::tc_fence_after();
-        const uint32_t t_lane = tmem + ((q * 32) << 16);
-        uint32_t* crow = ep.C + (uint64_t)row * ep.ldc;
-        const uint32_t col0 = n_blk * NT;
-#pragma unroll 1
-        for (int c = 0; c < NT; c += 16) {
-            uint64_t acc[16];
+        const uint32_t t_lane = tmem + ((q * 32) << 16) + half * PER * 8;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = 0;
+        for (int ch = 0; ch < PER; ++ch) {
+            uint32_t r[D][8];
 #pragma unroll
-            for (int s = 0; s < D; ++s) {
-                uint32_t r[16];
-                ptx::tmem_ld16(t_lane + s * NT + c, r);
-                ptx::tmem_ld_wait();
-                const uint64_t ws = ep.w[s];
+            for (int s2 = 0; s2 < D; ++s2) ptx::tmem_ld8(t_lane + s2 * NT + ch * 8, r[s2]);
+            ptx::tmem_ld_wait();
+            if (!row_ok) continue;
+            const uint32_t col = col_first + ch * 8;
+            uint32_t cv[8];
+            if (need_c) {
+                if (PREFETCH) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] += (uint64_t)r[j] * ws;
+                    for (int j = 0; j < 8; ++j) cv[j] = cpre[(PREFETCH ? ch * 8 : 0) + j];
+                } else if (vec) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
+                    const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
+                    cv[0] = a.x, cv[1] = a.y, cv[2] = a.z, cv[3] = a.w, cv[4] = b.x, cv[5] = b.y, cv[6] = b.z, cv[7] = b.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) cv[j] = col + j < ep.N ? crow[col + j] : 0u;
+                }
             }
-            if (row < ep.M) {
+            uint32_t out[8];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t col = col0 + c + j;
-                    if (col < ep.N) {
-                        const uint32_t prod = mod_u64(acc[j], ep.p, ep.mu);
+            for (int j = 0; j < 8; ++j) {
+                uint64_t acc = 0;
+#pragma unroll
+                for (int s2 = 0; s2 < D; ++s2) acc += (uint64_t)r[s2][j] * ep.w[s2];
+                const uint32_t prod = mod_u64(acc, ep.p, ep.mu);
+                switch (ep.mode) {
+                    case EPI_SUB: out[j] = cv[j] >= prod ? cv[j] - prod : cv[j] + ep.p - prod; break;
+                    case EPI_PROD: out[j] = prod; break;
+                    case EPI_ADD: {
+                        const uint32_t t = cv[j] + prod;
+                        out[j] = t >= ep.p ? t - ep.p : t;
+                        break;
+                    }
+                    default: {
                         uint64_t v = (uint64_t)ep.alpha * prod;
-                        if (ep.beta) v += (uint64_t)ep.beta * crow[col];
-                        crow[col] = mod_u64(v, ep.p, ep.mu);
+                        if (ep.beta) v += (uint64_t)ep.beta * cv[j];
+                        out[j] = mod_u64(v, ep.p, ep.mu);
                     }
                 }
+            }
+            if (vec) {
+                *reinterpret_cast<uint4*>(crow + col) = make_uint4(out[0], out[1], out[2], out[3]);
+                *reinterpret_cast<uint4*>(crow + col + 4) = make_uint4(out[4], out[5], out[6], out[7]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (col + j < ep.N) crow[col + j] = out[j];
             }
         }
         ptx::tc_fence_before();
@@ -455,12 +507,17 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
     ep.mu = F.mu;
     ep.alpha = alpha;
     ep.beta = beta;
+    ep.mode = (alpha == F.p - 1 && beta == 1 && F.p > 2) ? EPI_SUB
+              : (alpha == 1 && beta == 0)                ? EPI_PROD
+              : (alpha == 1 && beta == 1)                ? EPI_ADD
+                                                         : EPI_GENERIC;
+    ep.vec_ok = ((reinterpret_cast<uintptr_t>(C.d) & 15) == 0 && (C.ld & 3) == 0) ? 1u : 0u;
     for (int s = 0; s < 8; ++s) ep.w[s] = F.w[s];
     ep.kblocks = (uint32_t)(Kp / BK);
     ep.m_tiles = (uint32_t)(Mp / BM);
     ep.n_tiles = (uint32_t)(Np / S::NT);
     dim3 grid(ep.m_tiles * ep.n_tiles);
-    modgemm_kernel<L><<<grid, 256, S::TOTAL, st>>>(ma, mb, ep);
+    modgemm_kernel<L><<<grid, 384, S::TOTAL, st>>>(ma, mb, ep);
     FFG_CUDA(cudaGetLastError());
 }
 

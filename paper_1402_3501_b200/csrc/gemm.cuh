@@ -97,6 +97,26 @@ public:
     ~Workspace() {
         for (auto& kv : bufs_)
             if (kv.second.ptr) cudaFree(kv.second.ptr);
+        if (mapped_) cudaFreeHost(mapped_);
+        if (ev_) cudaEventDestroy(ev_);
+    }
+    // host-mapped pinned words the device writes directly (the base-case rank mailbox);
+    // allocated once per context, not per call
+    uint32_t* mapped_host(size_t words, uint32_t** dev_ptr) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (mapped_words_ < words) {
+            if (mapped_) FFG_CUDA(cudaFreeHost(mapped_));
+            mapped_ = nullptr;
+            FFG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped_), words * 4, cudaHostAllocMapped));
+            FFG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_dev_), mapped_, 0));
+            mapped_words_ = words;
+        }
+        *dev_ptr = mapped_dev_;
+        return mapped_;
+    }
+    cudaEvent_t sync_event() {
+        if (!ev_) FFG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
+        return ev_;
     }
     // scratch valid until the next get() on the same stream
     uint8_t* get(cudaStream_t st, size_t bytes) {
@@ -128,6 +148,10 @@ private:
     };
     std::mutex mu_;
     std::unordered_map<cudaStream_t, Buf> bufs_;
+    uint32_t* mapped_ = nullptr;
+    uint32_t* mapped_dev_ = nullptr;
+    size_t mapped_words_ = 0;
+    cudaEvent_t ev_ = nullptr;
 };
 
 // C <- alpha*A*B + beta*C mod p (blas.hpp:31-103 semantics), enqueued on st.

@@ -84,19 +84,15 @@ struct Driver {
 
     Driver(const Blas& bl, size_t t, size_t m, size_t n)
         : b(bl), thr(std::max<size_t>(1, t)), arena(8 * (m + n) + 4096, bl.st) {
-        FFG_CUDA(cudaMallocAsync(&info_dev, sizeof(BaseInfo), b.st));
-        FFG_CUDA(cudaMallocHost(&info_host, sizeof(BaseInfo)));
-        FFG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    }
-    ~Driver() {
-        if (info_dev) cudaFreeAsync(info_dev, b.st);
-        if (info_host) cudaFreeHost(info_host);
-        if (ev) cudaEventDestroy(ev);
+        uint32_t* dev = nullptr;
+        // the base kernel writes rank + moved ranges straight into host-mapped memory
+        info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4, &dev));
+        info_dev = reinterpret_cast<BaseInfo*>(dev);
+        ev = b.ws.sync_event();
     }
 
     NodeRes base(DView a, NodeRes res) {
         rr_base_launch(b, a, res.P, res.Q, info_dev);
-        FFG_CUDA(cudaMemcpyAsync(info_host, info_dev, sizeof(BaseInfo), cudaMemcpyDeviceToHost, b.st));
         FFG_CUDA(cudaEventRecord(ev, b.st));
         FFG_CUDA(cudaEventSynchronize(ev));  // the rank decides every later shape
         ++base_cases;

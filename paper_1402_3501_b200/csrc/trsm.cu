@@ -102,6 +102,112 @@ __global__ void __launch_bounds__(TRI_COLS * 32) tri_inv_kernel(const uint32_t* 
     }
 }
 
+// Direct small triangular solve (t <= TB): one launch, no inverse matrix, no limb staging.
+// Every case is rewritten as a forward substitution over "vectors" (columns of B for a
+// left solve, rows of B for a right solve) with coefficients C[i][k], k < i:
+//   left  lower: C = T,        forward      right upper: C = T^T,  forward
+//   left  upper: C = T,        reversed     right lower: C = T^T,  reversed
+// x_i = (b_i - sum_{k<i} C[i][k] x_k) * d_i,  d_i = 1 (unit) or T[i][i]^-1 (nonunit).
+// A CTA owns 64 vectors; rows go in chunks of 16: (1) all 256 threads form the chunk's
+// dot products with the solved rows (u64, exact), (2) 64 threads finish the 16 x 16
+// diagonal block with register-resident x.  Exact residues throughout.
+constexpr int SV = 64;   // vectors per CTA
+constexpr int SCH = 16;  // rows per chunk
+template <int SIDE, bool REV, bool UNIT>
+__global__ void __launch_bounds__(256) trsm_small_kernel(const uint32_t* __restrict__ T, uint64_t ldt, uint32_t t,
+                                                         uint32_t* __restrict__ B, uint64_t ldb, uint32_t nvec,
+                                                         uint32_t p, uint64_t mu) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    uint32_t* C = sm;                       // TB x TSTR
+    uint32_t* X = C + TB * TSTR;            // TB x (SV + 1)
+    uint32_t* Acc = X + TB * (SV + 1);      // SCH x SV
+    uint32_t* dg = Acc + SCH * SV;          // TB
+    uint32_t* dgp = dg + TB;                // TB
+    const uint32_t tid = threadIdx.x, v0 = blockIdx.x * SV;
+    const uint32_t nv = min((uint32_t)SV, nvec - v0);
+    // coefficients in forward order
+    for (uint32_t idx = tid; idx < t * t; idx += 256) {
+        const uint32_t i = idx / t, k = idx % t;
+        if (k > i || (UNIT && k == i)) continue;
+        const uint32_t oi = REV ? t - 1 - i : i, ok = REV ? t - 1 - k : k;
+        C[i * TSTR + k] = SIDE == 0 ? T[(uint64_t)oi * ldt + ok] : T[(uint64_t)ok * ldt + oi];
+    }
+    // vectors: X[i][v] = b_{oi} of vector v
+    if (SIDE == 0) {
+        for (uint32_t idx = tid; idx < t * SV; idx += 256) {
+            const uint32_t i = idx / SV, v = idx % SV;
+            const uint32_t oi = REV ? t - 1 - i : i;
+            X[i * (SV + 1) + v] = v < nv ? B[(uint64_t)oi * ldb + v0 + v] : 0u;
+        }
+    } else {
+        for (uint32_t idx = tid; idx < t * SV; idx += 256) {
+            const uint32_t v = idx / t, i = idx % t;
+            const uint32_t oi = REV ? t - 1 - i : i;
+            X[i * (SV + 1) + v] = v < nv ? B[(uint64_t)(v0 + v) * ldb + oi] : 0u;
+        }
+    }
+    __syncthreads();
+    if (!UNIT)
+        for (uint32_t i = tid; i < t; i += 256) {
+            dg[i] = inv_mod32(C[i * TSTR + i], p);
+            dgp[i] = shoup_pre(dg[i], p, mu);
+        }
+    const uint32_t v = tid % SV, rl = tid / SV;  // step-1 mapping: 4 row lanes x 64 vectors
+    for (uint32_t i0 = 0; i0 < t; i0 += SCH) {
+        // (1) dot products of the chunk rows with the already-solved rows k < i0
+        if (i0 > 0) {
+            for (uint32_t q = 0; q < SCH / 4; ++q) {
+                const uint32_t i = i0 + rl + 4 * q;
+                if (i >= t) continue;
+                uint64_t s = 0;
+                const uint32_t* crow = C + i * TSTR;
+                for (uint32_t k = 0; k < i0; ++k) s += (uint64_t)crow[k] * X[k * (SV + 1) + v];
+                Acc[(rl + 4 * q) * SV + v] = mod_u64(s, p, mu);
+            }
+        } else {
+            for (uint32_t q = 0; q < SCH / 4; ++q) Acc[(rl + 4 * q) * SV + v] = 0u;
+        }
+        __syncthreads();
+        // (2) the diagonal SCH x SCH block, one vector per thread
+        if (tid < SV) {
+            uint32_t xr[SCH];
+#pragma unroll
+            for (int ii = 0; ii < SCH; ++ii) {
+                const uint32_t i = i0 + ii;
+                uint32_t val = 0;
+                if (i < t) {
+                    uint64_t s = Acc[ii * SV + v];
+                    const uint32_t* crow = C + i * TSTR + i0;
+#pragma unroll
+                    for (int k = 0; k < ii; ++k) s += (uint64_t)crow[k] * xr[k];
+                    const uint32_t sm_ = mod_u64(s, p, mu);
+                    const uint32_t b = X[i * (SV + 1) + v];
+                    val = b >= sm_ ? b - sm_ : b + p - sm_;
+                    if (!UNIT) val = shoup_mul(val, dg[i], dgp[i], p);
+                    X[i * (SV + 1) + v] = val;
+                }
+                xr[ii] = val;
+            }
+        }
+        __syncthreads();
+    }
+    if (SIDE == 0) {
+        for (uint32_t idx = tid; idx < t * SV; idx += 256) {
+            const uint32_t i = idx / SV, vv = idx % SV;
+            if (vv >= nv) continue;
+            const uint32_t oi = REV ? t - 1 - i : i;
+            B[(uint64_t)oi * ldb + v0 + vv] = X[i * (SV + 1) + vv];
+        }
+    } else {
+        for (uint32_t idx = tid; idx < t * SV; idx += 256) {
+            const uint32_t vv = idx / t, i = idx % t;
+            if (vv >= nv) continue;
+            const uint32_t oi = REV ? t - 1 - i : i;
+            B[(uint64_t)(v0 + vv) * ldb + oi] = X[i * (SV + 1) + vv];
+        }
+    }
+}
+
 // smallest i with T[i][i] == 0 (blas.hpp:291-297 / 347-353)
 __global__ void first_zero_diag_kernel(const uint32_t* T, uint64_t ldt, uint32_t t, uint32_t* out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -112,15 +218,43 @@ namespace {
 
 struct TrsmCtx {
     const Blas& b;
-    int side, upper;
+    int side, upper, unit;
     DView T;
-    const uint32_t* Tinv;  // one TB x TB inverse per diagonal block
+    const uint32_t* Tinv;  // one TB x TB inverse per diagonal block (nullptr: direct leaves)
 };
+
+void trsm_small(const Blas& b, int side, int upper, int unit, DView T, DView B) {
+    const size_t t = T.rows;
+    const size_t nvec = side == 0 ? B.cols : B.rows;
+    const size_t smem = (TB * TSTR + TB * (SV + 1) + SCH * SV + 2 * TB) * sizeof(uint32_t);
+    using K = void (*)(const uint32_t*, uint64_t, uint32_t, uint32_t*, uint64_t, uint32_t, uint32_t, uint64_t);
+    static K kerns[8] = {trsm_small_kernel<0, false, false>, trsm_small_kernel<0, false, true>,
+                         trsm_small_kernel<0, true, false>,  trsm_small_kernel<0, true, true>,
+                         trsm_small_kernel<1, false, false>, trsm_small_kernel<1, false, true>,
+                         trsm_small_kernel<1, true, false>,  trsm_small_kernel<1, true, true>};
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        for (auto k : kerns) FFG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    });
+    // forward order: left lower / right upper; reversed: left upper / right lower
+    const bool rev = side == 0 ? upper != 0 : upper == 0;
+    K k = kerns[side * 4 + (rev ? 2 : 0) + (unit ? 1 : 0)];
+    b.ws.prof.begin(b.st);
+    k<<<(unsigned)ceil_div(nvec, SV), 256, smem, b.st>>>(T.d, T.ld, (uint32_t)t, B.d, B.ld, (uint32_t)nvec, b.F.p,
+                                                         b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 4.0 * (double)t * (t + 2.0 * nvec));
+    b.count();
+}
 
 // solve on the diagonal range [o, o + t) of T (o a multiple of TB) against B
 void trsm_rec(const TrsmCtx& c, size_t o, size_t t, DView B) {
     const uint32_t pm1 = c.b.F.p - 1;
     if (t <= (size_t)TB) {
+        if (!c.Tinv) {
+            trsm_small(c.b, c.side, c.upper, c.unit, c.T.sub(o, o, t, t), B);
+            return;
+        }
         DView inv{const_cast<uint32_t*>(c.Tinv) + (o / TB) * TB * TB, t, t, (size_t)TB};
         if (c.side == 0)
             c.b.gemm(1, inv, B, 0, B);
@@ -181,10 +315,16 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
             throw Error(FFG_ERR_SINGULAR_DIAGONAL, "zero diagonal entry " + std::to_string(h) + " in triangular solve",
                         h);
     }
+    const int upper = uplo == 1, unit = diag == 0;
+    static const bool inverse_leaves = getenv("FFG_TRSM_INV") && atoi(getenv("FFG_TRSM_INV")) != 0;
+    if (!inverse_leaves) {  // default: direct CUDA-core leaves, tensor-core Schur updates between them
+        TrsmCtx c{b, side, upper, unit, A, nullptr};
+        trsm_rec(c, 0, t, B);
+        return;
+    }
     const size_t nblk = ceil_div(t, TB);
     uint32_t* Tinv = nullptr;
     FFG_CUDA(cudaMallocAsync(&Tinv, nblk * TB * TB * sizeof(uint32_t), b.st));
-    const int upper = uplo == 1, unit = diag == 0;
     const size_t smem = (TB * TSTR + 2 * TB) * sizeof(uint32_t);
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -200,7 +340,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * nblk * TB * TB);
     b.count();
-    TrsmCtx c{b, side, upper, A, Tinv};
+    TrsmCtx c{b, side, upper, unit, A, Tinv};
     trsm_rec(c, 0, t, B);
     FFG_CUDA(cudaFreeAsync(Tinv, b.st));
 }
