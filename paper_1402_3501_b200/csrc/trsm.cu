@@ -102,6 +102,110 @@ __global__ void __launch_bounds__(TRI_COLS * 32) tri_inv_kernel(const uint32_t* 
     }
 }
 
+// Recursive block inverse of diagonal block b (log depth instead of a TB-step chain):
+// 8 x 8 leaves by substitution, then for block sizes 16, 32, 64, 128 every diagonal
+// block [X11 0; X21 X22] (lower) gets X21 = -X22 (L21 X11); upper: X12 = -X11 (U12 X22).
+// Each level is two small products over shared memory, all blocks of the level at once;
+// dot products are exact in u64 (<= 64 terms < 2^52), one Barrett fold per entry.
+constexpr int RI_THREADS = 512;
+constexpr int LEAF = 8;
+template <bool UPPER, bool UNIT>
+__global__ void __launch_bounds__(RI_THREADS) tri_inv_rec_kernel(const uint32_t* __restrict__ T, uint64_t ldt,
+                                                                uint32_t t, uint32_t* __restrict__ Tinv, uint32_t p,
+                                                                uint64_t mu) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* S = sm;                    // TB x TSTR: the triangle
+    uint32_t* X = S + TB * TSTR;         // TB x TSTR: its inverse
+    uint32_t* W = X + TB * TSTR;         // (TB/2) x (TB/2 + 1) temporaries
+    uint32_t* dinv = W + (TB / 2) * (TB / 2 + 1);
+    const uint32_t tid = threadIdx.x, o = blockIdx.x * TB;
+    const uint32_t tb = min((uint32_t)TB, t - o);
+    for (uint32_t idx = tid; idx < (uint32_t)TB * TB; idx += RI_THREADS) {
+        const uint32_t r = idx / TB, c = idx % TB;
+        S[r * TSTR + c] = (r < tb && c < tb) ? T[(uint64_t)(o + r) * ldt + o + c] : 0u;
+        X[r * TSTR + c] = 0u;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < (uint32_t)TB; i += RI_THREADS)
+        dinv[i] = UNIT ? 1u : (i < tb ? inv_mod32(S[i * TSTR + i], p) : 1u);
+    __syncthreads();
+    // leaves: thread per (leaf block, column)
+    if (tid < (uint32_t)TB) {
+        const uint32_t lb = tid / LEAF, j = tid % LEAF, base = lb * LEAF;
+        uint32_t x[LEAF];
+#pragma unroll
+        for (int i = 0; i < LEAF; ++i) x[i] = 0;
+        x[j] = dinv[base + j];
+        if (!UPPER) {
+#pragma unroll
+            for (int i = 0; i < LEAF; ++i) {
+                if (i <= (int)j) continue;
+                uint64_t s = 0;
+#pragma unroll
+                for (int k = 0; k < LEAF; ++k)
+                    if (k >= (int)j && k < i) s += (uint64_t)S[(base + i) * TSTR + base + k] * x[k];
+                uint32_t v = mod_u64(s, p, mu);
+                v = v ? p - v : 0u;
+                x[i] = UNIT ? v : mul_mod(v, dinv[base + i], p, mu);
+            }
+        } else {
+#pragma unroll
+            for (int i = LEAF - 1; i >= 0; --i) {
+                if (i >= (int)j) continue;
+                uint64_t s = 0;
+#pragma unroll
+                for (int k = 0; k < LEAF; ++k)
+                    if (k > i && k <= (int)j) s += (uint64_t)S[(base + i) * TSTR + base + k] * x[k];
+                uint32_t v = mod_u64(s, p, mu);
+                v = v ? p - v : 0u;
+                x[i] = UNIT ? v : mul_mod(v, dinv[base + i], p, mu);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < LEAF; ++i) X[(base + i) * TSTR + base + j] = x[i];
+    }
+    __syncthreads();
+    for (uint32_t b = 2 * LEAF; b <= (uint32_t)TB; b *= 2) {
+        const uint32_t h = b / 2, nblk = TB / b, per = h * h;
+        // W_blk = L21 X11 (lower) or U12 X22 (upper), stored per block at W + blk*per (fits: nblk*per = TB*h/2)
+        for (uint32_t idx = tid; idx < nblk * per; idx += RI_THREADS) {
+            const uint32_t blk = idx / per, e = idx % per, i = e / h, c = e % h, ob = blk * b;
+            uint64_t s = 0;
+            if (!UPPER) {  // L21[i][k] * X11[k][c], X11 lower -> k >= c
+                const uint32_t* lrow = S + (ob + h + i) * TSTR + ob;
+                for (uint32_t k = c; k < h; ++k) s += (uint64_t)lrow[k] * X[(ob + k) * TSTR + ob + c];
+            } else {  // U12[i][k] * X22[k][c], X22 upper -> k <= c
+                const uint32_t* urow = S + (ob + i) * TSTR + ob + h;
+                for (uint32_t k = 0; k <= c; ++k) s += (uint64_t)urow[k] * X[(ob + h + k) * TSTR + ob + h + c];
+            }
+            W[blk * per + i * h + c] = mod_u64(s, p, mu);
+        }
+        __syncthreads();
+        for (uint32_t idx = tid; idx < nblk * per; idx += RI_THREADS) {
+            const uint32_t blk = idx / per, e = idx % per, i = e / h, c = e % h, ob = blk * b;
+            const uint32_t* w = W + blk * per;
+            uint64_t s = 0;
+            if (!UPPER) {  // X21[i][c] = -sum_{k<=i} X22[i][k] W[k][c]
+                const uint32_t* xrow = X + (ob + h + i) * TSTR + ob + h;
+                for (uint32_t k = 0; k <= i; ++k) s += (uint64_t)xrow[k] * w[k * h + c];
+                const uint32_t v = mod_u64(s, p, mu);
+                X[(ob + h + i) * TSTR + ob + c] = v ? p - v : 0u;
+            } else {  // X12[i][c] = -sum_{k>=i} X11[i][k] W[k][c]
+                const uint32_t* xrow = X + (ob + i) * TSTR + ob;
+                for (uint32_t k = i; k < h; ++k) s += (uint64_t)xrow[k] * w[k * h + c];
+                const uint32_t v = mod_u64(s, p, mu);
+                X[(ob + i) * TSTR + ob + h + c] = v ? p - v : 0u;
+            }
+        }
+        __syncthreads();
+    }
+    uint32_t* out = Tinv + (uint64_t)blockIdx.x * TB * TB;
+    for (uint32_t idx = tid; idx < (uint32_t)TB * TB; idx += RI_THREADS) {
+        const uint32_t r = idx / TB, c = idx % TB;
+        out[idx] = (r < tb && c < tb) ? X[r * TSTR + c] : 0u;
+    }
+}
+
 // Direct small triangular solve (t <= TB): one launch, no inverse matrix, no limb staging.
 // Every case is rewritten as a forward substitution over "vectors" (columns of B for a
 // left solve, rows of B for a right solve) with coefficients C[i][k], k < i:
@@ -316,7 +420,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
                         h);
     }
     const int upper = uplo == 1, unit = diag == 0;
-    static const bool inverse_leaves = getenv("FFG_TRSM_INV") && atoi(getenv("FFG_TRSM_INV")) != 0;
+    static const bool inverse_leaves = !(getenv("FFG_TRSM_DIRECT") && atoi(getenv("FFG_TRSM_DIRECT")) != 0);
     if (!inverse_leaves) {  // default: direct CUDA-core leaves, tensor-core Schur updates between them
         TrsmCtx c{b, side, upper, unit, A, nullptr};
         trsm_rec(c, 0, t, B);
@@ -325,18 +429,33 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     const size_t nblk = ceil_div(t, TB);
     uint32_t* Tinv = nullptr;
     FFG_CUDA(cudaMallocAsync(&Tinv, nblk * TB * TB * sizeof(uint32_t), b.st));
-    const size_t smem = (TB * TSTR + 2 * TB) * sizeof(uint32_t);
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    });
-    auto kern = upper ? (unit ? tri_inv_kernel<true, true> : tri_inv_kernel<true, false>)
-                      : (unit ? tri_inv_kernel<false, true> : tri_inv_kernel<false, false>);
+    static const bool column_inverse = getenv("FFG_TRI_COLUMN") && atoi(getenv("FFG_TRI_COLUMN")) != 0;
     b.ws.prof.begin(b.st);
-    kern<<<(unsigned)(nblk * (TB / TRI_COLS)), TRI_COLS * 32, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
+    if (column_inverse) {  // per-column substitution (kept for A/B comparison)
+        const size_t smem = (TB * TSTR + 2 * TB) * sizeof(uint32_t);
+        static std::once_flag once;
+        std::call_once(once, [&] {
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        });
+        auto kern = upper ? (unit ? tri_inv_kernel<true, true> : tri_inv_kernel<true, false>)
+                          : (unit ? tri_inv_kernel<false, true> : tri_inv_kernel<false, false>);
+        kern<<<(unsigned)(nblk * (TB / TRI_COLS)), TRI_COLS * 32, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
+    } else {
+        const size_t smem = (2 * TB * TSTR + (TB / 2) * (TB / 2 + 1) + TB) * sizeof(uint32_t);
+        static std::once_flag once2;
+        std::call_once(once2, [&] {
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        });
+        auto kern = upper ? (unit ? tri_inv_rec_kernel<true, true> : tri_inv_rec_kernel<true, false>)
+                          : (unit ? tri_inv_rec_kernel<false, true> : tri_inv_rec_kernel<false, false>);
+        kern<<<(unsigned)nblk, RI_THREADS, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
+    }
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * nblk * TB * TB);
     b.count();
