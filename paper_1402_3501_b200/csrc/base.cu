@@ -24,12 +24,14 @@
 // Exhausted rows (rankrev.hpp:54-57) keep their zero Schur rows and zero L
 // entries for later pivots, as in the reference.
 #include "pluq.cuh"
+#include "triinv.cuh"
 
 namespace ffg {
 
 constexpr int BASE_THREADS = 256;
 constexpr size_t BASE_SMEM_LIMIT = 200 * 1024;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr uint32_t INV_MAX = 64;  // largest base-case rank whose factor inverses are cached
 
 __device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
 
@@ -65,7 +67,7 @@ template <bool IN_SMEM>
 __global__ void __launch_bounds__(BASE_THREADS)
     rr_base_kernel(uint32_t* __restrict__ A, uint64_t lda, BaseLayout lay, uint32_t* __restrict__ scratch,
                    uint32_t* __restrict__ Pd, uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p,
-                   uint64_t mu) {
+                   uint64_t mu, uint32_t* __restrict__ inv_out) {
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t m = lay.m, n = lay.n, ns = lay.ns, rmax = lay.rmax;
     // shared: prow | pcol | pivv | invp | invD (rmax each) | Psh m | Qsh n | rowrank m | colrank n
@@ -273,9 +275,44 @@ __global__ void __launch_bounds__(BASE_THREADS)
             dst[u] = v;
         }
     }
+    // inverses of the leading r x r factors (L unit lower, U upper) for the TRSMs that will use
+    // this block as their triangle: a base case is a leaf of every such TRSM
+    if (IN_SMEM && inv_out != nullptr) {
+        if (r == 0 || r > INV_MAX) {
+            if (tid == 0) info->cached = 0;
+            return;
+        }
+        __syncthreads();  // the packed block in A (global) is complete and visible to the CTA
+        uint32_t* Ts = S + (size_t)m * ns + (size_t)m * rmax;  // scratch after S and Lb
+        Ts += (4 - (reinterpret_cast<uintptr_t>(Ts) / 4) % 4) % 4;
+        uint32_t* Xs = Ts + INV_MAX * (INV_MAX + 1);
+        uint32_t* Ws = Xs + INV_MAX * (INV_MAX + 1);
+        uint32_t* dv = Ws + (INV_MAX / 2) * (INV_MAX / 2);
+        for (uint32_t idx = tid; idx < r * r; idx += BASE_THREADS) {
+            const uint32_t i = idx / r, j = idx % r;
+            Ts[i * (INV_MAX + 1) + j] = A[(uint64_t)i * lda + j];
+        }
+        __syncthreads();
+        for (int which = 0; which < 2; ++which) {
+            if (r <= 16) {
+                if (which == 0) tri_inverse_smem<false, 16>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
+                else tri_inverse_smem<true, 16>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
+            } else if (r <= 32) {
+                if (which == 0) tri_inverse_smem<false, 32>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
+                else tri_inverse_smem<true, 32>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
+            } else {
+                if (which == 0) tri_inverse_smem<false, 64>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
+                else tri_inverse_smem<true, 64>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
+            }
+            uint32_t* out = inv_out + (size_t)which * r * r;
+            for (uint32_t idx = tid; idx < r * r; idx += BASE_THREADS) out[idx] = Xs[(idx / r) * (INV_MAX + 1) + idx % r];
+            __syncthreads();
+        }
+        if (tid == 0) info->cached = 1;
+    }
 }
 
-void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev) {
+bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv_out) {
     BaseLayout lay;
     lay.m = (uint32_t)a.rows;
     lay.n = (uint32_t)a.cols;
@@ -284,6 +321,9 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const size_t fixed = ((size_t)5 * lay.rmax + 2 * ((size_t)lay.m + lay.n) + 4) * 4;
     const size_t blk = ((size_t)lay.m * lay.ns + (size_t)lay.m * lay.rmax) * 4;
     BaseInfo* info = static_cast<BaseInfo*>(info_dev);
+    // room for the factor inverses (two INV_MAX frames + workspace), only for ranks <= INV_MAX
+    const size_t inv_bytes = (2 * INV_MAX * (INV_MAX + 1) + (INV_MAX / 2) * (INV_MAX / 2) + INV_MAX + 8) * 4;
+    if (inv_out && (fixed + blk + inv_bytes > BASE_SMEM_LIMIT)) inv_out = nullptr;
     b.ws.prof.begin(b.st);
     if (fixed + blk <= BASE_SMEM_LIMIT) {
         static bool set = false;
@@ -292,9 +332,10 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
                                           (int)BASE_SMEM_LIMIT));
             set = true;
         }
-        rr_base_kernel<true><<<1, BASE_THREADS, fixed + blk, b.st>>>(a.d, a.ld, lay, nullptr, Pd, Qd, info, b.F.p,
-                                                                     b.F.mu);
+        rr_base_kernel<true><<<1, BASE_THREADS, fixed + blk + (inv_out ? inv_bytes : 0), b.st>>>(
+            a.d, a.ld, lay, nullptr, Pd, Qd, info, b.F.p, b.F.mu, inv_out);
     } else {
+        inv_out = nullptr;
         if (fixed > BASE_SMEM_LIMIT) throw Error(FFG_ERR_INVALID_BLOCK, "base case block too large");
         static bool set = false;
         if (!set) {
@@ -304,12 +345,14 @@ void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
         }
         uint32_t* scratch = nullptr;
         FFG_CUDA(cudaMallocAsync(&scratch, blk, b.st));
-        rr_base_kernel<false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, lay, scratch, Pd, Qd, info, b.F.p, b.F.mu);
+        rr_base_kernel<false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, lay, scratch, Pd, Qd, info, b.F.p, b.F.mu,
+                                                                nullptr);
         FFG_CUDA(cudaFreeAsync(scratch, b.st));
     }
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
     b.count();
+    return inv_out != nullptr;
 }
 
 }  // namespace ffg

@@ -19,6 +19,7 @@
 // the unmodified reference wherever r2 == 0 or r3 == 0 (all full-rank input).
 #include <algorithm>
 #include <cstring>
+#include <deque>
 #include <vector>
 
 #include "pluq.cuh"
@@ -47,6 +48,7 @@ struct NodeRes {
     uint32_t* P = nullptr;  // device index arrays (valid inside pr / qr)
     uint32_t* Q = nullptr;
     Range pr, qr;
+    Factor* fac = nullptr;  // structure of the leading r x r factor (for TRSMs that use it)
 };
 
 // device LIFO arena for permutation index arrays
@@ -81,25 +83,71 @@ struct Driver {
     BaseInfo* info_host = nullptr;
     cudaEvent_t ev = nullptr;
     uint64_t base_cases = 0;
+    // factor tree + the base cases' cached factor inverses (live for the whole call)
+    std::deque<Factor> factors;
+    uint32_t* inv_arena = nullptr;
+    size_t inv_cap = 0, inv_top = 0;
+    bool use_factors = true;
 
     Driver(const Blas& bl, size_t t, size_t m, size_t n)
         : b(bl), thr(std::max<size_t>(1, t)), arena(8 * (m + n) + 4096, bl.st) {
         uint32_t* dev = nullptr;
         // the base kernel writes rank + moved ranges straight into host-mapped memory
-        info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4, &dev));
+        info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4 + 2, &dev));
         info_dev = reinterpret_cast<BaseInfo*>(dev);
         ev = b.ws.sync_event();
+        // factor-tree TRSM (cached base-case inverses): opt-in, slower than blocked inverses today
+        static const bool on = getenv("FFG_FACTOR_TRSM") && atoi(getenv("FFG_FACTOR_TRSM")) != 0;
+        use_factors = on;
+        if (use_factors) {
+            // sum of r^2 over base cases <= min(m, n) * 64; two triangles each, plus one slot of slack
+            inv_cap = 2 * (std::min(m, n) * 64 + 64 * 64) + 64;
+            FFG_CUDA(cudaMallocAsync(&inv_arena, inv_cap * 4, b.st));
+        }
+    }
+    ~Driver() {
+        if (inv_arena) cudaFreeAsync(inv_arena, b.st);
+    }
+
+    Factor* new_factor(size_t rank) {
+        factors.emplace_back();
+        factors.back().rank = rank;
+        return &factors.back();
     }
 
     NodeRes base(DView a, NodeRes res) {
-        rr_base_launch(b, a, res.P, res.Q, info_dev);
+        const size_t rmax = std::min(a.rows, a.cols);
+        uint32_t* slot = nullptr;
+        if (use_factors && rmax <= 64 && inv_top + 2 * rmax * rmax <= inv_cap) slot = inv_arena + inv_top;
+        const bool asked = rr_base_launch(b, a, res.P, res.Q, info_dev, slot);
         FFG_CUDA(cudaEventRecord(ev, b.st));
         FFG_CUDA(cudaEventSynchronize(ev));  // the rank decides every later shape
         ++base_cases;
         res.rank = info_host->rank;
         res.pr = Range{info_host->plo, info_host->phi};
         res.qr = Range{info_host->qlo, info_host->qhi};
+        res.fac = new_factor(res.rank);
+        if (asked && info_host->cached && res.rank > 0) {
+            res.fac->invL = slot;
+            res.fac->invU = slot + res.rank * res.rank;
+            inv_top += 2 * res.rank * res.rank;
+        }
         return res;
+    }
+
+    // TRSMs of tile_rec always use a child's leading factor: walk its factor tree when every
+    // leaf has cached inverses, else the generic blocked-inverse TRSM
+    void trsm_lower_unit(const NodeRes& c, DView L, DView B) {
+        if (c.fac && c.fac->complete())
+            trsm_factor(b, 0, *c.fac, L, B);
+        else
+            ftrsm_dev(b, 0, 0, 0, L, B, false);
+    }
+    void trsm_upper_nonunit(const NodeRes& c, DView U, DView B) {
+        if (c.fac && c.fac->complete())
+            trsm_factor(b, 1, *c.fac, U, B);
+        else
+            ftrsm_dev(b, 1, 1, 1, U, B, false);
     }
 
     void apply(const NodeRes& c, int axis, DView v) {
@@ -108,8 +156,6 @@ struct Driver {
         perm_apply_range(b, v, axis, axis == 0 ? c.P : c.Q, r.lo, r.hi);
     }
 
-    void trsm_lower_unit(DView L, DView B) { ftrsm_dev(b, 0, 0, 0, L, B, false); }
-    void trsm_upper_nonunit(DView U, DView B) { ftrsm_dev(b, 1, 1, 1, U, B, false); }
     void gemm_sub(DView A, DView B, DView C) { b.gemm(b.F.p - 1, A, B, 1, C); }
 
     // compose a child's permutation into this node's array at offset off
@@ -157,9 +203,9 @@ struct Driver {
         DView G = a.sub(m1, r1, m - m1, n1 - r1);
         DView H = a.sub(m1, n1, m - m1, n - n1);
         if (r1 > 0) {                                            // :111-117
-            if (!D.empty()) trsm_lower_unit(L1, D);
+            if (!D.empty()) trsm_lower_unit(r1s, L1, D);
             if (!E.empty()) gemm_sub(M1, D, E);
-            if (!Fb.empty()) trsm_upper_nonunit(L1, Fb);
+            if (!Fb.empty()) trsm_upper_nonunit(r1s, L1, Fb);
             if (!G.empty() && !V1.empty()) gemm_sub(Fb, V1, G);
             if (!H.empty()) gemm_sub(Fb, D, H);
         }
@@ -184,8 +230,8 @@ struct Driver {
         DView N = a.sub(m1, n1 + r2, r3, n - n1 - r2);
         DView R = a.sub(m1 + r3, n1 + r2, m - m1 - r3, n - n1 - r2);
 
-        if (r2 > 0 && !I.empty()) trsm_upper_nonunit(U2, I);    // :144
-        if (r2 > 0 && !K.empty()) trsm_upper_nonunit(U2, K);    // :145
+        if (r2 > 0 && !I.empty()) trsm_upper_nonunit(r2s, U2, I);    // :144
+        if (r2 > 0 && !K.empty()) trsm_upper_nonunit(r2s, U2, K);    // :145
         uint32_t* jbuf = nullptr;
         DView J = I;
         if (r3 > 0 && !I.empty()) {                              // :146, J = L3^-1 I into a temporary
@@ -193,9 +239,9 @@ struct Driver {
             FFG_CUDA(cudaMemcpy2DAsync(jbuf, I.cols * 4, I.d, I.ld * 4, I.cols * 4, I.rows, cudaMemcpyDeviceToDevice,
                                        b.st));
             J = DView{jbuf, I.rows, I.cols, I.cols};
-            trsm_lower_unit(L3, J);
+            trsm_lower_unit(r3s, L3, J);
         }
-        if (r3 > 0 && !N.empty()) trsm_lower_unit(L3, N);       // :147
+        if (r3 > 0 && !N.empty()) trsm_lower_unit(r3s, L3, N);       // :147
         if (!N.empty() && !J.empty()) gemm_sub(J, V2, N);        // :148  O = N - J*V2
         if (!R.empty()) {                                        // :149-152
             if (!K.empty() && !V2.empty()) gemm_sub(K, V2, R);
@@ -229,6 +275,9 @@ struct Driver {
         rotate_block_dev(b, a, 1, r1 + r2 + r3, n1 + r2, r4);
 
         res.rank = r1 + r2 + r3 + r4;
+        res.fac = new_factor(res.rank);  // leading factor = children's factors in gather order
+        for (const NodeRes* c : {&r1s, &r2s, &r3s, &r4s})
+            if (c->rank > 0) res.fac->kids.push_back(c->fac);
         arena.reset(mark);  // children consumed (stream order protects the pending kernels)
         return res;
     }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -38,9 +39,28 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
 // rank + moved ranges of a base-case result (device -> pinned host)
 struct BaseInfo {
     uint32_t rank, plo, phi, qlo, qhi;
+    uint32_t cached;  // 1 when inv_out received inv(L_r), inv(U_r) (r x r each, ld r)
 };
-// one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info
-void rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev);
+// one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info; with
+// inv_out != nullptr also the inverses of the leading r x r L and U factors (r <= 64)
+// returns whether inverses were requested (the kernel still reports info->cached)
+bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev,
+                    uint32_t* inv_out = nullptr);
+
+// Structure of a node's leading r x r factor (tile_rec pivot gather order A1, E, G, R):
+// block triangular with the children's leading factors on the diagonal.  Leaves are base
+// cases whose inverses were cached by the base kernel.
+struct Factor {
+    size_t rank = 0;
+    const uint32_t* invL = nullptr;  // base case: inv(L) (unit lower), r x r, ld r
+    const uint32_t* invU = nullptr;  // base case: inv(U) (upper), r x r, ld r
+    std::vector<const Factor*> kids;  // internal node: children with rank > 0, in gather order
+    bool complete() const;           // every leaf carries cached inverses
+};
+
+// TRSM against a node's factor (T = its r x r leading packed block):
+// side 0: B <- L^-1 B (unit lower);  side 1: B <- B U^-1 (upper, non-unit)
+void trsm_factor(const Blas& b, int side, const Factor& f, DView T, DView B);
 
 // permutation kernels (perm.cu)
 void perm_apply_range(const Blas& b, DView a, int axis, const uint32_t* perm, size_t lo, size_t hi);

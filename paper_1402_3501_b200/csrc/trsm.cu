@@ -312,6 +312,108 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(const uint32_t* __restr
     }
 }
 
+// Leaf of a factor-tree TRSM: X = inv(L) B (left) or X = B inv(U) (right), in place, with the
+// inverse cached by the base case (d <= 64).  A CTA owns 64 vectors (columns of B for left,
+// rows for right) and stages them in shared memory before writing, so in place is safe.
+// 256 threads x (4 x 4) register tiles, exact u64 dot products (<= 64 terms).
+constexpr int LA = 64;
+template <int SIDE>
+__global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restrict__ inv, uint32_t d,
+                                                         uint32_t* __restrict__ B, uint64_t ldb, uint32_t nvec,
+                                                         uint32_t p, uint64_t mu) {
+    __shared__ uint32_t Cs[LA][LA + 1];  // Cs[i][k] = coefficient of x_k in output i
+    __shared__ uint32_t Bs[LA][LA + 1];  // Bs[k][v] = element k of vector v
+    const uint32_t tid = threadIdx.x, v0 = blockIdx.x * LA;
+    const uint32_t nv = min((uint32_t)LA, nvec - v0);
+    for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+        const uint32_t i = idx / LA, k = idx % LA;
+        Cs[i][k] = (i < d && k < d) ? (SIDE == 0 ? inv[i * d + k] : inv[k * d + i]) : 0u;
+    }
+    if (SIDE == 0) {
+        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+            const uint32_t k = idx / LA, v = idx % LA;
+            Bs[k][v] = (k < d && v < nv) ? B[(uint64_t)k * ldb + v0 + v] : 0u;
+        }
+    } else {
+        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+            const uint32_t v = idx / LA, k = idx % LA;
+            Bs[k][v] = (k < d && v < nv) ? B[(uint64_t)(v0 + v) * ldb + k] : 0u;
+        }
+    }
+    __syncthreads();
+    const uint32_t ti = tid / 16, tv = tid % 16;
+    uint64_t acc[4][4] = {};
+    for (uint32_t k = 0; k < d; ++k) {
+        uint32_t c[4], x[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) c[a] = Cs[ti * 4 + a][k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = Bs[k][tv * 4 + q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[a][q] += (uint64_t)c[a] * x[q];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const uint32_t i = ti * 4 + a;
+        if (i >= d) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t v = tv * 4 + q;
+            if (v >= nv) continue;
+            const uint32_t val = mod_u64(acc[a][q], p, mu);
+            if (SIDE == 0)
+                B[(uint64_t)i * ldb + v0 + v] = val;
+            else
+                B[(uint64_t)(v0 + v) * ldb + i] = val;
+        }
+    }
+}
+
+bool Factor::complete() const {
+    if (invL) return true;
+    if (kids.empty()) return rank == 0;
+    for (const Factor* k : kids)
+        if (!k->complete()) return false;
+    return true;
+}
+
+void trsm_factor(const Blas& b, int side, const Factor& f, DView T, DView B) {
+    const size_t r = f.rank;
+    if (r == 0 || B.empty()) return;
+    if (f.invL) {
+        const size_t nvec = side == 0 ? B.cols : B.rows;
+        b.ws.prof.begin(b.st);
+        if (side == 0)
+            leaf_apply_kernel<0><<<(unsigned)ceil_div(nvec, LA), 256, 0, b.st>>>(f.invL, (uint32_t)r, B.d, B.ld,
+                                                                               (uint32_t)nvec, b.F.p, b.F.mu);
+        else
+            leaf_apply_kernel<1><<<(unsigned)ceil_div(nvec, LA), 256, 0, b.st>>>(f.invU, (uint32_t)r, B.d, B.ld,
+                                                                               (uint32_t)nvec, b.F.p, b.F.mu);
+        FFG_CUDA(cudaGetLastError());
+        b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)r * nvec);
+        b.count();
+        return;
+    }
+    // block substitution over the children's factors (block triangular, gather order)
+    const uint32_t pm1 = b.F.p - 1;
+    size_t o = 0;
+    for (const Factor* k : f.kids) {
+        const size_t d = k->rank;
+        if (side == 0) {  // L X = B, row blocks
+            DView Bi = B.sub(o, 0, d, B.cols);
+            if (o > 0) b.gemm(pm1, T.sub(o, 0, d, o), B.sub(0, 0, o, B.cols), 1, Bi);
+            trsm_factor(b, 0, *k, T.sub(o, o, d, d), Bi);
+        } else {  // X U = B, column blocks
+            DView Bi = B.sub(0, o, B.rows, d);
+            if (o > 0) b.gemm(pm1, B.sub(0, 0, B.rows, o), T.sub(0, o, o, d), 1, Bi);
+            trsm_factor(b, 1, *k, T.sub(o, o, d, d), Bi);
+        }
+        o += d;
+    }
+}
+
 // smallest i with T[i][i] == 0 (blas.hpp:291-297 / 347-353)
 __global__ void first_zero_diag_kernel(const uint32_t* T, uint64_t ldt, uint32_t t, uint32_t* out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
