@@ -99,6 +99,11 @@ public:
             if (kv.second.ptr) cudaFree(kv.second.ptr);
         if (mapped_) cudaFreeHost(mapped_);
         if (ev_) cudaEventDestroy(ev_);
+        for (auto e : ev_pool_) cudaEventDestroy(e);
+        for (auto& kv : streams_) {
+            cudaStreamSynchronize(kv.second);
+            cudaStreamDestroy(kv.second);
+        }
     }
     // host-mapped pinned words the device writes directly (the base-case rank mailbox);
     // allocated once per context, not per call
@@ -117,6 +122,29 @@ public:
     cudaEvent_t sync_event() {
         if (!ev_) FFG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
         return ev_;
+    }
+    // streams owned by the context for the recursion's concurrency: id -> stream, created on
+    // first use with the given priority class (0 = highest, 1 = lowest)
+    cudaStream_t stream(int id, int low_priority) {
+        std::lock_guard<std::mutex> lk(mu_);
+        auto it = streams_.find(id);
+        if (it != streams_.end()) return it->second;
+        int least = 0, greatest = 0;
+        FFG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        cudaStream_t s;
+        FFG_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, low_priority ? least : greatest));
+        streams_[id] = s;
+        return s;
+    }
+    // events for fork/join within one call: recycled across calls (reset_events at call start)
+    void reset_events() { ev_cursor_ = 0; }
+    cudaEvent_t event() {
+        if (ev_cursor_ == ev_pool_.size()) {
+            cudaEvent_t e;
+            FFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev_pool_.push_back(e);
+        }
+        return ev_pool_[ev_cursor_++];
     }
     // scratch valid until the next get() on the same stream
     uint8_t* get(cudaStream_t st, size_t bytes) {
@@ -152,6 +180,9 @@ private:
     uint32_t* mapped_dev_ = nullptr;
     size_t mapped_words_ = 0;
     cudaEvent_t ev_ = nullptr;
+    std::unordered_map<int, cudaStream_t> streams_;
+    std::vector<cudaEvent_t> ev_pool_;
+    size_t ev_cursor_ = 0;
 };
 
 // C <- alpha*A*B + beta*C mod p (blas.hpp:31-103 semantics), enqueued on st.

@@ -76,7 +76,8 @@ private:
 };
 
 struct Driver {
-    const Blas& b;
+    const Blas& user;  // caller's stream: forked into `b` (high priority) and joined back at the end
+    Blas b;
     size_t thr;
     PermArena arena;
     BaseInfo* info_dev = nullptr;
@@ -89,8 +90,19 @@ struct Driver {
     size_t inv_cap = 0, inv_top = 0;
     bool use_factors = true;
 
+    bool use_streams = true;
+
     Driver(const Blas& bl, size_t t, size_t m, size_t n)
-        : b(bl), thr(std::max<size_t>(1, t)), arena(8 * (m + n) + 4096, bl.st) {
+        : user(bl),
+          b(Blas{bl.F, bl.ws, bl.ws.stream(0, 0), bl.launches}),
+          thr(std::max<size_t>(1, t)),
+          arena(8 * (m + n) + 4096, bl.ws.stream(0, 0)) {
+        b.ws.reset_events();
+        cudaEvent_t e = b.ws.event();  // critical stream starts after the caller's pending work
+        FFG_CUDA(cudaEventRecord(e, user.st));
+        FFG_CUDA(cudaStreamWaitEvent(b.st, e, 0));
+        static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
+        use_streams = !no_streams;
         uint32_t* dev = nullptr;
         // the base kernel writes rank + moved ranges straight into host-mapped memory
         info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4 + 2, &dev));
@@ -107,6 +119,25 @@ struct Driver {
     }
     ~Driver() {
         if (inv_arena) cudaFreeAsync(inv_arena, b.st);
+    }
+    // join the critical stream back into the caller's stream
+    void finish() {
+        cudaEvent_t e = b.ws.event();
+        FFG_CUDA(cudaEventRecord(e, b.st));
+        FFG_CUDA(cudaStreamWaitEvent(user.st, e, 0));
+    }
+    Blas on(cudaStream_t st) const { return Blas{b.F, b.ws, st, b.launches}; }
+    // a second critical-path stream per recursion depth (the node's independent TRSM), and a
+    // low-priority stream per depth for the look-ahead part of the trailing update
+    cudaStream_t twin(int depth) { return b.ws.stream(100 + depth, 0); }
+    cudaStream_t lookahead(int depth) { return b.ws.stream(200 + depth, 1); }
+    cudaEvent_t mark_event(cudaStream_t st) {
+        cudaEvent_t e = b.ws.event();
+        FFG_CUDA(cudaEventRecord(e, st));
+        return e;
+    }
+    void wait(cudaStream_t st, cudaEvent_t e) {
+        if (e) FFG_CUDA(cudaStreamWaitEvent(st, e, 0));
     }
 
     Factor* new_factor(size_t rank) {
@@ -137,17 +168,17 @@ struct Driver {
 
     // TRSMs of tile_rec always use a child's leading factor: walk its factor tree when every
     // leaf has cached inverses, else the generic blocked-inverse TRSM
-    void trsm_lower_unit(const NodeRes& c, DView L, DView B) {
+    void trsm_lower_unit(const Blas& bb, const NodeRes& c, DView L, DView B) {
         if (c.fac && c.fac->complete())
-            trsm_factor(b, 0, *c.fac, L, B);
+            trsm_factor(bb, 0, *c.fac, L, B);
         else
-            ftrsm_dev(b, 0, 0, 0, L, B, false);
+            ftrsm_dev(bb, 0, 0, 0, L, B, false);
     }
-    void trsm_upper_nonunit(const NodeRes& c, DView U, DView B) {
+    void trsm_upper_nonunit(const Blas& bb, const NodeRes& c, DView U, DView B) {
         if (c.fac && c.fac->complete())
-            trsm_factor(b, 1, *c.fac, U, B);
+            trsm_factor(bb, 1, *c.fac, U, B);
         else
-            ftrsm_dev(b, 1, 1, 1, U, B, false);
+            ftrsm_dev(bb, 1, 1, 1, U, B, false);
     }
 
     void apply(const NodeRes& c, int axis, DView v) {
@@ -157,6 +188,7 @@ struct Driver {
     }
 
     void gemm_sub(DView A, DView B, DView C) { b.gemm(b.F.p - 1, A, B, 1, C); }
+    void gemm_sub(const Blas& bb, DView A, DView B, DView C) { bb.gemm(bb.F.p - 1, A, B, 1, C); }
 
     // compose a child's permutation into this node's array at offset off
     void compose(uint32_t* arr, bool& init, size_t len, Range& acc, size_t off, const uint32_t* child,
@@ -179,17 +211,23 @@ struct Driver {
         acc.add(first, mid + cnt);
     }
 
-    NodeRes rec(DView a) {
+    // `pending`: work on the side streams that everything outside the top-left quadrant A1
+    // of `a` still depends on (the look-ahead part of the parent's trailing update)
+    NodeRes rec(DView a, int depth = 0, cudaEvent_t pending = nullptr) {
         const size_t m = a.rows, n = a.cols;
         NodeRes res;
         res.P = arena.alloc(std::max<size_t>(m, 1));
         res.Q = arena.alloc(std::max<size_t>(n, 1));
         if (m == 0 || n == 0) return res;                        // rankrev.hpp:91
-        if (std::min(m, n) <= thr) return base(a, res);          // :92
+        if (std::min(m, n) <= thr) {                             // :92
+            wait(b.st, pending);
+            return base(a, res);
+        }
         const size_t mark = arena.mark();
         const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;         // :95
 
-        NodeRes r1s = rec(a.sub(0, 0, m1, n1));                  // :97
+        NodeRes r1s = rec(a.sub(0, 0, m1, n1), depth + 1);       // :97
+        wait(b.st, pending);
         const size_t r1 = r1s.rank;
         apply(r1s, 0, a.sub(0, n1, m1, n - n1));                 // :99
         apply(r1s, 1, a.sub(m1, 0, m - m1, n1));                 // :100
@@ -202,16 +240,38 @@ struct Driver {
         DView Fb = a.sub(m1, 0, m - m1, r1);
         DView G = a.sub(m1, r1, m - m1, n1 - r1);
         DView H = a.sub(m1, n1, m - m1, n - n1);
+        cudaEvent_t pending_r = nullptr;
         if (r1 > 0) {                                            // :111-117
-            if (!D.empty()) trsm_lower_unit(r1s, L1, D);
-            if (!E.empty()) gemm_sub(M1, D, E);
-            if (!Fb.empty()) trsm_upper_nonunit(r1s, L1, Fb);
-            if (!G.empty() && !V1.empty()) gemm_sub(Fb, V1, G);
-            if (!H.empty()) gemm_sub(Fb, D, H);
+            // D = L1^-1 D and Fb = Fb U1^-1 are independent: Fb's chain runs on a twin stream
+            const bool fork = use_streams && !D.empty() && !Fb.empty();
+            const Blas side = fork ? on(twin(depth)) : b;
+            if (fork) wait(side.st, mark_event(b.st));
+            if (!D.empty()) trsm_lower_unit(b, r1s, L1, D);
+            if (!E.empty()) gemm_sub(b, M1, D, E);
+            if (!Fb.empty()) trsm_upper_nonunit(side, r1s, L1, Fb);
+            if (!G.empty() && !V1.empty()) gemm_sub(side, Fb, V1, G);
+            if (fork) wait(b.st, mark_event(side.st));
+            if (!H.empty()) {
+                // look-ahead: with E and G empty, R == H and R's recursion starts with its
+                // top-left quadrant; update that first on the critical stream, the rest on a
+                // low-priority stream that R waits for only after its first child
+                const size_t hm1 = (H.rows + 1) / 2, hn1 = (H.cols + 1) / 2;
+                if (use_streams && E.empty() && G.empty() && std::min(H.rows, H.cols) > thr) {
+                    gemm_sub(b, Fb.sub(0, 0, hm1, r1), D.sub(0, 0, r1, hn1), H.sub(0, 0, hm1, hn1));
+                    const Blas la = on(lookahead(depth));
+                    wait(la.st, mark_event(b.st));
+                    gemm_sub(la, Fb.sub(0, 0, hm1, r1), D.sub(0, hn1, r1, H.cols - hn1),
+                             H.sub(0, hn1, hm1, H.cols - hn1));
+                    gemm_sub(la, Fb.sub(hm1, 0, H.rows - hm1, r1), D, H.sub(hm1, 0, H.rows - hm1, H.cols));
+                    pending_r = mark_event(la.st);
+                } else {
+                    gemm_sub(b, Fb, D, H);
+                }
+            }
         }
 
-        NodeRes r2s = rec(E);                                    // :119-125 (E, G independent)
-        NodeRes r3s = rec(G);
+        NodeRes r2s = rec(E, depth + 1);                         // :119-125 (E, G independent)
+        NodeRes r3s = rec(G, depth + 1);
         const size_t r2 = r2s.rank, r3 = r3s.rank;
 
         apply(r2s, 0, a.sub(r1, 0, m1 - r1, r1));                // :128-133
@@ -230,8 +290,8 @@ struct Driver {
         DView N = a.sub(m1, n1 + r2, r3, n - n1 - r2);
         DView R = a.sub(m1 + r3, n1 + r2, m - m1 - r3, n - n1 - r2);
 
-        if (r2 > 0 && !I.empty()) trsm_upper_nonunit(r2s, U2, I);    // :144
-        if (r2 > 0 && !K.empty()) trsm_upper_nonunit(r2s, U2, K);    // :145
+        if (r2 > 0 && !I.empty()) trsm_upper_nonunit(b, r2s, U2, I);    // :144
+        if (r2 > 0 && !K.empty()) trsm_upper_nonunit(b, r2s, U2, K);    // :145
         uint32_t* jbuf = nullptr;
         DView J = I;
         if (r3 > 0 && !I.empty()) {                              // :146, J = L3^-1 I into a temporary
@@ -239,9 +299,9 @@ struct Driver {
             FFG_CUDA(cudaMemcpy2DAsync(jbuf, I.cols * 4, I.d, I.ld * 4, I.cols * 4, I.rows, cudaMemcpyDeviceToDevice,
                                        b.st));
             J = DView{jbuf, I.rows, I.cols, I.cols};
-            trsm_lower_unit(r3s, L3, J);
+            trsm_lower_unit(b, r3s, L3, J);
         }
-        if (r3 > 0 && !N.empty()) trsm_lower_unit(r3s, L3, N);       // :147
+        if (r3 > 0 && !N.empty()) trsm_lower_unit(b, r3s, L3, N);       // :147
         if (!N.empty() && !J.empty()) gemm_sub(J, V2, N);        // :148  O = N - J*V2
         if (!R.empty()) {                                        // :149-152
             if (!K.empty() && !V2.empty()) gemm_sub(K, V2, R);
@@ -249,7 +309,7 @@ struct Driver {
         }
         if (jbuf) FFG_CUDA(cudaFreeAsync(jbuf, b.st));
 
-        NodeRes r4s = rec(R);                                    // :154
+        NodeRes r4s = rec(R, depth + 1, pending_r);              // :154
         const size_t r4 = r4s.rank;
         apply(r4s, 0, a.sub(m1 + r3, 0, m - m1 - r3, r1 + r3));  // :156-161
         if (r2 > 0) apply(r4s, 0, a.sub(m1 + r3, n1, m - m1 - r3, r2));
@@ -304,6 +364,7 @@ struct Driver {
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
     Driver drv(b, threshold, a.rows, a.cols);
     NodeRes res = drv.rec(a);
+    drv.finish();
     drv.download(res, a.rows, a.cols, P, Q);
     return res.rank;
 }
@@ -311,6 +372,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
 size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q) {
     Driver drv(b, SIZE_MAX, a.rows, a.cols);
     NodeRes res = drv.rec(a);
+    drv.finish();
     drv.download(res, a.rows, a.cols, P, Q);
     return res.rank;
 }
