@@ -12,9 +12,11 @@ region; 1 GiB each, larger than L2, so no flush is needed).  The fgemm part
 of the metric (config 2, 8192^3 C <- C - A*B) is reported in the same line
 under "fgemm".
 
-N > 1 (torchrun, one process per GPU): every rank factors its own matrices --
-independent replicas, no data-path collective yet.
-value = all ranks' work / max-over-ranks device time; scaling "weak".
+N > 1 (torchrun, one process per GPU): the PLUQ workloads run PARTITIONED --
+all ranks factor the same matrix, each computing its slice of every large Schur
+GEMM/TRSM, exchanged with NCCL all-gathers (csrc/dist.cu, DESIGN.md "Multi-GPU");
+value = one matrix's work / max-over-ranks device time; scaling "strong".
+The fgemm workload runs as independent replicas (value = all ranks' work, "weak").
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 reference headers compiled unchanged + the rankrev.hpp:146 fix) on this box's
@@ -65,7 +67,9 @@ def workload_config(a, world):
     kind = "i.i.d. random_mat" if a.workload == "pluq" else f"L*R*U rank {a.n // 2}"
     cfgno = "3" if a.workload == "pluq" else "4"
     return {"workload": f"pluq_tile_recursive n={a.n} {kind} over GF({a.p}), threshold {a.thr} (BASELINE config {cfgno})",
-            "n": a.n, "p": a.p, "threshold": a.thr, "parallelism": f"replicas x{world}",
+            "n": a.n, "p": a.p, "threshold": a.thr,
+            "parallelism": "single GPU" if world == 1 else
+            f"partitioned x{world}: one matrix, replicated panel, Schur GEMM/TRSM output slices + NCCL all-gather",
             "l2": "inputs larger than L2 (a fresh 1 GiB matrix per step)"}
 
 
@@ -272,7 +276,12 @@ def our_arm(a, rank, world, local_rank):
             G.pluq_tile_recursive(p, mats[i], a.thr, ctx=ctx)
 
     # ---- inputs resident in HBM
-    seed0 = 1000 * rank + 1
+    # partitioned PLUQ: every rank holds the same matrix (same seeds) and owns slices of the
+    # large Schur operations; fgemm runs as independent replicas
+    partitioned = world > 1 and not is_fgemm
+    if partitioned:
+        G.dist.init_from_process_group(ctx)
+    seed0 = 1 if partitioned or world == 1 else 1000 * rank + 1
     if is_fgemm:
         mats = [make(seed0), make(seed0 + 1), make(seed0 + 2)]
     else:
@@ -286,7 +295,6 @@ def our_arm(a, rank, world, local_rank):
 
     # ---- timed region: exactly K steps
     launches0 = ctx.launches
-    ctx.profile(not a.no_prof)
     with ClockSampler(local_rank) as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -296,8 +304,6 @@ def our_arm(a, rank, world, local_rank):
             run_once(mats, a.warmup + i)
         e1.record(stream)
         barrier()
-    ctx.profile(False)
-    prof = ctx.profile_read()
     launches = ctx.launches - launches0
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -305,15 +311,35 @@ def our_arm(a, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ops_step = metric_ops(a)
-    value = world * a.steps * ops_step / (ms_max / 1e3) / 1e9
+    value = (1 if partitioned else world) * a.steps * ops_step / (ms_max / 1e3) / 1e9
     clocks = clk.summary()
+    # ---- per-kernel-class breakdown from ONE extra, untimed step with event profiling on
+    # (events around every launch perturb the schedule, so they stay out of the timed region)
+    prof, prof_ms = None, None
+    if not a.no_prof:
+        if is_fgemm:
+            pm = mats
+        else:
+            pm = [make(seed0 + 999)]
+            ctx.synchronize()
+        ctx.profile(True)
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        run_once(pm, 0)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        ctx.profile(False)
+        prof = ctx.profile_read()
+        prof_ms = p0.elapsed_time(p1)
+        del pm
     del mats
     torch.cuda.empty_cache()
 
     # ---- e2e through the public host API (pinned host buffers, copies inside the timed region)
     e2e = None
     if not a.no_e2e:
-        e2e = e2e_host(a, G, ctx, torch, np, dev, stream, rank, world)
+        e2e = e2e_host(a, G, ctx, torch, np, dev, stream, 0 if partitioned else rank, world, partitioned)
 
     # ---- secondary: fgemm config 2 alongside the PLUQ line
     fg = None
@@ -322,27 +348,35 @@ def our_arm(a, rank, world, local_rank):
 
     if rank != 0:
         return
-    peak = tensor_peak(torch)
-    g = prof["gemm"]
-    total_prof_ms = sum(v["ms"] for v in prof.values())
-    achieved = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roof = {"bound": "tensor", "kernel": "modgemm_kernel<L> (tcgen05 kind::i8 limb GEMM)",
-            "achieved": achieved, "peak": peak["int8_tops"], "unit": "TOPS (int8 tensor ops)",
-            "frac": achieved / peak["int8_tops"] if peak["int8_tops"] else None, "traffic": traffic,
-            "peak_source": peak["source"], "work_per_unit": "2*L^2 int8 ops per field MAC (L limbs)",
-            "gemm_launches": g["launches"], "gemm_ms": g["ms"],
-            "field_gops_in_gemm": g["field_ops"] / (g["ms"] / 1e3) / 1e9 if g["ms"] > 0 else None,
-            "share_of_step": g["ms"] / ms if ms else None,
-            "breakdown_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
-            "breakdown_launches": {k: v["launches"] for k, v in prof.items()},
-            "unprofiled_ms": round(ms - total_prof_ms, 3)}
+    roof = None
+    if prof is not None:
+        peak = tensor_peak(torch)
+        g = prof["gemm"]
+        total_prof_ms = sum(v["ms"] for v in prof.values())
+        achieved = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
+        # DRAM bytes per modgemm launch from an ncu capture of this same workload (see
+        # scripts/round_end.sh); null when no capture is committed
+        traffic, tfile = None, os.path.join(ROOT, "profiles", "pluq_gemm_traffic.json")
+        if os.path.exists(tfile) and not is_fgemm:
+            try:
+                tj = json.load(open(tfile))
+                if tj.get("n") == a.n and tj.get("p") == a.p and tj.get("threshold") == a.thr:
+                    traffic = tj.get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "tensor", "kernel": "modgemm_kernel<L> (tcgen05 kind::i8 limb GEMM)",
+                "achieved": achieved, "peak": peak["int8_tops"], "unit": "TOPS (int8 tensor ops)",
+                "frac": achieved / peak["int8_tops"] if peak["int8_tops"] else None, "traffic": traffic,
+                "peak_source": peak["source"], "work_per_unit": "2*L^2 int8 ops per field MAC (L limbs)",
+                "measured_on": "one extra untimed step with CUDA events around every launch "
+                               "(on each launch's own stream)",
+                "profiled_step_ms": prof_ms,
+                "gemm_launches": g["launches"], "gemm_ms": g["ms"],
+                "field_gops_in_gemm": g["field_ops"] / (g["ms"] / 1e3) / 1e9 if g["ms"] > 0 else None,
+                "share_of_step": g["ms"] / prof_ms if prof_ms else None,
+                "breakdown_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+                "breakdown_launches": {k: v["launches"] for k, v in prof.items()},
+                "overlap_or_gaps_ms": round(prof_ms - total_prof_ms, 3)}
     cpu = None
     if not a.no_cpu:
         try:
@@ -351,7 +385,8 @@ def our_arm(a, rank, world, local_rank):
             cpu = {"value": None, "unit": "Gop/s", "error": str(ex)[:200]}
     line = {"metric": METRIC_FGEMM if is_fgemm else METRIC, "value": value, "unit": "Gop/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32 residues (u8 limbs on tcgen05, s32 accum)",
+            "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
+            "dtype": "u32 residues (u8 limbs on tcgen05, s32 accum)",
             "data": "synthetic (seeded SplitMix64 random_mat / L*R*U, generated in HBM)",
             "config": workload_config(a, world), "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "roofline": roof, "cpu_baseline": cpu}
@@ -360,7 +395,7 @@ def our_arm(a, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
-def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world):
+def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world, partitioned=False):
     """Same metric through the host API: pinned host matrix -> ffg_* host entry point -> host result."""
     import torch.distributed as dist
     n, p = a.n, a.p
@@ -422,7 +457,8 @@ def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"value": world * metric_ops(a) / (ms / 1e3) / 1e9, "unit": "Gop/s", "h2d_bytes_per_step": h2d,
+    return {"value": (1 if partitioned else world) * metric_ops(a) / (ms / 1e3) / 1e9, "unit": "Gop/s",
+            "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
             "api": "ffg_fgemm (host buffers)" if a.workload == "fgemm" else "ffg_pluq_tile_recursive (host buffers)",
             "host_memory": "pinned"}
@@ -454,10 +490,17 @@ def fgemm_secondary(a, G, ctx, torch, dev, stream):
     del mats, A, B, C_
     torch.cuda.empty_cache()
     g = prof["gemm"]
+    traffic = algo = None  # ncu DRAM bytes of this launch (profiles/gemm_traffic.json)
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
+        traffic, algo = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
+    except Exception:
+        pass
     return {"metric": METRIC_FGEMM, "config": f"BASELINE config 2: M=N=K={n}, C <- C - A*B mod {p}",
             "value": 2.0 * n ** 3 / (ms / 1e3) / 1e9, "unit": "Gop/s", "ms_per_call": ms,
             "gemm_kernel_ms": g["ms"] / reps, "split_ms": prof["split"]["ms"] / reps,
-            "int8_tops_in_kernel": g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] else None}
+            "int8_tops_in_kernel": g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] else None,
+            "traffic": traffic, "algorithmic_bytes": algo}
 
 
 def cpu_baseline(a):

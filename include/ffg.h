@@ -133,6 +133,28 @@ uint64_t ffg_launch_count(ffg_ctx *ctx);
 int ffg_profile_enable(ffg_ctx *ctx, int on);
 int ffg_profile_read(ffg_ctx *ctx, double *out, int nclasses);
 
+/* ---- multi-GPU: partitioned PLUQ, one process per GPU ---------------------
+ * No reference counterpart (the reference parallelises over threads of one
+ * host: pool.hpp, pfgemm/pftrsm in blas.hpp:117-153, 401-419); this is the
+ * north_star's "trailing update partitioned across the GPUs of one box".
+ * After ffg_dist_init on every rank (same world, distinct ranks, the same id
+ * from ffg_dist_unique_id on one rank), ffg_pluq_tile_recursive[_dev] called
+ * by all ranks on identical inputs returns identical outputs on every rank:
+ * each Schur GEMM/TRSM of at least min_work MACs is split into per-rank
+ * output slices, exchanged with one NCCL all-gather; everything smaller runs
+ * replicated.  NCCL (libnccl.so.2) is loaded on first use.
+ * ffg_dist_init_virtual: one process computes every slice of a world of that
+ * size on its own GPU (no exchange) -- the single-GPU check of the partition;
+ * loopback != 0 also routes every slice through the exchange's pack/unpack.
+ * ffg_dist_partition: slice [lo, hi) of `total` for rank (pure host function). */
+int ffg_dist_unique_id(unsigned char id[128]);
+int ffg_dist_init(ffg_ctx *ctx, int world, int rank, const unsigned char id[128]);
+int ffg_dist_init_virtual(ffg_ctx *ctx, int world, int loopback);
+int ffg_dist_set_min_work(ffg_ctx *ctx, uint64_t macs);
+int ffg_dist_info(ffg_ctx *ctx, int *world, int *rank, int *is_virtual, uint64_t *exchanges, uint64_t *bytes);
+int ffg_dist_finalize(ffg_ctx *ctx);
+int ffg_dist_partition(size_t total, int world, int rank, size_t align, size_t *lo, size_t *hi);
+
 #ifdef __cplusplus
 }
 #endif

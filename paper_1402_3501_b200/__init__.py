@@ -13,6 +13,8 @@ from .ffpluq import (  # noqa: F401
     PluqResult,
     SingularDiagonal,
     default_context,
+    dist_partition,
+    dist_unique_id,
     fgemm,
     field_info,
     ftrsm,
@@ -22,3 +24,4 @@ from .ffpluq import (  # noqa: F401
     pluq_tile_recursive,
     rr_base,
 )
+from . import dist  # noqa: F401,E402

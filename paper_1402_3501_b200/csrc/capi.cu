@@ -237,13 +237,9 @@ int ffg_pluq_tile_recursive(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, siz
                             uint32_t* P, uint32_t* Q, size_t* rank) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
-        cudaStream_t st = ctx->stream;
-        DevMat dA(m, n, st);
-        dA.upload(A, lda);
-        ffg::Blas blas{F, ctx->ws, st, &ctx->launches};
-        size_t r = ffg::pluq_tile_recursive_dev(blas, dA.view(), threshold, P, Q);
-        dA.download(A, lda);
-        FFG_CUDA(cudaStreamSynchronize(st));
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        if (lda < n) throw ffg::Error(FFG_ERR_INVALID_DIM, "pluq: lda < n");
+        size_t r = ffg::pluq_tile_recursive_host(blas, A, m, n, lda, threshold, P, Q);
         if (rank) *rank = r;
     });
 }
@@ -270,6 +266,69 @@ int ffg_apply_perm_dev(ffg_ctx* ctx, uint32_t* A, size_t m, size_t n, size_t lda
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
         ffg::apply_perm_dev(blas, ffg::DView{A, m, n, lda}, axis, inverse, perm);
     });
+}
+
+int ffg_dist_unique_id(unsigned char id[128]) {
+    if (!id) return FFG_ERR_INVALID_ARG;
+    try {
+        ffg::nccl_unique_id(id);
+        return FFG_OK;
+    } catch (const ffg::Error& e) {
+        g_err = e.what();
+        return e.code;
+    }
+}
+
+int ffg_dist_init(ffg_ctx* ctx, int world, int rank, const unsigned char id[128]) {
+    return guarded(ctx, [&] {
+        if (!id) throw ffg::Error(FFG_ERR_INVALID_ARG, "dist: null unique id");
+        FFG_CUDA(cudaStreamSynchronize(ctx->stream));
+        ffg::dist_init_nccl(ctx->ws.dist, world, rank, id, ctx->device);
+    });
+}
+
+int ffg_dist_init_virtual(ffg_ctx* ctx, int world, int loopback) {
+    return guarded(ctx, [&] {
+        if (world < 1) throw ffg::Error(FFG_ERR_INVALID_ARG, "dist: world must be >= 1");
+        FFG_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->ws.dist.reset();
+        ctx->ws.dist.world = world;
+        ctx->ws.dist.virt = world > 1;
+        ctx->ws.dist.loopback = world > 1 && loopback != 0;
+    });
+}
+
+int ffg_dist_set_min_work(ffg_ctx* ctx, uint64_t macs) {
+    return guarded(ctx, [&] { ctx->ws.dist.min_work = macs; });
+}
+
+int ffg_dist_info(ffg_ctx* ctx, int* world, int* rank, int* is_virtual, uint64_t* exchanges, uint64_t* bytes) {
+    return guarded(ctx, [&] {
+        const ffg::Dist& d = ctx->ws.dist;
+        if (world) *world = d.world;
+        if (rank) *rank = d.rank;
+        if (is_virtual) *is_virtual = d.virt ? 1 : 0;
+        if (exchanges) *exchanges = d.exchanges;
+        if (bytes) *bytes = d.bytes;
+    });
+}
+
+int ffg_dist_finalize(ffg_ctx* ctx) {
+    return guarded(ctx, [&] {
+        FFG_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->ws.dist.reset();
+    });
+}
+
+int ffg_dist_partition(size_t total, int world, int rank, size_t align, size_t* lo, size_t* hi) {
+    if (world < 1 || rank < 0 || rank >= world || !lo || !hi) {
+        g_err = "dist: bad partition arguments";
+        return FFG_ERR_INVALID_ARG;
+    }
+    const ffg::Slice s = ffg::partition(total, world, rank, align);
+    *lo = s.lo;
+    *hi = s.hi;
+    return FFG_OK;
 }
 
 }  // extern "C"

@@ -575,7 +575,10 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         return a0 < b1 && b0 < a1;
     };
     // the CUDA-core kernel reads operands while other CTAs write C: only when C aliases nothing
-    if (use_simt(M, N, K) && !overlap(C, A) && !overlap(C, B)) {
+    const bool simt = use_simt(M, N, K) && !overlap(C, A) && !overlap(C, B);
+    static const bool log = getenv("FFG_GEMM_LOG") != nullptr;
+    if (log) fprintf(stderr, "FFG_GEMM %zu %zu %zu %d\n", M, N, K, (int)simt);
+    if (simt) {
         ws.prof.begin(st);
         dim3 g((unsigned)ceil_div(N, SG_T), (unsigned)ceil_div(M, SG_T));
         modgemm_simt_kernel<<<g, 256, 0, st>>>(A.d, A.ld, B.d, B.ld, C.d, C.ld, (uint32_t)M, (uint32_t)N, (uint32_t)K,

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "dist.cuh"
 
 namespace ffg {
 
@@ -94,6 +95,7 @@ private:
 class Workspace {
 public:
     Profiler prof;
+    Dist dist;  // multi-GPU partitioning of the recursion's large operations (dist.cuh)
     ~Workspace() {
         for (auto& kv : bufs_)
             if (kv.second.ptr) cudaFree(kv.second.ptr);

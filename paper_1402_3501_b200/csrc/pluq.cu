@@ -92,17 +92,33 @@ struct Driver {
 
     bool use_streams = true;
 
-    Driver(const Blas& bl, size_t t, size_t m, size_t n)
+    // host-pipelined entry (pluq_tile_recursive_host): the top-left spine of the recursion
+    // (the chain of first children from the root) starts on data already uploaded; spine[d]
+    // marks the upload of the depth-d spine block minus its first child's block
+    const uint32_t* spine_root = nullptr;
+    std::vector<cudaEvent_t> spine;
+    // early download of the root's top rows [0, m1), final once R's recursion starts unless R's
+    // permutations or the pivot-gather rotations reach back into them (top_touched)
+    struct EarlyTop {
+        bool armed = false, sent = false, top_touched = false;
+        cudaStream_t cs = nullptr;
+        uint32_t* host = nullptr;
+        size_t ldh = 0, rows = 0;
+    } early;
+
+    Driver(const Blas& bl, size_t t, size_t m, size_t n, bool keep_events = false)
         : user(bl),
           b(Blas{bl.F, bl.ws, bl.ws.stream(0, 0), bl.launches}),
           thr(std::max<size_t>(1, t)),
           arena(8 * (m + n) + 4096, bl.ws.stream(0, 0)) {
-        b.ws.reset_events();
+        if (!keep_events) b.ws.reset_events();
         cudaEvent_t e = b.ws.event();  // critical stream starts after the caller's pending work
         FFG_CUDA(cudaEventRecord(e, user.st));
         FFG_CUDA(cudaStreamWaitEvent(b.st, e, 0));
         static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
-        use_streams = !no_streams;
+        // partitioned (multi-GPU) runs keep one stream: every rank must issue its NCCL
+        // exchanges in the same order, and the replicated control flow guarantees that
+        use_streams = !no_streams && !bl.ws.dist.active();
         uint32_t* dev = nullptr;
         // the base kernel writes rank + moved ranges straight into host-mapped memory
         info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4 + 2, &dev));
@@ -190,6 +206,56 @@ struct Driver {
     void gemm_sub(DView A, DView B, DView C) { b.gemm(b.F.p - 1, A, B, 1, C); }
     void gemm_sub(const Blas& bb, DView A, DView B, DView C) { bb.gemm(bb.F.p - 1, A, B, 1, C); }
 
+    // ---- partitioned execution (dist.cuh): large operations split into per-rank output
+    // slices + one all-gather; small ones replicated.  Single-GPU runs take the plain calls.
+    static constexpr size_t kAlign = 128;  // slice granularity = the GEMM's M tile
+    bool split(double macs) const { return b.ws.dist.active() && macs >= (double)b.ws.dist.min_work; }
+    template <class Fn>
+    void slices(size_t total, Fn&& fn) {
+        const Dist& d = b.ws.dist;
+        for (int r = 0; r < d.world; ++r) {
+            if (!d.virt && r != d.rank) continue;
+            const Slice s = partition(total, d.world, r, kAlign);
+            if (s.hi > s.lo) fn(s.lo, s.hi - s.lo);
+        }
+    }
+    // C -= A B, split along C's longer side
+    void pgemm_sub(const Blas& bb, DView A, DView B, DView C) {
+        if (!split((double)C.rows * C.cols * A.cols)) {
+            gemm_sub(bb, A, B, C);
+            return;
+        }
+        const int axis = C.rows >= C.cols ? 0 : 1;
+        if (axis == 0)
+            slices(C.rows, [&](size_t lo, size_t len) {
+                gemm_sub(bb, A.sub(lo, 0, len, A.cols), B, C.sub(lo, 0, len, C.cols));
+            });
+        else
+            slices(C.cols, [&](size_t lo, size_t len) {
+                gemm_sub(bb, A, B.sub(0, lo, B.rows, len), C.sub(0, lo, C.rows, len));
+            });
+        dist_allgather(b.ws.dist, C.d, C.rows, C.cols, C.ld, axis, kAlign, bb.st);
+    }
+    // side 0: B <- L^-1 B (B's columns independent); side 1: B <- B U^-1 (B's rows independent)
+    void ptrsm(const Blas& bb, int side, const NodeRes& c, DView T, DView B) {
+        auto one = [&](DView X) {
+            if (side == 0)
+                trsm_lower_unit(bb, c, T, X);
+            else
+                trsm_upper_nonunit(bb, c, T, X);
+        };
+        const double w = side == 0 ? (double)B.cols : (double)B.rows;
+        if (!split(0.5 * (double)T.rows * T.rows * w)) {
+            one(B);
+            return;
+        }
+        if (side == 0)
+            slices(B.cols, [&](size_t lo, size_t len) { one(B.sub(0, lo, B.rows, len)); });
+        else
+            slices(B.rows, [&](size_t lo, size_t len) { one(B.sub(lo, 0, len, B.cols)); });
+        dist_allgather(b.ws.dist, B.d, B.rows, B.cols, B.ld, side == 0 ? 1 : 0, kAlign, bb.st);
+    }
+
     // compose a child's permutation into this node's array at offset off
     void compose(uint32_t* arr, bool& init, size_t len, Range& acc, size_t off, const uint32_t* child,
                  const Range& cr) {
@@ -226,7 +292,9 @@ struct Driver {
         const size_t mark = arena.mark();
         const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;         // :95
 
-        NodeRes r1s = rec(a.sub(0, 0, m1, n1), depth + 1);       // :97
+        cudaEvent_t spine_next = (spine_root && a.d == spine_root && (size_t)depth + 1 < spine.size())
+                                     ? spine[depth + 1] : nullptr;
+        NodeRes r1s = rec(a.sub(0, 0, m1, n1), depth + 1, spine_next);  // :97
         wait(b.st, pending);
         const size_t r1 = r1s.rank;
         apply(r1s, 0, a.sub(0, n1, m1, n - n1));                 // :99
@@ -246,10 +314,10 @@ struct Driver {
             const bool fork = use_streams && !D.empty() && !Fb.empty();
             const Blas side = fork ? on(twin(depth)) : b;
             if (fork) wait(side.st, mark_event(b.st));
-            if (!D.empty()) trsm_lower_unit(b, r1s, L1, D);
-            if (!E.empty()) gemm_sub(b, M1, D, E);
-            if (!Fb.empty()) trsm_upper_nonunit(side, r1s, L1, Fb);
-            if (!G.empty() && !V1.empty()) gemm_sub(side, Fb, V1, G);
+            if (!D.empty()) ptrsm(b, 0, r1s, L1, D);
+            if (!E.empty()) pgemm_sub(b, M1, D, E);
+            if (!Fb.empty()) ptrsm(side, 1, r1s, L1, Fb);
+            if (!G.empty() && !V1.empty()) pgemm_sub(side, Fb, V1, G);
             if (fork) wait(b.st, mark_event(side.st));
             if (!H.empty()) {
                 // look-ahead: with E and G empty, R == H and R's recursion starts with its
@@ -265,7 +333,7 @@ struct Driver {
                     gemm_sub(la, Fb.sub(hm1, 0, H.rows - hm1, r1), D, H.sub(hm1, 0, H.rows - hm1, H.cols));
                     pending_r = mark_event(la.st);
                 } else {
-                    gemm_sub(b, Fb, D, H);
+                    pgemm_sub(b, Fb, D, H);
                 }
             }
         }
@@ -290,8 +358,8 @@ struct Driver {
         DView N = a.sub(m1, n1 + r2, r3, n - n1 - r2);
         DView R = a.sub(m1 + r3, n1 + r2, m - m1 - r3, n - n1 - r2);
 
-        if (r2 > 0 && !I.empty()) trsm_upper_nonunit(b, r2s, U2, I);    // :144
-        if (r2 > 0 && !K.empty()) trsm_upper_nonunit(b, r2s, U2, K);    // :145
+        if (r2 > 0 && !I.empty()) ptrsm(b, 1, r2s, U2, I);      // :144
+        if (r2 > 0 && !K.empty()) ptrsm(b, 1, r2s, U2, K);      // :145
         uint32_t* jbuf = nullptr;
         DView J = I;
         if (r3 > 0 && !I.empty()) {                              // :146, J = L3^-1 I into a temporary
@@ -299,18 +367,29 @@ struct Driver {
             FFG_CUDA(cudaMemcpy2DAsync(jbuf, I.cols * 4, I.d, I.ld * 4, I.cols * 4, I.rows, cudaMemcpyDeviceToDevice,
                                        b.st));
             J = DView{jbuf, I.rows, I.cols, I.cols};
-            trsm_lower_unit(b, r3s, L3, J);
+            ptrsm(b, 0, r3s, L3, J);
         }
-        if (r3 > 0 && !N.empty()) trsm_lower_unit(b, r3s, L3, N);       // :147
-        if (!N.empty() && !J.empty()) gemm_sub(J, V2, N);        // :148  O = N - J*V2
+        if (r3 > 0 && !N.empty()) ptrsm(b, 0, r3s, L3, N);      // :147
+        if (!N.empty() && !J.empty()) pgemm_sub(b, J, V2, N);   // :148  O = N - J*V2
         if (!R.empty()) {                                        // :149-152
-            if (!K.empty() && !V2.empty()) gemm_sub(K, V2, R);
-            if (!N.empty()) gemm_sub(M3, N, R);
+            if (!K.empty() && !V2.empty()) pgemm_sub(b, K, V2, R);
+            if (!N.empty()) pgemm_sub(b, M3, N, R);
         }
         if (jbuf) FFG_CUDA(cudaFreeAsync(jbuf, b.st));
 
+        if (depth == 0 && early.armed && m1 > 0) {
+            // everything that writes rows [0, m1) before R's recursion is enqueued on b.st
+            wait(early.cs, mark_event(b.st));
+            FFG_CUDA(cudaMemcpy2DAsync(early.host, early.ldh * 4, a.d, a.ld * 4, n * 4, m1, cudaMemcpyDeviceToHost,
+                                       early.cs));
+            early.sent = true;
+            early.rows = m1;
+        }
         NodeRes r4s = rec(R, depth + 1, pending_r);              // :154
         const size_t r4 = r4s.rank;
+        if (depth == 0 && early.sent)  // the steps below that can still write rows [0, m1)
+            early.top_touched = (!r4s.qr.empty() && r1 + r2 > 0) || (m1 != r1 + r2 && r3 + r4 > 0) ||
+                                (n1 != r1 && r2 > 0) || (n1 + r2 != r1 + r2 + r3 && r4 > 0);
         apply(r4s, 0, a.sub(m1 + r3, 0, m - m1 - r3, r1 + r3));  // :156-161
         if (r2 > 0) apply(r4s, 0, a.sub(m1 + r3, n1, m - m1 - r3, r2));
         apply(r4s, 1, a.sub(0, n1 + r2, r1, n - n1 - r2));
@@ -367,6 +446,71 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
     drv.finish();
     drv.download(res, a.rows, a.cols, P, Q);
     return res.rank;
+}
+
+size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t n, size_t lda, size_t threshold,
+                                uint32_t* P, uint32_t* Q) {
+    if (m == 0 || n == 0) {
+        Driver drv(b, threshold, m, n);
+        NodeRes res = drv.rec(DView{nullptr, m, n, n});
+        drv.finish();
+        drv.download(res, m, n, P, Q);
+        return 0;
+    }
+    const size_t thr = std::max<size_t>(1, threshold);
+    cudaStream_t cs = b.ws.stream(300, 0);  // copy stream
+    uint32_t* d = nullptr;
+    FFG_CUDA(cudaMallocAsync(&d, m * n * 4, b.st));
+    b.ws.reset_events();
+    auto record = [&](cudaStream_t st) {
+        cudaEvent_t e = b.ws.event();
+        FFG_CUDA(cudaEventRecord(e, st));
+        return e;
+    };
+    FFG_CUDA(cudaStreamWaitEvent(cs, record(b.st), 0));
+    auto up = [&](size_t r0, size_t c0, size_t rows, size_t cols) {
+        if (rows && cols)
+            FFG_CUDA(cudaMemcpy2DAsync(d + r0 * n + c0, n * 4, host + r0 * lda + c0, lda * 4, cols * 4, rows,
+                                       cudaMemcpyHostToDevice, cs));
+    };
+    // spine blocks S_0 = whole matrix, S_{d+1} = top-left ceil-halves, down to ~16 MB or a leaf
+    std::vector<std::pair<size_t, size_t>> sp{{m, n}};
+    while (std::min(sp.back().first, sp.back().second) > thr && sp.back().first * sp.back().second > (size_t(1) << 22))
+        sp.push_back({(sp.back().first + 1) / 2, (sp.back().second + 1) / 2});
+    const size_t K = sp.size() - 1;
+    up(0, 0, sp[K].first, sp[K].second);
+    FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));  // the deepest spine block is in place
+    std::vector<cudaEvent_t> spine(K, nullptr);
+    for (size_t lv = K; lv-- > 0;) {  // S_lv minus S_{lv+1}: right strip, then the rows below
+        up(0, sp[lv + 1].second, sp[lv + 1].first, sp[lv].second - sp[lv + 1].second);
+        up(sp[lv + 1].first, 0, sp[lv].first - sp[lv + 1].first, sp[lv].second);
+        spine[lv] = record(cs);
+    }
+    size_t rank = 0;
+    {
+        // the Driver resets the event cursor: keep the events above alive by recording after it
+        Driver drv(b, thr, m, n, /*keep_events=*/true);
+        drv.spine_root = d;
+        drv.spine = spine;
+        drv.early.armed = true;
+        drv.early.cs = cs;
+        drv.early.host = host;
+        drv.early.ldh = lda;
+        NodeRes res = drv.rec(DView{d, m, n, n}, 0, K > 0 ? spine[0] : nullptr);
+        drv.finish();
+        const size_t r0 = drv.early.sent && !drv.early.top_touched ? drv.early.rows : 0;
+        // after the early copy: both write the host buffer (and share the D2H engine anyway)
+        if (drv.early.sent) FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));
+        if (m > r0)
+            FFG_CUDA(cudaMemcpy2DAsync(host + r0 * lda, lda * 4, d + r0 * n, n * 4, n * 4, m - r0,
+                                       cudaMemcpyDeviceToHost, b.st));
+        drv.download(res, m, n, P, Q);  // synchronizes the critical stream
+        FFG_CUDA(cudaStreamSynchronize(cs));
+        FFG_CUDA(cudaStreamSynchronize(b.st));
+        rank = res.rank;
+    }
+    FFG_CUDA(cudaFreeAsync(d, b.st));
+    return rank;
 }
 
 size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q) {

@@ -30,6 +30,12 @@ struct Blas {
 // scans the diagonal first (nonunit) and throws SingularDiagonal(i) like blas.hpp:291-297.
 void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bool check_diag);
 
+// pluq_tile_recursive on a HOST matrix (ld lda), pipelined: the recursion's top-left spine
+// starts while the rest uploads, the root's finished top rows download while its trailing
+// block recurses.  Same outputs as the device entry.
+size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t n, size_t lda, size_t threshold,
+                                uint32_t* P, uint32_t* Q);
+
 // rr_base (rankrev.hpp:29-78) on a device block; P/Q host arrays (to_array semantics).
 size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q);
 

@@ -12,6 +12,74 @@
 
 namespace ffg {
 
+// One doubling level (block size BS = 2h) of tri_inverse_smem, sizes compile-time so the
+// index arithmetic is shifts.  A thread owns 4 consecutive rows x 1 column of an h x h
+// product: one load of the shared operand column feeds four exact u64 accumulators.
+template <bool UPPER, int R, int BS>
+__device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, uint32_t* X, int xs, uint32_t* W,
+                                                   uint32_t t, uint32_t p, uint64_t mu) {
+    if constexpr (BS <= R) {
+        constexpr uint32_t h = BS / 2, nblk = R / BS, per_blk = (h / 4) * h;
+        const uint32_t tid = threadIdx.x, nth = blockDim.x;
+        for (uint32_t tile = tid; tile < nblk * per_blk; tile += nth) {
+            const uint32_t blk = tile / per_blk, e = tile % per_blk, i0 = (e / h) * 4, c = e % h, ob = blk * BS;
+            uint64_t s[4] = {0, 0, 0, 0};
+            if (!UPPER) {  // W = L21 X11 (X11 lower: k >= c); rows/cols >= t contribute nothing
+                const uint32_t row0 = ob + h + i0;
+                const uint32_t kend = t > ob ? min(h, t - ob) : 0u;
+                for (uint32_t k = c; k < kend; ++k) {
+                    const uint64_t xk = X[(ob + k) * xs + ob + c];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) s[a] += (uint64_t)S[(row0 + a) * ss + ob + k] * xk;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) W[blk * h * h + (i0 + a) * h + c] = row0 + a < t ? mod_u64(s[a], p, mu) : 0u;
+            } else {  // W = U12 X22 (X22 upper: k <= c)
+                const uint32_t row0 = ob + i0;
+                const uint32_t kend = t > ob + h ? min(c + 1, t - ob - h) : 0u;
+                for (uint32_t k = 0; k < kend; ++k) {
+                    const uint64_t xk = X[(ob + h + k) * xs + ob + h + c];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) s[a] += (uint64_t)S[(row0 + a) * ss + ob + h + k] * xk;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) W[blk * h * h + (i0 + a) * h + c] = row0 + a < t ? mod_u64(s[a], p, mu) : 0u;
+            }
+        }
+        __syncthreads();
+        for (uint32_t tile = tid; tile < nblk * per_blk; tile += nth) {
+            const uint32_t blk = tile / per_blk, e = tile % per_blk, i0 = (e / h) * 4, c = e % h, ob = blk * BS;
+            const uint32_t* w = W + blk * h * h;
+            uint64_t s[4] = {0, 0, 0, 0};
+            if (!UPPER) {  // X21 = -X22 W (X22 lower: k <= i; the zeros above its diagonal pad)
+                for (uint32_t k = 0; k < i0 + 4; ++k) {
+                    const uint64_t wk = w[k * h + c];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) s[a] += (uint64_t)X[(ob + h + i0 + a) * xs + ob + h + k] * wk;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const uint32_t v = mod_u64(s[a], p, mu);
+                    X[(ob + h + i0 + a) * xs + ob + c] = v ? p - v : 0u;
+                }
+            } else {  // X12 = -X11 W (X11 upper: k >= i)
+                for (uint32_t k = i0; k < h; ++k) {
+                    const uint64_t wk = w[k * h + c];
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) s[a] += (uint64_t)X[(ob + i0 + a) * xs + ob + k] * wk;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const uint32_t v = mod_u64(s[a], p, mu);
+                    X[(ob + i0 + a) * xs + ob + h + c] = v ? p - v : 0u;
+                }
+            }
+        }
+        __syncthreads();
+        tri_inverse_levels<UPPER, R, BS * 2>(S, ss, X, xs, W, t, p, mu);
+    }
+}
+
 template <bool UPPER, int R>
 __device__ void tri_inverse_smem(const uint32_t* S, int ss, uint32_t* X, int xs, uint32_t* W, uint32_t* dinv, uint32_t t,
                                  uint32_t p, uint64_t mu) {
@@ -55,41 +123,7 @@ __device__ void tri_inverse_smem(const uint32_t* S, int ss, uint32_t* X, int xs,
         for (int i = 0; i < LEAF; ++i) X[(base + i) * xs + base + j] = x[i];
     }
     __syncthreads();
-    for (uint32_t b = 2 * LEAF; b <= (uint32_t)R; b *= 2) {
-        const uint32_t h = b / 2, nblk = R / b, per = h * h;
-        for (uint32_t idx = tid; idx < nblk * per; idx += nth) {
-            const uint32_t blk = idx / per, e = idx % per, i = e / h, c = e % h, ob = blk * b;
-            uint64_t s = 0;
-            if (!UPPER) {  // W = L21 X11 (X11 lower: k >= c)
-                const uint32_t row = ob + h + i;
-                if (row < t)
-                    for (uint32_t k = c; k < h; ++k)
-                        if (ob + k < t) s += (uint64_t)S[row * ss + ob + k] * X[(ob + k) * xs + ob + c];
-            } else {  // W = U12 X22 (X22 upper: k <= c)
-                const uint32_t row = ob + i;
-                if (row < t)
-                    for (uint32_t k = 0; k <= c; ++k)
-                        if (ob + h + k < t) s += (uint64_t)S[row * ss + ob + h + k] * X[(ob + h + k) * xs + ob + h + c];
-            }
-            W[blk * per + i * h + c] = mod_u64(s, p, mu);
-        }
-        __syncthreads();
-        for (uint32_t idx = tid; idx < nblk * per; idx += nth) {
-            const uint32_t blk = idx / per, e = idx % per, i = e / h, c = e % h, ob = blk * b;
-            const uint32_t* w = W + blk * per;
-            uint64_t s = 0;
-            if (!UPPER) {  // X21 = -X22 W (X22 lower: k <= i)
-                for (uint32_t k = 0; k <= i; ++k) s += (uint64_t)X[(ob + h + i) * xs + ob + h + k] * w[k * h + c];
-                const uint32_t v = mod_u64(s, p, mu);
-                X[(ob + h + i) * xs + ob + c] = v ? p - v : 0u;
-            } else {  // X12 = -X11 W (X11 upper: k >= i)
-                for (uint32_t k = i; k < h; ++k) s += (uint64_t)X[(ob + i) * xs + ob + k] * w[k * h + c];
-                const uint32_t v = mod_u64(s, p, mu);
-                X[(ob + i) * xs + ob + h + c] = v ? p - v : 0u;
-            }
-        }
-        __syncthreads();
-    }
+    tri_inverse_levels<UPPER, R, 2 * LEAF>(S, ss, X, xs, W, t, p, mu);
 }
 
 }  // namespace ffg

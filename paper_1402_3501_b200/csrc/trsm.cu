@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "pluq.cuh"
+#include "triinv.cuh"
 
 namespace ffg {
 
@@ -371,6 +372,120 @@ __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restr
     }
 }
 
+// Fused small TRSM (t <= R <= 128): every CTA inverts the triangle in shared memory
+// (tri_inverse_smem, log depth) and applies it to its own 64 vectors in place --
+// one launch instead of inverse + limb split + tensor GEMM.  The inverse is recomputed per
+// CTA, which is cheap next to the launch chain it replaces for the small TRSMs of the
+// bottom recursion levels.
+template <int SIDE, bool UPPER, bool UNIT, int R>
+__global__ void __launch_bounds__(512) trsm_fused_kernel(const uint32_t* __restrict__ T, uint64_t ldt, uint32_t t,
+                                                         uint32_t* __restrict__ B, uint64_t ldb, uint32_t nvec,
+                                                         uint32_t p, uint64_t mu) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    constexpr int RS = R + 1;
+    uint32_t* Ts = sm;              // R x RS triangle, later the vector strip (R x 65)
+    uint32_t* Xs = Ts + R * RS;     // R x RS inverse
+    uint32_t* Ws = Xs + R * RS;     // (R/2)^2
+    uint32_t* dv = Ws + (R / 2) * (R / 2);
+    const uint32_t tid = threadIdx.x, v0 = blockIdx.x * LA;
+    const uint32_t nv = min((uint32_t)LA, nvec - v0);
+    for (uint32_t idx = tid; idx < t * t; idx += 512) {
+        const uint32_t i = idx / t, k = idx % t;
+        Ts[i * RS + k] = T[(uint64_t)i * ldt + k];
+    }
+    __syncthreads();
+    if (UNIT) {
+        tri_inverse_smem<false, R>(Ts, RS, Xs, RS, Ws, dv, t, p, mu);  // unit lower
+    } else {
+        tri_inverse_smem<true, R>(Ts, RS, Xs, RS, Ws, dv, t, p, mu);   // upper (tile_rec's pair)
+    }
+    // vectors into the triangle's frame: Bs[k][v]
+    uint32_t* Bs = Ts;
+    if (SIDE == 0) {
+        for (uint32_t idx = tid; idx < t * LA; idx += 512) {
+            const uint32_t k = idx / LA, v = idx % LA;
+            Bs[k * (LA + 1) + v] = v < nv ? B[(uint64_t)k * ldb + v0 + v] : 0u;
+        }
+    } else {
+        for (uint32_t idx = tid; idx < t * LA; idx += 512) {
+            const uint32_t v = idx / t, k = idx % t;
+            Bs[k * (LA + 1) + v] = v < nv ? B[(uint64_t)(v0 + v) * ldb + k] : 0u;
+        }
+    }
+    __syncthreads();
+    // out(i, v) = sum_k C[i][k] Bs[k][v], C = X (left) or X^T (right); 512 threads = 32 row
+    // groups x 16 vector groups, each R/32 rows x 4 vectors
+    constexpr int RPT = R / 32;
+    const uint32_t tr = tid / 16, tv = tid % 16;
+    uint64_t acc[RPT][4];
+#pragma unroll
+    for (int a = 0; a < RPT; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[a][q] = 0;
+    for (uint32_t k = 0; k < t; ++k) {
+        uint32_t x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = Bs[k * (LA + 1) + tv * 4 + q];
+#pragma unroll
+        for (int a = 0; a < RPT; ++a) {
+            const uint32_t i = tr * RPT + a;
+            const uint32_t c = SIDE == 0 ? Xs[i * RS + k] : Xs[k * RS + i];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[a][q] += (uint64_t)c * x[q];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < RPT; ++a) {
+        const uint32_t i = tr * RPT + a;
+        if (i >= t) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t v = tv * 4 + q;
+            if (v >= nv) continue;
+            const uint32_t val = mod_u64(acc[a][q], p, mu);
+            if (SIDE == 0)
+                B[(uint64_t)i * ldb + v0 + v] = val;
+            else
+                B[(uint64_t)(v0 + v) * ldb + i] = val;
+        }
+    }
+}
+
+template <int R>
+void trsm_fused_launch(const Blas& b, int side, int upper, int unit, DView T, DView B) {
+    const size_t nvec = side == 0 ? B.cols : B.rows;
+    const size_t smem = (2 * R * (R + 1) + (R / 2) * (R / 2) + R + 4) * sizeof(uint32_t);
+    using K = void (*)(const uint32_t*, uint64_t, uint32_t, uint32_t*, uint64_t, uint32_t, uint32_t, uint64_t);
+    // tile_rec pairs: (left, lower, unit) and (right, upper, nonunit); others use the generic path
+    K k = side == 0 ? trsm_fused_kernel<0, false, true, R> : trsm_fused_kernel<1, true, false, R>;
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        FFG_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<0, false, true, R>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FFG_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<1, true, false, R>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    });
+    b.ws.prof.begin(b.st);
+    k<<<(unsigned)ceil_div(nvec, LA), 512, smem, b.st>>>(T.d, T.ld, (uint32_t)T.rows, B.d, B.ld, (uint32_t)nvec,
+                                                         b.F.p, b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)T.rows * nvec);
+    b.count();
+}
+
+// true when the fused kernel handled the solve
+bool trsm_fused(const Blas& b, int side, int upper, int unit, DView T, DView B) {
+    static const bool off = getenv("FFG_NO_FUSED_TRSM") && atoi(getenv("FFG_NO_FUSED_TRSM")) != 0;
+    if (off) return false;
+    const bool pair = (side == 0 && !upper && unit) || (side == 1 && upper && !unit);
+    if (!pair || T.rows > 128 || T.rows == 0) return false;
+    if (T.rows <= 64)
+        trsm_fused_launch<64>(b, side, upper, unit, T, B);
+    else
+        trsm_fused_launch<128>(b, side, upper, unit, T, B);
+    return true;
+}
+
 bool Factor::complete() const {
     if (invL) return true;
     if (kids.empty()) return rank == 0;
@@ -522,6 +637,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
                         h);
     }
     const int upper = uplo == 1, unit = diag == 0;
+    if (trsm_fused(b, side, upper, unit, A, B)) return;
     static const bool inverse_leaves = !(getenv("FFG_TRSM_DIRECT") && atoi(getenv("FFG_TRSM_DIRECT")) != 0);
     if (!inverse_leaves) {  // default: direct CUDA-core leaves, tensor-core Schur updates between them
         TrsmCtx c{b, side, upper, unit, A, nullptr};

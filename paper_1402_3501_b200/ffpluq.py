@@ -111,6 +111,14 @@ def lib() -> C.CDLL:
         L.ffg_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.c_int]
         L.ffg_random_mat_dev.argtypes = [vp, u64, u64, vp, sz, sz, sz]
         L.ffg_lru_matrix_dev.argtypes = [vp, u64, u64, vp, sz, sz, sz, vp, vp]
+        L.ffg_dist_unique_id.argtypes = [C.c_char_p]
+        L.ffg_dist_init.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
+        L.ffg_dist_init_virtual.argtypes = [vp, C.c_int, C.c_int]
+        L.ffg_dist_set_min_work.argtypes = [vp, u64]
+        L.ffg_dist_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(u64), C.POINTER(u64)]
+        L.ffg_dist_finalize.argtypes = [vp]
+        L.ffg_dist_partition.argtypes = [sz, C.c_int, C.c_int, sz, C.POINTER(sz), C.POINTER(sz)]
         _lib = L
     return _lib
 
@@ -161,6 +169,32 @@ class Context:
         return {k: {"ms": buf[4 * i], "launches": int(buf[4 * i + 1]), "work": buf[4 * i + 2],
                     "field_ops": buf[4 * i + 3]} for i, k in enumerate(self.PROFILE_CLASSES)}
 
+    # ---- multi-GPU (include/ffg.h ffg_dist_*): partitioned PLUQ, one process per GPU
+    def dist_init(self, world: int, rank: int, unique_id: bytes) -> None:
+        """Join a world of `world` ranks (NCCL); `unique_id` from dist_unique_id() on one rank."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        _nccl_hint()
+        _check(lib().ffg_dist_init(self._h, world, rank, C.c_char_p(bytes(unique_id))))
+
+    def dist_init_virtual(self, world: int, loopback: bool = False) -> None:
+        """Compute every slice of a `world`-rank partition in this process (single-GPU check);
+        loopback also sends each slice through the exchange's pack/unpack staging."""
+        _check(lib().ffg_dist_init_virtual(self._h, world, 1 if loopback else 0))
+
+    def dist_set_min_work(self, macs: int) -> None:
+        _check(lib().ffg_dist_set_min_work(self._h, macs))
+
+    def dist_info(self) -> dict:
+        w, r, v = C.c_int(0), C.c_int(0), C.c_int(0)
+        ex, by = C.c_uint64(0), C.c_uint64(0)
+        _check(lib().ffg_dist_info(self._h, C.byref(w), C.byref(r), C.byref(v), C.byref(ex), C.byref(by)))
+        return {"world": w.value, "rank": r.value, "virtual": bool(v.value), "exchanges": ex.value,
+                "bytes": by.value}
+
+    def dist_finalize(self) -> None:
+        _check(lib().ffg_dist_finalize(self._h))
+
     def close(self) -> None:
         if self._h:
             lib().ffg_destroy(self._h)
@@ -189,6 +223,38 @@ def field_info(p: int) -> dict:
     kmax = C.c_uint64(0)
     _check(lib().ffg_field_info(p, C.byref(limbs), C.byref(kmax), C.byref(nt)))
     return {"limbs": limbs.value, "kmax": kmax.value, "nt": nt.value}
+
+
+def _nccl_hint() -> None:
+    """Point the library's NCCL loader at the copy torch bundles (nvidia-nccl wheel) so a later
+    `import torch` in this process reuses it instead of clashing with an older system copy."""
+    if "FFG_NCCL_LIB" in os.environ:
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for d in (list(spec.submodule_search_locations or []) if spec else []):
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["FFG_NCCL_LIB"] = cand
+            return
+
+
+def dist_unique_id() -> bytes:
+    """NCCL unique id (128 bytes) to broadcast to every rank before Context.dist_init."""
+    _nccl_hint()
+    buf = C.create_string_buffer(128)
+    _check(lib().ffg_dist_unique_id(buf))
+    return buf.raw
+
+
+def dist_partition(total: int, world: int, rank: int, align: int = 128) -> tuple[int, int]:
+    """Slice [lo, hi) of `total` rows/columns owned by `rank` (the library's own partition)."""
+    lo, hi = C.c_size_t(0), C.c_size_t(0)
+    _check(lib().ffg_dist_partition(total, world, rank, align, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 @dataclass

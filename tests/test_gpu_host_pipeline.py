@@ -1,0 +1,48 @@
+"""The pipelined host entry (ffg_pluq_tile_recursive: spine-first upload, early download of
+the root's top rows) against the device entry on the same inputs, at sizes where the spine
+has several levels, on full-rank and rank-deficient inputs (where R's permutations and the
+pivot-gather rotations reach back into the early-downloaded rows), with lda > n."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("shape", [(3000, 3000), (4500, 2600), (2600, 4500)])
+@pytest.mark.parametrize("gen", ["iid", "lru", "lowrank"])
+def test_host_entry_matches_device_entry(gpu, oracle_lib, shape, gen):
+    import torch
+
+    G, ctx = gpu
+    O = oracle_lib
+    p = 131071
+    m, n = shape
+    N = max(m, n)
+    if gen == "iid":
+        A = O.random_mat(p, m, n, m + n)
+    elif gen == "lru":
+        d = torch.empty((N, N), dtype=torch.int32, device="cuda")
+        G.lru_matrix_dev(p, d, N // 3, 5, ctx=ctx)
+        ctx.synchronize()
+        A = d.cpu().numpy().view(np.uint32)[:m, :n].copy()
+    else:  # rank 700 product: every block rank deficient, nontrivial permutations everywhere
+        L = O.random_mat(p, m, 700, 1).astype(np.uint64)
+        R = O.random_mat(p, 700, n, 2).astype(np.uint64)
+        A = np.zeros((m, n), np.uint32)
+        for k0 in range(0, 700, 64):
+            A = ((A.astype(np.uint64) + L[:, k0:k0 + 64] @ R[k0:k0 + 64, :]) % p).astype(np.uint32)
+    # device entry
+    d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+    rd = G.pluq_tile_recursive(p, d, 64, ctx=ctx)
+    ctx.synchronize()
+    want = d.cpu().numpy().view(np.uint32)
+    # host entry, with a padded leading dimension
+    ld = n + 37
+    buf = np.full((m, ld), 0xDEADBEEF, np.uint32)
+    buf[:, :n] = A
+    view = buf[:, :n]
+    rh = G.pluq_tile_recursive(p, view, 64, ctx=ctx)
+    assert rh.rank == rd.rank
+    assert np.array_equal(rh.P, rd.P) and np.array_equal(rh.Q, rd.Q)
+    assert np.array_equal(view, want)
+    assert np.all(buf[:, n:] == 0xDEADBEEF)  # padding untouched
