@@ -23,6 +23,9 @@
 //     L[i][k] = Lb[i][k] / piv_k,    U[k][:] = S_{p_k}[:] / (piv_0 ... piv_{k-1}).
 // Exhausted rows (rankrev.hpp:54-57) keep their zero Schur rows and zero L
 // entries for later pivots, as in the reference.
+#include <cstdio>
+#include <vector>
+
 #include "pluq.cuh"
 #include "triinv.cuh"
 
@@ -59,6 +62,16 @@ __device__ __forceinline__ uint32_t inv_mod_bin(uint32_t a, uint32_t p) {
     return u == 1 ? x1 : x2;
 }
 
+// diagnostics (FFG_BASE_DBG): per launch {clock64, globaltimer} at entry, end of pivoting, exit
+__device__ unsigned long long* g_base_dbg = nullptr;
+__device__ unsigned int g_base_dbg_n = 0;
+__device__ __forceinline__ void base_stamp(unsigned long long* slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    slot[0] = clock64();
+    slot[1] = t;
+}
+
 struct BaseLayout {
     uint32_t m, n, ns, rmax;  // ns = padded row stride of S (multiple of 8)
 };
@@ -70,6 +83,11 @@ __global__ void __launch_bounds__(BASE_THREADS)
                    uint64_t mu, uint32_t* __restrict__ inv_out) {
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t m = lay.m, n = lay.n, ns = lay.ns, rmax = lay.rmax;
+    unsigned long long* dbg = nullptr;
+    if (g_base_dbg && threadIdx.x == 0) {
+        dbg = g_base_dbg + 6 * (atomicAdd(&g_base_dbg_n, 1u) % 4096);
+        base_stamp(dbg);
+    }
     // shared: prow | pcol | pivv | invp | invD (rmax each) | Psh m | Qsh n | rowrank m | colrank n
     uint32_t* prow = sm;
     uint32_t* pcol = prow + rmax;
@@ -187,6 +205,7 @@ __global__ void __launch_bounds__(BASE_THREADS)
         __syncthreads();
     }
 
+    if (dbg) base_stamp(dbg + 2);
     // ---- phase 2: exact values (pivot inverses in parallel, prefix products, scaling)
     for (uint32_t k = tid; k < r; k += BASE_THREADS) invp[k] = inv_mod_bin(pivv[k], p);
     for (uint32_t i = tid; i < m; i += BASE_THREADS) rowrank[i] = NONE;
@@ -252,6 +271,7 @@ __global__ void __launch_bounds__(BASE_THREADS)
         }
     }
     __syncthreads();
+    if (dbg) base_stamp(dbg + 4);
     for (uint32_t i = tid; i < m; i += BASE_THREADS) Pd[i] = Psh[i];
     for (uint32_t j = tid; j < n; j += BASE_THREADS) Qd[j] = Qsh[j];
     // packed output: out[t][u] for original row i = P[t], column j = Q[u]
@@ -312,7 +332,41 @@ __global__ void __launch_bounds__(BASE_THREADS)
     }
 }
 
+void base_dbg_init() {
+    static bool done = false;
+    if (done || !getenv("FFG_BASE_DBG")) return;
+    done = true;
+    unsigned long long* buf = nullptr;
+    FFG_CUDA(cudaMalloc(&buf, 4096 * 6 * 8));
+    FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg, &buf, sizeof(buf)));
+}
+
+void base_dbg_dump() {
+    if (!getenv("FFG_BASE_DBG")) return;
+    unsigned long long* buf = nullptr;
+    unsigned int n = 0;
+    FFG_CUDA(cudaDeviceSynchronize());
+    FFG_CUDA(cudaMemcpyFromSymbol(&buf, g_base_dbg, sizeof(buf)));
+    FFG_CUDA(cudaMemcpyFromSymbol(&n, g_base_dbg_n, sizeof(n)));
+    if (!buf || n == 0) return;
+    n = std::min(n, 4096u);
+    std::vector<unsigned long long> h(6 * (size_t)n);
+    FFG_CUDA(cudaMemcpy(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost));
+    double piv_us = 0, tot_us = 0, mhz = 0;
+    for (unsigned i = 0; i < n; ++i) {
+        const unsigned long long* d = &h[6 * i];
+        piv_us += (d[3] - d[1]) / 1e3;
+        tot_us += (d[5] - d[1]) / 1e3;
+        mhz += (double)(d[4] - d[0]) / ((d[5] - d[1]) / 1e3);
+    }
+    fprintf(stderr, "BASE_DBG %u launches: pivoting %.2f us, to output %.2f us avg, SM clock %.0f MHz avg\n", n,
+            piv_us / n, tot_us / n, mhz / n);
+    unsigned int zero = 0;
+    FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg_n, &zero, sizeof(zero)));
+}
+
 bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv_out) {
+    base_dbg_init();
     BaseLayout lay;
     lay.m = (uint32_t)a.rows;
     lay.n = (uint32_t)a.cols;

@@ -126,6 +126,109 @@ struct EpiParams {
     uint32_t m_tiles, n_tiles;
 };
 
+// --------------------------------------------------------------------------- epilogue
+// 8 warps: TMEM -> registers -> sum_s D_s w_s mod p -> alpha/beta update of C.  `before_wait`
+// runs after the C prefetch and before waiting for the accumulator (the direct kernel stages
+// its operands there).
+template <int L, class TmemFn, class Hook>
+__device__ __forceinline__ void epilogue_tile(const EpiParams& ep, TmemFn&& get_tmem, uint64_t* tmem_full,
+                                              uint32_t m_blk, uint32_t n_blk, uint32_t warp, uint32_t lane,
+                                              Hook&& before_wait, uint32_t phase = 0,
+                                              uint64_t* tmem_empty = nullptr) {
+    constexpr int NT = TileCfg<L>::NT;
+    constexpr int D = 2 * L - 1;
+    // warp (4 + e): TMEM lane quarter e & 3, column half e >> 2 (8-column chunks)
+    constexpr int PER = NT / 16;                 // chunks per half
+    constexpr bool PREFETCH = PER * 8 <= 64;     // keep this thread's C values in registers
+    const uint32_t e = warp - 4, q = e & 3, half = e >> 2;
+    const uint32_t row = m_blk * BM + q * 32 + lane;
+    const uint32_t col_first = n_blk * NT + half * PER * 8;
+    const bool row_ok = row < ep.M;
+    uint32_t* crow = ep.C + (uint64_t)(row_ok ? row : 0) * ep.ldc;
+    const bool vec = ep.vec_ok && col_first + PER * 8 <= ep.N;
+    const bool need_c = ep.mode != EPI_PROD;
+    uint32_t cpre[PREFETCH ? PER * 8 : 1];
+    if (PREFETCH && need_c && row_ok) {  // overlap the C read with the mainloop
+#pragma unroll
+        for (int ch = 0; ch < (PREFETCH ? PER : 0); ++ch) {
+            const uint32_t col = col_first + ch * 8;
+            if (vec) {
+                const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
+                const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
+                cpre[ch * 8 + 0] = a.x, cpre[ch * 8 + 1] = a.y, cpre[ch * 8 + 2] = a.z, cpre[ch * 8 + 3] = a.w;
+                cpre[ch * 8 + 4] = b.x, cpre[ch * 8 + 5] = b.y, cpre[ch * 8 + 6] = b.z, cpre[ch * 8 + 7] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cpre[ch * 8 + j] = col + j < ep.N ? crow[col + j] : 0u;
+            }
+        }
+    }
+    before_wait();
+    ptx::mbar_wait(tmem_full, phase);
+    ptx::tc_fence_after();
+    const uint32_t tmem = get_tmem();
+    const uint32_t t_lane = tmem + ((q * 32) << 16) + half * PER * 8;
+#pragma unroll
+    for (int ch = 0; ch < PER; ++ch) {
+        uint32_t r[D][8];
+#pragma unroll
+        for (int s2 = 0; s2 < D; ++s2) ptx::tmem_ld8(t_lane + s2 * NT + ch * 8, r[s2]);
+        ptx::tmem_ld_wait();
+        if (ch == PER - 1 && tmem_empty) {  // accumulators read: the next tile's MMAs may start
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+        }
+        if (!row_ok) continue;
+        const uint32_t col = col_first + ch * 8;
+        uint32_t cv[8];
+        if (need_c) {
+            if (PREFETCH) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cv[j] = cpre[(PREFETCH ? ch * 8 : 0) + j];
+            } else if (vec) {
+                const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
+                const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
+                cv[0] = a.x, cv[1] = a.y, cv[2] = a.z, cv[3] = a.w, cv[4] = b.x, cv[5] = b.y, cv[6] = b.z, cv[7] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cv[j] = col + j < ep.N ? crow[col + j] : 0u;
+            }
+        }
+        uint32_t out[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint64_t acc = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < D; ++s2) acc += (uint64_t)r[s2][j] * ep.w[s2];
+            const uint32_t prod = mod_u64(acc, ep.p, ep.mu);
+            switch (ep.mode) {
+                case EPI_SUB: out[j] = cv[j] >= prod ? cv[j] - prod : cv[j] + ep.p - prod; break;
+                case EPI_PROD: out[j] = prod; break;
+                case EPI_ADD: {
+                    const uint32_t t = cv[j] + prod;
+                    out[j] = t >= ep.p ? t - ep.p : t;
+                    break;
+                }
+                default: {
+                    uint64_t v = (uint64_t)ep.alpha * prod;
+                    if (ep.beta) v += (uint64_t)ep.beta * cv[j];
+                    out[j] = mod_u64(v, ep.p, ep.mu);
+                }
+            }
+        }
+        if (vec) {
+            *reinterpret_cast<uint4*>(crow + col) = make_uint4(out[0], out[1], out[2], out[3]);
+            *reinterpret_cast<uint4*>(crow + col + 4) = make_uint4(out[4], out[5], out[6], out[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (col + j < ep.N) crow[col + j] = out[j];
+        }
+    }
+    ptx::tc_fence_before();
+}
+
 // --------------------------------------------------------------------------- the GEMM kernel
 template <int L>
 __global__ void __launch_bounds__(384, 1)
@@ -143,17 +246,21 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
-    // grouped rasterization: a wave covers GROUP_M row-blocks x a few column-blocks
-    const uint32_t pid = blockIdx.x;
-    const uint32_t in_group = GROUP_M * ep.n_tiles;
-    const uint32_t first_m = (pid / in_group) * GROUP_M;
-    const uint32_t gsize = min((uint32_t)GROUP_M, ep.m_tiles - first_m);
-    const uint32_t m_blk = first_m + (pid % in_group) % gsize;
-    const uint32_t n_blk = (pid % in_group) / gsize;
+    // Persistent over tiles (grid may be capped below the tile count so that a low-priority
+    // GEMM leaves SMs free for the critical path).  Grouped rasterization: a wave covers
+    // GROUP_M row-blocks x a few column-blocks.
+    const uint32_t tiles = ep.m_tiles * ep.n_tiles;
+    auto tile_coords = [&](uint32_t pid, uint32_t& m_blk, uint32_t& n_blk) {
+        const uint32_t in_group = GROUP_M * ep.n_tiles;
+        const uint32_t first_m = (pid / in_group) * GROUP_M;
+        const uint32_t gsize = min((uint32_t)GROUP_M, ep.m_tiles - first_m);
+        m_blk = first_m + (pid % in_group) % gsize;
+        n_blk = (pid % in_group) / gsize;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -161,6 +268,7 @@ __global__ void __launch_bounds__(384, 1)
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(tmem_full, 1);
+        ptx::mbar_init(tmem_empty, 8);  // one arrival per epilogue warp
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -174,19 +282,24 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer (runs ahead across tile boundaries)
         if (lane == 0) {
-            const int32_t a_row0 = (int32_t)(m_blk * BM);
-            const int32_t b_row0 = (int32_t)(n_blk * L * NT);
-            for (uint32_t kb = 0; kb < ep.kblocks; ++kb) {
-                const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
-                ptx::mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* st = smem + s * S::STAGE_BYTES;
-                ptx::mbar_expect_tx(&full[s], S::STAGE_BYTES);
-                for (int i = 0; i < L; ++i)
-                    ptx::tma_load_2d(st + i * BM * BK, &mapA, &full[s], (int32_t)(kb * BK),
-                                     a_row0 + i * (int32_t)(ep.m_tiles * BM));
-                ptx::tma_load_2d(st + S::A_BYTES, &mapB, &full[s], (int32_t)(kb * BK), b_row0);
+            uint32_t it = 0;
+            for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                uint32_t m_blk, n_blk;
+                tile_coords(tile, m_blk, n_blk);
+                const int32_t a_row0 = (int32_t)(m_blk * BM);
+                const int32_t b_row0 = (int32_t)(n_blk * L * NT);
+                for (uint32_t kb = 0; kb < ep.kblocks; ++kb, ++it) {
+                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * S::STAGE_BYTES;
+                    ptx::mbar_expect_tx(&full[s], S::STAGE_BYTES);
+                    for (int i = 0; i < L; ++i)
+                        ptx::tma_load_2d(st + i * BM * BK, &mapA, &full[s], (int32_t)(kb * BK),
+                                         a_row0 + i * (int32_t)(ep.m_tiles * BM));
+                    ptx::tma_load_2d(st + S::A_BYTES, &mapB, &full[s], (int32_t)(kb * BK), b_row0);
+                }
             }
         }
     } else if (warp == 1) {
@@ -195,87 +308,282 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t IDESC_FULL = ptx::idesc_u8(BM, L * NT);
             constexpr uint32_t IDESC_HEAD = ptx::idesc_u8(BM, (L > 1 ? (L - 1) : 1) * NT);
             constexpr uint32_t IDESC_TAIL = ptx::idesc_u8(BM, NT);
-            for (uint32_t kb = 0; kb < ep.kblocks; ++kb) {
-                const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1;
-                ptx::mbar_wait(&full[s], ph);
+            uint32_t it = 0, t = 0;
+            for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+                ptx::mbar_wait(tmem_empty, (t & 1) ^ 1);  // previous tile's accumulators drained
                 ptx::tc_fence_after();
-                const uint32_t a_base = ptx::smem_u32(smem + s * S::STAGE_BYTES);
-                const uint32_t b_base = a_base + S::A_BYTES;
+                for (uint32_t kb = 0; kb < ep.kblocks; ++kb, ++it) {
+                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(smem + s * S::STAGE_BYTES);
+                    const uint32_t b_base = a_base + S::A_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < BK / 32; ++kk) {
-                    const uint64_t bdesc = ptx::desc_kmajor_sw128(b_base + kk * 32);
+                    for (int kk = 0; kk < BK / 32; ++kk) {
+                        const uint64_t bdesc = ptx::desc_kmajor_sw128(b_base + kk * 32);
 #pragma unroll
-                    for (int i = 0; i < L; ++i) {
-                        const uint64_t adesc = ptx::desc_kmajor_sw128(a_base + i * BM * BK + kk * 32);
-                        if (kb != 0 || kk != 0) {
-                            ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_FULL, 1);
-                        } else if (i == 0) {
-                            ptx::mma_i8(tmem, adesc, bdesc, IDESC_FULL, 0);
-                        } else {
-                            // first K-step: diagonals i..i+L-2 already hold data, i+L-1 is fresh
-                            ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_HEAD, 1);
-                            const uint64_t btail = ptx::desc_kmajor_sw128(b_base + (L - 1) * NT * BK + kk * 32);
-                            ptx::mma_i8(tmem + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
+                        for (int i = 0; i < L; ++i) {
+                            const uint64_t adesc = ptx::desc_kmajor_sw128(a_base + i * BM * BK + kk * 32);
+                            if (kb != 0 || kk != 0) {
+                                ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_FULL, 1);
+                            } else if (i == 0) {
+                                ptx::mma_i8(tmem, adesc, bdesc, IDESC_FULL, 0);
+                            } else {
+                                // first K-step: diagonals i..i+L-2 already hold data, i+L-1 is fresh
+                                ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_HEAD, 1);
+                                const uint64_t btail =
+                                    ptx::desc_kmajor_sw128(b_base + (L - 1) * NT * BK + kk * 32);
+                                ptx::mma_i8(tmem + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
+                            }
                         }
                     }
+                    ptx::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
                 }
-                ptx::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
+                ptx::mma_commit(tmem_full);
             }
-            ptx::mma_commit(tmem_full);
         }
         __syncwarp();
     } else if (warp >= 4) {
-        // ---------------- epilogue (8 warps): TMEM -> registers -> mod p -> C
-        // warp (4 + e): TMEM lane quarter e & 3, column half e >> 2 (8-column chunks)
-        constexpr int PER = NT / 16;                 // chunks per half
-        constexpr bool PREFETCH = PER * 8 <= 64;     // keep this thread's C values in registers
-        const uint32_t e = warp - 4, q = e & 3, half = e >> 2;
-        const uint32_t row = m_blk * BM + q * 32 + lane;
-        const uint32_t col_first = n_blk * NT + half * PER * 8;
-        const bool row_ok = row < ep.M;
-        uint32_t* crow = ep.C + (uint64_t)(row_ok ? row : 0) * ep.ldc;
-        const bool vec = ep.vec_ok && col_first + PER * 8 <= ep.N;
-        const bool need_c = ep.mode != EPI_PROD;
-        uint32_t cpre[PREFETCH ? PER * 8 : 1];
-        if (PREFETCH && need_c && row_ok) {  // overlap the C read with the mainloop
+        uint32_t t = 0;
+        for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+            uint32_t m_blk, n_blk;
+            tile_coords(tile, m_blk, n_blk);
+            epilogue_tile<L>(ep, [&] { return tmem; }, tmem_full, m_blk, n_blk, warp, lane, [] {}, t & 1,
+                             tmem_empty);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// --------------------------------------------------------------------------- direct kernel (K <= 128 KB)
+// Small-K GEMMs (the Schur updates and TRSM splits of the lower recursion levels: K = 128 or
+// 256) are latency-bound; there the separate split launch and its round trip of limb planes
+// through HBM cost as much as the GEMM.  This kernel stages the WHOLE K extent of its tile
+// directly: all 12 warps read the u32 operands, cut them into limb bytes and store them in the
+// same SW128 K-major layout TMA would produce, then one thread issues every MMA.  Requires C
+// not to alias A or B (other CTAs' C writes would race with this CTA's operand reads).
+struct DirectArgs {
+    const uint32_t* A;
+    uint64_t lda;
+    const uint32_t* B;
+    uint64_t ldb;
+    uint32_t K;
+    uint32_t a_vec;  // A rows 16-byte aligned: A and lda multiples of 4 words
+    unsigned long long* dbg;  // diagnostics: %globaltimer stamps of CTA 0 (null = off)
+};
+__device__ __forceinline__ unsigned long long gtime() { return clock64(); }
+__device__ __forceinline__ unsigned long long gns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int L, int KB>
+struct DirectSmem {
+    static constexpr int NT = TileCfg<L>::NT;
+    static constexpr int A_PLANE = BM * BK;               // one limb plane of one K block
+    static constexpr int A_BYTES = KB * L * A_PLANE;
+    static constexpr int B_BLOCK = L * NT * BK;           // the L stacked planes of one K block
+    static constexpr int C_OFF = A_BYTES + KB * B_BLOCK;  // C tile prefetched by cp.async
+    static constexpr int CS = NT + 4;                     // C row stride in words (16-byte rows)
+    static constexpr int BAR_OFF = C_OFF + BM * CS * 4;
+    static constexpr int TOTAL = BAR_OFF + 64 + 1024;
+    static constexpr bool FITS = TOTAL <= 227 * 1024;
+};
+
+__device__ __forceinline__ uint32_t pack_limb(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, int sh) {
+    return ((v0 >> sh) & 0xFF) | (((v1 >> sh) & 0xFF) << 8) | (((v2 >> sh) & 0xFF) << 16) | (((v3 >> sh) & 0xFF) << 24);
+}
+
+// byte l of each of v0..v3, packed little-endian (three byte permutes)
+template <int l>
+__device__ __forceinline__ uint32_t limb_bytes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+    const uint32_t lo = __byte_perm(v0, v1, l | ((l + 4) << 4));
+    const uint32_t hi = __byte_perm(v2, v3, l | ((l + 4) << 4));
+    return __byte_perm(lo, hi, 0x5410);
+}
+
+__device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t kq) {  // byte offset of k = 4 kq in a row
+    return row * 128 + ((((kq >> 2) ^ row) & 7) << 4) + ((kq & 3) << 2);
+}
+
+// Code size matters here: each CTA runs this kernel body once, so straight-line unrolled code
+// is fetched cold from L2 (~6 KB L0 / 32 KB L1.5 I-cache).  Loops are therefore rolled, with
+// 4 loads in flight per thread and the C tile prefetched by cp.async into shared memory.
+template <int L, int KB>
+__global__ void __launch_bounds__(384, 1)
+    modgemm_direct_kernel(const DirectArgs da, const EpiParams ep) {
+    using S = DirectSmem<L, KB>;
+    constexpr int NT = S::NT, D = 2 * L - 1;
+    constexpr uint32_t TMEM_COLS = 512;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint32_t* Cs = reinterpret_cast<uint32_t*>(smem + S::C_OFF);
+    uint64_t* tmem_full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id(), tid = threadIdx.x;
+    const uint32_t m_blk = blockIdx.x % ep.m_tiles, n_blk = blockIdx.x / ep.m_tiles;
+    const bool need_c = ep.mode != EPI_PROD;
+    const bool dbg = da.dbg && blockIdx.x == 0 && tid == 0;
+    if (dbg) {
+        da.dbg[0] = gtime();
+        da.dbg[4] = gns();
+    }
+
+    if (tid == 0) {
+        ptx::mbar_init(tmem_full, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+    // epilogue warps: C prefetch for the rows / columns they will write
+    constexpr uint32_t PER = NT / 16;  // 8-column chunks per epilogue thread
+    const uint32_t e = warp - 4, q = e & 3, half = e >> 2;
+    const uint32_t r_in = q * 32 + lane, row = m_blk * BM + r_in;
+    const uint32_t c_in = half * PER * 8, col0 = n_blk * NT + c_in;
+    const bool row_ok = row < ep.M;
+    uint32_t* crow = ep.C + (uint64_t)(row_ok ? row : 0) * ep.ldc;
+    uint32_t* cs_row = Cs + r_in * S::CS + c_in;
+    const bool vec = ep.vec_ok && col0 + PER * 8 <= ep.N;
+    if (warp >= 4 && need_c && row_ok) {
+        if (vec) {
+            for (uint32_t i = 0; i < PER * 2; ++i) ptx::cp_async16(cs_row + 4 * i, crow + col0 + 4 * i);
+        } else {
+            for (uint32_t j = 0; j < PER * 8; ++j)
+                if (col0 + j < ep.N) ptx::cp_async4(cs_row + j, crow + col0 + j);
+        }
+        ptx::cp_async_commit();
+    }
+
+    // ---- stage the operands' limb planes (all 12 warps).  Rows >= M of A and columns >= N of
+    // B are left unstaged: they only feed output rows / columns that are never written.  A's
+    // k >= K entries are zero, which also neutralises whatever B holds there.
+    const uint32_t smem_s = ptx::smem_u32(smem);
+    const uint32_t a_rows = min((uint32_t)BM, ep.M - m_blk * BM);
+    const uint32_t b_cols = min((uint32_t)NT, ep.N - n_blk * NT);
+    const uint32_t kq_live = (da.K + 3) / 4;  // 4-element groups of B that hold data
+#pragma unroll 1
+    for (uint32_t kb = 0; kb < (uint32_t)KB; ++kb) {
+        const uint32_t ablk = smem_s + kb * L * S::A_PLANE;
+#pragma unroll 1
+        for (uint32_t base = tid; base < a_rows * 32; base += 4 * 384) {
+            uint4 v[4];
 #pragma unroll
-            for (int ch = 0; ch < (PREFETCH ? PER : 0); ++ch) {
-                const uint32_t col = col_first + ch * 8;
-                if (vec) {
-                    const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
-                    const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
-                    cpre[ch * 8 + 0] = a.x, cpre[ch * 8 + 1] = a.y, cpre[ch * 8 + 2] = a.z, cpre[ch * 8 + 3] = a.w;
-                    cpre[ch * 8 + 4] = b.x, cpre[ch * 8 + 5] = b.y, cpre[ch * 8 + 6] = b.z, cpre[ch * 8 + 7] = b.w;
-                } else {
+            for (int u = 0; u < 4; ++u) {  // A: row r, k = 4 (it & 31) .. + 3 of this K block
+                const uint32_t it = base + u * 384, r = it >> 5, k = kb * BK + (it & 31) * 4;
+                v[u] = make_uint4(0, 0, 0, 0);
+                if (it < a_rows * 32) {
+                    const uint32_t* src = da.A + (uint64_t)(m_blk * BM + r) * da.lda + k;
+                    if (da.a_vec && k + 3 < da.K) {
+                        v[u] = *reinterpret_cast<const uint4*>(src);
+                    } else {
+                        v[u].x = k < da.K ? src[0] : 0u;
+                        v[u].y = k + 1 < da.K ? src[1] : 0u;
+                        v[u].z = k + 2 < da.K ? src[2] : 0u;
+                        v[u].w = k + 3 < da.K ? src[3] : 0u;
+                    }
+                }
+            }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) cpre[ch * 8 + j] = col + j < ep.N ? crow[col + j] : 0u;
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t it = base + u * 384;
+                if (it < a_rows * 32) {
+                    const uint32_t off = ablk + sw128(it >> 5, it & 31);
+                    ptx::st_shared_u32(off, limb_bytes<0>(v[u].x, v[u].y, v[u].z, v[u].w));
+                    if (L > 1) ptx::st_shared_u32(off + S::A_PLANE, limb_bytes<1>(v[u].x, v[u].y, v[u].z, v[u].w));
+                    if (L > 2) ptx::st_shared_u32(off + 2 * S::A_PLANE, limb_bytes<2>(v[u].x, v[u].y, v[u].z, v[u].w));
+                    if (L > 3) ptx::st_shared_u32(off + 3 * S::A_PLANE, limb_bytes<3>(v[u].x, v[u].y, v[u].z, v[u].w));
                 }
             }
         }
+        const uint32_t bblk = smem_s + S::A_BYTES + kb * S::B_BLOCK;
+        const uint32_t kq_n = min(32u, kq_live > kb * 32 ? kq_live - kb * 32 : 0u);
+#pragma unroll 1
+        for (uint32_t base = tid; base < b_cols * kq_n; base += 4 * 384) {
+            uint32_t v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // B: column nn, k = 4 kq .. + 3 (rows of B)
+                const uint32_t it = base + u * 384, nn = it % b_cols, k = kb * BK + (it / b_cols) * 4;
+                const bool ok = it < b_cols * kq_n;
+                const uint32_t* src = da.B + (uint64_t)k * da.ldb + n_blk * NT + nn;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) v[u][t] = ok && k + t < da.K ? src[(uint64_t)t * da.ldb] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t it = base + u * 384;
+                if (it < b_cols * kq_n) {
+                    const uint32_t nn = it % b_cols, kq = it / b_cols;
+                    const uint32_t off = bblk + sw128(nn, kq);  // plane l at row l*NT + nn (NT % 8 == 0)
+                    ptx::st_shared_u32(off, limb_bytes<0>(v[u][0], v[u][1], v[u][2], v[u][3]));
+                    if (L > 1) ptx::st_shared_u32(off + NT * BK, limb_bytes<1>(v[u][0], v[u][1], v[u][2], v[u][3]));
+                    if (L > 2) ptx::st_shared_u32(off + 2 * NT * BK, limb_bytes<2>(v[u][0], v[u][1], v[u][2], v[u][3]));
+                    if (L > 3) ptx::st_shared_u32(off + 3 * NT * BK, limb_bytes<3>(v[u][0], v[u][1], v[u][2], v[u][3]));
+                }
+            }
+        }
+    }
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();  // operands staged, TMEM allocated, barrier initialised
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (dbg) da.dbg[1] = gtime();
+
+    if (warp == 1 && lane == 0) {
+        // ---- all MMAs of the tile (same diagonal scheme as modgemm_kernel)
+        constexpr uint32_t IDESC_FULL = ptx::idesc_u8(BM, L * NT);
+        constexpr uint32_t IDESC_HEAD = ptx::idesc_u8(BM, (L > 1 ? (L - 1) : 1) * NT);
+        constexpr uint32_t IDESC_TAIL = ptx::idesc_u8(BM, NT);
+#pragma unroll 1
+        for (uint32_t kb = 0; kb < (uint32_t)KB; ++kb) {
+            const uint32_t a_base = ptx::smem_u32(smem + kb * L * S::A_PLANE);
+            const uint32_t b_base = ptx::smem_u32(smem + S::A_BYTES + kb * S::B_BLOCK);
+#pragma unroll 1
+            for (uint32_t kk = 0; kk < BK / 32; ++kk) {
+                const uint64_t bdesc = ptx::desc_kmajor_sw128(b_base + kk * 32);
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    const uint64_t adesc = ptx::desc_kmajor_sw128(a_base + i * S::A_PLANE + kk * 32);
+                    if (kb != 0 || kk != 0) {
+                        ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_FULL, 1);
+                    } else if (i == 0) {
+                        ptx::mma_i8(tmem, adesc, bdesc, IDESC_FULL, 0);
+                    } else {
+                        ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_HEAD, 1);
+                        const uint64_t btail = ptx::desc_kmajor_sw128(b_base + (L - 1) * NT * BK + kk * 32);
+                        ptx::mma_i8(tmem + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
+                    }
+                }
+            }
+        }
+        ptx::mma_commit(tmem_full);
+    } else if (warp >= 4) {
+        // ---- epilogue: rolled over 8-column chunks, C from shared memory
+        if (need_c && row_ok) ptx::cp_async_wait_all();
         ptx::mbar_wait(tmem_full, 0);
         ptx::tc_fence_after();
-        const uint32_t t_lane = tmem + ((q * 32) << 16) + half * PER * 8;
-#pragma unroll
-        for (int ch = 0; ch < PER; ++ch) {
+        if (warp == 4 && lane == 0 && da.dbg && blockIdx.x == 0) da.dbg[2] = gtime();
+        const uint32_t t_lane = tmem + ((q * 32) << 16) + c_in;
+        // chunks past N and warps whose 32 rows are all past M have nothing to write (uniform
+        // per warp, so the warp-collective TMEM loads can be skipped with them)
+        const uint32_t n_ch = m_blk * BM + q * 32 >= ep.M ? 0u
+                              : col0 >= ep.N               ? 0u
+                                                           : min(PER, (ep.N - col0 + 7) / 8);
+#pragma unroll 1
+        for (uint32_t ch = 0; ch < n_ch; ++ch) {
             uint32_t r[D][8];
 #pragma unroll
             for (int s2 = 0; s2 < D; ++s2) ptx::tmem_ld8(t_lane + s2 * NT + ch * 8, r[s2]);
             ptx::tmem_ld_wait();
             if (!row_ok) continue;
-            const uint32_t col = col_first + ch * 8;
+            const uint32_t col = col0 + ch * 8;
             uint32_t cv[8];
             if (need_c) {
-                if (PREFETCH) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) cv[j] = cpre[(PREFETCH ? ch * 8 : 0) + j];
-                } else if (vec) {
-                    const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
-                    const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
-                    cv[0] = a.x, cv[1] = a.y, cv[2] = a.z, cv[3] = a.w, cv[4] = b.x, cv[5] = b.y, cv[6] = b.z, cv[7] = b.w;
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) cv[j] = col + j < ep.N ? crow[col + j] : 0u;
-                }
+                const uint4 a = ptx::ld_shared_v4(ptx::smem_u32(cs_row + ch * 8));
+                const uint4 b = ptx::ld_shared_v4(ptx::smem_u32(cs_row + ch * 8 + 4));
+                cv[0] = a.x, cv[1] = a.y, cv[2] = a.z, cv[3] = a.w, cv[4] = b.x, cv[5] = b.y, cv[6] = b.z, cv[7] = b.w;
             }
             uint32_t out[8];
 #pragma unroll
@@ -284,19 +592,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int s2 = 0; s2 < D; ++s2) acc += (uint64_t)r[s2][j] * ep.w[s2];
                 const uint32_t prod = mod_u64(acc, ep.p, ep.mu);
-                switch (ep.mode) {
-                    case EPI_SUB: out[j] = cv[j] >= prod ? cv[j] - prod : cv[j] + ep.p - prod; break;
-                    case EPI_PROD: out[j] = prod; break;
-                    case EPI_ADD: {
-                        const uint32_t t = cv[j] + prod;
-                        out[j] = t >= ep.p ? t - ep.p : t;
-                        break;
-                    }
-                    default: {
-                        uint64_t v = (uint64_t)ep.alpha * prod;
-                        if (ep.beta) v += (uint64_t)ep.beta * cv[j];
-                        out[j] = mod_u64(v, ep.p, ep.mu);
-                    }
+                if (ep.mode == EPI_SUB) {
+                    out[j] = cv[j] >= prod ? cv[j] - prod : cv[j] + ep.p - prod;
+                } else if (ep.mode == EPI_PROD) {
+                    out[j] = prod;
+                } else {
+                    uint64_t t = (uint64_t)ep.alpha * prod;
+                    if (ep.beta) t += (uint64_t)ep.beta * cv[j];
+                    out[j] = mod_u64(t, ep.p, ep.mu);
                 }
             }
             if (vec) {
@@ -308,9 +611,13 @@ __global__ void __launch_bounds__(384, 1)
                     if (col + j < ep.N) crow[col + j] = out[j];
             }
         }
-        ptx::tc_fence_before();
     }
+    ptx::tc_fence_before();
     __syncthreads();
+    if (dbg) {
+        da.dbg[3] = gtime();
+        da.dbg[5] = gns();
+    }
     if (warp == 2) ptx::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
@@ -332,9 +639,6 @@ struct SplitArgs {
     uint32_t a_blocks, b_kblocks;
 };
 
-__device__ __forceinline__ uint32_t pack_limb(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, int sh) {
-    return ((v0 >> sh) & 0xFF) | (((v1 >> sh) & 0xFF) << 8) | (((v2 >> sh) & 0xFF) << 16) | (((v3 >> sh) & 0xFF) << 24);
-}
 
 __global__ void __launch_bounds__(256) split_kernel(const SplitArgs a) {
     __shared__ uint32_t tile[64][65];
@@ -487,17 +791,7 @@ CUtensorMap make_map(const uint8_t* base, uint64_t inner_bytes, uint64_t rows, u
     return m;
 }
 
-template <int L>
-void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t* Ap, const uint8_t* Bp, size_t Mp,
-                    size_t Np, size_t Kp, DView C, cudaStream_t st) {
-    using S = Smem<L>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        FFG_CUDA(cudaFuncSetAttribute(modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
-        attr_set = true;
-    }
-    CUtensorMap ma = make_map(Ap, Kp, (uint64_t)L * Mp, BM);
-    CUtensorMap mb = make_map(Bp, Kp, (uint64_t)(Np / S::NT) * L * S::NT, L * S::NT);
+EpiParams make_ep(const Field& F, uint32_t alpha, uint32_t beta, DView C) {
     EpiParams ep;
     ep.C = C.d;
     ep.ldc = C.ld;
@@ -513,18 +807,102 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
                                                          : EPI_GENERIC;
     ep.vec_ok = ((reinterpret_cast<uintptr_t>(C.d) & 15) == 0 && (C.ld & 3) == 0) ? 1u : 0u;
     for (int s = 0; s < 8; ++s) ep.w[s] = F.w[s];
+    return ep;
+}
+
+template <int L>
+void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t* Ap, const uint8_t* Bp, size_t Mp,
+                    size_t Np, size_t Kp, DView C, cudaStream_t st, int sm_cap) {
+    using S = Smem<L>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        FFG_CUDA(cudaFuncSetAttribute(modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
+        attr_set = true;
+    }
+    CUtensorMap ma = make_map(Ap, Kp, (uint64_t)L * Mp, BM);
+    CUtensorMap mb = make_map(Bp, Kp, (uint64_t)(Np / S::NT) * L * S::NT, L * S::NT);
+    EpiParams ep = make_ep(F, alpha, beta, C);
     ep.kblocks = (uint32_t)(Kp / BK);
     ep.m_tiles = (uint32_t)(Mp / BM);
     ep.n_tiles = (uint32_t)(Np / S::NT);
-    dim3 grid(ep.m_tiles * ep.n_tiles);
+    const uint32_t tiles = ep.m_tiles * ep.n_tiles;
+    dim3 grid(sm_cap > 0 ? std::min<uint32_t>(tiles, (uint32_t)sm_cap) : tiles);
     modgemm_kernel<L><<<grid, 384, S::TOTAL, st>>>(ma, mb, ep);
     FFG_CUDA(cudaGetLastError());
 }
 
+bool direct_fits(int L, int KB) {
+    switch (L * 4 + KB) {
+        case 1 * 4 + 1: return DirectSmem<1, 1>::FITS;
+        case 1 * 4 + 2: return DirectSmem<1, 2>::FITS;
+        case 2 * 4 + 1: return DirectSmem<2, 1>::FITS;
+        case 2 * 4 + 2: return DirectSmem<2, 2>::FITS;
+        case 3 * 4 + 1: return DirectSmem<3, 1>::FITS;
+        case 3 * 4 + 2: return DirectSmem<3, 2>::FITS;
+        case 4 * 4 + 1: return DirectSmem<4, 1>::FITS;
+        case 4 * 4 + 2: return DirectSmem<4, 2>::FITS;
+        default: return false;
+    }
+}
+
+template <int L, int KB>
+void launch_direct(const Field& F, uint32_t alpha, uint32_t beta, DView A, DView B, DView C, cudaStream_t st) {
+    using S = DirectSmem<L, KB>;
+    if constexpr (!S::FITS) {
+        throw Error(FFG_ERR_INTERNAL, "direct GEMM tile does not fit shared memory");
+    } else {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        FFG_CUDA(cudaFuncSetAttribute(modgemm_direct_kernel<L, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      S::TOTAL));
+    });
+    EpiParams ep = make_ep(F, alpha, beta, C);
+    ep.kblocks = KB;
+    ep.m_tiles = (uint32_t)ceil_div(C.rows, BM);
+    ep.n_tiles = (uint32_t)ceil_div(C.cols, S::NT);
+    DirectArgs da;
+    da.A = A.d;
+    da.lda = A.ld;
+    da.B = B.d;
+    da.ldb = B.ld;
+    da.K = (uint32_t)A.cols;
+    da.a_vec = ((reinterpret_cast<uintptr_t>(A.d) & 15) == 0 && (A.ld & 3) == 0) ? 1u : 0u;
+    static unsigned long long* dbg_buf = nullptr;
+    static const bool dbg_on = getenv("FFG_DIRECT_DBG") != nullptr;
+    if (dbg_on && !dbg_buf) FFG_CUDA(cudaMalloc(&dbg_buf, 64));
+    da.dbg = dbg_on ? dbg_buf : nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (dbg_on) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    modgemm_direct_kernel<L, KB><<<ep.m_tiles * ep.n_tiles, 384, S::TOTAL, st>>>(da, ep);
+    FFG_CUDA(cudaGetLastError());
+    if (dbg_on) {
+        cudaEventRecord(e1, st);
+        cudaStreamSynchronize(st);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long h[6];
+        cudaMemcpy(h, dbg_buf, 48, cudaMemcpyDeviceToHost);
+        const double c2us = (double)(h[5] - h[4]) / 1e3 / (double)(h[3] - h[0]);  // measured clock
+        fprintf(stderr, "DIRECT_DBG clock %.0f MHz, body %.2f us (globaltimer)\n", 1.0 / c2us,
+                (h[5] - h[4]) / 1e3);
+        fprintf(stderr, "DIRECT_DBG %zux%zux%zu staged %.2f us, mma %.2f us, epilogue %.2f us, body %.2f us, event %.2f us\n",
+                C.rows, C.cols, A.cols, (h[1] - h[0]) * c2us, (h[2] - h[1]) * c2us, (h[3] - h[2]) * c2us,
+                (h[3] - h[0]) * c2us, ms * 1e3);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    }
+}
+
 }  // namespace
 
-// Small problems: one CUDA-core launch beats split + tensor-core launches (tuned on B200).
-size_t g_simt_macs = size_t(1) << 24;
+// CUDA-core path for problems with M*N*K <= g_simt_macs.  Off by default: measured inside the PLUQ,
+// the direct tensor-core kernel beats it at every size (FFG_SIMT_MACS re-enables it).
+size_t g_simt_macs = 0;
 bool use_simt(size_t M, size_t N, size_t K) { return M * N * K <= g_simt_macs; }
 
 size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k) {
@@ -535,7 +913,7 @@ size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k) {
 }
 
 void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, DView C, cudaStream_t st,
-               Workspace& ws, uint64_t* launches) {
+               Workspace& ws, uint64_t* launches, int sm_cap) {
     if (A.cols != B.rows || C.rows != A.rows || C.cols != B.cols)
         throw Error(FFG_ERR_DIM_MISMATCH, "gemm: non-conforming shapes");  // blas.hpp:21-24
     const size_t M = C.rows, N = C.cols, K = A.cols;
@@ -589,6 +967,28 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         return;
     }
     const int L = F.limbs, NT = tile_n(L);
+    static const int cap_env = getenv("FFG_GEMM_SM_CAP") ? atoi(getenv("FFG_GEMM_SM_CAP")) : 0;
+    if (sm_cap <= 0) sm_cap = cap_env;  // test hook: force the persistent multi-tile path
+    // small K, no aliasing: operands staged by the GEMM itself (one launch, no limb planes in HBM)
+    static const bool no_direct = getenv("FFG_NO_DIRECT") && atoi(getenv("FFG_NO_DIRECT")) != 0;
+    // in place on B (the TRSM leaf X = inv(T) X) is race-free with one row tile: each CTA stages
+    // its whole column strip of B before the CTA's own epilogue overwrites exactly that strip
+    const bool c_is_b = C.d == B.d && C.ld == B.ld && C.rows == B.rows && C.cols == B.cols && M <= (size_t)BM;
+    const size_t kb_need = ceil_div(K, (size_t)BK);
+    const bool fits = kb_need == 1 ? direct_fits(L, 1) : (kb_need == 2 && direct_fits(L, 2));
+    if (!no_direct && fits && !overlap(C, A) && (c_is_b || !overlap(C, B))) {
+        ws.prof.begin(st);
+        const bool one = kb_need == 1;
+        switch (L) {
+            case 1: one ? launch_direct<1, 1>(F, alpha, beta, A, B, C, st) : launch_direct<1, 2>(F, alpha, beta, A, B, C, st); break;
+            case 2: one ? launch_direct<2, 1>(F, alpha, beta, A, B, C, st) : launch_direct<2, 2>(F, alpha, beta, A, B, C, st); break;
+            case 3: one ? launch_direct<3, 1>(F, alpha, beta, A, B, C, st) : launch_direct<3, 2>(F, alpha, beta, A, B, C, st); break;
+            default: one ? launch_direct<4, 1>(F, alpha, beta, A, B, C, st) : launch_direct<4, 2>(F, alpha, beta, A, B, C, st); break;
+        }
+        ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * K, 2.0 * (double)M * N * K);
+        if (launches) ++*launches;
+        return;
+    }
     const size_t Mp = round_up(M, BM), Np = round_up(N, NT);
     for (size_t k0 = 0; k0 < K; k0 += F.kmax) {  // delayed reduction: one fold per kmax chunk
         const size_t kc = std::min<size_t>(K - k0, F.kmax);
@@ -623,10 +1023,10 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         const uint32_t b = (k0 == 0) ? beta : 1u;
         ws.prof.begin(st);
         switch (L) {
-            case 1: launch_modgemm<1>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
-            case 2: launch_modgemm<2>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
-            case 3: launch_modgemm<3>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
-            default: launch_modgemm<4>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st); break;
+            case 1: launch_modgemm<1>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st, sm_cap); break;
+            case 2: launch_modgemm<2>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st, sm_cap); break;
+            case 3: launch_modgemm<3>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st, sm_cap); break;
+            default: launch_modgemm<4>(F, alpha, b, Ap, Bp, Mp, Np, Kp, C, st, sm_cap); break;
         }
         // algorithmic work: L^2 u8 limb products per field MAC -> 2 L^2 M N kc int8 tensor ops
         ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * kc, 2.0 * (double)M * N * kc);

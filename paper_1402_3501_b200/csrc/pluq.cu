@@ -91,6 +91,7 @@ struct Driver {
     bool use_factors = true;
 
     bool use_streams = true;
+    int lookahead_sms = 0;  // SM cap of the look-ahead GEMMs (FFG_LOOKAHEAD_SMS, default SMs - 32)
 
     // host-pipelined entry (pluq_tile_recursive_host): the top-left spine of the recursion
     // (the chain of first children from the root) starts on data already uploaded; spine[d]
@@ -119,6 +120,16 @@ struct Driver {
         // partitioned (multi-GPU) runs keep one stream: every rank must issue its NCCL
         // exchanges in the same order, and the replicated control flow guarantees that
         use_streams = !no_streams && !bl.ws.dist.active();
+        {
+            static int sms = -1;
+            if (sms < 0) {
+                int dev = 0;
+                FFG_CUDA(cudaGetDevice(&dev));
+                FFG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            }
+            static const char* env = getenv("FFG_LOOKAHEAD_SMS");
+            lookahead_sms = env ? atoi(env) : std::max(1, sms - 32);
+        }
         uint32_t* dev = nullptr;
         // the base kernel writes rank + moved ranges straight into host-mapped memory
         info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4 + 2, &dev));
@@ -326,7 +337,8 @@ struct Driver {
                 const size_t hm1 = (H.rows + 1) / 2, hn1 = (H.cols + 1) / 2;
                 if (use_streams && E.empty() && G.empty() && std::min(H.rows, H.cols) > thr) {
                     gemm_sub(b, Fb.sub(0, 0, hm1, r1), D.sub(0, 0, r1, hn1), H.sub(0, 0, hm1, hn1));
-                    const Blas la = on(lookahead(depth));
+                    Blas la = on(lookahead(depth));
+                    la.sm_cap = lookahead_sms;  // keep SMs free for the critical path
                     wait(la.st, mark_event(b.st));
                     gemm_sub(la, Fb.sub(0, 0, hm1, r1), D.sub(0, hn1, r1, H.cols - hn1),
                              H.sub(0, hn1, hm1, H.cols - hn1));
@@ -440,11 +452,14 @@ struct Driver {
 
 }  // namespace
 
+void base_dbg_dump();
+
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
     Driver drv(b, threshold, a.rows, a.cols);
     NodeRes res = drv.rec(a);
     drv.finish();
     drv.download(res, a.rows, a.cols, P, Q);
+    base_dbg_dump();
     return res.rank;
 }
 

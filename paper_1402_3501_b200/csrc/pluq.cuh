@@ -18,8 +18,9 @@ struct Blas {
     Workspace& ws;
     cudaStream_t st;
     uint64_t* launches;
+    int sm_cap = 0;  // > 0: tensor-core GEMMs on this stream use at most this many SMs
     void gemm(uint32_t alpha, DView A, DView B, uint32_t beta, DView C) const {
-        fgemm_dev(F, alpha, A, B, beta, C, st, ws, launches);
+        fgemm_dev(F, alpha, A, B, beta, C, st, ws, launches, sm_cap);
     }
     void count(uint64_t n = 1) const {
         if (launches) *launches += n;

@@ -249,3 +249,26 @@ def test_pluq_properties(gpu, oracle_lib, p, n, thr, kind):
         a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
         assert r_o == res.rank and np.array_equal(P_o, res.P) and np.array_equal(Q_o, res.Q)
         assert np.array_equal(a_o, packed)
+
+
+def test_simt_path_still_exact(gpu, oracle_lib, monkeypatch):
+    """The CUDA-core small-GEMM kernel (off by default, FFG_SIMT_MACS) stays bit-exact."""
+    G, _ = gpu
+    O = oracle_lib
+    p = 131071
+    monkeypatch.setenv("FFG_SIMT_MACS", str(1 << 24))
+    ctx = G.Context(0)  # the threshold is read at context creation
+    try:
+        rng = np.random.default_rng(5)
+        for (m, n, k) in ((1, 1, 1), (64, 64, 64), (100, 37, 250), (130, 70, 33)):
+            A = O.random_mat(p, m, k, int(rng.integers(1 << 30)))
+            B = O.random_mat(p, k, n, int(rng.integers(1 << 30)))
+            C0 = O.random_mat(p, m, n, int(rng.integers(1 << 30)))
+            want = O.fgemm(p, p - 1, A, B, 1, C0.copy())
+            got = C0.copy()
+            G.fgemm(p, p - 1, A, B, 1, got, ctx=ctx)
+            assert np.array_equal(got, want)
+    finally:
+        ctx.close()
+        monkeypatch.setenv("FFG_SIMT_MACS", "0")
+        G.Context(0).close()  # restore the default threshold
