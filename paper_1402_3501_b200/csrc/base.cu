@@ -24,6 +24,7 @@
 // Exhausted rows (rankrev.hpp:54-57) keep their zero Schur rows and zero L
 // entries for later pivots, as in the reference.
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include "pluq.cuh"
@@ -76,8 +77,9 @@ struct BaseLayout {
     uint32_t m, n, ns, rmax;  // ns = padded row stride of S (multiple of 8)
 };
 
-template <bool IN_SMEM>
-__global__ void __launch_bounds__(BASE_THREADS)
+constexpr int BASE_THREADS_REG = 512;
+template <bool IN_SMEM, bool REG>
+__global__ void __launch_bounds__(REG ? BASE_THREADS_REG : BASE_THREADS, 1)
     rr_base_kernel(uint32_t* __restrict__ A, uint64_t lda, BaseLayout lay, uint32_t* __restrict__ scratch,
                    uint32_t* __restrict__ Pd, uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p,
                    uint64_t mu, uint32_t* __restrict__ inv_out) {
@@ -103,115 +105,259 @@ __global__ void __launch_bounds__(BASE_THREADS)
     uint32_t* S = IN_SMEM ? tail : scratch;             // m x ns
     uint32_t* Lb = IN_SMEM ? tail + (size_t)m * ns : scratch + (size_t)m * ns;  // m x rmax numerators
 
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = BASE_THREADS / 32;
-    for (uint32_t t = warp; t < m; t += nwarps) {
-        for (uint32_t u = lane; u < ns; u += 32) S[(size_t)t * ns + u] = u < n ? A[(uint64_t)t * lda + u] : 0u;
-        for (uint32_t u = lane; u < rmax; u += 32) Lb[(size_t)t * rmax + u] = 0u;
-    }
-    __syncthreads();
+    constexpr uint32_t NTH = REG ? BASE_THREADS_REG : BASE_THREADS;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = NTH / 32;
+    uint32_t r = 0;
+    if constexpr (REG) {
+        // ---- phase 1, register-resident (m, n <= 64).  Row i lives in the registers of the 8
+        // lanes 8i..8i+7 (8 columns each; 16 warps x 4 rows) and, for indexed reads, in S.
+        // Values are kept lazily reduced in [0, 4p): an update is two Shoup products without
+        // their final corrections plus one add (7 instructions per element); zero tests and
+        // the pivot row use fully reduced values.  Per pivot one barrier: the warp holding the
+        // first row after the pivot finds the next pivot (first nonzero row, first nonzero
+        // column: rr_base's row-major search, rankrev.hpp:40-57) and publishes it; only when
+        // that warp's rows are all zero (rank deficiency) does every warp search (slow path).
+        constexpr uint32_t FULL = 0xffffffffu;
+        constexpr uint32_t LEAD_NONE = NONE - 1;  // the lead warp found no nonzero row
+        uint32_t* hdr = Lb + (size_t)m * rmax;    // [2] x {row, col, value, shoup(value)}
+        hdr += (4 - (reinterpret_cast<uintptr_t>(hdr) / 4) % 4) % 4;
+        uint32_t* cand = hdr + 8;                 // [2][64] pivot row (reduced)
+        uint32_t* srow = cand + 128;              // [16] slow path: candidate row per warp
+        uint32_t* sval = srow + 16;               // [16][64] slow path: candidate values
+        uint32_t* shdr = sval + 16 * 64;          // [16] x {col, value, shoup(value), -}
+        const uint32_t i = tid >> 3, c0 = (tid & 7) * 8;
+        const uint32_t p2 = 2 * p;
+        auto red = [&](uint32_t x) {  // [0, 4p) -> [0, p)
+            x = min(x, x - p2);
+            return min(x, x - p);
+        };
+        uint32_t v[8];
+        {
+            const uint32_t* src = A + (uint64_t)(i < m ? i : 0) * lda;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (i < m && c0 + u < n) ? src[c0 + u] : 0u;
+        }
+        auto store_row = [&]() {
+            if (i < m && c0 < ns) {
+                uint4* d = reinterpret_cast<uint4*>(S + (size_t)i * ns + c0);
+                d[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                d[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            }
+        };
+        store_row();  // numerators are read back from S by column index
+        for (uint32_t idx = tid; idx < m * rmax; idx += NTH) Lb[idx] = 0u;
+        // first nonzero row >= first of this warp: reduced-OR per row, ballot over the warp
+        auto warp_first = [&](uint32_t first) -> uint32_t {
+            uint32_t o = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) o |= red(v[u]);
+            o |= __shfl_xor_sync(FULL, o, 1);
+            o |= __shfl_xor_sync(FULL, o, 2);
+            o |= __shfl_xor_sync(FULL, o, 4);
+            const uint32_t bal = __ballot_sync(FULL, i < m && i >= first && o != 0);
+            return bal ? (warp * 4 + ((__ffs(bal) - 1) >> 3)) : NONE;
+        };
+        // the row c of this warp becomes a candidate: its reduced values to dst[64], then the
+        // first nonzero column by two ballots over the stored row
+        auto emit = [&](uint32_t c, uint32_t* dst, uint32_t* out_col, uint32_t* out_val, uint32_t* out_pre) {
+            if (i == c) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = red(v[u]);
+                uint4* d = reinterpret_cast<uint4*>(dst + c0);
+                d[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                d[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            }
+            __syncwarp();
+            const uint32_t x0 = dst[lane], x1 = dst[lane + 32];
+            const uint32_t b0 = __ballot_sync(FULL, x0 != 0), b1 = __ballot_sync(FULL, x1 != 0);
+            const uint32_t pj = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
+            if (lane == 0) {
+                const uint32_t pv = dst[pj];
+                *out_col = pj;
+                *out_val = pv;
+                *out_pre = shoup_pre(pv, p, mu);
+            }
+        };
+        auto lead_publish = [&](uint32_t buf, uint32_t first) {  // rows >= first are eligible
+            if (first >= m) {
+                if (tid == 0) hdr[buf * 4] = NONE;
+                return;
+            }
+            if (warp != first / 4) return;
+            const uint32_t c = warp_first(first);
+            if (c == NONE) {
+                if (lane == 0) hdr[buf * 4] = LEAD_NONE;
+                return;
+            }
+            emit(c, cand + buf * 64, hdr + buf * 4 + 1, hdr + buf * 4 + 2, hdr + buf * 4 + 3);
+            if (lane == 0) hdr[buf * 4] = c;
+        };
+        lead_publish(0, 0);
+        __syncthreads();
+        uint32_t buf = 0, first = 0;
+        const uint32_t warp_last_row = warp * 4 + 3;
+        while (r < n) {
+            const uint4 hh = reinterpret_cast<const uint4*>(hdr)[buf];
+            uint32_t pi = hh.x, pj = hh.y, pv = hh.z, pvp = hh.w;
+            const uint32_t* prw = cand + buf * 64;
+            if (pi == LEAD_NONE) {  // slow path (uniform): every warp offers its first nonzero row
+                const uint32_t c = warp_first(first);
+                if (lane == 0) srow[warp] = c;
+                if (c != NONE) emit(c, sval + warp * 64, shdr + warp * 4, shdr + warp * 4 + 1, shdr + warp * 4 + 2);
+                __syncthreads();
+                uint32_t ws = NONE;
+                for (uint32_t w = 0; w < nwarps && ws == NONE; ++w)
+                    if (srow[w] != NONE) ws = w;
+                if (ws == NONE) break;  // uniform: no nonzero row left
+                pi = srow[ws];
+                pj = shdr[ws * 4];
+                pv = shdr[ws * 4 + 1];
+                pvp = shdr[ws * 4 + 2];
+                prw = sval + ws * 64;
+            } else if (pi == NONE) {
+                break;  // uniform
+            }
+            if (tid == 0) {
+                prow[r] = pi;
+                pcol[r] = pj;
+                pivv[r] = pv;
+            }
+            if (warp_last_row > pi && i > pi && i < m) {  // warps past their last row only keep step
+                const uint32_t numer = red(S[(size_t)i * ns + pj]);
+                if ((tid & 7) == 0) Lb[(size_t)i * rmax + r] = numer;
+                const uint32_t nump = shoup_pre(numer, p, mu);
+                const uint4 b0 = reinterpret_cast<const uint4*>(prw + c0)[0];
+                const uint4 b1 = reinterpret_cast<const uint4*>(prw + c0)[1];
+                const uint32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t a = v[u] * pv - __umulhi(v[u], pvp) * p;   // [0, 2p)
+                    const uint32_t s = b[u] * numer - __umulhi(b[u], nump) * p;  // [0, 2p)
+                    v[u] = a + p2 - s;                                          // (0, 4p)
+                }
+                store_row();
+            }
+            ++r;
+            buf ^= 1;
+            first = pi + 1;
+            lead_publish(buf, first);
+            __syncthreads();
+        }
+        // reduced final rows for phase 2
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = red(v[u]);
+        store_row();
+        __syncthreads();
+    } else {
+        for (uint32_t t = warp; t < m; t += nwarps) {
+            for (uint32_t u = lane; u < ns; u += 32) S[(size_t)t * ns + u] = u < n ? A[(uint64_t)t * lda + u] : 0u;
+            for (uint32_t u = lane; u < rmax; u += 32) Lb[(size_t)t * rmax + u] = 0u;
+        }
+        __syncthreads();
 
-    const uint32_t ngroups = ns / 8;
-    uint32_t lg = 0;  // row segment = 2^lg lanes >= ngroups
-    while ((1u << lg) < ngroups) ++lg;
-    const uint32_t seg = 1u << lg;
-    uint32_t r = 0, cur = 0;
-    while (cur < m && r < n) {
-        // row-major pivot search (rankrev.hpp:40-57), done redundantly by every warp so no
-        // barrier separates it from the update; pivot columns are already 0 in rows >= cur,
-        // and rows in [cur, pi] are never written during this step
-        uint32_t pi = m, pj = n;
-        for (uint32_t i = cur; i < m && pi == m; ++i) {
-            const uint32_t* row = S + (size_t)i * ns;
-            for (uint32_t jc = 0; jc < n; jc += 32) {
-                const uint32_t j = jc + lane;
-                const uint32_t bal = __ballot_sync(0xffffffffu, j < n && row[j] != 0);
-                if (bal) {
-                    pi = i;
-                    pj = jc + __ffs(bal) - 1;
-                    break;
+        const uint32_t ngroups = ns / 8;
+        uint32_t lg = 0;  // row segment = 2^lg lanes >= ngroups
+        while ((1u << lg) < ngroups) ++lg;
+        const uint32_t seg = 1u << lg;
+        uint32_t cur = 0;
+        while (cur < m && r < n) {
+            // row-major pivot search (rankrev.hpp:40-57), done redundantly by every warp so no
+            // barrier separates it from the update; pivot columns are already 0 in rows >= cur,
+            // and rows in [cur, pi] are never written during this step
+            uint32_t pi = m, pj = n;
+            for (uint32_t i = cur; i < m && pi == m; ++i) {
+                const uint32_t* row = S + (size_t)i * ns;
+                for (uint32_t jc = 0; jc < n; jc += 32) {
+                    const uint32_t j = jc + lane;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, j < n && row[j] != 0);
+                    if (bal) {
+                        pi = i;
+                        pj = jc + __ffs(bal) - 1;
+                        break;
+                    }
                 }
             }
-        }
-        if (pi >= m) break;  // uniform: every warp found the same (pi, pj)
-        const uint32_t* prw = S + (size_t)pi * ns;
-        const uint32_t pv = prw[pj];
-        const uint32_t pvp = shoup_pre(pv, p, mu);
-        if (tid == 0) {
-            prow[r] = pi;
-            pcol[r] = pj;
-            pivv[r] = pv;
-        }
-        const uint32_t rows_below = m - pi - 1;
-        if (seg <= 32) {
-            // a row's column groups sit in one warp segment of `seg` lanes: the lane holding
-            // column pj broadcasts the numerator by shuffle before anyone overwrites it
-            const uint32_t lseg = lane & (seg - 1), sbase = lane - lseg, owner = sbase + (pj >> 3);
-            const uint32_t q = pj & 7;
-            for (uint32_t r0 = warp << (5 - lg); r0 < rows_below; r0 += nwarps << (5 - lg)) {
-                const uint32_t i = pi + 1 + r0 + (lane >> lg);
-                const bool live = i < m && lseg < ngroups;
-                const uint32_t g = live ? lseg : 0u;
-                uint32_t* row = S + (size_t)(live ? i : pi) * ns + g * 8;
-                const uint4 a0 = reinterpret_cast<const uint4*>(row)[0], a1 = reinterpret_cast<const uint4*>(row)[1];
-                const uint4 b0 = reinterpret_cast<const uint4*>(prw + g * 8)[0];
-                const uint4 b1 = reinterpret_cast<const uint4*>(prw + g * 8)[1];
-                const uint32_t lo = (q & 2) ? ((q & 1) ? a0.w : a0.z) : ((q & 1) ? a0.y : a0.x);
-                const uint32_t hi = (q & 2) ? ((q & 1) ? a1.w : a1.z) : ((q & 1) ? a1.y : a1.x);
-                const uint32_t numer = __shfl_sync(0xffffffffu, (q & 4) ? hi : lo, owner);
-                if (!live) continue;
-                const uint32_t nump = shoup_pre(numer, p, mu);
-                uint4 o0, o1;
-                o0.x = sub_mod(shoup_mul(a0.x, pv, pvp, p), shoup_mul(b0.x, numer, nump, p), p);
-                o0.y = sub_mod(shoup_mul(a0.y, pv, pvp, p), shoup_mul(b0.y, numer, nump, p), p);
-                o0.z = sub_mod(shoup_mul(a0.z, pv, pvp, p), shoup_mul(b0.z, numer, nump, p), p);
-                o0.w = sub_mod(shoup_mul(a0.w, pv, pvp, p), shoup_mul(b0.w, numer, nump, p), p);
-                o1.x = sub_mod(shoup_mul(a1.x, pv, pvp, p), shoup_mul(b1.x, numer, nump, p), p);
-                o1.y = sub_mod(shoup_mul(a1.y, pv, pvp, p), shoup_mul(b1.y, numer, nump, p), p);
-                o1.z = sub_mod(shoup_mul(a1.z, pv, pvp, p), shoup_mul(b1.z, numer, nump, p), p);
-                o1.w = sub_mod(shoup_mul(a1.w, pv, pvp, p), shoup_mul(b1.w, numer, nump, p), p);
-                if (lseg == (pj >> 3)) Lb[(size_t)i * rmax + r] = numer;
-                reinterpret_cast<uint4*>(row)[0] = o0;
-                reinterpret_cast<uint4*>(row)[1] = o1;
+            if (pi >= m) break;  // uniform: every warp found the same (pi, pj)
+            const uint32_t* prw = S + (size_t)pi * ns;
+            const uint32_t pv = prw[pj];
+            const uint32_t pvp = shoup_pre(pv, p, mu);
+            if (tid == 0) {
+                prow[r] = pi;
+                pcol[r] = pj;
+                pivv[r] = pv;
             }
-        } else {
-            // wide rows: save the L numerators of column pj before the update zeroes it
-            __syncthreads();  // every warp has finished reading the pivot row / numerators
-            for (uint32_t i = pi + 1 + tid; i < m; i += BASE_THREADS)
-                Lb[(size_t)i * rmax + r] = S[(size_t)i * ns + pj];
+            const uint32_t rows_below = m - pi - 1;
+            if (seg <= 32) {
+                // a row's column groups sit in one warp segment of `seg` lanes: the lane holding
+                // column pj broadcasts the numerator by shuffle before anyone overwrites it
+                const uint32_t lseg = lane & (seg - 1), sbase = lane - lseg, owner = sbase + (pj >> 3);
+                const uint32_t q = pj & 7;
+                for (uint32_t r0 = warp << (5 - lg); r0 < rows_below; r0 += nwarps << (5 - lg)) {
+                    const uint32_t i = pi + 1 + r0 + (lane >> lg);
+                    const bool live = i < m && lseg < ngroups;
+                    const uint32_t g = live ? lseg : 0u;
+                    uint32_t* row = S + (size_t)(live ? i : pi) * ns + g * 8;
+                    const uint4 a0 = reinterpret_cast<const uint4*>(row)[0], a1 = reinterpret_cast<const uint4*>(row)[1];
+                    const uint4 b0 = reinterpret_cast<const uint4*>(prw + g * 8)[0];
+                    const uint4 b1 = reinterpret_cast<const uint4*>(prw + g * 8)[1];
+                    const uint32_t lo = (q & 2) ? ((q & 1) ? a0.w : a0.z) : ((q & 1) ? a0.y : a0.x);
+                    const uint32_t hi = (q & 2) ? ((q & 1) ? a1.w : a1.z) : ((q & 1) ? a1.y : a1.x);
+                    const uint32_t numer = __shfl_sync(0xffffffffu, (q & 4) ? hi : lo, owner);
+                    if (!live) continue;
+                    const uint32_t nump = shoup_pre(numer, p, mu);
+                    uint4 o0, o1;
+                    o0.x = sub_mod(shoup_mul(a0.x, pv, pvp, p), shoup_mul(b0.x, numer, nump, p), p);
+                    o0.y = sub_mod(shoup_mul(a0.y, pv, pvp, p), shoup_mul(b0.y, numer, nump, p), p);
+                    o0.z = sub_mod(shoup_mul(a0.z, pv, pvp, p), shoup_mul(b0.z, numer, nump, p), p);
+                    o0.w = sub_mod(shoup_mul(a0.w, pv, pvp, p), shoup_mul(b0.w, numer, nump, p), p);
+                    o1.x = sub_mod(shoup_mul(a1.x, pv, pvp, p), shoup_mul(b1.x, numer, nump, p), p);
+                    o1.y = sub_mod(shoup_mul(a1.y, pv, pvp, p), shoup_mul(b1.y, numer, nump, p), p);
+                    o1.z = sub_mod(shoup_mul(a1.z, pv, pvp, p), shoup_mul(b1.z, numer, nump, p), p);
+                    o1.w = sub_mod(shoup_mul(a1.w, pv, pvp, p), shoup_mul(b1.w, numer, nump, p), p);
+                    if (lseg == (pj >> 3)) Lb[(size_t)i * rmax + r] = numer;
+                    reinterpret_cast<uint4*>(row)[0] = o0;
+                    reinterpret_cast<uint4*>(row)[1] = o1;
+                }
+            } else {
+                // wide rows: save the L numerators of column pj before the update zeroes it
+                __syncthreads();  // every warp has finished reading the pivot row / numerators
+                for (uint32_t i = pi + 1 + tid; i < m; i += NTH)
+                    Lb[(size_t)i * rmax + r] = S[(size_t)i * ns + pj];
+                __syncthreads();
+                for (uint32_t idx = tid; idx < rows_below * ngroups; idx += NTH) {
+                    const uint32_t i = pi + 1 + idx / ngroups, g = idx % ngroups;
+                    uint32_t* row = S + (size_t)i * ns + g * 8;
+                    const uint32_t numer = Lb[(size_t)i * rmax + r];
+                    const uint32_t nump = shoup_pre(numer, p, mu);
+                    const uint4 a0 = reinterpret_cast<const uint4*>(row)[0], a1 = reinterpret_cast<const uint4*>(row)[1];
+                    const uint4 b0 = reinterpret_cast<const uint4*>(prw + g * 8)[0];
+                    const uint4 b1 = reinterpret_cast<const uint4*>(prw + g * 8)[1];
+                    uint4 o0, o1;
+                    o0.x = sub_mod(shoup_mul(a0.x, pv, pvp, p), shoup_mul(b0.x, numer, nump, p), p);
+                    o0.y = sub_mod(shoup_mul(a0.y, pv, pvp, p), shoup_mul(b0.y, numer, nump, p), p);
+                    o0.z = sub_mod(shoup_mul(a0.z, pv, pvp, p), shoup_mul(b0.z, numer, nump, p), p);
+                    o0.w = sub_mod(shoup_mul(a0.w, pv, pvp, p), shoup_mul(b0.w, numer, nump, p), p);
+                    o1.x = sub_mod(shoup_mul(a1.x, pv, pvp, p), shoup_mul(b1.x, numer, nump, p), p);
+                    o1.y = sub_mod(shoup_mul(a1.y, pv, pvp, p), shoup_mul(b1.y, numer, nump, p), p);
+                    o1.z = sub_mod(shoup_mul(a1.z, pv, pvp, p), shoup_mul(b1.z, numer, nump, p), p);
+                    o1.w = sub_mod(shoup_mul(a1.w, pv, pvp, p), shoup_mul(b1.w, numer, nump, p), p);
+                    reinterpret_cast<uint4*>(row)[0] = o0;
+                    reinterpret_cast<uint4*>(row)[1] = o1;
+                }
+            }
+            ++r;
+            cur = pi + 1;
             __syncthreads();
-            for (uint32_t idx = tid; idx < rows_below * ngroups; idx += BASE_THREADS) {
-                const uint32_t i = pi + 1 + idx / ngroups, g = idx % ngroups;
-                uint32_t* row = S + (size_t)i * ns + g * 8;
-                const uint32_t numer = Lb[(size_t)i * rmax + r];
-                const uint32_t nump = shoup_pre(numer, p, mu);
-                const uint4 a0 = reinterpret_cast<const uint4*>(row)[0], a1 = reinterpret_cast<const uint4*>(row)[1];
-                const uint4 b0 = reinterpret_cast<const uint4*>(prw + g * 8)[0];
-                const uint4 b1 = reinterpret_cast<const uint4*>(prw + g * 8)[1];
-                uint4 o0, o1;
-                o0.x = sub_mod(shoup_mul(a0.x, pv, pvp, p), shoup_mul(b0.x, numer, nump, p), p);
-                o0.y = sub_mod(shoup_mul(a0.y, pv, pvp, p), shoup_mul(b0.y, numer, nump, p), p);
-                o0.z = sub_mod(shoup_mul(a0.z, pv, pvp, p), shoup_mul(b0.z, numer, nump, p), p);
-                o0.w = sub_mod(shoup_mul(a0.w, pv, pvp, p), shoup_mul(b0.w, numer, nump, p), p);
-                o1.x = sub_mod(shoup_mul(a1.x, pv, pvp, p), shoup_mul(b1.x, numer, nump, p), p);
-                o1.y = sub_mod(shoup_mul(a1.y, pv, pvp, p), shoup_mul(b1.y, numer, nump, p), p);
-                o1.z = sub_mod(shoup_mul(a1.z, pv, pvp, p), shoup_mul(b1.z, numer, nump, p), p);
-                o1.w = sub_mod(shoup_mul(a1.w, pv, pvp, p), shoup_mul(b1.w, numer, nump, p), p);
-                reinterpret_cast<uint4*>(row)[0] = o0;
-                reinterpret_cast<uint4*>(row)[1] = o1;
-            }
         }
-        ++r;
-        cur = pi + 1;
-        __syncthreads();
     }
 
     if (dbg) base_stamp(dbg + 2);
     // ---- phase 2: exact values (pivot inverses in parallel, prefix products, scaling)
-    for (uint32_t k = tid; k < r; k += BASE_THREADS) invp[k] = inv_mod_bin(pivv[k], p);
-    for (uint32_t i = tid; i < m; i += BASE_THREADS) rowrank[i] = NONE;
-    for (uint32_t j = tid; j < n; j += BASE_THREADS) colrank[j] = NONE;
+    for (uint32_t k = tid; k < r; k += NTH) invp[k] = inv_mod_bin(pivv[k], p);
+    for (uint32_t i = tid; i < m; i += NTH) rowrank[i] = NONE;
+    for (uint32_t j = tid; j < n; j += NTH) colrank[j] = NONE;
     __syncthreads();
-    for (uint32_t k = tid; k < r; k += BASE_THREADS) {
+    for (uint32_t k = tid; k < r; k += NTH) {
         rowrank[prow[k]] = k;
         colrank[pcol[k]] = k;
     }
@@ -272,8 +418,8 @@ __global__ void __launch_bounds__(BASE_THREADS)
     }
     __syncthreads();
     if (dbg) base_stamp(dbg + 4);
-    for (uint32_t i = tid; i < m; i += BASE_THREADS) Pd[i] = Psh[i];
-    for (uint32_t j = tid; j < n; j += BASE_THREADS) Qd[j] = Qsh[j];
+    for (uint32_t i = tid; i < m; i += NTH) Pd[i] = Psh[i];
+    for (uint32_t j = tid; j < n; j += NTH) Qd[j] = Qsh[j];
     // packed output: out[t][u] for original row i = P[t], column j = Q[u]
     for (uint32_t t = warp; t < m; t += nwarps) {
         const uint32_t i = Psh[t];
@@ -308,7 +454,7 @@ __global__ void __launch_bounds__(BASE_THREADS)
         uint32_t* Xs = Ts + INV_MAX * (INV_MAX + 1);
         uint32_t* Ws = Xs + INV_MAX * (INV_MAX + 1);
         uint32_t* dv = Ws + (INV_MAX / 2) * (INV_MAX / 2);
-        for (uint32_t idx = tid; idx < r * r; idx += BASE_THREADS) {
+        for (uint32_t idx = tid; idx < r * r; idx += NTH) {
             const uint32_t i = idx / r, j = idx % r;
             Ts[i * (INV_MAX + 1) + j] = A[(uint64_t)i * lda + j];
         }
@@ -325,7 +471,7 @@ __global__ void __launch_bounds__(BASE_THREADS)
                 else tri_inverse_smem<true, 64>(Ts, INV_MAX + 1, Xs, INV_MAX + 1, Ws, dv, r, p, mu);
             }
             uint32_t* out = inv_out + (size_t)which * r * r;
-            for (uint32_t idx = tid; idx < r * r; idx += BASE_THREADS) out[idx] = Xs[(idx / r) * (INV_MAX + 1) + idx % r];
+            for (uint32_t idx = tid; idx < r * r; idx += NTH) out[idx] = Xs[(idx / r) * (INV_MAX + 1) + idx % r];
             __syncthreads();
         }
         if (tid == 0) info->cached = 1;
@@ -337,7 +483,7 @@ void base_dbg_init() {
     if (done || !getenv("FFG_BASE_DBG")) return;
     done = true;
     unsigned long long* buf = nullptr;
-    FFG_CUDA(cudaMalloc(&buf, 4096 * 6 * 8));
+    FFG_CUDA(cudaMalloc(&buf, 4097 * 6 * 8));
     FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg, &buf, sizeof(buf)));
 }
 
@@ -379,28 +525,38 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const size_t inv_bytes = (2 * INV_MAX * (INV_MAX + 1) + (INV_MAX / 2) * (INV_MAX / 2) + INV_MAX + 8) * 4;
     if (inv_out && (fixed + blk + inv_bytes > BASE_SMEM_LIMIT)) inv_out = nullptr;
     b.ws.prof.begin(b.st);
-    if (fixed + blk <= BASE_SMEM_LIMIT) {
-        static bool set = false;
-        if (!set) {
-            FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static const bool no_reg = getenv("FFG_BASE_SMEM") && atoi(getenv("FFG_BASE_SMEM")) != 0;
+    const bool reg = !no_reg && lay.m <= 64 && lay.n <= 64;
+    const size_t slots = (8 + 128 + 16 + 16 * 64 + 64 + 4) * 4;  // candidate slots of the register path
+    if (reg && fixed + blk + slots <= BASE_SMEM_LIMIT) {
+        inv_out = nullptr;  // the register path does not cache factor inverses
+        static std::once_flag once;
+        std::call_once(once, [] {
+            FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)BASE_SMEM_LIMIT));
-            set = true;
-        }
-        rr_base_kernel<true><<<1, BASE_THREADS, fixed + blk + (inv_out ? inv_bytes : 0), b.st>>>(
+        });
+        rr_base_kernel<true, true><<<1, BASE_THREADS_REG, fixed + blk + slots, b.st>>>(a.d, a.ld, lay, nullptr, Pd, Qd,
+                                                                                   info, b.F.p, b.F.mu, nullptr);
+    } else if (fixed + blk <= BASE_SMEM_LIMIT) {
+        static std::once_flag once;
+        std::call_once(once, [] {
+            FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)BASE_SMEM_LIMIT));
+        });
+        rr_base_kernel<true, false><<<1, BASE_THREADS, fixed + blk + (inv_out ? inv_bytes : 0), b.st>>>(
             a.d, a.ld, lay, nullptr, Pd, Qd, info, b.F.p, b.F.mu, inv_out);
     } else {
         inv_out = nullptr;
         if (fixed > BASE_SMEM_LIMIT) throw Error(FFG_ERR_INVALID_BLOCK, "base case block too large");
-        static bool set = false;
-        if (!set) {
-            FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        static std::once_flag once;
+        std::call_once(once, [] {
+            FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)BASE_SMEM_LIMIT));
-            set = true;
-        }
+        });
         uint32_t* scratch = nullptr;
         FFG_CUDA(cudaMallocAsync(&scratch, blk, b.st));
-        rr_base_kernel<false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, lay, scratch, Pd, Qd, info, b.F.p, b.F.mu,
-                                                                nullptr);
+        rr_base_kernel<false, false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, lay, scratch, Pd, Qd, info, b.F.p,
+                                                                       b.F.mu, nullptr);
         FFG_CUDA(cudaFreeAsync(scratch, b.st));
     }
     FFG_CUDA(cudaGetLastError());

@@ -577,10 +577,19 @@ void trsm_rec(const TrsmCtx& c, size_t o, size_t t, DView B) {
             return;
         }
         DView inv{const_cast<uint32_t*>(c.Tinv) + (o / TB) * TB * TB, t, t, (size_t)TB};
-        if (c.side == 0)
-            c.b.gemm(1, inv, B, 0, B);
-        else
-            c.b.gemm(1, B, inv, 0, B);
+        if (c.side == 0) {
+            c.b.gemm(1, inv, B, 0, B);  // t <= 128 rows: in place on B is safe in the direct GEMM
+        } else {
+            // X = B inv in place would alias the A operand across column tiles (split path);
+            // out of place through a pooled temporary keeps it on the one-launch direct GEMM
+            uint32_t* tmp = nullptr;
+            FFG_CUDA(cudaMallocAsync(&tmp, B.rows * B.cols * 4, c.b.st));
+            DView X{tmp, B.rows, B.cols, B.cols};
+            c.b.gemm(1, B, inv, 0, X);
+            FFG_CUDA(cudaMemcpy2DAsync(B.d, B.ld * 4, tmp, B.cols * 4, B.cols * 4, B.rows, cudaMemcpyDeviceToDevice,
+                                       c.b.st));
+            FFG_CUDA(cudaFreeAsync(tmp, c.b.st));
+        }
         return;
     }
     const size_t nb = ceil_div(t, TB);
