@@ -66,6 +66,7 @@ __device__ __forceinline__ uint32_t inv_mod_bin(uint32_t a, uint32_t p) {
 // diagnostics (FFG_BASE_DBG): per launch {clock64, globaltimer} at entry, end of pivoting, exit
 __device__ unsigned long long* g_base_dbg = nullptr;
 __device__ unsigned int g_base_dbg_n = 0;
+__device__ int g_base_skip = 0;  // experiment: skip the update arithmetic (timing only)
 __device__ __forceinline__ void base_stamp(unsigned long long* slot) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -82,7 +83,7 @@ template <bool IN_SMEM, bool REG>
 __global__ void __launch_bounds__(REG ? BASE_THREADS_REG : BASE_THREADS, 1)
     rr_base_kernel(uint32_t* __restrict__ A, uint64_t lda, BaseLayout lay, uint32_t* __restrict__ scratch,
                    uint32_t* __restrict__ Pd, uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p,
-                   uint64_t mu, uint32_t* __restrict__ inv_out) {
+                   uint64_t mu, uint32_t* __restrict__ inv_out, uint32_t seq) {
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t m = lay.m, n = lay.n, ns = lay.ns, rmax = lay.rmax;
     unsigned long long* dbg = nullptr;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(REG ? BASE_THREADS_REG : BASE_THREADS, 1)
                 pcol[r] = pj;
                 pivv[r] = pv;
             }
-            if (warp_last_row > pi && i > pi && i < m) {  // warps past their last row only keep step
+            if (!g_base_skip && warp_last_row > pi && i > pi && i < m) {  // warps past their last row only keep step
                 const uint32_t numer = red(S[(size_t)i * ns + pj]);
                 if ((tid & 7) == 0) Lb[(size_t)i * rmax + r] = numer;
                 const uint32_t nump = shoup_pre(numer, p, mu);
@@ -443,11 +444,9 @@ __global__ void __launch_bounds__(REG ? BASE_THREADS_REG : BASE_THREADS, 1)
     }
     // inverses of the leading r x r factors (L unit lower, U upper) for the TRSMs that will use
     // this block as their triangle: a base case is a leaf of every such TRSM
-    if (IN_SMEM && inv_out != nullptr) {
-        if (r == 0 || r > INV_MAX) {
-            if (tid == 0) info->cached = 0;
-            return;
-        }
+    if (IN_SMEM && inv_out != nullptr && (r == 0 || r > INV_MAX)) {
+        if (tid == 0) info->cached = 0;
+    } else if (IN_SMEM && inv_out != nullptr) {
         __syncthreads();  // the packed block in A (global) is complete and visible to the CTA
         uint32_t* Ts = S + (size_t)m * ns + (size_t)m * rmax;  // scratch after S and Lb
         Ts += (4 - (reinterpret_cast<uintptr_t>(Ts) / 4) % 4) % 4;
@@ -476,6 +475,13 @@ __global__ void __launch_bounds__(REG ? BASE_THREADS_REG : BASE_THREADS, 1)
         }
         if (tid == 0) info->cached = 1;
     }
+    // completion mailbox: every info field above is written before the sequence number the host
+    // spins on (barrier + system fence by the publishing thread, which is cumulative)
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+    }
 }
 
 void base_dbg_init() {
@@ -485,6 +491,10 @@ void base_dbg_init() {
     unsigned long long* buf = nullptr;
     FFG_CUDA(cudaMalloc(&buf, 4097 * 6 * 8));
     FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg, &buf, sizeof(buf)));
+    if (getenv("FFG_BASE_SKIP")) {
+        int one = 1;
+        FFG_CUDA(cudaMemcpyToSymbol(g_base_skip, &one, sizeof(one)));
+    }
 }
 
 void base_dbg_dump() {
@@ -511,7 +521,8 @@ void base_dbg_dump() {
     FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg_n, &zero, sizeof(zero)));
 }
 
-bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv_out) {
+bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv_out,
+                    uint32_t seq) {
     base_dbg_init();
     BaseLayout lay;
     lay.m = (uint32_t)a.rows;
@@ -536,7 +547,7 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
                                           (int)BASE_SMEM_LIMIT));
         });
         rr_base_kernel<true, true><<<1, BASE_THREADS_REG, fixed + blk + slots, b.st>>>(a.d, a.ld, lay, nullptr, Pd, Qd,
-                                                                                   info, b.F.p, b.F.mu, nullptr);
+                                                                                   info, b.F.p, b.F.mu, nullptr, seq);
     } else if (fixed + blk <= BASE_SMEM_LIMIT) {
         static std::once_flag once;
         std::call_once(once, [] {
@@ -544,7 +555,7 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
                                           (int)BASE_SMEM_LIMIT));
         });
         rr_base_kernel<true, false><<<1, BASE_THREADS, fixed + blk + (inv_out ? inv_bytes : 0), b.st>>>(
-            a.d, a.ld, lay, nullptr, Pd, Qd, info, b.F.p, b.F.mu, inv_out);
+            a.d, a.ld, lay, nullptr, Pd, Qd, info, b.F.p, b.F.mu, inv_out, seq);
     } else {
         inv_out = nullptr;
         if (fixed > BASE_SMEM_LIMIT) throw Error(FFG_ERR_INVALID_BLOCK, "base case block too large");
@@ -556,7 +567,7 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
         uint32_t* scratch = nullptr;
         FFG_CUDA(cudaMallocAsync(&scratch, blk, b.st));
         rr_base_kernel<false, false><<<1, BASE_THREADS, fixed, b.st>>>(a.d, a.ld, lay, scratch, Pd, Qd, info, b.F.p,
-                                                                       b.F.mu, nullptr);
+                                                                       b.F.mu, nullptr, seq);
         FFG_CUDA(cudaFreeAsync(scratch, b.st));
     }
     FFG_CUDA(cudaGetLastError());

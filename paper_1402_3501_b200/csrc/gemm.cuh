@@ -95,6 +95,7 @@ private:
 class Workspace {
 public:
     Profiler prof;
+    uint32_t base_seq = 0;  // sequence numbers of base-case completion mailboxes
     Dist dist;  // multi-GPU partitioning of the recursion's large operations (dist.cuh)
     ~Workspace() {
         for (auto& kv : bufs_)

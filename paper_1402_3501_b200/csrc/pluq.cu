@@ -18,6 +18,7 @@
 // "O = N - J*V2" describes.  Outputs equal the fixed reference everywhere and
 // the unmodified reference wherever r2 == 0 or r3 == 0 (all full-rank input).
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <deque>
 #include <vector>
@@ -173,13 +174,34 @@ struct Driver {
         return &factors.back();
     }
 
+    // The base kernel writes its result into host-mapped memory and then the launch's sequence
+    // number; spinning on it returns within a few microseconds of the kernel's end (an event
+    // wait costs tens).  A slow or failed kernel falls back to the blocking event wait, which
+    // also reports launch errors.
+    void wait_mailbox(uint32_t seq) {
+        volatile uint32_t* s = &info_host->seq;
+        for (int it = 0; it < (1 << 18); ++it) {
+            if (*s == seq) {
+                std::atomic_thread_fence(std::memory_order_acquire);
+                return;
+            }
+#if defined(__x86_64__) || defined(__i386__)
+            __builtin_ia32_pause();
+#endif
+        }
+        FFG_CUDA(cudaEventRecord(ev, b.st));
+        FFG_CUDA(cudaEventSynchronize(ev));
+        if (*s != seq) throw Error(FFG_ERR_INTERNAL, "base case did not report its rank");
+        std::atomic_thread_fence(std::memory_order_acquire);
+    }
+
     NodeRes base(DView a, NodeRes res) {
         const size_t rmax = std::min(a.rows, a.cols);
         uint32_t* slot = nullptr;
         if (use_factors && rmax <= 64 && inv_top + 2 * rmax * rmax <= inv_cap) slot = inv_arena + inv_top;
-        const bool asked = rr_base_launch(b, a, res.P, res.Q, info_dev, slot);
-        FFG_CUDA(cudaEventRecord(ev, b.st));
-        FFG_CUDA(cudaEventSynchronize(ev));  // the rank decides every later shape
+        const uint32_t seq = ++b.ws.base_seq;
+        const bool asked = rr_base_launch(b, a, res.P, res.Q, info_dev, slot, seq);
+        wait_mailbox(seq);  // the rank decides every later shape
         ++base_cases;
         res.rank = info_host->rank;
         res.pr = Range{info_host->plo, info_host->phi};

@@ -47,12 +47,13 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
 struct BaseInfo {
     uint32_t rank, plo, phi, qlo, qhi;
     uint32_t cached;  // 1 when inv_out received inv(L_r), inv(U_r) (r x r each, ld r)
+    uint32_t seq;     // written last: the launch's sequence number (host spins on it)
 };
 // one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info; with
 // inv_out != nullptr also the inverses of the leading r x r L and U factors (r <= 64)
 // returns whether inverses were requested (the kernel still reports info->cached)
 bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev,
-                    uint32_t* inv_out = nullptr);
+                    uint32_t* inv_out = nullptr, uint32_t seq = 0);
 
 // Structure of a node's leading r x r factor (tile_rec pivot gather order A1, E, G, R):
 // block triangular with the children's leading factors on the diagonal.  Leaves are base
