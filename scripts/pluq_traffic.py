@@ -1,13 +1,14 @@
 """DRAM traffic of the tensor-core GEMM launches inside one PLUQ, from an ncu metrics capture.
 
     FFG_GEMM_LOG=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-        --clock-control none -k regex:modgemm_kernel --csv --log-file gemm_dram.csv \
+        --clock-control none -k regex:modgemm --csv --log-file gemm_dram.csv \
         python scripts/gemm_shapes.py --run --n 16384 2> shapes.log
     python scripts/pluq_traffic.py gemm_dram.csv shapes.log --n 16384 --p 131071 --thr 64 \
         > profiles/pluq_gemm_traffic.json
 
-Algorithmic bytes per launch: the limb planes of A and B read once (L bytes per residue) plus C
-read and written once (4 + 4 bytes per residue) -- the GEMM's own operands, not the split pass.
+Algorithmic bytes per launch: A and B read once (4 bytes per residue for the direct kernel,
+K <= 256; L limb bytes for the TMA kernel) plus C read and written once (4 + 4 bytes per residue)
+-- the GEMM kernel's own operands, not the split pass.
 """
 import argparse
 import csv
@@ -27,7 +28,7 @@ hdr, body = rows[0], rows[1:]
 ci = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
 per = {}
 for r in body:
-    if "modgemm_kernel" not in r[ci["Kernel Name"]]:
+    if "modgemm" not in r[ci["Kernel Name"]] or "simt" in r[ci["Kernel Name"]]:
         continue
     v = float(r[ci["Metric Value"]].replace(",", ""))
     name = r[ci["Metric Name"]]
@@ -49,7 +50,9 @@ for line in open(a.shapes):
         if simt:
             continue
         tc += 1
-        algo += limbs * (m * k + k * nn) + 8.0 * m * nn
+        # direct kernel (K <= 256) reads the u32 operands; the TMA kernel reads limb planes
+        opb = 4 if k <= 256 else limbs
+        algo += opb * (m * k + k * nn) + 8.0 * m * nn
 out = {"n": a.n, "p": a.p, "threshold": a.thr, "limbs": limbs, "modgemm_launches": launches,
        "tc_gemm_calls_logged": tc,
        "dram_bytes_per_launch": dram / launches if launches else None,
@@ -57,5 +60,5 @@ out = {"n": a.n, "p": a.p, "threshold": a.thr, "limbs": limbs, "modgemm_launches
        "dram_over_algorithmic": (dram / launches) / (algo / tc) if launches and tc and algo else None,
        "ncu_serialized_gemm_ms": ns / 1e6,
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                 "-k regex:modgemm_kernel over one PLUQ (scripts/pluq_traffic.py)"}
+                 "-k regex:modgemm over one PLUQ (scripts/pluq_traffic.py)"}
 print(json.dumps(out, indent=1))

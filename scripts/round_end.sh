@@ -1,14 +1,26 @@
 #!/bin/bash
-# Round-end style evidence run on one B200 (writes gpurun_out/*)
+# Round-end style evidence run on one B200 (writes gpurun_out/*); every ncu pass runs only
+# after the same command exited 0 without ncu.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "ref rc=$?"
+python bench.py --workload lru --steps 1 --warmup 1 --no-cpu --no-fgemm > gpurun_out/bench_config4.json 2> gpurun_out/bench_config4.err
+python bench.py --p 251 --n 32768 --steps 2 --warmup 1 --no-cpu --no-fgemm > gpurun_out/bench_config5.json 2> gpurun_out/bench_config5.err
 python scripts/trace_pluq.py --n 16384 --json gpurun_out/trace_n16384.json > gpurun_out/trace_n16384.txt 2>&1
+# fgemm 8192^3: one full ncu capture of the tcgen05 kernel
 python scripts/prof_gemm.py > gpurun_out/prof_gemm_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:modgemm -s 1 -c 1 -o gpurun_out/gemm_full python scripts/prof_gemm.py > gpurun_out/ncu_gemm.log 2>&1
+# launch list of one bench step (durations only)
 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/bench_small.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 13344 -c 5000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/ncu_bench.log 2>&1
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/ncu_bench.log 2>&1
+# DRAM traffic of every tensor-core GEMM launch inside one n = 16384 PLUQ
+FFG_GEMM_LOG=1 python scripts/gemm_shapes.py --run --n 16384 2> gpurun_out/shapes.log && \
+  FFG_GEMM_LOG=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:modgemm --csv --log-file gpurun_out/gemm_dram.csv python scripts/gemm_shapes.py --run --n 16384 \
+    2> gpurun_out/shapes_ncu.log > gpurun_out/ncu_dram.log
+python scripts/pluq_traffic.py gpurun_out/gemm_dram.csv gpurun_out/shapes.log --n 16384 --p 131071 --thr 64 \
+  > gpurun_out/pluq_gemm_traffic.json 2> gpurun_out/pluq_traffic.err
 echo done
