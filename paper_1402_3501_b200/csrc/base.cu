@@ -484,12 +484,284 @@ __global__ void __launch_bounds__(REG ? BASE_THREADS_REG : BASE_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Blocked base case for m, n <= 64: rr_base evaluated as the reference's slab algorithm
+// (pluq_slab_iterative, rankrev.hpp:244-282, which equals rr_base for every slab height --
+// tests/test_oracle_pins.py::test_rr_base_equals_slab_iterative), rows and columns left in
+// place, 16-row slabs, one warp per slab row (2 columns per lane):
+//   (A) the slab rows' exact Schur complements w.r.t. the R earlier pivots: each warp sweeps
+//       k = 0..R-1 right-looking with the EXACT earlier U rows (l_ik = S_i[q_k] / U_k[q_k],
+//       S_i -= l_ik U_k), using per-column Shoup factors of U and Shoup-ready pivot inverses --
+//       one shuffle and a few multiplies per pivot, no barrier;
+//   (B) rr_base's greedy search on the slab (rankrev.hpp:40-57): fraction-free, lazily reduced
+//       values in registers, one barrier per pivot, every eligible warp publishing its row into
+//       a double-buffered slot and the lowest row winning through a shared atomicMin;
+//   (C) the slab's pivots normalised with ONE modular inverse (prefix products): exact U rows
+//       (+ their Shoup factors for later slabs), exact pivot inverses, exact in-slab L.
+constexpr int SLAB = 16;
+constexpr int SL_THREADS = 512;
+constexpr int SS = 68;  // row stride of the block (16-byte rows, banks shifted per row)
+constexpr int LS = 65;  // row stride of L
+
+__device__ __forceinline__ uint32_t red4p(uint32_t x, uint32_t p) {  // [0, 4p) -> [0, p)
+    x = min(x, x - 2 * p);
+    return min(x, x - p);
+}
+
+__global__ void __launch_bounds__(SL_THREADS, 1)
+    rr_base_slab_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t m, uint32_t n, uint32_t* __restrict__ Pd,
+                        uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p, uint64_t mu,
+                        uint32_t seq) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    uint32_t* S = sm;                    // 64 x SS: the block; exact U rows after normalisation
+    uint32_t* Uf = S + 64 * SS;          // 64 x SS: Shoup factors of the exact U rows (by pivot index)
+    uint32_t* Lx = Uf + 64 * SS;         // 64 x LS: exact L (row i, pivot k)
+    uint32_t* slot = Lx + 64 * LS;       // [2][16] x 132: candidate rows: 64 values, 64 Shoup
+                                         // factors, {row, col, val, shoup(val)}
+    uint32_t* prow = slot + 2 * 16 * 132;  // 64
+    uint32_t* pcol = prow + 64;          // 64
+    uint32_t* ipv = pcol + 64;           // 64 inverses of the exact pivot values
+    uint32_t* ipf = ipv + 64;            // 64 their Shoup factors
+    uint32_t* sl = ipf + 64;             // per slab: piv_ff[16], D[16], invD[16], invp[16]
+    uint32_t* Psh = sl + 64;             // 64
+    uint32_t* Qsh = Psh + 64;            // 64
+    uint32_t* rowrank = Qsh + 64;        // 64
+    uint32_t* colrank = rowrank + 64;    // 64
+    uint32_t* misc = colrank + 64;       // [0] slab rank, [2..4] winning row, rotating per step
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr uint32_t FULL = 0xffffffffu;
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tq = clock64();
+    auto stamp = [&](int k) {
+        const unsigned long long t2 = clock64();
+        ph[k] += t2 - tq;
+        tq = t2;
+    };
+
+    for (uint32_t idx = tid; idx < 64 * 64; idx += SL_THREADS) {
+        const uint32_t i = idx >> 6, j = idx & 63;
+        S[i * SS + j] = (i < m && j < n) ? A[(uint64_t)i * lda + j] : 0u;
+        Lx[i * LS + j] = 0u;
+    }
+    __syncthreads();
+    stamp(0);
+
+    uint32_t R = 0;
+    for (uint32_t i0 = 0; i0 < m; i0 += SLAB) {
+        const uint32_t rows = min((uint32_t)SLAB, m - i0);
+        const uint32_t i = i0 + warp;
+        const bool live = warp < rows;
+        uint32_t x0 = live ? S[i * SS + lane] : 0u, x1 = live ? S[i * SS + lane + 32] : 0u;
+        // (A) exact Schur rows against the earlier pivots (x stays in [0, p) after each step)
+        if (live) {
+#pragma unroll 2
+            for (uint32_t k = 0; k < R; ++k) {
+                const uint32_t q = pcol[k];
+                const uint32_t* u = S + prow[k] * SS;
+                const uint32_t* uf = Uf + k * SS;
+                const uint32_t u0 = u[lane], u1 = u[lane + 32], f0 = uf[lane], f1 = uf[lane + 32];
+                const uint32_t v = __shfl_sync(FULL, q < 32 ? x0 : x1, q & 31);
+                const uint32_t l = shoup_mul(v, ipv[k], ipf[k], p);  // exact multiplier
+                if (lane == 0) Lx[i * LS + k] = l;
+                x0 = red4p(x0 + 2 * p - (l * u0 - __umulhi(l, f0) * p), p);
+                x1 = red4p(x1 + 2 * p - (l * u1 - __umulhi(l, f1) * p), p);
+            }
+        }
+        stamp(1);
+        // (B) sequential pivoting inside the slab: warp w <-> row i0 + w
+        uint32_t last = i0 == 0 ? NONE : i0 - 1;  // rows <= last are done
+        uint32_t t = 0;
+        bool is_pivot = false;
+        if (tid == 0) misc[2] = misc[3] = misc[4] = NONE;
+        __syncthreads();
+        // one barrier per pivot: slots are double-buffered and the winner cell rotates over three,
+        // so a cell is reset only after every thread has passed the barrier following its last read
+        uint32_t rot = 0;
+        while (R + t < n) {
+            const uint32_t par = t & 1;
+            uint32_t* my = slot + (par * 16 + warp) * 132;
+            if (live && (last == NONE || i > last) && !is_pivot) {
+                x0 = red4p(x0, p);
+                x1 = red4p(x1, p);
+                const uint32_t b0 = __ballot_sync(FULL, x0 != 0u), b1 = __ballot_sync(FULL, x1 != 0u);
+                if (b0 | b1) {
+                    my[lane] = x0;
+                    my[lane + 32] = x1;
+                    my[64 + lane] = shoup_pre(x0, p, mu);
+                    my[96 + lane] = shoup_pre(x1, p, mu);
+                    const uint32_t pj = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
+                    const uint32_t pv = __shfl_sync(FULL, pj < 32 ? x0 : x1, pj & 31);
+                    if (lane == 0) {
+                        my[128] = i;
+                        my[129] = pj;
+                        my[130] = pv;
+                        my[131] = shoup_pre(pv, p, mu);
+                        atomicMin(misc + 2 + rot, i);
+                    }
+                }
+            }
+            if (tid == 0) misc[2 + (rot == 2 ? 0 : rot + 1)] = NONE;  // the next step's cell
+            __syncthreads();
+            const uint32_t pi = misc[2 + rot];
+            rot = rot == 2 ? 0 : rot + 1;
+            if (pi == NONE) break;  // uniform: the slab has no nonzero row left
+            const uint32_t* pr = slot + (par * 16 + (pi - i0)) * 132;
+            const uint32_t pj = pr[129], pv = pr[130], pvp = pr[131];
+            const uint32_t k = R + t;
+            if (tid == 0) {
+                prow[k] = pi;
+                pcol[k] = pj;
+                sl[t] = pv;  // fraction-free pivot value
+            }
+            if (live && i > pi) {
+                const uint32_t numer = red4p(__shfl_sync(FULL, pj < 32 ? x0 : x1, pj & 31), p);
+                if (lane == 0) Lx[i * LS + k] = numer;  // fraction-free numerator, scaled below
+                const uint32_t b0 = pr[lane], b1 = pr[lane + 32], f0 = pr[64 + lane], f1 = pr[96 + lane];
+                x0 = (x0 * pv - __umulhi(x0, pvp) * p) + 2 * p - (numer * b0 - __umulhi(numer, f0) * p);
+                x1 = (x1 * pv - __umulhi(x1, pvp) * p) + 2 * p - (numer * b1 - __umulhi(numer, f1) * p);
+            }
+            if (i == pi) is_pivot = true;  // its registers hold the published (reduced) row
+            last = pi;
+            ++t;
+        }
+        __syncthreads();
+        if (live) {  // pivot rows: scaled U; other rows: zero Schur complement
+            S[i * SS + lane] = red4p(x0, p);
+            S[i * SS + lane + 32] = red4p(x1, p);
+        }
+        if (tid == 0) misc[0] = t;
+        __syncthreads();
+        stamp(2);
+        const uint32_t rs = misc[0];
+        if (rs == 0) continue;
+        // (C) D_t = prod_{j<t} piv_j; one inverse of the total, suffix products for the rest
+        if (warp == 0) {
+            const uint32_t v = lane < rs ? sl[lane] : 1u;
+            uint32_t inc = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_up_sync(FULL, inc, off);
+                if (lane >= (uint32_t)off) inc = mul_mod(inc, o, p, mu);
+            }
+            uint32_t exc = __shfl_up_sync(FULL, inc, 1);
+            if (lane == 0) exc = 1u % p;
+            const uint32_t total = __shfl_sync(FULL, inc, rs - 1);
+            const uint32_t tinv = __shfl_sync(FULL, lane == 0 ? inv_mod_bin(total, p) : 0u, 0);
+            uint32_t suf = lane + 1 < rs ? sl[lane + 1] : 1u;  // prod_{j>t} piv_j by a suffix scan
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t o = __shfl_down_sync(FULL, suf, off);
+                if (lane + off < 32) suf = mul_mod(suf, o, p, mu);
+            }
+            const uint32_t inv_incl = mul_mod(tinv, suf, p, mu);  // 1 / prod_{j<=t}
+            const uint32_t inv_exc = __shfl_up_sync(FULL, inv_incl, 1);
+            if (lane < rs) {
+                const uint32_t invD = lane == 0 ? 1u % p : inv_exc;
+                const uint32_t invp = mul_mod(exc, inv_incl, p, mu);  // 1 / piv_t
+                sl[32 + lane] = invD;
+                sl[48 + lane] = invp;
+                // exact pivot value piv_t / D_t; its inverse D_t / piv_t
+                const uint32_t ip = mul_mod(exc, invp, p, mu);
+                ipv[R + lane] = ip;
+                ipf[R + lane] = shoup_pre(ip, p, mu);
+            }
+        }
+        __syncthreads();
+        // exact U rows (and their Shoup factors) and the slab's exact L entries
+        for (uint32_t idx = tid; idx < rs * 64; idx += SL_THREADS) {
+            const uint32_t tt = idx >> 6, j = idx & 63;
+            uint32_t* u = S + prow[R + tt] * SS;
+            const uint32_t e = mul_mod(u[j], sl[32 + tt], p, mu);
+            u[j] = e;
+            Uf[(R + tt) * SS + j] = shoup_pre(e, p, mu);
+        }
+        for (uint32_t idx = tid; idx < rows * rs; idx += SL_THREADS) {
+            const uint32_t ii = i0 + idx / rs, tt = idx % rs;
+            if (ii > prow[R + tt]) Lx[ii * LS + R + tt] = mul_mod(Lx[ii * LS + R + tt], sl[48 + tt], p, mu);
+        }
+        __syncthreads();
+        stamp(3);
+        R += rs;
+    }
+    const uint32_t r = R;
+
+    // ---- permutations and packed output (exact L and U already in place)
+    for (uint32_t ii = tid; ii < 64; ii += SL_THREADS) {
+        rowrank[ii] = NONE;
+        colrank[ii] = NONE;
+    }
+    __syncthreads();
+    for (uint32_t k = tid; k < r; k += SL_THREADS) {
+        rowrank[prow[k]] = k;
+        colrank[pcol[k]] = k;
+    }
+    __syncthreads();
+    if (warp < 2) {
+        const uint32_t dim = warp == 0 ? m : n;
+        const uint32_t* rank_of = warp == 0 ? rowrank : colrank;
+        const uint32_t* order = warp == 0 ? prow : pcol;
+        uint32_t* out = warp == 0 ? Psh : Qsh;
+        uint32_t base = 0;
+        for (uint32_t c = 0; c < dim; c += 32) {
+            const uint32_t ii = c + lane;
+            const bool np = ii < dim && rank_of[ii] == NONE;
+            const uint32_t bal = __ballot_sync(FULL, np);
+            if (np) out[r + base + __popc(bal & ((1u << lane) - 1u))] = ii;
+            base += __popc(bal);
+        }
+        for (uint32_t k = lane; k < r; k += 32) out[k] = order[k];
+        __syncwarp();
+        uint32_t lo = NONE, hi = 0;
+        for (uint32_t ii = lane; ii < dim; ii += 32)
+            if (out[ii] != ii) {
+                lo = min(lo, ii);
+                hi = max(hi, ii + 1);
+            }
+        lo = __reduce_min_sync(FULL, lo);
+        hi = __reduce_max_sync(FULL, hi);
+        if (lane == 0) {
+            if (warp == 0) {
+                info->rank = r;
+                info->plo = lo < hi ? lo : 0;
+                info->phi = lo < hi ? hi : 0;
+            } else {
+                info->qlo = lo < hi ? lo : 0;
+                info->qhi = lo < hi ? hi : 0;
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t ii = tid; ii < m; ii += SL_THREADS) Pd[ii] = Psh[ii];
+    for (uint32_t j = tid; j < n; j += SL_THREADS) Qd[j] = Qsh[j];
+    for (uint32_t idx = tid; idx < m * n; idx += SL_THREADS) {
+        const uint32_t tt = idx / n, u = idx % n;
+        const uint32_t ii = Psh[tt], j = Qsh[u];
+        const uint32_t k = rowrank[ii], tc = colrank[j];
+        uint32_t v;
+        if (tc < r && tc < k)  // L entry (k == NONE for non-pivot rows)
+            v = Lx[ii * LS + tc];
+        else  // U row k, or the zero Schur complement of a non-pivot row
+            v = S[ii * SS + j];
+        A[(uint64_t)tt * lda + u] = v;
+    }
+    __syncthreads();
+    stamp(7);
+    if (tid == 0 && g_base_dbg) {
+        unsigned long long* d = g_base_dbg + 6 * 4096 + 8 * (atomicAdd(&g_base_dbg_n, 1u) % 64);
+        for (int q = 0; q < 8; ++q) d[q] = ph[q];
+    }
+    if (tid == 0) {
+        info->cached = 0;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+    }
+}
+
 void base_dbg_init() {
     static bool done = false;
     if (done || !getenv("FFG_BASE_DBG")) return;
     done = true;
     unsigned long long* buf = nullptr;
-    FFG_CUDA(cudaMalloc(&buf, 4097 * 6 * 8));
+    FFG_CUDA(cudaMalloc(&buf, (4096 * 6 + 8 * 64) * 8));
     FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg, &buf, sizeof(buf)));
     if (getenv("FFG_BASE_SKIP")) {
         int one = 1;
@@ -505,6 +777,17 @@ void base_dbg_dump() {
     FFG_CUDA(cudaMemcpyFromSymbol(&buf, g_base_dbg, sizeof(buf)));
     FFG_CUDA(cudaMemcpyFromSymbol(&n, g_base_dbg_n, sizeof(n)));
     if (!buf || n == 0) return;
+    {
+        std::vector<unsigned long long> ph(8 * 64);
+        FFG_CUDA(cudaMemcpy(ph.data(), buf + 6 * 4096, ph.size() * 8, cudaMemcpyDeviceToHost));
+        double acc[8] = {0};
+        const unsigned cnt = std::min(n, 64u);
+        for (unsigned i = 0; i < cnt; ++i)
+            for (int q = 0; q < 8; ++q) acc[q] += ph[8 * i + q];
+        fprintf(stderr, "SLAB_DBG cycles/launch: load %.0f schur %.0f pivot %.0f norm %.0f - %.0f - %.0f out %.0f (%.0f)\n",
+                acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt, acc[6] / cnt,
+                acc[7] / cnt);
+    }
     n = std::min(n, 4096u);
     std::vector<unsigned long long> h(6 * (size_t)n);
     FFG_CUDA(cudaMemcpy(h.data(), buf, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -537,6 +820,19 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     if (inv_out && (fixed + blk + inv_bytes > BASE_SMEM_LIMIT)) inv_out = nullptr;
     b.ws.prof.begin(b.st);
     static const bool no_reg = getenv("FFG_BASE_SMEM") && atoi(getenv("FFG_BASE_SMEM")) != 0;
+    static const bool no_slab = getenv("FFG_BASE_NO_SLAB") && atoi(getenv("FFG_BASE_NO_SLAB")) != 0;
+    if (!no_reg && !no_slab && lay.m <= 64 && lay.n <= 64) {
+        const size_t smem = (2 * 64 * SS + 64 * LS + 2 * 16 * 132 + 64 * 11 + 8) * 4;
+        static std::once_flag once;
+        std::call_once(once, [smem] {
+            FFG_CUDA(cudaFuncSetAttribute(rr_base_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        });
+        rr_base_slab_kernel<<<1, SL_THREADS, smem, b.st>>>(a.d, a.ld, lay.m, lay.n, Pd, Qd, info, b.F.p, b.F.mu, seq);
+        FFG_CUDA(cudaGetLastError());
+        b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
+        b.count();
+        return false;
+    }
     const bool reg = !no_reg && lay.m <= 64 && lay.n <= 64;
     const size_t slots = (8 + 128 + 16 + 16 * 64 + 64 + 4) * 4;  // candidate slots of the register path
     if (reg && fixed + blk + slots <= BASE_SMEM_LIMIT) {

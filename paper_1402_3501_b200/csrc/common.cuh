@@ -95,19 +95,20 @@ __host__ __device__ __forceinline__ uint32_t inv_mod32(uint32_t a, uint32_t p) {
 }
 
 // Shoup multiplication by a fixed factor w: wp = floor(w * 2^32 / p); x*w mod p in 32-bit ops
+// Branch-free: for x = w * 2^32, hi64(x * mu) = w * mu_hi + hi32(w * mu_lo) (two products), and
+// the Barrett estimate with mu = floor((2^64 - 1) / p) is short by at most 2.
 __host__ __device__ __forceinline__ uint32_t shoup_pre(uint32_t w, uint32_t p, uint64_t mu) {
     const uint64_t x = (uint64_t)w << 32;
 #ifdef __CUDA_ARCH__
-    uint64_t q = __umul64hi(x, mu);
+    uint64_t q = (uint64_t)w * (uint32_t)(mu >> 32) + __umulhi(w, (uint32_t)mu);
 #else
     uint64_t q = (uint64_t)(((unsigned __int128)x * mu) >> 64);
 #endif
-    uint64_t r = x - q * p;
-    while (r >= p) {
-        r -= p;
-        ++q;
-    }
-    return (uint32_t)q;
+    uint32_t r = (uint32_t)(x - q * p);  // in [0, 3p): exact in 32 bits
+    const uint32_t c1 = r >= p;
+    r -= c1 * p;
+    const uint32_t c2 = r >= p;
+    return (uint32_t)q + c1 + c2;
 }
 __device__ __forceinline__ uint32_t shoup_mul(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
     const uint32_t q = __umulhi(x, wp);
