@@ -925,7 +925,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
             dim3 g((unsigned)ceil_div(N, 256), (unsigned)M);
             scale_kernel<<<g, 256, 0, st>>>(C.d, C.ld, (uint32_t)M, (uint32_t)N, beta, F.p, F.mu);
             FFG_CUDA(cudaGetLastError());
-            if (launches) ++*launches;
+            if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
         }
         return;
     }
@@ -963,7 +963,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
                                                alpha, beta, F.p, F.mu);
         FFG_CUDA(cudaGetLastError());
         ws.prof.end(st, PROF_SIMT, 2.0 * (double)M * N * K, 2.0 * (double)M * N * K);
-        if (launches) ++*launches;
+        if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
         return;
     }
     const int L = F.limbs, NT = tile_n(L);
@@ -986,7 +986,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
             default: one ? launch_direct<4, 1>(F, alpha, beta, A, B, C, st) : launch_direct<4, 2>(F, alpha, beta, A, B, C, st); break;
         }
         ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * K, 2.0 * (double)M * N * K);
-        if (launches) ++*launches;
+        if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
         return;
     }
     const size_t Mp = round_up(M, BM), Np = round_up(N, NT);
@@ -1030,7 +1030,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         }
         // algorithmic work: L^2 u8 limb products per field MAC -> 2 L^2 M N kc int8 tensor ops
         ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * kc, 2.0 * (double)M * N * kc);
-        if (launches) *launches += 2;
+        if (launches) __atomic_add_fetch(launches, 2, __ATOMIC_RELAXED);
     }
 }
 

@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -95,7 +97,7 @@ private:
 class Workspace {
 public:
     Profiler prof;
-    uint32_t base_seq = 0;  // sequence numbers of base-case completion mailboxes
+    std::atomic<uint32_t> base_seq{0};  // sequence numbers of base-case completion mailboxes
     Dist dist;  // multi-GPU partitioning of the recursion's large operations (dist.cuh)
     ~Workspace() {
         for (auto& kv : bufs_)
@@ -108,21 +110,36 @@ public:
             cudaStreamDestroy(kv.second);
         }
     }
-    // host-mapped pinned words the device writes directly (the base-case rank mailbox);
-    // allocated once per context, not per call
-    uint32_t* mapped_host(size_t words, uint32_t** dev_ptr) {
+    // host-mapped pinned mailboxes the device writes directly (base-case rank + moved ranges),
+    // one per concurrently running recursion driver; allocated once per context
+    static constexpr int MAILBOXES = 64, MAILBOX_WORDS = 16;
+    uint32_t* mailbox(int slot, uint32_t** dev_ptr) {
         std::lock_guard<std::mutex> lk(mu_);
-        if (mapped_words_ < words) {
-            if (mapped_) FFG_CUDA(cudaFreeHost(mapped_));
-            mapped_ = nullptr;
-            FFG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped_), words * 4, cudaHostAllocMapped));
+        if (!mapped_) {
+            FFG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mapped_), MAILBOXES * MAILBOX_WORDS * 4,
+                                   cudaHostAllocMapped));
             FFG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_dev_), mapped_, 0));
-            mapped_words_ = words;
+            std::memset(mapped_, 0, MAILBOXES * MAILBOX_WORDS * 4);
         }
-        *dev_ptr = mapped_dev_;
-        return mapped_;
+        *dev_ptr = mapped_dev_ + slot * MAILBOX_WORDS;
+        return mapped_ + slot * MAILBOX_WORDS;
+    }
+    // driver slots (mailbox + stream-id range) for concurrent subtrees; slot 0 is the root's
+    int acquire_slot() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (int s = 1; s < MAILBOXES; ++s)
+            if (!slot_busy_[s]) {
+                slot_busy_[s] = true;
+                return s;
+            }
+        return -1;
+    }
+    void release_slot(int s) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (s > 0) slot_busy_[s] = false;
     }
     cudaEvent_t sync_event() {
+        std::lock_guard<std::mutex> lk(mu_);
         if (!ev_) FFG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
         return ev_;
     }
@@ -140,8 +157,12 @@ public:
         return s;
     }
     // events for fork/join within one call: recycled across calls (reset_events at call start)
-    void reset_events() { ev_cursor_ = 0; }
+    void reset_events() {
+        std::lock_guard<std::mutex> lk(mu_);
+        ev_cursor_ = 0;
+    }
     cudaEvent_t event() {
+        std::lock_guard<std::mutex> lk(mu_);
         if (ev_cursor_ == ev_pool_.size()) {
             cudaEvent_t e;
             FFG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -181,7 +202,7 @@ private:
     std::unordered_map<cudaStream_t, Buf> bufs_;
     uint32_t* mapped_ = nullptr;
     uint32_t* mapped_dev_ = nullptr;
-    size_t mapped_words_ = 0;
+    bool slot_busy_[MAILBOXES] = {};
     cudaEvent_t ev_ = nullptr;
     std::unordered_map<int, cudaStream_t> streams_;
     std::vector<cudaEvent_t> ev_pool_;

@@ -21,6 +21,9 @@
 #include <atomic>
 #include <cstring>
 #include <deque>
+#include <future>
+#include <thread>
+#include <memory>
 #include <vector>
 
 #include "pluq.cuh"
@@ -61,6 +64,7 @@ public:
     ~PermArena() {
         if (base_) cudaFreeAsync(base_, st_);
     }
+    void free_on(cudaStream_t st) { st_ = st; }  // the stream whose later work reads these arrays
     uint32_t* alloc(size_t words) {
         if (top_ + words > cap_) throw Error(FFG_ERR_INTERNAL, "permutation arena exhausted");
         uint32_t* p = base_ + top_;
@@ -108,12 +112,20 @@ struct Driver {
         size_t ldh = 0, rows = 0;
     } early;
 
-    Driver(const Blas& bl, size_t t, size_t m, size_t n, bool keep_events = false)
+    // slot: 0 for the root driver of a call; a concurrent subtree (E || G) gets its own slot =
+    // its own streams (ids slot*1000 + ...) and base-case mailbox
+    int slot = 0;
+    int device = 0;
+    static int sid(int slot, int k) { return slot * 1000 + k; }
+
+    Driver(const Blas& bl, size_t t, size_t m, size_t n, bool keep_events = false, int slot_ = 0)
         : user(bl),
-          b(Blas{bl.F, bl.ws, bl.ws.stream(0, 0), bl.launches}),
+          b(Blas{bl.F, bl.ws, bl.ws.stream(sid(slot_, 0), 0), bl.launches}),
           thr(std::max<size_t>(1, t)),
-          arena(8 * (m + n) + 4096, bl.ws.stream(0, 0)) {
+          arena(8 * (m + n) + 4096, bl.ws.stream(sid(slot_, 0), 0)),
+          slot(slot_) {
         if (!keep_events) b.ws.reset_events();
+        FFG_CUDA(cudaGetDevice(&device));
         cudaEvent_t e = b.ws.event();  // critical stream starts after the caller's pending work
         FFG_CUDA(cudaEventRecord(e, user.st));
         FFG_CUDA(cudaStreamWaitEvent(b.st, e, 0));
@@ -133,9 +145,10 @@ struct Driver {
         }
         uint32_t* dev = nullptr;
         // the base kernel writes rank + moved ranges straight into host-mapped memory
-        info_host = reinterpret_cast<BaseInfo*>(b.ws.mapped_host(sizeof(BaseInfo) / 4 + 2, &dev));
+        static_assert(sizeof(BaseInfo) <= Workspace::MAILBOX_WORDS * 4, "mailbox too small");
+        info_host = reinterpret_cast<BaseInfo*>(b.ws.mailbox(slot, &dev));
         info_dev = reinterpret_cast<BaseInfo*>(dev);
-        ev = b.ws.sync_event();
+        ev = b.ws.event();
         // factor-tree TRSM (cached base-case inverses): opt-in, slower than blocked inverses today
         static const bool on = getenv("FFG_FACTOR_TRSM") && atoi(getenv("FFG_FACTOR_TRSM")) != 0;
         use_factors = on;
@@ -147,6 +160,7 @@ struct Driver {
     }
     ~Driver() {
         if (inv_arena) cudaFreeAsync(inv_arena, b.st);
+        b.ws.release_slot(slot);
     }
     // join the critical stream back into the caller's stream
     void finish() {
@@ -157,8 +171,28 @@ struct Driver {
     Blas on(cudaStream_t st) const { return Blas{b.F, b.ws, st, b.launches}; }
     // a second critical-path stream per recursion depth (the node's independent TRSM), and a
     // low-priority stream per depth for the look-ahead part of the trailing update
-    cudaStream_t twin(int depth) { return b.ws.stream(100 + depth, 0); }
-    cudaStream_t lookahead(int depth) { return b.ws.stream(200 + depth, 1); }
+    cudaStream_t twin(int depth) { return b.ws.stream(sid(slot, 100 + depth), 0); }
+    cudaStream_t lookahead(int depth) { return b.ws.stream(sid(slot, 200 + depth), 1); }
+
+    // ---- concurrent subtrees: G's recursion (rankrev.hpp:123) is independent of E's (:119) --
+    // disjoint blocks, results combined only afterwards -- so a large G runs in a child driver
+    // on its own host thread, streams and mailbox while this thread recurses into E.  The
+    // per-base-case rank round trip is what bounds rank-deficient inputs (4-way recursion), so
+    // this overlaps exactly that latency.
+    static std::atomic<int>& active_children() {
+        static std::atomic<int> n{0};
+        return n;
+    }
+    bool can_fork(const DView& E, const DView& G) const {
+        // each child thread spins on its mailbox: keep them within the host's cores
+        const int max_threads =  // read per call (tests switch it)
+            getenv("FFG_SUBTREE_THREADS")
+                ? atoi(getenv("FFG_SUBTREE_THREADS"))
+                : std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2));
+        return max_threads > 0 && use_streams && !b.ws.prof.on && !use_factors && !E.empty() && !G.empty() &&
+               std::min(G.rows, G.cols) > 2 * thr && std::min(E.rows, E.cols) > thr &&
+               active_children().load() < max_threads;
+    }
     cudaEvent_t mark_event(cudaStream_t st) {
         cudaEvent_t e = b.ws.event();
         FFG_CUDA(cudaEventRecord(e, st));
@@ -199,15 +233,15 @@ struct Driver {
         const size_t rmax = std::min(a.rows, a.cols);
         uint32_t* slot = nullptr;
         if (use_factors && rmax <= 64 && inv_top + 2 * rmax * rmax <= inv_cap) slot = inv_arena + inv_top;
-        const uint32_t seq = ++b.ws.base_seq;
+        const uint32_t seq = b.ws.base_seq.fetch_add(1) + 1;
         const bool asked = rr_base_launch(b, a, res.P, res.Q, info_dev, slot, seq);
         wait_mailbox(seq);  // the rank decides every later shape
         ++base_cases;
         res.rank = info_host->rank;
         res.pr = Range{info_host->plo, info_host->phi};
         res.qr = Range{info_host->qlo, info_host->qhi};
-        res.fac = new_factor(res.rank);
-        if (asked && info_host->cached && res.rank > 0) {
+        res.fac = use_factors ? new_factor(res.rank) : nullptr;  // factor trees: opt-in TRSM path only
+        if (res.fac && asked && info_host->cached && res.rank > 0) {
             res.fac->invL = slot;
             res.fac->invU = slot + res.rank * res.rank;
             inv_top += 2 * res.rank * res.rank;
@@ -372,8 +406,33 @@ struct Driver {
             }
         }
 
-        NodeRes r2s = rec(E, depth + 1);                         // :119-125 (E, G independent)
-        NodeRes r3s = rec(G, depth + 1);
+        NodeRes r2s, r3s;                                        // :119-125 (E, G independent)
+        std::unique_ptr<Driver> child;
+        int cslot = can_fork(E, G) ? b.ws.acquire_slot() : -1;
+        if (cslot > 0) {
+            active_children().fetch_add(1);
+            // the child's streams start after everything enqueued so far (G's updates included)
+            child.reset(new Driver(b, thr, G.rows, G.cols, /*keep_events=*/true, cslot));
+            Driver* c = child.get();
+            std::future<NodeRes> fut = std::async(std::launch::async, [c, G, depth] {
+                FFG_CUDA(cudaSetDevice(c->device));
+                return c->rec(G, depth + 1);
+            });
+            try {
+                r2s = rec(E, depth + 1);
+            } catch (...) {
+                fut.wait();
+                active_children().fetch_sub(1);
+                throw;
+            }
+            r3s = fut.get();  // rethrows the child's failure
+            active_children().fetch_sub(1);
+            child->finish();                  // this driver's stream waits for the subtree
+            child->arena.free_on(b.st);       // r3s's index arrays are read on this stream
+        } else {
+            r2s = rec(E, depth + 1);
+            r3s = rec(G, depth + 1);
+        }
         const size_t r2 = r2s.rank, r3 = r3s.rank;
 
         apply(r2s, 0, a.sub(r1, 0, m1 - r1, r1));                // :128-133
@@ -448,9 +507,11 @@ struct Driver {
         rotate_block_dev(b, a, 1, r1 + r2 + r3, n1 + r2, r4);
 
         res.rank = r1 + r2 + r3 + r4;
-        res.fac = new_factor(res.rank);  // leading factor = children's factors in gather order
-        for (const NodeRes* c : {&r1s, &r2s, &r3s, &r4s})
-            if (c->rank > 0) res.fac->kids.push_back(c->fac);
+        if (use_factors) {  // leading factor = children's factors in gather order
+            res.fac = new_factor(res.rank);
+            for (const NodeRes* c : {&r1s, &r2s, &r3s, &r4s})
+                if (c->rank > 0) res.fac->kids.push_back(c->fac);
+        }
         arena.reset(mark);  // children consumed (stream order protects the pending kernels)
         return res;
     }

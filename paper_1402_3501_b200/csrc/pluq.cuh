@@ -23,7 +23,7 @@ struct Blas {
         fgemm_dev(F, alpha, A, B, beta, C, st, ws, launches, sm_cap);
     }
     void count(uint64_t n = 1) const {
-        if (launches) *launches += n;
+        if (launches) __atomic_add_fetch(launches, n, __ATOMIC_RELAXED);
     }
 };
 

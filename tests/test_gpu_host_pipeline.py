@@ -46,3 +46,26 @@ def test_host_entry_matches_device_entry(gpu, oracle_lib, shape, gen):
     assert np.array_equal(rh.P, rd.P) and np.array_equal(rh.Q, rd.Q)
     assert np.array_equal(view, want)
     assert np.all(buf[:, n:] == 0xDEADBEEF)  # padding untouched
+
+
+@pytest.mark.parametrize("threads", ["0", "4"])
+def test_concurrent_subtrees_match_oracle(gpu, oracle_lib, threads, monkeypatch):
+    """Rank-deficient L*R*U input with many E/G forks (thr 16): the concurrent-subtree driver
+    (E || G on separate host threads / streams / mailboxes) is bit-identical to the oracle."""
+    import torch
+
+    G, ctx = gpu
+    O = oracle_lib
+    p = 131071
+    n = 1024
+    d = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    G.lru_matrix_dev(p, d, n // 2, 11, ctx=ctx)
+    ctx.synchronize()
+    A = d.cpu().numpy().view(np.uint32).copy()
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 16)
+    monkeypatch.setenv("FFG_SUBTREE_THREADS", threads)
+    a_g = A.copy()
+    res = G.pluq_tile_recursive(p, a_g, 16, ctx=ctx)
+    assert res.rank == r_o == n // 2
+    assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+    assert np.array_equal(a_g, a_o)
