@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "pluq.cuh"
+#include "ptx.cuh"
 #include "triinv.cuh"
 
 namespace ffg {
@@ -536,6 +537,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
         ph[k] += t2 - tq;
         tq = t2;
     };
+    ptx::pdl_enter();
 
     for (uint32_t idx = tid; idx < 64 * 64; idx += SL_THREADS) {
         const uint32_t i = idx >> 6, j = idx & 63;
@@ -819,15 +821,20 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const size_t inv_bytes = (2 * INV_MAX * (INV_MAX + 1) + (INV_MAX / 2) * (INV_MAX / 2) + INV_MAX + 8) * 4;
     if (inv_out && (fixed + blk + inv_bytes > BASE_SMEM_LIMIT)) inv_out = nullptr;
     b.ws.prof.begin(b.st);
-    static const bool no_reg = getenv("FFG_BASE_SMEM") && atoi(getenv("FFG_BASE_SMEM")) != 0;
-    static const bool no_slab = getenv("FFG_BASE_NO_SLAB") && atoi(getenv("FFG_BASE_NO_SLAB")) != 0;
+    // kernel choice (read per launch so tests can exercise every path): FFG_BASE_SMEM=1 forces the
+    // shared-memory right-looking kernel, FFG_BASE_NO_SLAB=1 the register right-looking one
+    const char* e_smem = getenv("FFG_BASE_SMEM");
+    const char* e_slab = getenv("FFG_BASE_NO_SLAB");
+    const bool no_reg = e_smem && atoi(e_smem) != 0;
+    const bool no_slab = e_slab && atoi(e_slab) != 0;
     if (!no_reg && !no_slab && lay.m <= 64 && lay.n <= 64) {
         const size_t smem = (2 * 64 * SS + 64 * LS + 2 * 16 * 132 + 64 * 11 + 8) * 4;
         static std::once_flag once;
         std::call_once(once, [smem] {
             FFG_CUDA(cudaFuncSetAttribute(rr_base_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         });
-        rr_base_slab_kernel<<<1, SL_THREADS, smem, b.st>>>(a.d, a.ld, lay.m, lay.n, Pd, Qd, info, b.F.p, b.F.mu, seq);
+        launch_k(rr_base_slab_kernel, dim3(1), dim3(SL_THREADS), smem, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd, info,
+                 b.F.p, b.F.mu, seq);
         FFG_CUDA(cudaGetLastError());
         b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
         b.count();

@@ -98,6 +98,7 @@ int ffg_create(ffg_ctx** out, int device) {
     }
     c->stream = c->own_stream;
     if (const char* s = getenv("FFG_SIMT_MACS")) ffg::g_simt_macs = strtoull(s, nullptr, 10);
+    if (const char* s = getenv("FFG_SIMT_KMAX")) ffg::g_simt_kmax = strtoull(s, nullptr, 10);
     // keep freed stream-ordered allocations cached in the pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

@@ -3,6 +3,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdexcept>
 #include <string>
@@ -117,6 +119,28 @@ __device__ __forceinline__ uint32_t shoup_mul(uint32_t x, uint32_t w, uint32_t w
 }
 
 inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+// Kernel launch with programmatic stream serialization (PDL): the kernel may start while its
+// predecessor on the stream finishes; every kernel launched this way calls ptx::pdl_wait()
+// before its first global-memory access.  FFG_NO_PDL=1 launches plainly.
+inline bool pdl_enabled() {
+    static const bool on = !(getenv("FFG_NO_PDL") && atoi(getenv("FFG_NO_PDL")) != 0);
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    FFG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 inline size_t ceil_div(size_t x, size_t m) { return (x + m - 1) / m; }
 
 }  // namespace ffg

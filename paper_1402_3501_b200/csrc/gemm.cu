@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(384, 1)
         ptx::tma_prefetch(&mapA);
         ptx::tma_prefetch(&mapB);
     }
+    ptx::pdl_enter();
     if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_init(tmem_full, 1);
         ptx::fence_mbar_init();
     }
+    ptx::pdl_enter();
     if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
     // epilogue warps: C prefetch for the rows / columns they will write
     constexpr uint32_t PER = NT / 16;  // 8-column chunks per epilogue thread
@@ -642,6 +644,7 @@ struct SplitArgs {
 
 __global__ void __launch_bounds__(256) split_kernel(const SplitArgs a) {
     __shared__ uint32_t tile[64][65];
+    ptx::pdl_enter();
     if (blockIdx.x < a.a_blocks) {
         const uint32_t kq_per_row = a.Kp >> 2;
         for (uint32_t it = 0; it < 4; ++it) {
@@ -691,6 +694,7 @@ __global__ void __launch_bounds__(256) modgemm_simt_kernel(const uint32_t* __res
                                                           uint32_t p, uint64_t mu) {
     __shared__ uint32_t As[SG_K][SG_T + 1];  // transposed: As[k][m]
     __shared__ uint32_t Bs[SG_K][SG_T];
+    ptx::pdl_enter();
     const uint32_t m0 = blockIdx.y * SG_T, n0 = blockIdx.x * SG_T;
     const uint32_t tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 outputs each
     uint64_t acc[4][4];
@@ -750,6 +754,7 @@ __global__ void __launch_bounds__(256) modgemm_simt_kernel(const uint32_t* __res
 // C <- beta*C (alpha == 0 or K == 0 path, blas.hpp:39-51)
 __global__ void scale_kernel(uint32_t* C, uint64_t ldc, uint32_t M, uint32_t N, uint32_t beta, uint32_t p,
                              uint64_t mu) {
+    ptx::pdl_enter();
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
     if (i < M && j < N) {
         uint32_t& c = C[(uint64_t)i * ldc + j];
@@ -827,7 +832,7 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
     ep.n_tiles = (uint32_t)(Np / S::NT);
     const uint32_t tiles = ep.m_tiles * ep.n_tiles;
     dim3 grid(sm_cap > 0 ? std::min<uint32_t>(tiles, (uint32_t)sm_cap) : tiles);
-    modgemm_kernel<L><<<grid, 384, S::TOTAL, st>>>(ma, mb, ep);
+    launch_k(modgemm_kernel<L>, grid, dim3(384), S::TOTAL, st, ma, mb, ep);
     FFG_CUDA(cudaGetLastError());
 }
 
@@ -877,7 +882,7 @@ void launch_direct(const Field& F, uint32_t alpha, uint32_t beta, DView A, DView
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
     }
-    modgemm_direct_kernel<L, KB><<<ep.m_tiles * ep.n_tiles, 384, S::TOTAL, st>>>(da, ep);
+    launch_k(modgemm_direct_kernel<L, KB>, dim3(ep.m_tiles * ep.n_tiles), dim3(384), S::TOTAL, st, da, ep);
     FFG_CUDA(cudaGetLastError());
     if (dbg_on) {
         cudaEventRecord(e1, st);
@@ -900,10 +905,13 @@ void launch_direct(const Field& F, uint32_t alpha, uint32_t beta, DView A, DView
 
 }  // namespace
 
-// CUDA-core path for problems with M*N*K <= g_simt_macs.  Off by default: measured inside the PLUQ,
-// the direct tensor-core kernel beats it at every size (FFG_SIMT_MACS re-enables it).
+// CUDA-core path for problems with M*N*K <= g_simt_macs (off by default: inside the PLUQ the
+// direct tensor-core kernel wins from K = 64 up) or with a tiny inner dimension K <= g_simt_kmax:
+// the rank-sized updates of rank-deficient blocks (K = 1..32), where the tensor-core kernel's
+// fixed cost (TMEM, staging a 128-row tile, epilogue) is all there is.
 size_t g_simt_macs = 0;
-bool use_simt(size_t M, size_t N, size_t K) { return M * N * K <= g_simt_macs; }
+size_t g_simt_kmax = 32;
+bool use_simt(size_t M, size_t N, size_t K) { return M * N * K <= g_simt_macs || K <= g_simt_kmax; }
 
 size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k) {
     const int L = F.limbs, NT = tile_n(L);
@@ -923,7 +931,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     if (alpha == 0 || K == 0) {
         if (beta != 1) {
             dim3 g((unsigned)ceil_div(N, 256), (unsigned)M);
-            scale_kernel<<<g, 256, 0, st>>>(C.d, C.ld, (uint32_t)M, (uint32_t)N, beta, F.p, F.mu);
+            launch_k(scale_kernel, g, dim3(256), 0, st, C.d, C.ld, (uint32_t)M, (uint32_t)N, beta, F.p, F.mu);
             FFG_CUDA(cudaGetLastError());
             if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
         }
@@ -959,8 +967,8 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     if (simt) {
         ws.prof.begin(st);
         dim3 g((unsigned)ceil_div(N, SG_T), (unsigned)ceil_div(M, SG_T));
-        modgemm_simt_kernel<<<g, 256, 0, st>>>(A.d, A.ld, B.d, B.ld, C.d, C.ld, (uint32_t)M, (uint32_t)N, (uint32_t)K,
-                                               alpha, beta, F.p, F.mu);
+        launch_k(modgemm_simt_kernel, g, dim3(256), 0, st, A.d, A.ld, B.d, B.ld, C.d, C.ld, (uint32_t)M, (uint32_t)N,
+                 (uint32_t)K, alpha, beta, F.p, F.mu);
         FFG_CUDA(cudaGetLastError());
         ws.prof.end(st, PROF_SIMT, 2.0 * (double)M * N * K, 2.0 * (double)M * N * K);
         if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
@@ -1015,7 +1023,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
             sa.a_blocks = (uint32_t)ceil_div(Mp * (Kp / 4), 1024);
             sa.b_kblocks = (uint32_t)ceil_div(Kp, 64);
             const size_t nblk = sa.a_blocks + (size_t)sa.b_kblocks * ceil_div(Np, 64);
-            split_kernel<<<(unsigned)nblk, 256, 0, st>>>(sa);
+            launch_k(split_kernel, dim3((unsigned)nblk), dim3(256), 0, st, sa);
             FFG_CUDA(cudaGetLastError());
         }
         // split traffic: read M*kc + kc*N residues (4 B), write the padded limb planes

@@ -217,6 +217,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
 size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k);
 int tile_n(int limbs);
 extern size_t g_simt_macs;  // problems with M*N*K <= this use the CUDA-core kernel
+extern size_t g_simt_kmax;  // ... and so do problems with K <= this
 bool use_simt(size_t M, size_t N, size_t K);
 
 }  // namespace ffg

@@ -7,6 +7,7 @@
 // gather over the moved range only: HBM traffic = 2 reads + 2 writes of the
 // rows/columns that actually move, nothing for the rest.
 #include "pluq.cuh"
+#include "ptx.cuh"
 
 namespace ffg {
 
@@ -23,16 +24,19 @@ struct PermSrc {
 
 __global__ void rows_gather_kernel(const uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows, uint32_t ncols,
                                    PermSrc src, uint32_t* __restrict__ tmp) {
+    ptx::pdl_enter();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
     if (c < ncols && t < nrows) tmp[(uint64_t)t * ncols + c] = A[(uint64_t)src.at(t) * lda + c];
 }
 __global__ void rows_store_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows, uint32_t ncols,
                                   const uint32_t* __restrict__ tmp) {
+    ptx::pdl_enter();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x, t = blockIdx.y;
     if (c < ncols && t < nrows) A[(uint64_t)t * lda + c] = tmp[(uint64_t)t * ncols + c];
 }
 __global__ void cols_gather_kernel(const uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows, uint32_t ncols,
                                    PermSrc src, uint32_t* __restrict__ tmp) {
+    ptx::pdl_enter();
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
     if (u < ncols && r < nrows) tmp[(uint64_t)r * ncols + u] = A[(uint64_t)r * lda + src.at(u)];
 }
@@ -40,16 +44,19 @@ __global__ void cols_gather_kernel(const uint32_t* __restrict__ A, uint64_t lda,
 // in-place gather of an index array range through shared memory: a[t] = old[src(t)]
 __global__ void array_gather_kernel(uint32_t* __restrict__ a, uint32_t len, PermSrc src) {
     extern __shared__ uint32_t s[];
+    ptx::pdl_enter();
     for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) s[t] = a[t];
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) a[t] = s[src.at(t)];
 }
 __global__ void array_gather_global_kernel(const uint32_t* __restrict__ a, uint32_t len, PermSrc src,
                                           uint32_t* __restrict__ out) {
+    ptx::pdl_enter();
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < len) out[t] = a[src.at(t)];
 }
 __global__ void iota_kernel(uint32_t* a, uint32_t len) {
+    ptx::pdl_enter();
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < len) a[t] = t;
 }
@@ -61,8 +68,8 @@ void gather_rows(const Blas& b, DView a, PermSrc src) {
     FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
     dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
     b.ws.prof.begin(b.st);
-    rows_gather_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
-    rows_store_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
+    launch_k(rows_gather_kernel, g, dim3(256), 0, b.st, a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
+    launch_k(rows_store_kernel, g, dim3(256), 0, b.st, a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
     b.ws.prof.end(b.st, PROF_PERM, 16.0 * a.rows * a.cols);
     FFG_CUDA(cudaGetLastError());
     FFG_CUDA(cudaFreeAsync(tmp, b.st));
@@ -74,8 +81,8 @@ void gather_cols(const Blas& b, DView a, PermSrc src) {
     FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
     dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
     b.ws.prof.begin(b.st);
-    cols_gather_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
-    rows_store_kernel<<<g, 256, 0, b.st>>>(a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
+    launch_k(cols_gather_kernel, g, dim3(256), 0, b.st, a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, src, tmp);
+    launch_k(rows_store_kernel, g, dim3(256), 0, b.st, a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, tmp);
     b.ws.prof.end(b.st, PROF_PERM, 16.0 * a.rows * a.cols);
     FFG_CUDA(cudaGetLastError());
     FFG_CUDA(cudaFreeAsync(tmp, b.st));
@@ -111,12 +118,13 @@ static void array_gather(const Blas& b, uint32_t* a, size_t len, PermSrc src) {
             FFG_CUDA(cudaFuncSetAttribute(array_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             set = true;
         }
-        array_gather_kernel<<<1, 1024, bytes, b.st>>>(a, (uint32_t)len, src);
+        launch_k(array_gather_kernel, dim3(1), dim3(1024), bytes, b.st, a, (uint32_t)len, src);
         b.count();
     } else {
         uint32_t* tmp = nullptr;
         FFG_CUDA(cudaMallocAsync(&tmp, bytes, b.st));
-        array_gather_global_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, b.st>>>(a, (uint32_t)len, src, tmp);
+        launch_k(array_gather_global_kernel, dim3((unsigned)ceil_div(len, 256)), dim3(256), 0, b.st, a, (uint32_t)len,
+                 src, tmp);
         FFG_CUDA(cudaMemcpyAsync(a, tmp, bytes, cudaMemcpyDeviceToDevice, b.st));
         FFG_CUDA(cudaFreeAsync(tmp, b.st));
         b.count();
@@ -139,7 +147,7 @@ void perm_rot_dev(const Blas& b, uint32_t* arr, size_t first, size_t mid, size_t
 
 void perm_iota_dev(const Blas& b, uint32_t* arr, size_t len) {
     if (!len) return;
-    iota_kernel<<<(unsigned)ceil_div(len, 256), 256, 0, b.st>>>(arr, (uint32_t)len);
+    launch_k(iota_kernel, dim3((unsigned)ceil_div(len, 256)), dim3(256), 0, b.st, arr, (uint32_t)len);
     FFG_CUDA(cudaGetLastError());
     b.count();
 }

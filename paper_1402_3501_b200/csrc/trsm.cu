@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "pluq.cuh"
+#include "ptx.cuh"
 #include "triinv.cuh"
 
 namespace ffg {
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(RI_THREADS) tri_inv_rec_kernel(const uint32_t*
     uint32_t* S = sm;                    // TB x TSTR: the triangle
     uint32_t* X = S + TB * TSTR;         // TB x TSTR: its inverse
     uint32_t* W = X + TB * TSTR;         // (TB/2) x (TB/2 + 1) temporaries
+    ptx::pdl_enter();
     uint32_t* dinv = W + (TB / 2) * (TB / 2 + 1);
     const uint32_t tid = threadIdx.x, o = blockIdx.x * TB;
     const uint32_t tb = min((uint32_t)TB, t - o);
@@ -389,6 +391,7 @@ __global__ void __launch_bounds__(512) trsm_fused_kernel(const uint32_t* __restr
     uint32_t* dv = Ws + (R / 2) * (R / 2);
     const uint32_t tid = threadIdx.x, v0 = blockIdx.x * LA;
     const uint32_t nv = min((uint32_t)LA, nvec - v0);
+    ptx::pdl_enter();
     for (uint32_t idx = tid; idx < t * t; idx += 512) {
         const uint32_t i = idx / t, k = idx % t;
         Ts[i * RS + k] = T[(uint64_t)i * ldt + k];
@@ -466,8 +469,8 @@ void trsm_fused_launch(const Blas& b, int side, int upper, int unit, DView T, DV
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     b.ws.prof.begin(b.st);
-    k<<<(unsigned)ceil_div(nvec, LA), 512, smem, b.st>>>(T.d, T.ld, (uint32_t)T.rows, B.d, B.ld, (uint32_t)nvec,
-                                                         b.F.p, b.F.mu);
+    launch_k(k, dim3((unsigned)ceil_div(nvec, LA)), dim3(512), smem, b.st, T.d, T.ld, (uint32_t)T.rows, B.d, B.ld,
+             (uint32_t)nvec, b.F.p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)T.rows * nvec);
     b.count();
@@ -681,7 +684,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
         });
         auto kern = upper ? (unit ? tri_inv_rec_kernel<true, true> : tri_inv_rec_kernel<true, false>)
                           : (unit ? tri_inv_rec_kernel<false, true> : tri_inv_rec_kernel<false, false>);
-        kern<<<(unsigned)nblk, RI_THREADS, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
+        launch_k(kern, dim3((unsigned)nblk), dim3(RI_THREADS), smem, b.st, A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
     }
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * nblk * TB * TB);
