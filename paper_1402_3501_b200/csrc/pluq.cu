@@ -103,14 +103,30 @@ struct Driver {
     // marks the upload of the depth-d spine block minus its first child's block
     const uint32_t* spine_root = nullptr;
     std::vector<cudaEvent_t> spine;
-    // early download of the root's top rows [0, m1), final once R's recursion starts unless R's
-    // permutations or the pivot-gather rotations reach back into them (top_touched)
+    // Early download (host entry only).  On the recursion's right spine (root, its R, R's R, ...)
+    // a node whose E and G are empty has finished everything outside R when R's recursion
+    // starts: its top rows and its left block (L1\U1, D, Fb) go to the host on the copy stream
+    // while R recurses, and only the last spine node's R is left for the end.  A region that a
+    // later permutation touches (R's P/Q, or a rank-deficient A1's pivot gather) is re-copied.
     struct EarlyTop {
-        bool armed = false, sent = false, top_touched = false;
+        struct Reg {
+            size_t r0 = 0, c0 = 0, rows = 0, cols = 0;
+        };
+        bool armed = false, spine_ok = true;
         cudaStream_t cs = nullptr;
         uint32_t* host = nullptr;
-        size_t ldh = 0, rows = 0;
+        size_t ldh = 0;
+        const uint32_t* root = nullptr;
+        size_t ld = 0;
+        Reg tail;               // still to copy after the recursion
+        std::vector<Reg> redo;  // early copies made stale by later permutations
     } early;
+    void early_copy(const EarlyTop::Reg& g, cudaStream_t st) {
+        if (g.rows && g.cols)
+            FFG_CUDA(cudaMemcpy2DAsync(early.host + g.r0 * early.ldh + g.c0, early.ldh * 4,
+                                       early.root + g.r0 * early.ld + g.c0, early.ld * 4, g.cols * 4, g.rows,
+                                       cudaMemcpyDeviceToHost, st));
+    }
 
     // slot: 0 for the root driver of a call; a concurrent subtree (E || G) gets its own slot =
     // its own streams (ids slot*1000 + ...) and base-case mailbox
@@ -346,7 +362,50 @@ struct Driver {
 
     // `pending`: work on the side streams that everything outside the top-left quadrant A1
     // of `a` still depends on (the look-ahead part of the parent's trailing update)
-    NodeRes rec(DView a, int depth = 0, cudaEvent_t pending = nullptr) {
+    // ---- diagnostics (FFG_LEVEL_TIMING, root driver): critical-stream time per recursion depth,
+    // split into a node's own work (between its children) and its base cases
+    struct LevelRec {
+        int depth;
+        bool leaf;
+        cudaEvent_t e[4];
+    };
+    bool level_timing = false;
+    std::vector<LevelRec> levels;
+    cudaEvent_t tev() {
+        cudaEvent_t e;
+        FFG_CUDA(cudaEventCreate(&e));
+        FFG_CUDA(cudaEventRecord(e, b.st));
+        return e;
+    }
+    void level_report() {
+        if (levels.empty()) return;
+        FFG_CUDA(cudaStreamSynchronize(b.st));
+        std::vector<double> self(64, 0.0), leaf(64, 0.0);
+        std::vector<int> cnt(64, 0), lcnt(64, 0);
+        for (auto& L : levels) {
+            float a = 0, c = 0;
+            if (L.leaf) {
+                cudaEventElapsedTime(&a, L.e[0], L.e[1]);
+                leaf[L.depth] += a;
+                ++lcnt[L.depth];
+            } else {
+                cudaEventElapsedTime(&a, L.e[0], L.e[1]);  // after A1 -> before R
+                cudaEventElapsedTime(&c, L.e[2], L.e[3]);  // after R -> end
+                self[L.depth] += a + c;
+                ++cnt[L.depth];
+            }
+            for (auto e : L.e)
+                if (e) cudaEventDestroy(e);
+        }
+        for (int d = 0; d < 64; ++d)
+            if (cnt[d] || lcnt[d])
+                fprintf(stderr, "LEVEL depth %2d: %5d nodes  own %8.3f ms (%.1f us/node) | %5d base cases %8.3f ms (%.1f us each)\n",
+                        d, cnt[d], self[d], cnt[d] ? 1e3 * self[d] / cnt[d] : 0.0, lcnt[d], leaf[d],
+                        lcnt[d] ? 1e3 * leaf[d] / lcnt[d] : 0.0);
+        levels.clear();
+    }
+
+    NodeRes rec(DView a, int depth = 0, cudaEvent_t pending = nullptr, bool rspine = false) {
         const size_t m = a.rows, n = a.cols;
         NodeRes res;
         res.P = arena.alloc(std::max<size_t>(m, 1));
@@ -354,14 +413,23 @@ struct Driver {
         if (m == 0 || n == 0) return res;                        // rankrev.hpp:91
         if (std::min(m, n) <= thr) {                             // :92
             wait(b.st, pending);
+            if (level_timing) {
+                LevelRec L{depth, true, {tev(), nullptr, nullptr, nullptr}};
+                NodeRes r = base(a, res);
+                L.e[1] = tev();
+                levels.push_back(L);
+                return r;
+            }
             return base(a, res);
         }
+        LevelRec LR{depth, false, {nullptr, nullptr, nullptr, nullptr}};
         const size_t mark = arena.mark();
         const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;         // :95
 
         cudaEvent_t spine_next = (spine_root && a.d == spine_root && (size_t)depth + 1 < spine.size())
                                      ? spine[depth + 1] : nullptr;
         NodeRes r1s = rec(a.sub(0, 0, m1, n1), depth + 1, spine_next);  // :97
+        if (level_timing) LR.e[0] = tev();
         wait(b.st, pending);
         const size_t r1 = r1s.rank;
         apply(r1s, 0, a.sub(0, n1, m1, n - n1));                 // :99
@@ -470,19 +538,34 @@ struct Driver {
         }
         if (jbuf) FFG_CUDA(cudaFreeAsync(jbuf, b.st));
 
-        if (depth == 0 && early.armed && m1 > 0) {
-            // everything that writes rows [0, m1) before R's recursion is enqueued on b.st
-            wait(early.cs, mark_event(b.st));
-            FFG_CUDA(cudaMemcpy2DAsync(early.host, early.ldh * 4, a.d, a.ld * 4, n * 4, m1, cudaMemcpyDeviceToHost,
-                                       early.cs));
-            early.sent = true;
-            early.rows = m1;
+        bool early_here = false;
+        EarlyTop::Reg reg_top, reg_left;
+        if (rspine && early.armed && early.spine_ok) {
+            if (r2 == 0 && r3 == 0) {
+                // everything that writes outside R before R's recursion is enqueued on b.st
+                const size_t off = (size_t)(a.d - early.root);
+                const size_t r0 = off / early.ld, c0 = off % early.ld;
+                reg_top = EarlyTop::Reg{r0, c0, m1, n};
+                reg_left = EarlyTop::Reg{r0 + m1, c0, m - m1, n1};
+                wait(early.cs, mark_event(b.st));
+                early_copy(reg_top, early.cs);
+                early_copy(reg_left, early.cs);
+                early.tail = EarlyTop::Reg{r0 + m1, c0 + n1, m - m1, n - n1};  // = R when r2 = r3 = 0
+                early_here = true;
+            } else {
+                early.spine_ok = false;  // this node's whole region stays in the tail
+            }
         }
-        NodeRes r4s = rec(R, depth + 1, pending_r);              // :154
+        if (level_timing) LR.e[1] = tev();
+        NodeRes r4s = rec(R, depth + 1, pending_r, rspine);      // :154
+        if (level_timing) LR.e[2] = tev();
         const size_t r4 = r4s.rank;
-        if (depth == 0 && early.sent)  // the steps below that can still write rows [0, m1)
-            early.top_touched = (!r4s.qr.empty() && r1 + r2 > 0) || (m1 != r1 + r2 && r3 + r4 > 0) ||
-                                (n1 != r1 && r2 > 0) || (n1 + r2 != r1 + r2 + r3 && r4 > 0);
+        if (early_here && (!r4s.pr.empty() || !r4s.qr.empty() || r1 != m1 || r1 != n1)) {
+            // R's permutations or this node's pivot gather move rows/columns of the early copies --
+            // its own and, through the gather rotations, those of every spine node below: re-copy
+            // the whole node region at the end
+            early.redo.push_back(EarlyTop::Reg{reg_top.r0, reg_top.c0, m, n});
+        }
         apply(r4s, 0, a.sub(m1 + r3, 0, m - m1 - r3, r1 + r3));  // :156-161
         if (r2 > 0) apply(r4s, 0, a.sub(m1 + r3, n1, m - m1 - r3, r2));
         apply(r4s, 1, a.sub(0, n1 + r2, r1, n - n1 - r2));
@@ -513,6 +596,10 @@ struct Driver {
                 if (c->rank > 0) res.fac->kids.push_back(c->fac);
         }
         arena.reset(mark);  // children consumed (stream order protects the pending kernels)
+        if (level_timing) {
+            LR.e[3] = tev();
+            levels.push_back(LR);
+        }
         return res;
     }
 
@@ -539,7 +626,9 @@ void base_dbg_dump();
 
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
     Driver drv(b, threshold, a.rows, a.cols);
+    drv.level_timing = getenv("FFG_LEVEL_TIMING") != nullptr;
     NodeRes res = drv.rec(a);
+    drv.level_report();
     drv.finish();
     drv.download(res, a.rows, a.cols, P, Q);
     base_dbg_dump();
@@ -594,14 +683,16 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
         drv.early.cs = cs;
         drv.early.host = host;
         drv.early.ldh = lda;
-        NodeRes res = drv.rec(DView{d, m, n, n}, 0, K > 0 ? spine[0] : nullptr);
+        drv.early.root = d;
+        drv.early.ld = n;
+        drv.early.tail = Driver::EarlyTop::Reg{0, 0, m, n};
+        NodeRes res = drv.rec(DView{d, m, n, n}, 0, K > 0 ? spine[0] : nullptr, /*rspine=*/true);
         drv.finish();
-        const size_t r0 = drv.early.sent && !drv.early.top_touched ? drv.early.rows : 0;
-        // after the early copy: both write the host buffer (and share the D2H engine anyway)
-        if (drv.early.sent) FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));
-        if (m > r0)
-            FFG_CUDA(cudaMemcpy2DAsync(host + r0 * lda, lda * 4, d + r0 * n, n * 4, n * 4, m - r0,
-                                       cudaMemcpyDeviceToHost, b.st));
+        // after the early copies (same host buffer, same D2H engine): the tail and stale regions
+        FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));
+        drv.early.cs = b.st;
+        drv.early_copy(drv.early.tail, b.st);
+        for (const auto& g : drv.early.redo) drv.early_copy(g, b.st);
         drv.download(res, m, n, P, Q);  // synchronizes the critical stream
         FFG_CUDA(cudaStreamSynchronize(cs));
         FFG_CUDA(cudaStreamSynchronize(b.st));
