@@ -15,12 +15,20 @@ namespace ffg {
 // One doubling level (block size BS = 2h) of tri_inverse_smem, sizes compile-time so the
 // index arithmetic is shifts.  A thread owns 4 consecutive rows x 1 column of an h x h
 // product: one load of the shared operand column feeds four exact u64 accumulators.
+// barrier over the participating threads: the whole CTA (id 0) or a named subset
+__device__ __forceinline__ void tri_bar(uint32_t id, uint32_t nth) {
+    if (id == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nth) : "memory");
+}
+
 template <bool UPPER, int R, int BS>
 __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, uint32_t* X, int xs, uint32_t* W,
-                                                   uint32_t t, uint32_t p, uint64_t mu) {
+                                                   uint32_t t, uint32_t p, uint64_t mu, uint32_t tid, uint32_t nth,
+                                                   uint32_t bar) {
     if constexpr (BS <= R) {
         constexpr uint32_t h = BS / 2, nblk = R / BS, per_blk = (h / 4) * h;
-        const uint32_t tid = threadIdx.x, nth = blockDim.x;
         for (uint32_t tile = tid; tile < nblk * per_blk; tile += nth) {
             const uint32_t blk = tile / per_blk, e = tile % per_blk, i0 = (e / h) * 4, c = e % h, ob = blk * BS;
             uint64_t s[4] = {0, 0, 0, 0};
@@ -46,7 +54,7 @@ __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, ui
                 for (int a = 0; a < 4; ++a) W[blk * h * h + (i0 + a) * h + c] = row0 + a < t ? mod_u64(s[a], p, mu) : 0u;
             }
         }
-        __syncthreads();
+        tri_bar(bar, nth);
         for (uint32_t tile = tid; tile < nblk * per_blk; tile += nth) {
             const uint32_t blk = tile / per_blk, e = tile % per_blk, i0 = (e / h) * 4, c = e % h, ob = blk * BS;
             const uint32_t* w = W + blk * h * h;
@@ -75,20 +83,22 @@ __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, ui
                 }
             }
         }
-        __syncthreads();
-        tri_inverse_levels<UPPER, R, BS * 2>(S, ss, X, xs, W, t, p, mu);
+        tri_bar(bar, nth);
+        tri_inverse_levels<UPPER, R, BS * 2>(S, ss, X, xs, W, t, p, mu, tid, nth, bar);
     }
 }
 
+// All participating threads call it: the whole CTA (tri_inverse_smem) or a subset of nth
+// threads with local index tid synchronising on named barrier `bar` (tri_inverse_part), so two
+// inverses can run side by side in one CTA.
 template <bool UPPER, int R>
-__device__ void tri_inverse_smem(const uint32_t* S, int ss, uint32_t* X, int xs, uint32_t* W, uint32_t* dinv, uint32_t t,
-                                 uint32_t p, uint64_t mu) {
+__device__ void tri_inverse_part(const uint32_t* S, int ss, uint32_t* X, int xs, uint32_t* W, uint32_t* dinv,
+                                 uint32_t t, uint32_t p, uint64_t mu, uint32_t tid, uint32_t nth, uint32_t bar) {
     constexpr int LEAF = 8;
-    const uint32_t tid = threadIdx.x, nth = blockDim.x;
     for (uint32_t idx = tid; idx < (uint32_t)R * R; idx += nth) X[(idx / R) * xs + idx % R] = 0u;
     for (uint32_t i = tid; i < (uint32_t)R; i += nth)
         dinv[i] = (!UPPER || i >= t) ? 1u : inv_mod32(S[i * ss + i], p);
-    __syncthreads();
+    tri_bar(bar, nth);
     if (tid < (uint32_t)R) {  // leaves: thread per (leaf block, column)
         const uint32_t base = (tid / LEAF) * LEAF, j = tid % LEAF;
         uint32_t x[LEAF];
@@ -122,8 +132,14 @@ __device__ void tri_inverse_smem(const uint32_t* S, int ss, uint32_t* X, int xs,
 #pragma unroll
         for (int i = 0; i < LEAF; ++i) X[(base + i) * xs + base + j] = x[i];
     }
-    __syncthreads();
-    tri_inverse_levels<UPPER, R, 2 * LEAF>(S, ss, X, xs, W, t, p, mu);
+    tri_bar(bar, nth);
+    tri_inverse_levels<UPPER, R, 2 * LEAF>(S, ss, X, xs, W, t, p, mu, tid, nth, bar);
+}
+
+template <bool UPPER, int R>
+__device__ void tri_inverse_smem(const uint32_t* S, int ss, uint32_t* X, int xs, uint32_t* W, uint32_t* dinv, uint32_t t,
+                                 uint32_t p, uint64_t mu) {
+    tri_inverse_part<UPPER, R>(S, ss, X, xs, W, dinv, t, p, mu, threadIdx.x, blockDim.x, 0);
 }
 
 }  // namespace ffg
