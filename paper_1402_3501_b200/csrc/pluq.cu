@@ -662,7 +662,9 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     };
     // spine blocks S_0 = whole matrix, S_{d+1} = top-left ceil-halves, down to ~16 MB or a leaf
     std::vector<std::pair<size_t, size_t>> sp{{m, n}};
-    while (std::min(sp.back().first, sp.back().second) > thr && sp.back().first * sp.back().second > (size_t(1) << 22))
+    static const bool no_spine = getenv("FFG_NO_SPINE") != nullptr;  // diagnostics: upload all first
+    while (!no_spine && std::min(sp.back().first, sp.back().second) > thr &&
+           sp.back().first * sp.back().second > (size_t(1) << 22))
         sp.push_back({(sp.back().first + 1) / 2, (sp.back().second + 1) / 2});
     const size_t K = sp.size() - 1;
     up(0, 0, sp[K].first, sp[K].second);
@@ -679,7 +681,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
         Driver drv(b, thr, m, n, /*keep_events=*/true);
         drv.spine_root = d;
         drv.spine = spine;
-        drv.early.armed = true;
+        drv.early.armed = getenv("FFG_NO_EARLY") == nullptr;  // diagnostics: download all at the end
         drv.early.cs = cs;
         drv.early.host = host;
         drv.early.ldh = lda;

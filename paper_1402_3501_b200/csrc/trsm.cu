@@ -129,6 +129,16 @@ __global__ void __launch_bounds__(RI_THREADS) tri_inv_rec_kernel(const uint32_t*
         X[r * TSTR + c] = 0u;
     }
     __syncthreads();
+    if constexpr ((!UPPER && UNIT) || (UPPER && !UNIT)) {
+        // tile_rec's two triangles: the compile-time-level inverse with register tiles (triinv.cuh)
+        tri_inverse_smem<UPPER, TB>(S, TSTR, X, TSTR, W, dinv, tb, p, mu);
+        uint32_t* out = Tinv + (uint64_t)blockIdx.x * TB * TB;
+        for (uint32_t idx = tid; idx < (uint32_t)TB * TB; idx += RI_THREADS) {
+            const uint32_t r = idx / TB, c = idx % TB;
+            out[idx] = (r < tb && c < tb) ? X[r * TSTR + c] : 0u;
+        }
+        return;
+    }
     for (uint32_t i = tid; i < (uint32_t)TB; i += RI_THREADS)
         dinv[i] = UNIT ? 1u : (i < tb ? inv_mod32(S[i * TSTR + i], p) : 1u);
     __syncthreads();
