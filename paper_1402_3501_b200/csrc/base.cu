@@ -720,6 +720,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
             }
         lo = __reduce_min_sync(FULL, lo);
         hi = __reduce_max_sync(FULL, hi);
+        if (lane == 0) misc[5 + warp] = lo < hi ? 1u : 0u;  // this permutation moves something
         if (lane == 0) {
             if (warp == 0) {
                 info->rank = r;
@@ -753,6 +754,9 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
     }
     if (tid == 0) {
         info->cached = 0;
+        // speculative launch (top bit of seq): the host assumed full rank and identity P, Q
+        if ((seq & SPEC_BIT) && (r != min(m, n) || misc[5] || misc[6]))
+            *reinterpret_cast<volatile uint32_t*>(&info->spec_fail) = 1u;
         __threadfence_system();
         *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
     }
@@ -825,8 +829,9 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     // shared-memory right-looking kernel, FFG_BASE_NO_SLAB=1 the register right-looking one
     const char* e_smem = getenv("FFG_BASE_SMEM");
     const char* e_slab = getenv("FFG_BASE_NO_SLAB");
-    const bool no_reg = e_smem && atoi(e_smem) != 0;
-    const bool no_slab = e_slab && atoi(e_slab) != 0;
+    const bool spec = (seq & SPEC_BIT) != 0;  // speculative launches need the slab kernel's check
+    const bool no_reg = !spec && e_smem && atoi(e_smem) != 0;
+    const bool no_slab = !spec && e_slab && atoi(e_slab) != 0;
     if (!no_reg && !no_slab && lay.m <= 64 && lay.n <= 64) {
         const size_t smem = (2 * 64 * SS + 64 * LS + 2 * 16 * 132 + 64 * 11 + 8) * 4;
         static std::once_flag once;

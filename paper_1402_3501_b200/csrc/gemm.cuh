@@ -98,6 +98,7 @@ class Workspace {
 public:
     Profiler prof;
     std::atomic<uint32_t> base_seq{0};  // sequence numbers of base-case completion mailboxes
+    int spec_rest = 0;                   // calls left before speculative full rank is tried again
     Dist dist;  // multi-GPU partitioning of the recursion's large operations (dist.cuh)
     ~Workspace() {
         for (auto& kv : bufs_)

@@ -205,7 +205,7 @@ struct Driver {
             getenv("FFG_SUBTREE_THREADS")
                 ? atoi(getenv("FFG_SUBTREE_THREADS"))
                 : std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2));
-        return max_threads > 0 && use_streams && !b.ws.prof.on && !use_factors && !E.empty() && !G.empty() &&
+        return max_threads > 0 && !spec && use_streams && !b.ws.prof.on && !use_factors && !E.empty() && !G.empty() &&
                std::min(G.rows, G.cols) > 2 * thr && std::min(E.rows, E.cols) > thr &&
                active_children().load() < max_threads;
     }
@@ -245,11 +245,32 @@ struct Driver {
         std::atomic_thread_fence(std::memory_order_acquire);
     }
 
+    // ---- speculative full-rank mode: every base case is assumed to return full rank with identity
+    // permutations -- what i.i.d. input does with probability ~1 - m/p per block -- so the host never
+    // waits for a rank and the whole recursion is enqueued at once.  Each base kernel compares and
+    // raises the sticky spec_fail flag in its mailbox; the caller keeps a backup of the input and
+    // reruns without speculation when the flag is seen (the outputs are then those of the exact
+    // path, so correctness never depends on the guess).
+    struct SpecAbort {};
+    bool spec = false;
+
     NodeRes base(DView a, NodeRes res) {
+        if (spec) {
+            if (a.rows > 64 || a.cols > 64) throw SpecAbort{};  // only the slab kernel checks
+            if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) throw SpecAbort{};
+            const uint32_t seq = ((b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT) | SPEC_BIT;
+            rr_base_launch(b, a, res.P, res.Q, info_dev, nullptr, seq);
+            ++base_cases;
+            res.rank = std::min(a.rows, a.cols);
+            res.pr = Range{};
+            res.qr = Range{};
+            res.fac = nullptr;
+            return res;
+        }
         const size_t rmax = std::min(a.rows, a.cols);
         uint32_t* slot = nullptr;
         if (use_factors && rmax <= 64 && inv_top + 2 * rmax * rmax <= inv_cap) slot = inv_arena + inv_top;
-        const uint32_t seq = b.ws.base_seq.fetch_add(1) + 1;
+        const uint32_t seq = (b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT;
         const bool asked = rr_base_launch(b, a, res.P, res.Q, info_dev, slot, seq);
         wait_mailbox(seq);  // the rank decides every later shape
         ++base_cases;
@@ -624,7 +645,49 @@ struct Driver {
 
 void base_dbg_dump();
 
+// Speculation is tried unless disabled (FFG_NO_SPEC), partitioned, profiled, or recently failed in
+// this context (then it rests for a few calls: rank-deficient workloads pay one failed try).
+static bool spec_allowed(const Blas& b, const DView& a) {
+    static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
+    if (off || b.ws.dist.active() || a.rows == 0 || a.cols == 0) return false;
+    if (b.ws.spec_rest > 0) {
+        --b.ws.spec_rest;
+        return false;
+    }
+    return true;
+}
+
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
+    if (spec_allowed(b, a)) {
+        const size_t m = a.rows, n = a.cols;
+        uint32_t* bk = nullptr;
+        FFG_CUDA(cudaMallocAsync(&bk, m * n * 4, b.st));
+        FFG_CUDA(cudaMemcpy2DAsync(bk, n * 4, a.d, a.ld * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
+        bool ok = false;
+        size_t rank = 0;
+        {
+            Driver drv(b, threshold, m, n);
+            drv.spec = true;
+            *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
+            try {
+                NodeRes res = drv.rec(a);
+                drv.finish();
+                drv.download(res, m, n, P, Q);  // synchronizes: every base kernel has reported
+                ok = *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
+                rank = res.rank;
+            } catch (const Driver::SpecAbort&) {
+                ok = false;
+            }
+            if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // all speculative work retired
+        }
+        if (ok) {
+            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            return rank;
+        }
+        FFG_CUDA(cudaMemcpy2DAsync(a.d, a.ld * 4, bk, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
+        FFG_CUDA(cudaFreeAsync(bk, b.st));
+        b.ws.spec_rest = 8;
+    }
     Driver drv(b, threshold, a.rows, a.cols);
     drv.level_timing = getenv("FFG_LEVEL_TIMING") != nullptr;
     NodeRes res = drv.rec(a);
@@ -648,6 +711,12 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     cudaStream_t cs = b.ws.stream(300, 0);  // copy stream
     uint32_t* d = nullptr;
     FFG_CUDA(cudaMallocAsync(&d, m * n * 4, b.st));
+    // speculative full rank (see Driver::spec) is off here: its device backup would share the copy
+    // stream with the spine uploads and delay them more than the saved rank round trips gain
+    // (measured: e2e 75 ms with, 63 ms without).  The machinery below stays ready for it.
+    const bool spec = false;
+    uint32_t* bk = nullptr;
+    if (spec) FFG_CUDA(cudaMallocAsync(&bk, m * n * 4, b.st));
     b.ws.reset_events();
     auto record = [&](cudaStream_t st) {
         cudaEvent_t e = b.ws.event();
@@ -656,9 +725,12 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     };
     FFG_CUDA(cudaStreamWaitEvent(cs, record(b.st), 0));
     auto up = [&](size_t r0, size_t c0, size_t rows, size_t cols) {
-        if (rows && cols)
-            FFG_CUDA(cudaMemcpy2DAsync(d + r0 * n + c0, n * 4, host + r0 * lda + c0, lda * 4, cols * 4, rows,
-                                       cudaMemcpyHostToDevice, cs));
+        if (!rows || !cols) return;
+        FFG_CUDA(cudaMemcpy2DAsync(d + r0 * n + c0, n * 4, host + r0 * lda + c0, lda * 4, cols * 4, rows,
+                                   cudaMemcpyHostToDevice, cs));
+        if (bk)
+            FFG_CUDA(cudaMemcpy2DAsync(bk + r0 * n + c0, n * 4, d + r0 * n + c0, n * 4, cols * 4, rows,
+                                       cudaMemcpyDeviceToDevice, cs));
     };
     // spine blocks S_0 = whole matrix, S_{d+1} = top-left ceil-halves, down to ~16 MB or a leaf
     std::vector<std::pair<size_t, size_t>> sp{{m, n}};
@@ -675,12 +747,16 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
         up(sp[lv + 1].first, 0, sp[lv].first - sp[lv + 1].first, sp[lv].second);
         spine[lv] = record(cs);
     }
-    size_t rank = 0;
-    {
+    // one factorisation of d with early downloads; false when a speculative guess failed
+    auto run = [&](bool speculative, bool upload_pending, size_t& rank) -> bool {
         // the Driver resets the event cursor: keep the events above alive by recording after it
         Driver drv(b, thr, m, n, /*keep_events=*/true);
-        drv.spine_root = d;
-        drv.spine = spine;
+        drv.spec = speculative;
+        if (speculative) *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
+        if (upload_pending) {
+            drv.spine_root = d;
+            drv.spine = spine;
+        }
         drv.early.armed = getenv("FFG_NO_EARLY") == nullptr;  // diagnostics: download all at the end
         drv.early.cs = cs;
         drv.early.host = host;
@@ -688,18 +764,33 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
         drv.early.root = d;
         drv.early.ld = n;
         drv.early.tail = Driver::EarlyTop::Reg{0, 0, m, n};
-        NodeRes res = drv.rec(DView{d, m, n, n}, 0, K > 0 ? spine[0] : nullptr, /*rspine=*/true);
-        drv.finish();
-        // after the early copies (same host buffer, same D2H engine): the tail and stale regions
-        FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));
-        drv.early.cs = b.st;
-        drv.early_copy(drv.early.tail, b.st);
-        for (const auto& g : drv.early.redo) drv.early_copy(g, b.st);
-        drv.download(res, m, n, P, Q);  // synchronizes the critical stream
-        FFG_CUDA(cudaStreamSynchronize(cs));
-        FFG_CUDA(cudaStreamSynchronize(b.st));
-        rank = res.rank;
+        try {
+            NodeRes res = drv.rec(DView{d, m, n, n}, 0, upload_pending && K > 0 ? spine[0] : nullptr,
+                                  /*rspine=*/true);
+            drv.finish();
+            // after the early copies (same host buffer, same D2H engine): the tail and stale regions
+            FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));
+            drv.early.cs = b.st;
+            drv.early_copy(drv.early.tail, b.st);
+            for (const auto& g : drv.early.redo) drv.early_copy(g, b.st);
+            drv.download(res, m, n, P, Q);  // synchronizes the critical stream
+            FFG_CUDA(cudaStreamSynchronize(cs));
+            FFG_CUDA(cudaStreamSynchronize(b.st));
+            rank = res.rank;
+        } catch (const Driver::SpecAbort&) {
+            FFG_CUDA(cudaDeviceSynchronize());
+            return false;
+        }
+        return !speculative || *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
+    };
+    size_t rank = 0;
+    if (!run(spec, true, rank)) {
+        FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
+        FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, bk, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
+        b.ws.spec_rest = 8;
+        run(false, false, rank);
     }
+    if (bk) FFG_CUDA(cudaFreeAsync(bk, b.st));
     FFG_CUDA(cudaFreeAsync(d, b.st));
     return rank;
 }

@@ -46,9 +46,12 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
 // rank + moved ranges of a base-case result (device -> pinned host)
 struct BaseInfo {
     uint32_t rank, plo, phi, qlo, qhi;
-    uint32_t cached;  // 1 when inv_out received inv(L_r), inv(U_r) (r x r each, ld r)
-    uint32_t seq;     // written last: the launch's sequence number (host spins on it)
+    uint32_t cached;     // 1 when inv_out received inv(L_r), inv(U_r) (r x r each, ld r)
+    uint32_t seq;        // written last: the launch's sequence number (host spins on it)
+    uint32_t spec_fail;  // sticky: a speculative launch (seq & SPEC_BIT) did not see full rank +
+                         // identity permutations
 };
+constexpr uint32_t SPEC_BIT = 0x80000000u;
 // one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info; with
 // inv_out != nullptr also the inverses of the leading r x r L and U factors (r <= 64)
 // returns whether inverses were requested (the kernel still reports info->cached)
