@@ -570,7 +570,11 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
         }
         stamp(1);
         // (B) sequential pivoting inside the slab: warp w <-> row i0 + w
-        uint32_t last = i0 == 0 ? NONE : i0 - 1;  // rows <= last are done
+        // Normally only the warp of the next row publishes (the lead): on full-rank input the next
+        // row always is the pivot.  If that row is zero the lead posts SLOW and every warp offers its
+        // row in an extra round (rank deficiency only).
+        constexpr uint32_t SLOW = NONE - 1;
+        uint32_t first = i0;  // rows < first are done
         uint32_t t = 0;
         bool is_pivot = false;
         if (tid == 0) misc[2] = misc[3] = misc[4] = NONE;
@@ -578,33 +582,42 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
         // one barrier per pivot: slots are double-buffered and the winner cell rotates over three,
         // so a cell is reset only after every thread has passed the barrier following its last read
         uint32_t rot = 0;
+        auto offer = [&](uint32_t* my, uint32_t* cell) -> bool {  // whole warp; true if nonzero
+            x0 = red4p(x0, p);
+            x1 = red4p(x1, p);
+            const uint32_t b0 = __ballot_sync(FULL, x0 != 0u), b1 = __ballot_sync(FULL, x1 != 0u);
+            if (!(b0 | b1)) return false;
+            my[lane] = x0;
+            my[lane + 32] = x1;
+            my[64 + lane] = shoup_pre(x0, p, mu);
+            my[96 + lane] = shoup_pre(x1, p, mu);
+            const uint32_t pj = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
+            const uint32_t pv = __shfl_sync(FULL, pj < 32 ? x0 : x1, pj & 31);
+            if (lane == 0) {
+                my[128] = i;
+                my[129] = pj;
+                my[130] = pv;
+                my[131] = shoup_pre(pv, p, mu);
+                atomicMin(cell, i);
+            }
+            return true;
+        };
         while (R + t < n) {
             const uint32_t par = t & 1;
             uint32_t* my = slot + (par * 16 + warp) * 132;
-            if (live && (last == NONE || i > last) && !is_pivot) {
-                x0 = red4p(x0, p);
-                x1 = red4p(x1, p);
-                const uint32_t b0 = __ballot_sync(FULL, x0 != 0u), b1 = __ballot_sync(FULL, x1 != 0u);
-                if (b0 | b1) {
-                    my[lane] = x0;
-                    my[lane + 32] = x1;
-                    my[64 + lane] = shoup_pre(x0, p, mu);
-                    my[96 + lane] = shoup_pre(x1, p, mu);
-                    const uint32_t pj = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
-                    const uint32_t pv = __shfl_sync(FULL, pj < 32 ? x0 : x1, pj & 31);
-                    if (lane == 0) {
-                        my[128] = i;
-                        my[129] = pj;
-                        my[130] = pv;
-                        my[131] = shoup_pre(pv, p, mu);
-                        atomicMin(misc + 2 + rot, i);
-                    }
-                }
-            }
+            uint32_t* cell = misc + 2 + rot;
+            if (live && i == first && !offer(my, cell) && lane == 0) atomicMin(cell, SLOW);
             if (tid == 0) misc[2 + (rot == 2 ? 0 : rot + 1)] = NONE;  // the next step's cell
             __syncthreads();
-            const uint32_t pi = misc[2 + rot];
+            uint32_t pi = *cell;
             rot = rot == 2 ? 0 : rot + 1;
+            if (pi == SLOW) {  // uniform: the next row is zero -- every later row offers itself
+                if (tid == 0) misc[5] = NONE;
+                __syncthreads();
+                if (live && i > first && !is_pivot) offer(my, misc + 5);
+                __syncthreads();
+                pi = misc[5];
+            }
             if (pi == NONE) break;  // uniform: the slab has no nonzero row left
             const uint32_t* pr = slot + (par * 16 + (pi - i0)) * 132;
             const uint32_t pj = pr[129], pv = pr[130], pvp = pr[131];
@@ -622,7 +635,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
                 x1 = (x1 * pv - __umulhi(x1, pvp) * p) + 2 * p - (numer * b1 - __umulhi(numer, f1) * p);
             }
             if (i == pi) is_pivot = true;  // its registers hold the published (reduced) row
-            last = pi;
+            first = pi + 1;                // rows between the previous pivot and pi were zero
             ++t;
         }
         __syncthreads();
