@@ -426,6 +426,62 @@ struct Driver {
         levels.clear();
     }
 
+    // ---- panel mode (speculative runs on square input): with full rank and identity
+    // permutations the TRSMs of tile_rec (:111-114) need not wait for a whole child: every base
+    // case solves its entire right panel (its rows, all later columns) with its L and its entire
+    // bottom panel with its U right after it is factored, and every internal node, once its A1
+    // child is done, updates [H | right panel of R's rows] and the bottom panel of R's columns
+    // with two wide GEMMs.  This is tile_rec's arithmetic evaluated right-looking inside the same
+    // recursion; L, U (unique for full rank without pivoting) come out identical, and no TRSM
+    // chain remains above the base cases.  Any failed guess reruns the exact path anyway.
+    bool panel = false;
+    const uint32_t* proot = nullptr;
+    size_t pld = 0, prows = 0, pcols = 0;
+
+    NodeRes rec_panel(DView a, int depth) {
+        const size_t m = a.rows, n = a.cols;  // square
+        NodeRes res;
+        res.P = arena.alloc(std::max<size_t>(m, 1));
+        res.Q = arena.alloc(std::max<size_t>(n, 1));
+        if (m == 0 || n == 0) return res;
+        const size_t off = (size_t)(a.d - proot), r0 = off / pld, c0 = off % pld;
+        if (std::min(m, n) <= thr) {
+            res = base(a, res);  // speculative: no wait
+            // whole right panel (L^-1, left) and bottom panel (U^-1, right) of this block
+            DView right{a.d + n, m, pcols - (c0 + n), pld};
+            DView bottom{a.d + m * pld, prows - (r0 + m), n, pld};
+            const bool both = !right.empty() && !bottom.empty();
+            const Blas side = both ? on(twin(depth)) : b;
+            if (both) wait(side.st, mark_event(b.st));
+            if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
+            if (!bottom.empty()) ftrsm_dev(side, 1, 1, 1, a, bottom, false);
+            if (both) wait(b.st, mark_event(side.st));
+            return res;
+        }
+        const size_t mark = arena.mark();
+        const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;
+        rec_panel(a.sub(0, 0, m1, n1), depth + 1);
+        // A1's panels solved D and Fb (and the parts of A1's rows / columns beyond this node)
+        DView Fb = a.sub(m1, 0, m - m1, n1);                                  // rows of R, cols of A1
+        DView Dx{a.d + n1, m1, pcols - (c0 + n1), pld};                       // A1 rows, cols >= n1
+        DView HR{a.d + m1 * pld + n1, m - m1, pcols - (c0 + n1), pld};        // [H | right panel]
+        DView Fbelow{a.d + m * pld, prows - (r0 + m), n1, pld};               // below the node, A1 cols
+        DView Dn = a.sub(0, n1, m1, n - n1);                                  // D
+        DView BP{a.d + m * pld + n1, prows - (r0 + m), n - n1, pld};          // below the node, R cols
+        const bool both = !BP.empty();
+        const Blas side = both ? on(twin(depth)) : b;
+        if (both) wait(side.st, mark_event(b.st));
+        if (!HR.empty()) gemm_sub(b, Fb, Dx, HR);
+        if (both) gemm_sub(side, Fbelow, Dn, BP);
+        if (both) wait(b.st, mark_event(side.st));
+        rec_panel(a.sub(m1, n1, m - m1, n - n1), depth + 1);
+        res.rank = std::min(m, n);
+        res.pr = Range{};
+        res.qr = Range{};
+        arena.reset(mark);
+        return res;
+    }
+
     NodeRes rec(DView a, int depth = 0, cudaEvent_t pending = nullptr, bool rspine = false) {
         const size_t m = a.rows, n = a.cols;
         NodeRes res;
@@ -669,8 +725,14 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             Driver drv(b, threshold, m, n);
             drv.spec = true;
             *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
+            const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
+            drv.panel = !no_panel && m == n && std::min(m, n) > 0 && drv.use_streams;
+            drv.proot = a.d;
+            drv.pld = a.ld;
+            drv.prows = m;
+            drv.pcols = n;
             try {
-                NodeRes res = drv.rec(a);
+                NodeRes res = drv.panel ? drv.rec_panel(a, 0) : drv.rec(a);
                 drv.finish();
                 drv.download(res, m, n, P, Q);  // synchronizes: every base kernel has reported
                 ok = *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
