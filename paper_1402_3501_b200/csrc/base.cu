@@ -775,6 +775,160 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Speculative base case (m, n <= 64): the caller assumed full rank with identity permutations,
+// i.e. that the pivot of step k is (k, k).  Then rr_base is plain LU without pivoting -- the
+// pivot search picks row k (the first remaining row; it is nonzero at column k) and column k (its
+// first nonzero entry, every earlier column having been eliminated) -- so the kernel runs that LU
+// with no search and checks the guess: a zero diagonal pivot raises spec_fail and the caller
+// reruns exactly (the outputs of a failed launch are never used).
+//
+// Fraction-free over the whole block: row_i <- pv_k * row_i - row_i[k] * row_k keeps row_i =
+// D_k * (exact Schur row) with D_k = prod_{j<k} pv_j, so no inverse is needed while eliminating;
+// at the end one modular inverse (prefix / suffix products) gives U_k = row_k / D_k and
+// L_ik = numer_ik / pv_k (numer_ik = row_i[k] at step k, frozen in place in the register of
+// column k).  Rows stay in registers (warp w owns rows w, w+16, w+32, w+48; lane l columns l and
+// l+32); the owner of row k+1 publishes it (reduced, with Shoup factors) right after its step-k
+// update into a double-buffered slot -- one barrier per pivot, no slab phases.
+constexpr int SP_WARPS = 16;
+constexpr int SP_THREADS = SP_WARPS * 32;
+constexpr int SP_RPW = 64 / SP_WARPS;  // rows per warp
+
+__global__ void __launch_bounds__(SP_THREADS, 1)
+    rr_base_spec_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t m, uint32_t n, uint32_t* __restrict__ Pd,
+                        uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p, uint64_t mu,
+                        uint32_t seq) {
+    __shared__ __align__(16) uint32_t buf[2][128];  // published pivot row: 64 values, 64 Shoup factors
+    __shared__ uint32_t pvs[64];                     // fraction-free pivots
+    __shared__ uint32_t invd[64], invdf[64];         // 1 / D_k and its Shoup factor
+    __shared__ uint32_t invp[64], invpf[64];         // 1 / pv_k and its Shoup factor
+    __shared__ uint32_t fail;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t r = min(m, n);
+    ptx::pdl_enter();
+
+    uint32_t x[SP_RPW][2];
+#pragma unroll
+    for (int j = 0; j < SP_RPW; ++j) {
+        const uint32_t i = warp + SP_WARPS * j;
+        const uint32_t* row = A + (uint64_t)i * lda;
+        x[j][0] = (i < m && lane < n) ? row[lane] : 0u;
+        x[j][1] = (i < m && lane + 32 < n) ? row[lane + 32] : 0u;
+    }
+    auto publish = [&](uint32_t& a0, uint32_t& a1, uint32_t* dst) {
+        a0 = red4p(a0, p);
+        a1 = red4p(a1, p);
+        dst[lane] = a0;
+        dst[lane + 32] = a1;
+        dst[64 + lane] = shoup_pre(a0, p, mu);
+        dst[96 + lane] = shoup_pre(a1, p, mu);
+    };
+    if (tid == 0) fail = 0u;
+    if (warp == 0 && r > 0) publish(x[0][0], x[0][1], buf[0]);
+    __syncthreads();
+
+    for (uint32_t k = 0; k < r; ++k) {
+        const uint32_t* pr = buf[k & 1];
+        const uint32_t pv = pr[k], pvp = pr[64 + k];
+        const uint32_t b0 = pr[lane], b1 = pr[lane + 32], f0 = pr[64 + lane], f1 = pr[96 + lane];
+        if (tid == 0) {
+            pvs[k] = pv;
+            if (pv == 0u) fail = 1u;
+        }
+        const uint32_t nxt = k + 1;
+#pragma unroll
+        for (int j = 0; j < SP_RPW; ++j) {
+            const uint32_t i = warp + SP_WARPS * j;
+            if (i > k && i < m) {  // warp-uniform
+                const uint32_t numer = red4p(__shfl_sync(FULL, k < 32 ? x[j][0] : x[j][1], k & 31), p);
+                const uint32_t u0 = (x[j][0] * pv - __umulhi(x[j][0], pvp) * p) + 2 * p -
+                                    (numer * b0 - __umulhi(numer, f0) * p);
+                const uint32_t u1 = (x[j][1] * pv - __umulhi(x[j][1], pvp) * p) + 2 * p -
+                                    (numer * b1 - __umulhi(numer, f1) * p);
+                // columns > k take the update; column k keeps the L numerator; earlier ones stay
+                x[j][0] = lane > k ? u0 : (lane == k ? numer : x[j][0]);
+                x[j][1] = lane + 32 > k ? u1 : (lane + 32 == k ? numer : x[j][1]);
+                if (i == nxt && nxt < r) publish(x[j][0], x[j][1], buf[nxt & 1]);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- one inverse: D_k = prod_{j<k} pv_j, 1/D_k and 1/pv_k = D_k / D_{k+1}
+    if (warp == 0 && r > 0 && !fail) {
+        const uint32_t e0 = 2 * lane, e1 = 2 * lane + 1;
+        const uint32_t v0 = e0 < r ? pvs[e0] : 1u, v1 = e1 < r ? pvs[e1] : 1u;
+        uint32_t inc = mul_mod(v0, v1, p, mu);  // inclusive scan of pair products
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(FULL, inc, off);
+            if (lane >= (uint32_t)off) inc = mul_mod(inc, o, p, mu);
+        }
+        uint32_t exc = __shfl_up_sync(FULL, inc, 1);
+        if (lane == 0) exc = 1u % p;
+        const uint32_t D0 = exc, D1 = mul_mod(exc, v0, p, mu);  // D_{e0}, D_{e1}
+        const uint32_t total = __shfl_sync(FULL, inc, 31);
+        const uint32_t tinv = __shfl_sync(FULL, lane == 0 ? inv_mod_bin(total, p) : 0u, 0);
+        uint32_t suf = mul_mod(v0, v1, p, mu);  // inclusive suffix scan of pair products
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_down_sync(FULL, suf, off);
+            if (lane + off < 32) suf = mul_mod(suf, o, p, mu);
+        }
+        // 1/D_e = tinv * prod_{j >= e} pv_j
+        const uint32_t iD0 = mul_mod(tinv, suf, p, mu);
+        const uint32_t sufx = __shfl_down_sync(FULL, suf, 1);
+        const uint32_t iD2 = mul_mod(tinv, lane == 31 ? 1u % p : sufx, p, mu);  // 1/D_{e0+2}
+        const uint32_t iD1 = mul_mod(iD2, v1, p, mu);
+        if (e0 < r) {
+            invd[e0] = iD0;
+            invdf[e0] = shoup_pre(iD0, p, mu);
+            const uint32_t ip = mul_mod(D0, iD1, p, mu);  // D_e0 / D_{e0+1}
+            invp[e0] = ip;
+            invpf[e0] = shoup_pre(ip, p, mu);
+        }
+        if (e1 < r) {
+            invd[e1] = iD1;
+            invdf[e1] = shoup_pre(iD1, p, mu);
+            const uint32_t ip = mul_mod(D1, iD2, p, mu);
+            invp[e1] = ip;
+            invpf[e1] = shoup_pre(ip, p, mu);
+        }
+    }
+    __syncthreads();
+    if (!fail) {
+#pragma unroll
+        for (int j = 0; j < SP_RPW; ++j) {
+            const uint32_t i = warp + SP_WARPS * j;
+            if (i >= m) continue;
+            uint32_t* row = A + (uint64_t)i * lda;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t c = lane + 32 * h;
+                if (c >= n) continue;
+                uint32_t v;
+                if (c < i)  // L entry (c < r: every column is a pivot column when i >= r)
+                    v = shoup_mul(x[j][h], invp[c], invpf[c], p);
+                else  // U entry of pivot row i < r
+                    v = shoup_mul(x[j][h], invd[i], invdf[i], p);
+                row[c] = v;
+            }
+        }
+    }
+    for (uint32_t ii = tid; ii < m; ii += SP_THREADS) Pd[ii] = ii;
+    for (uint32_t jj = tid; jj < n; jj += SP_THREADS) Qd[jj] = jj;
+    __syncthreads();
+    if (tid == 0) {
+        info->rank = r;
+        info->plo = info->phi = info->qlo = info->qhi = 0;
+        info->cached = 0;
+        if ((seq & SPEC_BIT) && fail) *reinterpret_cast<volatile uint32_t*>(&info->spec_fail) = 1u;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+    }
+}
+
 void base_dbg_init() {
     static bool done = false;
     if (done || !getenv("FFG_BASE_DBG")) return;
@@ -845,6 +999,15 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const bool spec = (seq & SPEC_BIT) != 0;  // speculative launches need the slab kernel's check
     const bool no_reg = !spec && e_smem && atoi(e_smem) != 0;
     const bool no_slab = !spec && e_slab && atoi(e_slab) != 0;
+    const char* e_spec = getenv("FFG_SPEC_SLAB");  // diagnostics: speculative launches on the slab kernel
+    if (spec && lay.m <= 64 && lay.n <= 64 && !(e_spec && atoi(e_spec) != 0)) {
+        launch_k(rr_base_spec_kernel, dim3(1), dim3(SP_THREADS), 0, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd, info,
+                 b.F.p, b.F.mu, seq);
+        FFG_CUDA(cudaGetLastError());
+        b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
+        b.count();
+        return false;
+    }
     if (!no_reg && !no_slab && lay.m <= 64 && lay.n <= 64) {
         const size_t smem = (2 * 64 * SS + 64 * LS + 2 * 16 * 132 + 64 * 11 + 8) * 4;
         static std::once_flag once;

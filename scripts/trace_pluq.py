@@ -25,6 +25,7 @@ ap.add_argument("--p", type=int, default=131071)
 ap.add_argument("--thr", type=int, default=64)
 ap.add_argument("--lru", action="store_true")
 ap.add_argument("--json", default=None)
+ap.add_argument("--chrome", default=None, help="also export the raw chrome trace here")
 a = ap.parse_args()
 
 st = torch.cuda.Stream()
@@ -48,6 +49,8 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     e1.record(st)
     torch.cuda.synchronize()
 wall = e0.elapsed_time(e1)
+if a.chrome:
+    prof.export_chrome_trace(a.chrome)
 evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.device_time_total > 0]
 ks = []
 for e in evs:
