@@ -6,6 +6,8 @@
 // an index array (PermSeq::to_array() semantics) and every application is one
 // gather over the moved range only: HBM traffic = 2 reads + 2 writes of the
 // rows/columns that actually move, nothing for the rest.
+#include <algorithm>
+
 #include "pluq.cuh"
 #include "ptx.cuh"
 
@@ -170,6 +172,35 @@ void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_
     b.count();
     perm_apply_range(b, a, axis, invp, 0, dim);
     FFG_CUDA(cudaFreeAsync(invp, b.st));
+}
+
+// dst <- src (same shape): 16-byte accesses when both views allow them.  The host entry's
+// speculative path backs its input up in HBM with this (a kernel, not a DMA copy: the copy
+// engines are busy with the PCIe transfers).
+__global__ void copy_block_kernel(const uint32_t* __restrict__ S, uint64_t lds, uint32_t* __restrict__ D, uint64_t ldd,
+                                  uint32_t rows, uint32_t cols, uint32_t vec) {
+    const uint32_t per = vec ? cols / 4 : cols;
+    const uint64_t total = (uint64_t)rows * per;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = t / per, c = t % per;
+        if (vec)
+            reinterpret_cast<uint4*>(D + r * ldd)[c] = reinterpret_cast<const uint4*>(S + r * lds)[c];
+        else
+            D[r * ldd + c] = S[r * lds + c];
+    }
+}
+
+void copy_block_dev(const Blas& b, DView src, DView dst) {
+    if (src.empty()) return;
+    const bool vec = src.cols % 4 == 0 && src.ld % 4 == 0 && dst.ld % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(src.d) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst.d) & 15) == 0;
+    const uint64_t items = (uint64_t)src.rows * (vec ? src.cols / 4 : src.cols);
+    int sms = 148;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(items, 256), (uint64_t)sms * 4);
+    copy_block_kernel<<<grid, 256, 0, b.st>>>(src.d, src.ld, dst.d, dst.ld, (uint32_t)src.rows, (uint32_t)src.cols,
+                                              vec ? 1u : 0u);
+    FFG_CUDA(cudaGetLastError());
+    b.count();
 }
 
 }  // namespace ffg

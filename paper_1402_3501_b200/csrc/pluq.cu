@@ -438,6 +438,60 @@ struct Driver {
     const uint32_t* proot = nullptr;
     size_t pld = 0, prows = 0, pcols = 0;
 
+    // ---- streamed host entry (panel mode on host buffers).  Panel mode touches the matrix in
+    // L-shaped bands of increasing index -- band [a, e) = rows [a, e) x cols [a, n) plus rows
+    // [e, n) x cols [a, e) -- and a band is final once its last base case has solved its panels,
+    // so band c uploads while earlier bands factor and downloads as soon as it is done.  Band
+    // ends sit on node boundaries of the recursion (band_bounds).
+    struct Bands {
+        bool on = false;
+        std::vector<size_t> end;                              // band c = [end[c-1], end[c])
+        std::vector<cudaEvent_t> ready;                       // band c uploaded (and backed up)
+        std::vector<std::pair<cudaStream_t, size_t>> waited;  // per stream: bands already waited for
+        cudaStream_t down = nullptr;                          // D2H copy stream
+        uint32_t* host = nullptr;
+        size_t ldh = 0, next_down = 0;
+    } bands;
+    void band_copy(size_t c, bool to_host, cudaStream_t st) {
+        const size_t a0 = c ? bands.end[c - 1] : 0, e = bands.end[c], n = pcols, m = prows;
+        auto rect = [&](size_t r0, size_t c0, size_t rows, size_t cols) {
+            if (!rows || !cols) return;
+            uint32_t* dv = const_cast<uint32_t*>(proot) + r0 * pld + c0;
+            uint32_t* hv = bands.host + r0 * bands.ldh + c0;
+            if (to_host)
+                FFG_CUDA(cudaMemcpy2DAsync(hv, bands.ldh * 4, dv, pld * 4, cols * 4, rows, cudaMemcpyDeviceToHost, st));
+            else
+                FFG_CUDA(cudaMemcpy2DAsync(dv, pld * 4, hv, bands.ldh * 4, cols * 4, rows, cudaMemcpyHostToDevice, st));
+        };
+        rect(a0, a0, e - a0, n - a0);
+        rect(e, a0, m - e, e - a0);
+    }
+    // every later operation on `st` may touch rows / columns < hi
+    void need(cudaStream_t st, size_t hi) {
+        if (!bands.on) return;
+        const size_t c = (size_t)(std::lower_bound(bands.end.begin(), bands.end.end(), hi) - bands.end.begin());
+        if (c >= bands.ready.size()) return;
+        size_t* w = nullptr;
+        for (auto& pr : bands.waited)
+            if (pr.first == st) w = &pr.second;
+        if (!w) {
+            bands.waited.push_back({st, 0});
+            w = &bands.waited.back().second;
+        }
+        if (*w < c + 1) {
+            wait(st, bands.ready[c]);
+            *w = c + 1;
+        }
+    }
+    // every operation on rows / columns < hi is enqueued (and joined into the critical stream)
+    void band_done(size_t hi) {
+        if (!bands.on) return;
+        while (bands.next_down < bands.end.size() && bands.end[bands.next_down] <= hi) {
+            wait(bands.down, mark_event(b.st));
+            band_copy(bands.next_down++, true, bands.down);
+        }
+    }
+
     NodeRes rec_panel(DView a, int depth) {
         const size_t m = a.rows, n = a.cols;  // square
         NodeRes res;
@@ -446,6 +500,7 @@ struct Driver {
         if (m == 0 || n == 0) return res;
         const size_t off = (size_t)(a.d - proot), r0 = off / pld, c0 = off % pld;
         if (std::min(m, n) <= thr) {
+            need(b.st, r0 + m);
             res = base(a, res);  // speculative: no wait
             // whole right panel (L^-1, left) and bottom panel (U^-1, right) of this block
             DView right{a.d + n, m, pcols - (c0 + n), pld};
@@ -456,6 +511,7 @@ struct Driver {
             if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
             if (!bottom.empty()) ftrsm_dev(side, 1, 1, 1, a, bottom, false);
             if (both) wait(b.st, mark_event(side.st));
+            band_done(r0 + m);
             return res;
         }
         const size_t mark = arena.mark();
@@ -470,11 +526,13 @@ struct Driver {
         DView BP{a.d + m * pld + n1, prows - (r0 + m), n - n1, pld};          // below the node, R cols
         const bool both = !BP.empty();
         const Blas side = both ? on(twin(depth)) : b;
+        need(b.st, r0 + m);
         if (both) wait(side.st, mark_event(b.st));
         if (!HR.empty()) gemm_sub(b, Fb, Dx, HR);
         if (both) gemm_sub(side, Fbelow, Dn, BP);
         if (both) wait(b.st, mark_event(side.st));
         rec_panel(a.sub(m1, n1, m - m1, n - n1), depth + 1);
+        band_done(r0 + m);
         res.rank = std::min(m, n);
         res.pr = Range{};
         res.qr = Range{};
@@ -713,8 +771,77 @@ static bool spec_allowed(const Blas& b, const DView& a) {
     return true;
 }
 
+// band ends for the streamed host entry: the recursion's nodes of size <= T in order (finer at
+// the start so that the first base case waits for a small first band)
+static void band_bounds(size_t o, size_t s, size_t thr, size_t T, size_t Tmin, std::vector<size_t>& out) {
+    if (s <= thr || s <= std::min(T, std::max(Tmin, o))) {
+        out.push_back(o + s);
+        return;
+    }
+    const size_t h = (s + 1) / 2;
+    band_bounds(o, h, thr, T, Tmin, out);
+    band_bounds(o + h, s - h, thr, T, Tmin, out);
+}
+
+// Streamed speculative attempt of the host entry (square input, panel mode): band c uploads on
+// one copy engine, is backed up in HBM by a copy kernel, factors, and downloads on the other copy
+// engine as soon as its last base case is done -- PCIe in both directions overlaps the
+// factorisation.  false: the guess failed (or was abandoned); d then holds the input again.
+static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t lda, size_t thr, uint32_t* d,
+                               uint32_t* P, uint32_t* Q, size_t& rank) {
+    uint32_t* bk = nullptr;
+    FFG_CUDA(cudaMallocAsync(&bk, n * n * 4, b.st));
+    bool ok = false;
+    {
+        Driver drv(b, thr, n, n);
+        drv.spec = true;
+        *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
+        drv.panel = true;
+        drv.proot = d;
+        drv.pld = n;
+        drv.prows = n;
+        drv.pcols = n;
+        cudaStream_t up = b.ws.stream(300, 0), down = b.ws.stream(301, 0), bks = b.ws.stream(302, 0);
+        cudaEvent_t start = drv.b.ws.event();  // d and bk are allocated on the caller's stream
+        FFG_CUDA(cudaEventRecord(start, b.st));
+        for (cudaStream_t st : {up, down, bks}) drv.wait(st, start);
+        const size_t T = std::max<size_t>(256, n / 16);
+        band_bounds(0, n, thr, T, std::max<size_t>(64, T / 4), drv.bands.end);
+        drv.bands.on = true;
+        drv.bands.host = host;
+        drv.bands.ldh = lda;
+        drv.bands.down = down;
+        const Blas bb = drv.on(bks);
+        for (size_t c = 0; c < drv.bands.end.size(); ++c) {
+            drv.band_copy(c, false, up);
+            drv.wait(bks, drv.mark_event(up));
+            const size_t a0 = c ? drv.bands.end[c - 1] : 0, e = drv.bands.end[c];
+            copy_block_dev(bb, DView{d + a0 * n + a0, e - a0, n - a0, n}, DView{bk + a0 * n + a0, e - a0, n - a0, n});
+            copy_block_dev(bb, DView{d + e * n + a0, n - e, e - a0, n}, DView{bk + e * n + a0, n - e, e - a0, n});
+            drv.bands.ready.push_back(drv.mark_event(bks));
+        }
+        try {
+            NodeRes res = drv.rec_panel(DView{d, n, n, n}, 0);
+            drv.finish();
+            drv.download(res, n, n, P, Q);  // synchronizes the critical stream
+            FFG_CUDA(cudaStreamSynchronize(down));
+            ok = *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
+            rank = res.rank;
+        } catch (const Driver::SpecAbort&) {
+            ok = false;
+        }
+        if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
+    }
+    if (!ok) {
+        FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, bk, n * 4, n * 4, n, cudaMemcpyDeviceToDevice, b.st));
+        b.ws.spec_rest = 8;
+    }
+    FFG_CUDA(cudaFreeAsync(bk, b.st));
+    return ok;
+}
+
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
-    if (spec_allowed(b, a)) {
+    if (threshold <= 64 && spec_allowed(b, a)) {
         const size_t m = a.rows, n = a.cols;
         uint32_t* bk = nullptr;
         FFG_CUDA(cudaMallocAsync(&bk, m * n * 4, b.st));
@@ -773,6 +900,19 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     cudaStream_t cs = b.ws.stream(300, 0);  // copy stream
     uint32_t* d = nullptr;
     FFG_CUDA(cudaMallocAsync(&d, m * n * 4, b.st));
+    static const bool no_stream_spec = getenv("FFG_NO_HOST_SPEC") != nullptr;
+    static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
+    static const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
+    bool restored = false;  // d already holds the input (a failed speculative attempt restored it)
+    if (m == n && thr <= 64 && !no_stream_spec && !no_streams && !no_panel && spec_allowed(b, DView{host, m, n, lda})) {
+        size_t rank = 0;
+        if (host_streamed_spec(b, host, n, lda, thr, d, P, Q, rank)) {
+            FFG_CUDA(cudaFreeAsync(d, b.st));
+            FFG_CUDA(cudaStreamSynchronize(b.st));
+            return rank;
+        }
+        restored = true;
+    }
     // speculative full rank (see Driver::spec) is off here: its device backup would share the copy
     // stream with the spine uploads and delay them more than the saved rank round trips gain
     // (measured: e2e 75 ms with, 63 ms without).  The machinery below stays ready for it.
@@ -797,11 +937,11 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     // spine blocks S_0 = whole matrix, S_{d+1} = top-left ceil-halves, down to ~16 MB or a leaf
     std::vector<std::pair<size_t, size_t>> sp{{m, n}};
     static const bool no_spine = getenv("FFG_NO_SPINE") != nullptr;  // diagnostics: upload all first
-    while (!no_spine && std::min(sp.back().first, sp.back().second) > thr &&
+    while (!restored && !no_spine && std::min(sp.back().first, sp.back().second) > thr &&
            sp.back().first * sp.back().second > (size_t(1) << 22))
         sp.push_back({(sp.back().first + 1) / 2, (sp.back().second + 1) / 2});
     const size_t K = sp.size() - 1;
-    up(0, 0, sp[K].first, sp[K].second);
+    if (!restored) up(0, 0, sp[K].first, sp[K].second);
     FFG_CUDA(cudaStreamWaitEvent(b.st, record(cs), 0));  // the deepest spine block is in place
     std::vector<cudaEvent_t> spine(K, nullptr);
     for (size_t lv = K; lv-- > 0;) {  // S_lv minus S_{lv+1}: right strip, then the rows below
@@ -846,7 +986,9 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
         return !speculative || *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
     };
     size_t rank = 0;
-    if (!run(spec, true, rank)) {
+    if (restored) {
+        run(false, false, rank);
+    } else if (!run(spec, true, rank)) {
         FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
         FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, bk, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
         b.ws.spec_rest = 8;

@@ -87,4 +87,7 @@ void lru_matrix_dev(const Blas& b, DView M, size_t r, uint64_t seed, uint32_t* r
 // row (axis 0) / column (axis 1) gather by a device index array
 void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_t* perm);
 
+// dst <- src, same shape (device copy kernel)
+void copy_block_dev(const Blas& b, DView src, DView dst);
+
 }  // namespace ffg

@@ -69,3 +69,31 @@ def test_concurrent_subtrees_match_oracle(gpu, oracle_lib, threads, monkeypatch)
     assert res.rank == r_o == n // 2
     assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
     assert np.array_equal(a_g, a_o)
+
+
+@pytest.mark.parametrize("n,dup", [(2048, None), (1500, None), (2048, (1900, 5)), (2048, (200, 7)), (777, None)])
+def test_streamed_speculative_host_entry(gpu, oracle_lib, n, dup):
+    """Square input through the host entry takes the streamed speculative path (bands upload,
+    factor and download concurrently).  A duplicated row makes a late (1900) or early (200) base
+    case rank deficient: the guess fails after earlier bands already reached the host buffer, and
+    the exact rerun from the HBM backup must still produce the oracle's outputs."""
+    G, _ = gpu
+    O = oracle_lib
+    p = 131071
+    A = O.random_mat(p, n, n, 40 + n)
+    if dup:
+        A[dup[0], :] = A[dup[1], :]
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 64)
+    ctx = G.Context(0)  # fresh: no rest period from an earlier failed guess
+    try:
+        ld = n + 5
+        buf = np.full((n, ld), 0xDEADBEEF, np.uint32)
+        buf[:, :n] = A
+        view = buf[:, :n]
+        res = G.pluq_tile_recursive(p, view, 64, ctx=ctx)
+        assert res.rank == r_o
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.array_equal(view, a_o)
+        assert np.all(buf[:, n:] == 0xDEADBEEF)
+    finally:
+        ctx.close()
