@@ -446,7 +446,10 @@ struct Driver {
     struct Bands {
         bool on = false;
         std::vector<size_t> end;                              // band c = [end[c-1], end[c])
-        std::vector<cudaEvent_t> ready;                       // band c uploaded (and backed up)
+        std::vector<cudaEvent_t> uploaded;                    // band c is in HBM
+        std::vector<cudaEvent_t> ready;                       // ... and backed up (enqueued lazily)
+        uint32_t* backup = nullptr;
+        cudaStream_t bks = nullptr;
         std::vector<std::pair<cudaStream_t, size_t>> waited;  // per stream: bands already waited for
         cudaStream_t down = nullptr;                          // D2H copy stream
         uint32_t* host = nullptr;
@@ -470,7 +473,21 @@ struct Driver {
     void need(cudaStream_t st, size_t hi) {
         if (!bands.on) return;
         const size_t c = (size_t)(std::lower_bound(bands.end.begin(), bands.end.end(), hi) - bands.end.begin());
-        if (c >= bands.ready.size()) return;
+        if (c >= bands.uploaded.size()) return;
+        // Backups are enqueued only when a band is first needed: a stream waiting on a late
+        // upload at the head of a shared hardware queue would stall every later launch behind it.
+        while (bands.ready.size() <= c) {
+            const size_t k = bands.ready.size();
+            const size_t a0 = k ? bands.end[k - 1] : 0, e = bands.end[k], n = pcols, m = prows;
+            uint32_t* d = const_cast<uint32_t*>(proot);
+            const Blas bb = on(bands.bks);
+            wait(bands.bks, bands.uploaded[k]);
+            copy_block_dev(bb, DView{d + a0 * pld + a0, e - a0, n - a0, pld},
+                           DView{bands.backup + a0 * pld + a0, e - a0, n - a0, pld});
+            copy_block_dev(bb, DView{d + e * pld + a0, m - e, e - a0, pld},
+                           DView{bands.backup + e * pld + a0, m - e, e - a0, pld});
+            bands.ready.push_back(mark_event(bands.bks));
+        }
         size_t* w = nullptr;
         for (auto& pr : bands.waited)
             if (pr.first == st) w = &pr.second;
@@ -771,8 +788,8 @@ static bool spec_allowed(const Blas& b, const DView& a) {
     return true;
 }
 
-// band ends for the streamed host entry: the recursion's nodes of size <= T in order (finer at
-// the start so that the first base case waits for a small first band)
+// band ends for the streamed host entry: the recursion's nodes of size <= min(T, max(Tmin, o)) in
+// order -- finer at the start, where the factorisation waits for each band
 static void band_bounds(size_t o, size_t s, size_t thr, size_t T, size_t Tmin, std::vector<size_t>& out) {
     if (s <= thr || s <= std::min(T, std::max(Tmin, o))) {
         out.push_back(o + s);
@@ -806,22 +823,22 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         FFG_CUDA(cudaEventRecord(start, b.st));
         for (cudaStream_t st : {up, down, bks}) drv.wait(st, start);
         const size_t T = std::max<size_t>(256, n / 16);
-        band_bounds(0, n, thr, T, std::max<size_t>(64, T / 4), drv.bands.end);
+        // bands of 256 rows first (a narrower band's column strip is a 2-D copy of short rows,
+        // which the copy engines move slowly: 128-row bands measured slower)
+        band_bounds(0, n, thr, T, 256, drv.bands.end);
         drv.bands.on = true;
         drv.bands.host = host;
         drv.bands.ldh = lda;
         drv.bands.down = down;
-        const Blas bb = drv.on(bks);
+        drv.bands.backup = bk;
+        drv.bands.bks = bks;
         for (size_t c = 0; c < drv.bands.end.size(); ++c) {
             drv.band_copy(c, false, up);
-            drv.wait(bks, drv.mark_event(up));
-            const size_t a0 = c ? drv.bands.end[c - 1] : 0, e = drv.bands.end[c];
-            copy_block_dev(bb, DView{d + a0 * n + a0, e - a0, n - a0, n}, DView{bk + a0 * n + a0, e - a0, n - a0, n});
-            copy_block_dev(bb, DView{d + e * n + a0, n - e, e - a0, n}, DView{bk + e * n + a0, n - e, e - a0, n});
-            drv.bands.ready.push_back(drv.mark_event(bks));
+            drv.bands.uploaded.push_back(drv.mark_event(up));
         }
         try {
             NodeRes res = drv.rec_panel(DView{d, n, n, n}, 0);
+            drv.need(drv.b.st, n);  // every band backed up before the call returns
             drv.finish();
             drv.download(res, n, n, P, Q);  // synchronizes the critical stream
             FFG_CUDA(cudaStreamSynchronize(down));
@@ -829,6 +846,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             rank = res.rank;
         } catch (const Driver::SpecAbort&) {
             ok = false;
+            drv.need(drv.b.st, n);  // bands no operation touched yet are still pristine: back them up too
         }
         if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
     }

@@ -45,3 +45,18 @@ for c in sorted(cps, key=lambda e: e.time_range.start):
     s, e = (c.time_range.start - t0) / 1e3, (c.time_range.end - t0) / 1e3
     if e - s > 0.05:
         print(f"  {c.name[:28]:28s} {s:8.2f} -> {e:8.2f} ms ({e - s:6.2f} ms)")
+bases = sorted((e for e in ks if "rr_base" in e.name), key=lambda e: e.time_range.start)
+if bases:
+    print("base cases (every 16th): " + " ".join(
+        f"{(b.time_range.start - t0) / 1e3:.1f}" for b in bases[::16]) + f" | last ends {(bases[-1].time_range.end - t0) / 1e3:.2f} ms")
+end = max(e.time_range.end for e in evs) - t0
+for lo in range(0, int(end / 1e3) + 5, 5):
+    w0, w1 = lo * 1e3, (lo + 5) * 1e3
+
+    def ov(e):
+        s, t = e.time_range.start - t0, e.time_range.end - t0
+        return max(0.0, min(t, w1) - max(s, w0))
+    kb = sum(ov(e) for e in ks)
+    h2d = sum(ov(e) for e in cps if "HtoD" in e.name)
+    d2h = sum(ov(e) for e in cps if "DtoH" in e.name)
+    print(f"  [{lo:3d},{lo + 5:3d}) ms: kernel-time {kb / 1e3:6.2f} ms  H2D busy {h2d / 1e3:5.2f}  D2H busy {d2h / 1e3:5.2f}")
