@@ -174,7 +174,12 @@ struct Driver {
             FFG_CUDA(cudaMallocAsync(&inv_arena, inv_cap * 4, b.st));
         }
     }
+    void alloc_panel_inv() {
+        static const bool off = getenv("FFG_PANEL_FUSED_TRSM") && atoi(getenv("FFG_PANEL_FUSED_TRSM")) != 0;
+        if (!off && !panel_inv) FFG_CUDA(cudaMallocAsync(&panel_inv, 2 * 64 * 64 * 4, b.st));
+    }
     ~Driver() {
+        if (panel_inv) cudaFreeAsync(panel_inv, b.st);
         if (inv_arena) cudaFreeAsync(inv_arena, b.st);
         b.ws.release_slot(slot);
     }
@@ -435,6 +440,7 @@ struct Driver {
     // recursion; L, U (unique for full rank without pivoting) come out identical, and no TRSM
     // chain remains above the base cases.  Any failed guess reruns the exact path anyway.
     bool panel = false;
+    uint32_t* panel_inv = nullptr;  // 2 x 64 x 64: the current base case's factor inverses
     const uint32_t* proot = nullptr;
     size_t pld = 0, prows = 0, pcols = 0;
 
@@ -469,8 +475,39 @@ struct Driver {
         rect(a0, a0, e - a0, n - a0);
         rect(e, a0, m - e, e - a0);
     }
+    // ---- look-ahead pieces (panel mode): a node of size >= la_min does not update its whole
+    // trailing region [H | right panel] + bottom panel before R's recursion.  The update is cut
+    // into R's L-shaped bands of doubling width (64, 64, 128, 256, ...): the first band on the
+    // critical stream, the rest on a low-priority look-ahead stream (SM-capped), each band's
+    // completion event waited for by the first operation of R's recursion that reaches it.
+    struct Piece {
+        size_t a;  // band [a, e): operations touching rows / columns >= a must wait
+        cudaEvent_t ev;
+    };
+    std::vector<Piece> pieces;
+    size_t la_min = 0;  // 0: off
+    DView at(size_t r, size_t c, size_t rows, size_t cols) const {
+        return DView{const_cast<uint32_t*>(proot) + r * pld + c, rows, cols, pld};
+    }
+    // band [x, e) of the trailing update of node (o, m) whose first half [o, o + h) is factored:
+    // rows [x, e) x cols [x, N) and rows [e, M) x cols [x, e), both -= L(., A1 cols) U(A1 rows, .)
+    void piece(const Blas& rows_bl, const Blas& cols_bl, size_t o, size_t h, size_t x, size_t e) {
+        if (pcols > x) gemm_sub(rows_bl, at(x, o, e - x, h), at(o, x, h, pcols - x), at(x, x, e - x, pcols - x));
+        if (prows > e) gemm_sub(cols_bl, at(e, o, prows - e, h), at(o, x, h, e - x), at(e, x, prows - e, e - x));
+    }
+
     // every later operation on `st` may touch rows / columns < hi
     void need(cudaStream_t st, size_t hi) {
+        for (size_t i = 0; i < pieces.size();) {
+            if (pieces[i].a < hi) {
+                wait(st, pieces[i].ev);
+                if (st == b.st) {  // every other stream forks from the critical one
+                    pieces.erase(pieces.begin() + (long)i);
+                    continue;
+                }
+            }
+            ++i;
+        }
         if (!bands.on) return;
         const size_t c = (size_t)(std::lower_bound(bands.end.begin(), bands.end.end(), hi) - bands.end.begin());
         if (c >= bands.uploaded.size()) return;
@@ -524,9 +561,17 @@ struct Driver {
             DView bottom{a.d + m * pld, prows - (r0 + m), n, pld};
             const bool both = !right.empty() && !bottom.empty();
             const Blas side = both ? on(twin(depth)) : b;
-            if (both) wait(side.st, mark_event(b.st));
-            if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
-            if (!bottom.empty()) ftrsm_dev(side, 1, 1, 1, a, bottom, false);
+            if (panel_inv && m == n && m <= 64) {
+                // inverses once, then every strip of both panels only applies them
+                panel_inverses_dev(b, a, panel_inv);
+                if (both) wait(side.st, mark_event(b.st));
+                panel_apply_dev(b, 0, panel_inv, m, right);
+                panel_apply_dev(side, 1, panel_inv, m, bottom);
+            } else {
+                if (both) wait(side.st, mark_event(b.st));
+                if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
+                if (!bottom.empty()) ftrsm_dev(side, 1, 1, 1, a, bottom, false);
+            }
             if (both) wait(b.st, mark_event(side.st));
             band_done(r0 + m);
             return res;
@@ -543,11 +588,31 @@ struct Driver {
         DView BP{a.d + m * pld + n1, prows - (r0 + m), n - n1, pld};          // below the node, R cols
         const bool both = !BP.empty();
         const Blas side = both ? on(twin(depth)) : b;
-        need(b.st, r0 + m);
-        if (both) wait(side.st, mark_event(b.st));
-        if (!HR.empty()) gemm_sub(b, Fb, Dx, HR);
-        if (both) gemm_sub(side, Fbelow, Dn, BP);
-        if (both) wait(b.st, mark_event(side.st));
+        if (la_min && m >= la_min && m - m1 > thr) {
+            const size_t A = r0 + m1, E = r0 + m;  // R's rows / columns
+            const size_t e1 = A + thr;
+            need(b.st, e1);
+            cudaEvent_t forked = mark_event(b.st);
+            Blas la = on(lookahead(depth));
+            la.sm_cap = lookahead_sms;  // keep SMs free for the critical path
+            need(la.st, E);             // older pieces overlapping R
+            wait(la.st, forked);
+            wait(side.st, forked);
+            piece(b, side, r0, m1, A, e1);
+            wait(b.st, mark_event(side.st));
+            for (size_t x = e1; x < E;) {
+                const size_t e = std::min(E, x + std::max(thr, x - A));
+                piece(la, la, r0, m1, x, e);
+                pieces.push_back(Piece{x, mark_event(la.st)});
+                x = e;
+            }
+        } else {
+            need(b.st, r0 + m);
+            if (both) wait(side.st, mark_event(b.st));
+            if (!HR.empty()) gemm_sub(b, Fb, Dx, HR);
+            if (both) gemm_sub(side, Fbelow, Dn, BP);
+            if (both) wait(b.st, mark_event(side.st));
+        }
         rec_panel(a.sub(m1, n1, m - m1, n - n1), depth + 1);
         band_done(r0 + m);
         res.rank = std::min(m, n);
@@ -788,6 +853,13 @@ static bool spec_allowed(const Blas& b, const DView& a) {
     return true;
 }
 
+// panel-mode nodes of at least this size cut their trailing update into look-ahead pieces
+// (FFG_PANEL_LA, read per call so tests can sweep it; 0 = off)
+static size_t panel_lookahead_min() {
+    const char* e = getenv("FFG_PANEL_LA");
+    return e ? (size_t)atoll(e) : 0;
+}
+
 // band ends for the streamed host entry: the recursion's nodes of size <= min(T, max(Tmin, o)) in
 // order -- finer at the start, where the factorisation waits for each band
 static void band_bounds(size_t o, size_t s, size_t thr, size_t T, size_t Tmin, std::vector<size_t>& out) {
@@ -814,6 +886,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         drv.spec = true;
         *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
         drv.panel = true;
+        drv.la_min = panel_lookahead_min();
+        drv.alloc_panel_inv();
         drv.proot = d;
         drv.pld = n;
         drv.prows = n;
@@ -872,6 +946,8 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
             const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
             drv.panel = !no_panel && m == n && std::min(m, n) > 0 && drv.use_streams;
+            drv.la_min = panel_lookahead_min();
+            if (drv.panel) drv.alloc_panel_inv();
             drv.proot = a.d;
             drv.pld = a.ld;
             drv.prows = m;

@@ -31,6 +31,11 @@ struct Blas {
 // scans the diagonal first (nonunit) and throws SingularDiagonal(i) like blas.hpp:291-297.
 void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bool check_diag);
 
+// panel schedule: both factor inverses of a packed square block (<= 64) into inv (2 t^2 words),
+// then B <- inv(L) B (side 0) or B <- B inv(U) (side 1) over any number of strips
+void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv);
+void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B);
+
 // pluq_tile_recursive on a HOST matrix (ld lda), pipelined: the recursion's top-left spine
 // starts while the rest uploads, the root's finished top rows download while its trailing
 // block recurses.  Same outputs as the device entry.

@@ -328,58 +328,73 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(const uint32_t* __restr
 // Leaf of a factor-tree TRSM: X = inv(L) B (left) or X = B inv(U) (right), in place, with the
 // inverse cached by the base case (d <= 64).  A CTA owns 64 vectors (columns of B for left,
 // rows for right) and stages them in shared memory before writing, so in place is safe.
-// 256 threads x (4 x 4) register tiles, exact u64 dot products (<= 64 terms).
+// 256 threads x (4 x 4) register tiles fed by two 16-byte shared loads per k (coefficients
+// stored transposed), exact u64 dot products (<= 64 terms), results staged back through shared
+// memory so both sides store whole rows.
 constexpr int LA = 64;
+constexpr int LAS = LA + 4;  // 16-byte aligned rows
 template <int SIDE>
 __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restrict__ inv, uint32_t d,
                                                          uint32_t* __restrict__ B, uint64_t ldb, uint32_t nvec,
                                                          uint32_t p, uint64_t mu) {
-    __shared__ uint32_t Cs[LA][LA + 1];  // Cs[i][k] = coefficient of x_k in output i
-    __shared__ uint32_t Bs[LA][LA + 1];  // Bs[k][v] = element k of vector v
+    __shared__ __align__(16) uint32_t Ct[LA][LAS];  // Ct[k][i] = coefficient of x_k in output i
+    __shared__ __align__(16) uint32_t Bs[LA][LAS];  // Bs[k][v] = element k of vector v (later outputs)
     const uint32_t tid = threadIdx.x, v0 = blockIdx.x * LA;
     const uint32_t nv = min((uint32_t)LA, nvec - v0);
-    for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
-        const uint32_t i = idx / LA, k = idx % LA;
-        Cs[i][k] = (i < d && k < d) ? (SIDE == 0 ? inv[i * d + k] : inv[k * d + i]) : 0u;
+    ptx::pdl_enter();
+    // all 32 loads of a thread in flight at once (a rolled loop serialises their latencies)
+    constexpr int PER = LA * LA / 256;
+    uint32_t rc[PER], rb[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
+        rc[r] = (lo < d && hi < d) ? (SIDE == 0 ? inv[lo * d + hi] : inv[hi * d + lo]) : 0u;
+        if (SIDE == 0)  // hi = k, lo = v
+            rb[r] = (hi < d && lo < nv) ? B[(uint64_t)hi * ldb + v0 + lo] : 0u;
+        else  // hi = v, lo = k
+            rb[r] = (lo < d && hi < nv) ? B[(uint64_t)(v0 + hi) * ldb + lo] : 0u;
     }
-    if (SIDE == 0) {
-        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
-            const uint32_t k = idx / LA, v = idx % LA;
-            Bs[k][v] = (k < d && v < nv) ? B[(uint64_t)k * ldb + v0 + v] : 0u;
-        }
-    } else {
-        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
-            const uint32_t v = idx / LA, k = idx % LA;
-            Bs[k][v] = (k < d && v < nv) ? B[(uint64_t)(v0 + v) * ldb + k] : 0u;
-        }
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+        const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
+        Ct[hi][lo] = rc[r];
+        if (SIDE == 0)
+            Bs[hi][lo] = rb[r];
+        else
+            Bs[lo][hi] = rb[r];
     }
     __syncthreads();
     const uint32_t ti = tid / 16, tv = tid % 16;
     uint64_t acc[4][4] = {};
     for (uint32_t k = 0; k < d; ++k) {
-        uint32_t c[4], x[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) c[a] = Cs[ti * 4 + a][k];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = Bs[k][tv * 4 + q];
+        const uint4 c = *reinterpret_cast<const uint4*>(&Ct[k][ti * 4]);
+        const uint4 x = *reinterpret_cast<const uint4*>(&Bs[k][tv * 4]);
+        const uint32_t cc[4] = {c.x, c.y, c.z, c.w}, xx[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[a][q] += (uint64_t)c[a] * x[q];
+            for (int q = 0; q < 4; ++q) acc[a][q] += (uint64_t)cc[a] * xx[q];
     }
+    __syncthreads();  // every thread is done reading Bs: reuse it for the outputs Os[i][v]
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const uint32_t i = ti * 4 + a;
-        if (i >= d) continue;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t v = tv * 4 + q;
-            if (v >= nv) continue;
-            const uint32_t val = mod_u64(acc[a][q], p, mu);
-            if (SIDE == 0)
-                B[(uint64_t)i * ldb + v0 + v] = val;
-            else
-                B[(uint64_t)(v0 + v) * ldb + i] = val;
+        uint4 o;
+        o.x = mod_u64(acc[a][0], p, mu);
+        o.y = mod_u64(acc[a][1], p, mu);
+        o.z = mod_u64(acc[a][2], p, mu);
+        o.w = mod_u64(acc[a][3], p, mu);
+        *reinterpret_cast<uint4*>(&Bs[ti * 4 + a][tv * 4]) = o;
+    }
+    __syncthreads();
+    if (SIDE == 0) {
+        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+            const uint32_t i = idx / LA, v = idx % LA;
+            if (i < d && v < nv) B[(uint64_t)i * ldb + v0 + v] = Bs[i][v];
+        }
+    } else {
+        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+            const uint32_t v = idx / LA, i = idx % LA;
+            if (i < d && v < nv) B[(uint64_t)(v0 + v) * ldb + i] = Bs[i][v];
         }
     }
 }
@@ -483,6 +498,74 @@ void trsm_fused_launch(const Blas& b, int side, int upper, int unit, DView T, DV
              (uint32_t)nvec, b.F.p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)T.rows * nvec);
+    b.count();
+}
+
+// Both factor inverses of a packed t x t block (t <= 64, full rank): inv(L) (unit lower) by
+// threads 0..255 and inv(U) (upper, non-unit) by threads 256..511 side by side, each half
+// synchronising on its own named barrier.  inv[0, t*t) = inv(L), inv[t*t, 2t*t) = inv(U), ld t.
+// The panel schedule computes them once per base case; every strip of its right / bottom panel
+// then only applies them (leaf_apply_kernel) instead of re-inverting per CTA.
+constexpr int PI_RS = 65;
+__global__ void __launch_bounds__(512) panel_inv_kernel(const uint32_t* __restrict__ T, uint64_t ldt, uint32_t t,
+                                                        uint32_t* __restrict__ inv, uint32_t p, uint64_t mu) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    uint32_t* Ts = sm;  // 64 x 65
+    const uint32_t tid = threadIdx.x, half = tid >> 8, lt = tid & 255;
+    uint32_t* X = Ts + 64 * PI_RS + half * (64 * PI_RS + 32 * 32 + 64);
+    uint32_t* W = X + 64 * PI_RS;
+    uint32_t* dv = W + 32 * 32;
+    ptx::pdl_enter();
+    {
+        uint32_t r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t idx = tid + 512 * q, i = idx / 64, k = idx % 64;
+            r[q] = (i < t && k < t) ? T[(uint64_t)i * ldt + k] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t idx = tid + 512 * q;
+            Ts[(idx / 64) * PI_RS + idx % 64] = r[q];
+        }
+    }
+    __syncthreads();
+    if (half == 0)
+        tri_inverse_part<false, 64>(Ts, PI_RS, X, PI_RS, W, dv, t, p, mu, lt, 256, 1);
+    else
+        tri_inverse_part<true, 64>(Ts, PI_RS, X, PI_RS, W, dv, t, p, mu, lt, 256, 2);
+    uint32_t* out = inv + (size_t)half * t * t;
+    for (uint32_t idx = lt; idx < t * t; idx += 256) out[idx] = X[(idx / t) * PI_RS + idx % t];
+}
+
+void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
+    const uint32_t t = (uint32_t)T.rows;
+    if (t == 0 || t > 64 || T.cols != T.rows) throw Error(FFG_ERR_INTERNAL, "panel_inverses: block must be square <= 64");
+    const size_t smem = (64 * PI_RS + 2 * (64 * PI_RS + 32 * 32 + 64)) * 4;
+    static std::once_flag once;
+    std::call_once(once, [smem] {
+        FFG_CUDA(cudaFuncSetAttribute(panel_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    });
+    b.ws.prof.begin(b.st);
+    launch_k(panel_inv_kernel, dim3(1), dim3(512), smem, b.st, T.d, T.ld, t, inv, b.F.p, b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * t * t);
+    b.count();
+}
+
+// side 0: B <- inv(L) B; side 1: B <- B inv(U), with the inverses of panel_inverses_dev
+void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B) {
+    if (B.empty()) return;
+    const size_t nvec = side == 0 ? B.cols : B.rows;
+    b.ws.prof.begin(b.st);
+    if (side == 0)
+        launch_k(leaf_apply_kernel<0>, dim3((unsigned)ceil_div(nvec, LA)), dim3(256), 0, b.st, inv, (uint32_t)t, B.d,
+                 B.ld, (uint32_t)nvec, b.F.p, b.F.mu);
+    else
+        launch_k(leaf_apply_kernel<1>, dim3((unsigned)ceil_div(nvec, LA)), dim3(256), 0, b.st, inv + t * t,
+                 (uint32_t)t, B.d, B.ld, (uint32_t)nvec, b.F.p, b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)t * nvec);
     b.count();
 }
 

@@ -83,3 +83,29 @@ for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
 if a.json:
     json.dump({"n": a.n, "thr": a.thr, "event_ms": wall, "busy_ms": busy, "span_ms": span, "launches": len(ks),
                "kernels": {k: {"count": v[0], "ms": v[1]} for k, v in agg.items()}}, open(a.json, "w"), indent=1)
+
+# ---- per-step view (panel mode): kernels between consecutive base cases, grouped by the size of
+# the node whose GEMMs follow base k (k's trailing one bits)
+bases = [k for k in ks if "rr_base" in k[2]]
+if len(bases) > 2:
+    byt = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for i in range(len(bases) - 1):
+        t = 0
+        while (i >> t) & 1:
+            t += 1
+        gap = (bases[i + 1][0] - bases[i][0]) / 1e3
+        byt[t][0] += 1
+        byt[t][1] += gap
+        byt[t][2] += (bases[i][1] - bases[i][0]) / 1e3
+    print("step type (node size after base k) | steps | avg base-to-base us | avg base us | total ms")
+    for t in sorted(byt):
+        c, g, b = byt[t]
+        print(f"  node {64 << (t + 1):6d} | {c:5d} | {1e3 * g / c:9.1f} | {1e3 * b / c:7.1f} | {g:8.2f}")
+    for i in list(range(100, 104)) + [126, 127]:
+        if i + 1 >= len(bases):
+            break
+        b0 = bases[i][0]
+        print(f"step {i}:")
+        for s, t_, nm in ks:
+            if b0 <= s < bases[i + 1][0] + 1:
+                print(f"   +{(s - b0) / 1e3 * 1e3:8.1f} us  {((t_ - s) / 1e3) * 1e3:7.1f} us  {nm}")

@@ -336,3 +336,34 @@ def test_panel_mode_matches_oracle(gpu, oracle_lib, case, n, monkeypatch):
         assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
         assert np.array_equal(got, a_o)
         outs.append(got)
+
+
+@pytest.mark.parametrize("la", ["0", "128", "256", "1024"])
+@pytest.mark.parametrize("n,thr", [(1000, 16), (2048, 64), (1537, 64)])
+def test_panel_lookahead_pieces_match_oracle(gpu, oracle_lib, la, n, thr, monkeypatch):
+    """Panel mode with the trailing update of every node >= FFG_PANEL_LA cut into look-ahead
+    pieces (R's bands of doubling width, the first on the critical stream, the rest on a
+    low-priority stream whose events R's recursion waits for): bit-exact against the oracle
+    through the device entry and the streamed host entry."""
+    import torch
+
+    G, _ = gpu
+    O = oracle_lib
+    p = 131071
+    A = O.random_mat(p, n, n, 9 + n)
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+    monkeypatch.setenv("FFG_PANEL_LA", la)
+    ctx = G.Context(0)
+    try:
+        d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+        res = G.pluq_tile_recursive(p, d, thr, ctx=ctx)
+        ctx.synchronize()
+        assert res.rank == r_o
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), a_o)
+        h = A.copy()
+        res = G.pluq_tile_recursive(p, h, thr, ctx=ctx)
+        assert res.rank == r_o and np.array_equal(h, a_o)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+    finally:
+        ctx.close()
