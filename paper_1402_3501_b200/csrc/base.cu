@@ -794,12 +794,18 @@ constexpr int SP_WARPS = 16;
 constexpr int SP_THREADS = SP_WARPS * 32;
 constexpr int SP_RPW = 64 / SP_WARPS;  // rows per warp
 
+// allow_q (panel schedule, square blocks): the guess is only "full rank"; a zero diagonal Schur
+// entry is handled like rr_base does -- the pivot of row k is its first nonzero column among the
+// columns not yet chosen (rr_base's rotations keep the remaining columns in original order), so
+// the kernel tracks physical pivot columns c_k and writes the block in logical (rotated) order,
+// with Q[t] = c_t.  Full rank implies P = identity.  Without allow_q any c_k != k fails the guess.
 __global__ void __launch_bounds__(SP_THREADS, 1)
     rr_base_spec_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t m, uint32_t n, uint32_t* __restrict__ Pd,
                         uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p, uint64_t mu,
-                        uint32_t seq) {
+                        uint32_t seq, uint32_t allow_q) {
     __shared__ __align__(16) uint32_t buf[2][128];  // published pivot row: 64 values, 64 Shoup factors
     __shared__ uint32_t pvs[64];                     // fraction-free pivots
+    __shared__ uint32_t pcol[64];                    // physical column of pivot k
     __shared__ uint32_t invd[64], invdf[64];         // 1 / D_k and its Shoup factor
     __shared__ uint32_t invp[64], invpf[64];         // 1 / pv_k and its Shoup factor
     __shared__ uint32_t fail;
@@ -816,6 +822,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
         x[j][0] = (i < m && lane < n) ? row[lane] : 0u;
         x[j][1] = (i < m && lane + 32 < n) ? row[lane + 32] : 0u;
     }
+    // publish row k (reduced, with Shoup factors)
     auto publish = [&](uint32_t& a0, uint32_t& a1, uint32_t* dst) {
         a0 = red4p(a0, p);
         a1 = red4p(a1, p);
@@ -828,28 +835,65 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     if (warp == 0 && r > 0) publish(x[0][0], x[0][1], buf[0]);
     __syncthreads();
 
+    // Every thread finds the pivot column itself from the published row: while every pivot so far
+    // sat on the diagonal (`diag`, uniform) and the diagonal entry is nonzero it is column k at no
+    // extra cost; otherwise a ballot over the row picks its first nonzero column outside `used`.
+    uint64_t used = 0;  // maintained once the first pivot left the diagonal
+    bool diag = true;
     for (uint32_t k = 0; k < r; ++k) {
         const uint32_t* pr = buf[k & 1];
-        const uint32_t pv = pr[k], pvp = pr[64 + k];
         const uint32_t b0 = pr[lane], b1 = pr[lane + 32], f0 = pr[64 + lane], f1 = pr[96 + lane];
+        uint32_t c = k, pv = pr[k], pvp = pr[64 + k];
+        if (!diag || pv == 0u) {  // uniform
+            if (diag) used = k ? (~0ull >> (64 - k)) : 0ull;  // columns < k
+            const uint32_t m0 = __ballot_sync(FULL, b0 != 0u && lane < n && !((used >> lane) & 1u));
+            const uint32_t m1 = __ballot_sync(FULL, b1 != 0u && lane + 32 < n && !((used >> (lane + 32)) & 1u));
+            c = m0 ? (uint32_t)__ffs(m0) - 1 : (m1 ? 31u + (uint32_t)__ffs(m1) : 64u);
+            if (c == 64u || (!allow_q && c != k)) {
+                if (tid == 0) fail = 1u;
+                c = k;  // keep going on a harmless column; the outputs are discarded
+            }
+            pv = pr[c];
+            pvp = pr[64 + c];
+            diag = diag && c == k;
+        }
         if (tid == 0) {
             pvs[k] = pv;
-            if (pv == 0u) fail = 1u;
+            pcol[k] = c;
         }
         const uint32_t nxt = k + 1;
+        if (diag) {  // uniform: the pivot is (k, k)
 #pragma unroll
-        for (int j = 0; j < SP_RPW; ++j) {
-            const uint32_t i = warp + SP_WARPS * j;
-            if (i > k && i < m) {  // warp-uniform
-                const uint32_t numer = red4p(__shfl_sync(FULL, k < 32 ? x[j][0] : x[j][1], k & 31), p);
-                const uint32_t u0 = (x[j][0] * pv - __umulhi(x[j][0], pvp) * p) + 2 * p -
-                                    (numer * b0 - __umulhi(numer, f0) * p);
-                const uint32_t u1 = (x[j][1] * pv - __umulhi(x[j][1], pvp) * p) + 2 * p -
-                                    (numer * b1 - __umulhi(numer, f1) * p);
-                // columns > k take the update; column k keeps the L numerator; earlier ones stay
-                x[j][0] = lane > k ? u0 : (lane == k ? numer : x[j][0]);
-                x[j][1] = lane + 32 > k ? u1 : (lane + 32 == k ? numer : x[j][1]);
-                if (i == nxt && nxt < r) publish(x[j][0], x[j][1], buf[nxt & 1]);
+            for (int j = 0; j < SP_RPW; ++j) {
+                const uint32_t i = warp + SP_WARPS * j;
+                if (i > k && i < m) {  // warp-uniform
+                    const uint32_t numer = red4p(__shfl_sync(FULL, k < 32 ? x[j][0] : x[j][1], k & 31), p);
+                    const uint32_t u0 = (x[j][0] * pv - __umulhi(x[j][0], pvp) * p) + 2 * p -
+                                        (numer * b0 - __umulhi(numer, f0) * p);
+                    const uint32_t u1 = (x[j][1] * pv - __umulhi(x[j][1], pvp) * p) + 2 * p -
+                                        (numer * b1 - __umulhi(numer, f1) * p);
+                    // columns > k take the update; column k keeps the L numerator; earlier ones stay
+                    x[j][0] = lane > k ? u0 : (lane == k ? numer : x[j][0]);
+                    x[j][1] = lane + 32 > k ? u1 : (lane + 32 == k ? numer : x[j][1]);
+                    if (i == nxt && nxt < r) publish(x[j][0], x[j][1], buf[nxt & 1]);
+                }
+            }
+        } else {  // pivot (k, c): the columns outside `used` and c take the update
+            used |= 1ull << c;
+            const bool up0 = !((used >> lane) & 1u), up1 = !((used >> (lane + 32)) & 1u);
+#pragma unroll
+            for (int j = 0; j < SP_RPW; ++j) {
+                const uint32_t i = warp + SP_WARPS * j;
+                if (i > k && i < m) {  // warp-uniform
+                    const uint32_t numer = red4p(__shfl_sync(FULL, c < 32 ? x[j][0] : x[j][1], c & 31), p);
+                    const uint32_t u0 = (x[j][0] * pv - __umulhi(x[j][0], pvp) * p) + 2 * p -
+                                        (numer * b0 - __umulhi(numer, f0) * p);
+                    const uint32_t u1 = (x[j][1] * pv - __umulhi(x[j][1], pvp) * p) + 2 * p -
+                                        (numer * b1 - __umulhi(numer, f1) * p);
+                    x[j][0] = up0 ? u0 : (lane == c ? numer : x[j][0]);
+                    x[j][1] = up1 ? u1 : (lane + 32 == c ? numer : x[j][1]);
+                    if (i == nxt && nxt < r) publish(x[j][0], x[j][1], buf[nxt & 1]);
+                }
             }
         }
         __syncthreads();
@@ -898,10 +942,21 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     }
     __syncthreads();
     if (!fail) {
+        // logical column t of the output holds physical column pcol[t] (t < r); beyond r (wide
+        // blocks, identity guess only) the columns stay in place
+        const uint32_t s0 = (!diag && lane < r) ? pcol[lane] : lane;
+        const uint32_t s1 = (!diag && lane + 32 < r) ? pcol[lane + 32] : lane + 32;
 #pragma unroll
         for (int j = 0; j < SP_RPW; ++j) {
             const uint32_t i = warp + SP_WARPS * j;
-            if (i >= m) continue;
+            if (i >= m) continue;  // warp-uniform
+            uint32_t g[2] = {x[j][0], x[j][1]};
+            if (!diag) {  // uniform: gather the logical columns
+                const uint32_t g00 = __shfl_sync(FULL, x[j][0], s0 & 31), g01 = __shfl_sync(FULL, x[j][1], s0 & 31);
+                const uint32_t g10 = __shfl_sync(FULL, x[j][0], s1 & 31), g11 = __shfl_sync(FULL, x[j][1], s1 & 31);
+                g[0] = s0 < 32 ? g00 : g01;
+                g[1] = s1 < 32 ? g10 : g11;
+            }
             uint32_t* row = A + (uint64_t)i * lda;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -909,15 +964,15 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
                 if (c >= n) continue;
                 uint32_t v;
                 if (c < i)  // L entry (c < r: every column is a pivot column when i >= r)
-                    v = shoup_mul(x[j][h], invp[c], invpf[c], p);
+                    v = shoup_mul(g[h], invp[c], invpf[c], p);
                 else  // U entry of pivot row i < r
-                    v = shoup_mul(x[j][h], invd[i], invdf[i], p);
+                    v = shoup_mul(g[h], invd[i], invdf[i], p);
                 row[c] = v;
             }
         }
     }
     for (uint32_t ii = tid; ii < m; ii += SP_THREADS) Pd[ii] = ii;
-    for (uint32_t jj = tid; jj < n; jj += SP_THREADS) Qd[jj] = jj;
+    for (uint32_t jj = tid; jj < n; jj += SP_THREADS) Qd[jj] = jj < r ? pcol[jj] : jj;
     __syncthreads();
     if (tid == 0) {
         info->rank = r;
@@ -978,7 +1033,7 @@ void base_dbg_dump() {
 }
 
 bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv_out,
-                    uint32_t seq) {
+                    uint32_t seq, bool allow_q) {
     base_dbg_init();
     BaseLayout lay;
     lay.m = (uint32_t)a.rows;
@@ -1002,7 +1057,7 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const char* e_spec = getenv("FFG_SPEC_SLAB");  // diagnostics: speculative launches on the slab kernel
     if (spec && lay.m <= 64 && lay.n <= 64 && !(e_spec && atoi(e_spec) != 0)) {
         launch_k(rr_base_spec_kernel, dim3(1), dim3(SP_THREADS), 0, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd, info,
-                 b.F.p, b.F.mu, seq);
+                 b.F.p, b.F.mu, seq, (uint32_t)(allow_q && lay.m == lay.n));
         FFG_CUDA(cudaGetLastError());
         b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
         b.count();

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -99,6 +100,11 @@ public:
     Profiler prof;
     std::atomic<uint32_t> base_seq{0};  // sequence numbers of base-case completion mailboxes
     int spec_rest = 0;                   // calls left before speculative full rank is tried again
+    int spec_fails = 0;                  // consecutive failed guesses (the rest doubles with them)
+    void spec_failed() {
+        ++spec_fails;
+        spec_rest = (1 << std::min(spec_fails - 1, 3)) - 1;  // 0, 1, 3, 7 calls
+    }
     Dist dist;  // multi-GPU partitioning of the recursion's large operations (dist.cuh)
     ~Workspace() {
         for (auto& kv : bufs_)

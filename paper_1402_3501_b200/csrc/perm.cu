@@ -203,4 +203,29 @@ void copy_block_dev(const Blas& b, DView src, DView dst) {
     b.count();
 }
 
+// a.cols <= 64 columns of every row of a gathered by a local index array: a[i][t] <- a[i][q[t]].
+// One warp per row; all reads before any write.  The panel schedule applies a base case's column
+// pivots to the rows above its block with it (tile_rec applies R's Q to D, rankrev.hpp:158-161).
+__global__ void block_cols_perm_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t rows, uint32_t s,
+                                       const uint32_t* __restrict__ q) {
+    ptx::pdl_enter();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= rows) return;
+    uint32_t* r = A + (uint64_t)row * lda;
+    const uint32_t v0 = lane < s ? r[q[lane]] : 0u, v1 = lane + 32 < s ? r[q[lane + 32]] : 0u;
+    __syncwarp();
+    if (lane < s) r[lane] = v0;
+    if (lane + 32 < s) r[lane + 32] = v1;
+}
+
+void block_cols_perm_dev(const Blas& b, DView a, const uint32_t* q) {
+    if (a.empty()) return;
+    if (a.cols > 64) throw Error(FFG_ERR_INTERNAL, "block_cols_perm: more than 64 columns");
+    launch_k(block_cols_perm_kernel, dim3((unsigned)ceil_div(a.rows, 8)), dim3(256), 0, b.st, a.d, a.ld,
+             (uint32_t)a.rows, (uint32_t)a.cols, q);
+    FFG_CUDA(cudaGetLastError());
+    b.count();
+}
+
 }  // namespace ffg

@@ -176,9 +176,45 @@ struct Driver {
     }
     void alloc_panel_inv() {
         static const bool off = getenv("FFG_PANEL_FUSED_TRSM") && atoi(getenv("FFG_PANEL_FUSED_TRSM")) != 0;
+        static const bool no_q = getenv("FFG_SPEC_NO_Q") && atoi(getenv("FFG_SPEC_NO_Q")) != 0;
         if (!off && !panel_inv) FFG_CUDA(cudaMallocAsync(&panel_inv, 2 * 64 * 64 * 4, b.st));
+        // column pivots need the inverse-apply path (it gathers the bottom panel through Q)
+        if (panel_inv && !no_q && !gq && pcols) {
+            FFG_CUDA(cudaMallocAsync(&gq, pcols * 4, b.st));
+            allow_q = true;
+        }
+    }
+    // End of a speculative panel run whose guess held: Q = the base cases' column pivots (P is the
+    // identity), and each base case's pivots applied to the rows above its block -- what tile_rec's
+    // ancestors do with R's Q (rankrev.hpp:158-161).  Synchronizes.  `fixed` receives the regions
+    // rewritten here (the host entry re-downloads them).
+    void panel_finish(uint32_t* P, uint32_t* Q, std::vector<std::pair<size_t, size_t>>* fixed) {
+        std::vector<uint32_t> ql(gq ? pcols : 0);
+        if (gq) FFG_CUDA(cudaMemcpyAsync(ql.data(), gq, pcols * 4, cudaMemcpyDeviceToHost, b.st));
+        FFG_CUDA(cudaStreamSynchronize(b.st));
+        if (P)
+            for (size_t i = 0; i < prows; ++i) P[i] = (uint32_t)i;
+        if (Q)
+            for (size_t j = 0; j < pcols; ++j) Q[j] = (uint32_t)j;
+        if (!gq || *reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) return;
+        bool any = false;
+        for (const auto& lf : leaves) {
+            const size_t o = lf.first, sz = lf.second;
+            bool id = true;
+            for (size_t t = 0; t < sz; ++t) {
+                if (Q) Q[o + t] = (uint32_t)(o + ql[o + t]);
+                id = id && ql[o + t] == t;
+            }
+            if (!id && o > 0) {
+                block_cols_perm_dev(b, at(0, o, o, sz), gq + o);
+                if (fixed) fixed->push_back(lf);
+                any = true;
+            }
+        }
+        if (any) FFG_CUDA(cudaStreamSynchronize(b.st));
     }
     ~Driver() {
+        if (gq) cudaFreeAsync(gq, b.st);
         if (panel_inv) cudaFreeAsync(panel_inv, b.st);
         if (inv_arena) cudaFreeAsync(inv_arena, b.st);
         b.ws.release_slot(slot);
@@ -258,13 +294,39 @@ struct Driver {
     // path, so correctness never depends on the guess).
     struct SpecAbort {};
     bool spec = false;
+    bool allow_q = false;  // panel schedule: the guess is full rank only (column pivots allowed)
+    // the host stays at most spec_window base cases ahead of the device, so a failed guess is
+    // noticed (and the queue drained) within a few steps instead of after the whole recursion
+    size_t spec_window = 32;
+    std::vector<uint32_t> spec_seqs;
+    void spec_throttle() {
+        if (spec_seqs.size() < spec_window) return;
+        const uint32_t target = spec_seqs[spec_seqs.size() - spec_window] & ~SPEC_BIT;
+        volatile uint32_t* sq = &info_host->seq;
+        volatile uint32_t* sf = &info_host->spec_fail;
+        for (uint64_t it = 0;; ++it) {
+            if (*sf) throw SpecAbort{};
+            const uint32_t cur = *sq & ~SPEC_BIT;
+            if (((cur - target) & ~SPEC_BIT) < 0x40000000u) return;  // cur at or after target (mod 2^31)
+            if (it > (1u << 24)) {  // slow or failed kernel: block on the stream (reports errors)
+                FFG_CUDA(cudaStreamSynchronize(b.st));
+                if (*sf) throw SpecAbort{};
+                return;
+            }
+#if defined(__x86_64__) || defined(__i386__)
+            __builtin_ia32_pause();
+#endif
+        }
+    }
 
     NodeRes base(DView a, NodeRes res) {
         if (spec) {
             if (a.rows > 64 || a.cols > 64) throw SpecAbort{};  // only the slab kernel checks
             if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) throw SpecAbort{};
+            spec_throttle();
             const uint32_t seq = ((b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT) | SPEC_BIT;
-            rr_base_launch(b, a, res.P, res.Q, info_dev, nullptr, seq);
+            rr_base_launch(b, a, res.P, res.Q, info_dev, nullptr, seq, allow_q && a.rows == a.cols);
+            spec_seqs.push_back(seq);
             ++base_cases;
             res.rank = std::min(a.rows, a.cols);
             res.pr = Range{};
@@ -441,6 +503,8 @@ struct Driver {
     // chain remains above the base cases.  Any failed guess reruns the exact path anyway.
     bool panel = false;
     uint32_t* panel_inv = nullptr;  // 2 x 64 x 64: the current base case's factor inverses
+    uint32_t* gq = nullptr;         // base cases' column pivots (local indices) at their columns
+    std::vector<std::pair<size_t, size_t>> leaves;  // (offset, size) of every base case
     const uint32_t* proot = nullptr;
     size_t pld = 0, prows = 0, pcols = 0;
 
@@ -555,6 +619,8 @@ struct Driver {
         const size_t off = (size_t)(a.d - proot), r0 = off / pld, c0 = off % pld;
         if (std::min(m, n) <= thr) {
             need(b.st, r0 + m);
+            if (gq) res.Q = gq + c0;
+            leaves.push_back({c0, n});
             res = base(a, res);  // speculative: no wait
             // whole right panel (L^-1, left) and bottom panel (U^-1, right) of this block
             DView right{a.d + n, m, pcols - (c0 + n), pld};
@@ -566,7 +632,7 @@ struct Driver {
                 panel_inverses_dev(b, a, panel_inv);
                 if (both) wait(side.st, mark_event(b.st));
                 panel_apply_dev(b, 0, panel_inv, m, right);
-                panel_apply_dev(side, 1, panel_inv, m, bottom);
+                panel_apply_dev(side, 1, panel_inv, m, bottom, gq ? gq + c0 : nullptr);
             } else {
                 if (both) wait(side.st, mark_event(b.st));
                 if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
@@ -843,9 +909,16 @@ void base_dbg_dump();
 
 // Speculation is tried unless disabled (FFG_NO_SPEC), partitioned, profiled, or recently failed in
 // this context (then it rests for a few calls: rank-deficient workloads pay one failed try).
-static bool spec_allowed(const Blas& b, const DView& a) {
+static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
     static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
     if (off || b.ws.dist.active() || a.rows == 0 || a.cols == 0) return false;
+    // A base block of i.i.d. residues is rank deficient with probability ~1/p: with
+    // min(m, n) / thr blocks the guess holds with probability ~exp(-blocks / p).  Do not
+    // speculate where it is likely to fail (small fields: config 5's GF(251) at n = 32768 has
+    // ~2 rank-deficient blocks per matrix on average); FFG_SPEC_FORCE=1 overrides.
+    static const bool force = getenv("FFG_SPEC_FORCE") && atoi(getenv("FFG_SPEC_FORCE")) != 0;
+    const double blocks = (double)std::min(a.rows, a.cols) / (double)std::max<size_t>(thr, 1);
+    if (!force && blocks > 0.25 * (double)b.F.p) return false;
     if (b.ws.spec_rest > 0) {
         --b.ws.spec_rest;
         return false;
@@ -887,11 +960,11 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
         drv.panel = true;
         drv.la_min = panel_lookahead_min();
-        drv.alloc_panel_inv();
         drv.proot = d;
         drv.pld = n;
         drv.prows = n;
         drv.pcols = n;
+        drv.alloc_panel_inv();
         cudaStream_t up = b.ws.stream(300, 0), down = b.ws.stream(301, 0), bks = b.ws.stream(302, 0);
         cudaEvent_t start = drv.b.ws.event();  // d and bk are allocated on the caller's stream
         FFG_CUDA(cudaEventRecord(start, b.st));
@@ -914,9 +987,16 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             NodeRes res = drv.rec_panel(DView{d, n, n, n}, 0);
             drv.need(drv.b.st, n);  // every band backed up before the call returns
             drv.finish();
-            drv.download(res, n, n, P, Q);  // synchronizes the critical stream
             FFG_CUDA(cudaStreamSynchronize(down));
+            std::vector<std::pair<size_t, size_t>> fixed;
+            drv.panel_finish(P, Q, &fixed);  // synchronizes the critical stream
             ok = *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
+            if (ok && !fixed.empty()) {  // rows above a pivoted block changed after their band left
+                for (const auto& f : fixed)
+                    FFG_CUDA(cudaMemcpy2DAsync(host + f.first, lda * 4, d + f.first, n * 4, f.second * 4, f.first,
+                                               cudaMemcpyDeviceToHost, drv.b.st));
+                FFG_CUDA(cudaStreamSynchronize(drv.b.st));
+            }
             rank = res.rank;
         } catch (const Driver::SpecAbort&) {
             ok = false;
@@ -926,14 +1006,16 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
     }
     if (!ok) {
         FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, bk, n * 4, n * 4, n, cudaMemcpyDeviceToDevice, b.st));
-        b.ws.spec_rest = 8;
+        b.ws.spec_failed();
+    } else {
+        b.ws.spec_fails = 0;
     }
     FFG_CUDA(cudaFreeAsync(bk, b.st));
     return ok;
 }
 
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
-    if (threshold <= 64 && spec_allowed(b, a)) {
+    if (threshold <= 64 && spec_allowed(b, a, threshold)) {
         const size_t m = a.rows, n = a.cols;
         uint32_t* bk = nullptr;
         FFG_CUDA(cudaMallocAsync(&bk, m * n * 4, b.st));
@@ -947,15 +1029,18 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
             drv.panel = !no_panel && m == n && std::min(m, n) > 0 && drv.use_streams;
             drv.la_min = panel_lookahead_min();
-            if (drv.panel) drv.alloc_panel_inv();
             drv.proot = a.d;
             drv.pld = a.ld;
             drv.prows = m;
             drv.pcols = n;
+            if (drv.panel) drv.alloc_panel_inv();
             try {
                 NodeRes res = drv.panel ? drv.rec_panel(a, 0) : drv.rec(a);
                 drv.finish();
-                drv.download(res, m, n, P, Q);  // synchronizes: every base kernel has reported
+                if (drv.panel)
+                    drv.panel_finish(P, Q, nullptr);  // synchronizes: every base kernel has reported
+                else
+                    drv.download(res, m, n, P, Q);
                 ok = *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) == 0u;
                 rank = res.rank;
             } catch (const Driver::SpecAbort&) {
@@ -963,13 +1048,16 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             }
             if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // all speculative work retired
         }
+        static const bool log = getenv("FFG_SPEC_LOG") != nullptr;
+        if (log) fprintf(stderr, "SPEC %s (panel %d, %zu base cases enqueued)\n", ok ? "ok" : "failed", (int)(m == n), (size_t)b.ws.base_seq.load());
         if (ok) {
+            b.ws.spec_fails = 0;
             FFG_CUDA(cudaFreeAsync(bk, b.st));
             return rank;
         }
         FFG_CUDA(cudaMemcpy2DAsync(a.d, a.ld * 4, bk, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
         FFG_CUDA(cudaFreeAsync(bk, b.st));
-        b.ws.spec_rest = 8;
+        b.ws.spec_failed();
     }
     Driver drv(b, threshold, a.rows, a.cols);
     drv.level_timing = getenv("FFG_LEVEL_TIMING") != nullptr;
@@ -998,7 +1086,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
     static const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
     bool restored = false;  // d already holds the input (a failed speculative attempt restored it)
-    if (m == n && thr <= 64 && !no_stream_spec && !no_streams && !no_panel && spec_allowed(b, DView{host, m, n, lda})) {
+    if (m == n && thr <= 64 && !no_stream_spec && !no_streams && !no_panel && spec_allowed(b, DView{host, m, n, lda}, thr)) {
         size_t rank = 0;
         if (host_streamed_spec(b, host, n, lda, thr, d, P, Q, rank)) {
             FFG_CUDA(cudaFreeAsync(d, b.st));
@@ -1085,7 +1173,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     } else if (!run(spec, true, rank)) {
         FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
         FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, bk, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
-        b.ws.spec_rest = 8;
+        b.ws.spec_failed();
         run(false, false, rank);
     }
     if (bk) FFG_CUDA(cudaFreeAsync(bk, b.st));

@@ -34,7 +34,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
 // panel schedule: both factor inverses of a packed square block (<= 64) into inv (2 t^2 words),
 // then B <- inv(L) B (side 0) or B <- B inv(U) (side 1) over any number of strips
 void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv);
-void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B);
+void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B, const uint32_t* qperm = nullptr);
 
 // pluq_tile_recursive on a HOST matrix (ld lda), pipelined: the recursion's top-left spine
 // starts while the rest uploads, the root's finished top rows download while its trailing
@@ -60,8 +60,10 @@ constexpr uint32_t SPEC_BIT = 0x80000000u;
 // one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info; with
 // inv_out != nullptr also the inverses of the leading r x r L and U factors (r <= 64)
 // returns whether inverses were requested (the kernel still reports info->cached)
+// allow_q (speculative launches on square blocks): the guess is full rank only, column pivots
+// allowed (Qd receives them; P is then the identity)
 bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev,
-                    uint32_t* inv_out = nullptr, uint32_t seq = 0);
+                    uint32_t* inv_out = nullptr, uint32_t seq = 0, bool allow_q = false);
 
 // Structure of a node's leading r x r factor (tile_rec pivot gather order A1, E, G, R):
 // block triangular with the children's leading factors on the diagonal.  Leaves are base
@@ -91,6 +93,9 @@ void lru_matrix_dev(const Blas& b, DView M, size_t r, uint64_t seed, uint32_t* r
 
 // row (axis 0) / column (axis 1) gather by a device index array
 void apply_perm_dev(const Blas& b, DView a, int axis, int inverse, const uint32_t* perm);
+
+// a[i][t] <- a[i][q[t]] for t < a.cols <= 64 (q: device, local indices)
+void block_cols_perm_dev(const Blas& b, DView a, const uint32_t* q);
 
 // dst <- src, same shape (device copy kernel)
 void copy_block_dev(const Blas& b, DView src, DView dst);

@@ -333,10 +333,12 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(const uint32_t* __restr
 // memory so both sides store whole rows.
 constexpr int LA = 64;
 constexpr int LAS = LA + 4;  // 16-byte aligned rows
+// qp (right side only, may be null): the vectors' elements are read through this local column
+// permutation first (the base case's column pivots applied to its bottom panel, in place)
 template <int SIDE>
 __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restrict__ inv, uint32_t d,
                                                          uint32_t* __restrict__ B, uint64_t ldb, uint32_t nvec,
-                                                         uint32_t p, uint64_t mu) {
+                                                         uint32_t p, uint64_t mu, const uint32_t* __restrict__ qp) {
     __shared__ __align__(16) uint32_t Ct[LA][LAS];  // Ct[k][i] = coefficient of x_k in output i
     __shared__ __align__(16) uint32_t Bs[LA][LAS];  // Bs[k][v] = element k of vector v (later outputs)
     const uint32_t tid = threadIdx.x, v0 = blockIdx.x * LA;
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restr
         if (SIDE == 0)  // hi = k, lo = v
             rb[r] = (hi < d && lo < nv) ? B[(uint64_t)hi * ldb + v0 + lo] : 0u;
         else  // hi = v, lo = k
-            rb[r] = (lo < d && hi < nv) ? B[(uint64_t)(v0 + hi) * ldb + lo] : 0u;
+            rb[r] = (lo < d && hi < nv) ? B[(uint64_t)(v0 + hi) * ldb + (qp ? qp[lo] : lo)] : 0u;
     }
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
@@ -554,16 +556,16 @@ void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
 }
 
 // side 0: B <- inv(L) B; side 1: B <- B inv(U), with the inverses of panel_inverses_dev
-void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B) {
+void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B, const uint32_t* qperm) {
     if (B.empty()) return;
     const size_t nvec = side == 0 ? B.cols : B.rows;
     b.ws.prof.begin(b.st);
     if (side == 0)
         launch_k(leaf_apply_kernel<0>, dim3((unsigned)ceil_div(nvec, LA)), dim3(256), 0, b.st, inv, (uint32_t)t, B.d,
-                 B.ld, (uint32_t)nvec, b.F.p, b.F.mu);
+                 B.ld, (uint32_t)nvec, b.F.p, b.F.mu, (const uint32_t*)nullptr);
     else
         launch_k(leaf_apply_kernel<1>, dim3((unsigned)ceil_div(nvec, LA)), dim3(256), 0, b.st, inv + t * t,
-                 (uint32_t)t, B.d, B.ld, (uint32_t)nvec, b.F.p, b.F.mu);
+                 (uint32_t)t, B.d, B.ld, (uint32_t)nvec, b.F.p, b.F.mu, qperm);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)t * nvec);
     b.count();
@@ -598,10 +600,10 @@ void trsm_factor(const Blas& b, int side, const Factor& f, DView T, DView B) {
         b.ws.prof.begin(b.st);
         if (side == 0)
             leaf_apply_kernel<0><<<(unsigned)ceil_div(nvec, LA), 256, 0, b.st>>>(f.invL, (uint32_t)r, B.d, B.ld,
-                                                                               (uint32_t)nvec, b.F.p, b.F.mu);
+                                                                               (uint32_t)nvec, b.F.p, b.F.mu, nullptr);
         else
             leaf_apply_kernel<1><<<(unsigned)ceil_div(nvec, LA), 256, 0, b.st>>>(f.invU, (uint32_t)r, B.d, B.ld,
-                                                                               (uint32_t)nvec, b.F.p, b.F.mu);
+                                                                               (uint32_t)nvec, b.F.p, b.F.mu, nullptr);
         FFG_CUDA(cudaGetLastError());
         b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)r * nvec);
         b.count();

@@ -367,3 +367,51 @@ def test_panel_lookahead_pieces_match_oracle(gpu, oracle_lib, la, n, thr, monkey
         assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
     finally:
         ctx.close()
+
+
+def _zero_schur_pivot(A, p, ks, seed=5):
+    """Row k's first k+1 entries become a combination of rows 0..k-1 (the rest stays random): the
+    Schur diagonal at k is zero and row k pivots on a later column -- a column rotation inside its
+    base block when k % 64 < 63, a rank-deficient block when k is its last row."""
+    rng = np.random.default_rng(seed)
+    A = A.copy()
+    for k in ks:
+        c = rng.integers(0, p, size=k, dtype=np.uint64)
+        comb = np.zeros(k + 1, np.uint64)
+        for i in range(k):
+            comb = (comb + c[i] * A[i, :k + 1].astype(np.uint64)) % p
+        A[k, :k + 1] = comb.astype(np.uint32)
+    return A
+
+
+@pytest.mark.parametrize("ks", [[0], [100], [127], [100, 700], [5, 64, 65, 300, 1000]])
+@pytest.mark.parametrize("n", [1000, 2048])
+def test_panel_column_pivots_match_oracle(gpu, oracle_lib, ks, n):
+    """Speculative panel runs guess only full rank: a zero Schur diagonal inside a base block
+    pivots on a later column (rr_base's rotation), the column pivots are gathered into the bottom
+    panel, applied to the rows above the block at the end, and returned in Q -- bit-exact against
+    the oracle through both entries; a rank-deficient block (k = 127) falls back to the exact path."""
+    import torch
+
+    G, _ = gpu
+    O = oracle_lib
+    p = 131071
+    ks = [k for k in ks if k < n]
+    A = _zero_schur_pivot(O.random_mat(p, n, n, 3 + n), p, ks)
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 64)
+    for entry in ("dev", "host"):
+        ctx = G.Context(0)
+        try:
+            if entry == "dev":
+                d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+                res = G.pluq_tile_recursive(p, d, 64, ctx=ctx)
+                ctx.synchronize()
+                got = d.cpu().numpy().view(np.uint32)
+            else:
+                got = A.copy()
+                res = G.pluq_tile_recursive(p, got, 64, ctx=ctx)
+            assert res.rank == r_o
+            assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o), entry
+            assert np.array_equal(got, a_o), entry
+        finally:
+            ctx.close()
