@@ -177,7 +177,7 @@ struct Driver {
     void alloc_panel_inv() {
         static const bool off = getenv("FFG_PANEL_FUSED_TRSM") && atoi(getenv("FFG_PANEL_FUSED_TRSM")) != 0;
         static const bool no_q = getenv("FFG_SPEC_NO_Q") && atoi(getenv("FFG_SPEC_NO_Q")) != 0;
-        if (!off && !panel_inv) FFG_CUDA(cudaMallocAsync(&panel_inv, 2 * 64 * 64 * 4, b.st));
+        if (!off && !panel_inv) FFG_CUDA(cudaMallocAsync(&panel_inv, 2 * 2 * 64 * 64 * 4, b.st));
         // column pivots need the inverse-apply path (it gathers the bottom panel through Q)
         if (panel_inv && !no_q && !gq && pcols) {
             FFG_CUDA(cudaMallocAsync(&gq, pcols * 4, b.st));
@@ -502,7 +502,8 @@ struct Driver {
     // recursion; L, U (unique for full rank without pivoting) come out identical, and no TRSM
     // chain remains above the base cases.  Any failed guess reruns the exact path anyway.
     bool panel = false;
-    uint32_t* panel_inv = nullptr;  // 2 x 64 x 64: the current base case's factor inverses
+    uint32_t* panel_inv = nullptr;  // 2 slots x (2 x 64 x 64): factor inverses of the last two base cases
+    uint32_t* inv_slot() const { return panel_inv + (leaves.size() & 1) * 2 * 64 * 64; }  // current leaf's
     uint32_t* gq = nullptr;         // base cases' column pivots (local indices) at their columns
     std::vector<std::pair<size_t, size_t>> leaves;  // (offset, size) of every base case
     const uint32_t* proot = nullptr;
@@ -610,6 +611,62 @@ struct Driver {
         }
     }
 
+    // Two-leaf node (A1, R both base cases): R's base case waits only for a one-CTA corner update
+    // (A1's panel blocks inside the node and A(R, R) -= L(R, A1) U(A1, R)); A1's wide panels beyond
+    // the node and their updates of R's rows / columns run on two side streams meanwhile, and R's
+    // own panels wait for them.  Same arithmetic as the generic node, reordered.
+    void two_leaf(DView a, int depth, NodeRes& res) {
+        const size_t m = a.rows, t1 = (m + 1) / 2, t2 = m - t1;
+        const size_t off = (size_t)(a.d - proot), r0 = off / pld, c0 = off % pld;
+        need(b.st, r0 + m);
+        const uint32_t* q1 = gq ? gq + c0 : nullptr;
+        // A1
+        NodeRes r1;
+        r1.P = arena.alloc(t1);
+        r1.Q = gq ? gq + c0 : arena.alloc(t1);
+        base(a.sub(0, 0, t1, t1), r1);
+        uint32_t* inv1 = inv_slot();
+        leaves.push_back({c0, t1});
+        panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
+        panel_corner_dev(b, a, t1, inv1, q1);
+        const cudaEvent_t f = mark_event(b.st);
+        const Blas sa = on(b.ws.stream(sid(slot, 400), 0)), sb = on(b.ws.stream(sid(slot, 401), 0));
+        wait(sa.st, f);
+        wait(sb.st, f);
+        DView rightA{a.d + m, t1, pcols - (c0 + m), pld};       // A1 rows, columns beyond the node
+        DView bottomA{a.d + m * pld, prows - (r0 + m), t1, pld};  // rows beyond the node, A1 columns
+        panel_apply_dev(sa, 0, inv1, t1, rightA);
+        panel_apply_dev(sb, 1, inv1, t1, bottomA, q1);
+        DView HRp{a.d + t1 * pld + m, t2, pcols - (c0 + m), pld};  // R rows beyond the node
+        DView BPp{a.d + m * pld + t1, prows - (r0 + m), t2, pld};  // beyond the node, R columns
+        if (!HRp.empty()) gemm_sub(sa, a.sub(t1, 0, t2, t1), rightA, HRp);
+        if (!BPp.empty()) gemm_sub(sb, bottomA, a.sub(0, t1, t1, t2), BPp);
+        const cudaEvent_t ea = mark_event(sa.st), eb = mark_event(sb.st);
+        // R
+        DView Rb = a.sub(t1, t1, t2, t2);
+        NodeRes r2;
+        r2.P = arena.alloc(t2);
+        r2.Q = gq ? gq + c0 + t1 : arena.alloc(t2);
+        base(Rb, r2);
+        uint32_t* inv2 = inv_slot();
+        leaves.push_back({c0 + t1, t2});
+        panel_inverses_dev(b, Rb, inv2);
+        wait(b.st, ea);
+        wait(b.st, eb);
+        DView rightR{Rb.d + t2, t2, pcols - (c0 + m), pld};
+        DView bottomR{Rb.d + t2 * pld, prows - (r0 + m), t2, pld};
+        const bool both = !rightR.empty() && !bottomR.empty();
+        const Blas side = both ? on(twin(depth)) : b;
+        if (both) wait(side.st, mark_event(b.st));
+        panel_apply_dev(b, 0, inv2, t2, rightR);
+        panel_apply_dev(side, 1, inv2, t2, bottomR, gq ? gq + c0 + t1 : nullptr);
+        if (both) wait(b.st, mark_event(side.st));
+        band_done(r0 + m);
+        res.rank = m;
+        res.pr = Range{};
+        res.qr = Range{};
+    }
+
     NodeRes rec_panel(DView a, int depth) {
         const size_t m = a.rows, n = a.cols;  // square
         NodeRes res;
@@ -620,7 +677,6 @@ struct Driver {
         if (std::min(m, n) <= thr) {
             need(b.st, r0 + m);
             if (gq) res.Q = gq + c0;
-            leaves.push_back({c0, n});
             res = base(a, res);  // speculative: no wait
             // whole right panel (L^-1, left) and bottom panel (U^-1, right) of this block
             DView right{a.d + n, m, pcols - (c0 + n), pld};
@@ -629,21 +685,29 @@ struct Driver {
             const Blas side = both ? on(twin(depth)) : b;
             if (panel_inv && m == n && m <= 64) {
                 // inverses once, then every strip of both panels only applies them
-                panel_inverses_dev(b, a, panel_inv);
+                uint32_t* inv = inv_slot();
+                panel_inverses_dev(b, a, inv);
                 if (both) wait(side.st, mark_event(b.st));
-                panel_apply_dev(b, 0, panel_inv, m, right);
-                panel_apply_dev(side, 1, panel_inv, m, bottom, gq ? gq + c0 : nullptr);
+                panel_apply_dev(b, 0, inv, m, right);
+                panel_apply_dev(side, 1, inv, m, bottom, gq ? gq + c0 : nullptr);
             } else {
                 if (both) wait(side.st, mark_event(b.st));
                 if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
                 if (!bottom.empty()) ftrsm_dev(side, 1, 1, 1, a, bottom, false);
             }
             if (both) wait(b.st, mark_event(side.st));
+            leaves.push_back({c0, n});
             band_done(r0 + m);
             return res;
         }
         const size_t mark = arena.mark();
         const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;
+        static const bool no_corner = getenv("FFG_NO_CORNER") && atoi(getenv("FFG_NO_CORNER")) != 0;
+        if (!no_corner && panel_inv && m == n && m1 <= thr && m1 <= 64 && m - m1 > 0) {
+            two_leaf(a, depth, res);
+            arena.reset(mark);
+            return res;
+        }
         rec_panel(a.sub(0, 0, m1, n1), depth + 1);
         // A1's panels solved D and Fb (and the parts of A1's rows / columns beyond this node)
         DView Fb = a.sub(m1, 0, m - m1, n1);                                  // rows of R, cols of A1

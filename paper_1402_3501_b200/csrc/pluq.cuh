@@ -36,6 +36,9 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
 void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv);
 void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B, const uint32_t* qperm = nullptr);
 
+// two-leaf node of the panel schedule: A1's panel blocks inside the node and R's update (see trsm.cu)
+void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv, const uint32_t* q);
+
 // pluq_tile_recursive on a HOST matrix (ld lda), pipelined: the recursion's top-left spine
 // starts while the rest uploads, the root's finished top rows download while its trailing
 // block recurses.  Same outputs as the device entry.
