@@ -419,19 +419,23 @@ def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world, partitioned=False):
             C.copy_(C0)
             return lambda: G.fgemm(p, p - 1, An, Bn, 1, Cn, ctx=ctx)
     else:
-        H0 = torch.empty((n, n), dtype=torch.int32).pin_memory()
-        H = torch.empty((n, n), dtype=torch.int32).pin_memory()
+        # small fields (config 5, p <= 256) are stored as bytes: ffg_pluq_tile_recursive_u8
+        byte = p <= 256
+        hdt = torch.uint8 if byte else torch.int32
+        H0 = torch.empty((n, n), dtype=hdt).pin_memory()
+        H = torch.empty((n, n), dtype=hdt).pin_memory()
         d = torch.empty((n, n), dtype=torch.int32, device=dev)
         if a.workload == "lru":
             G.lru_matrix_dev(p, d, n // 2, 7 + rank, ctx=ctx)
         else:
             G.random_mat_dev(p, d, 7 + rank, ctx=ctx)
         ctx.synchronize()
-        H0.copy_(d.cpu())
+        H0.copy_(d.to(torch.uint8).cpu() if byte else d.cpu())
         del d
-        Hn = H.numpy().view(np.uint32)
-        h2d = n * n * 4
-        d2h = n * n * 4 + 2 * n * 4  # packed factors + P and Q
+        Hn = H.numpy() if byte else H.numpy().view(np.uint32)
+        es = 1 if byte else 4
+        h2d = n * n * es
+        d2h = n * n * es + 2 * n * 4  # packed factors + P and Q
 
         def step():
             H.copy_(H0)  # restore the in/out host buffer (untimed)
@@ -460,7 +464,9 @@ def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world, partitioned=False):
     return {"value": (1 if partitioned else world) * metric_ops(a) / (ms / 1e3) / 1e9, "unit": "Gop/s",
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": k,
-            "api": "ffg_fgemm (host buffers)" if a.workload == "fgemm" else "ffg_pluq_tile_recursive (host buffers)",
+            "api": "ffg_fgemm (host buffers)" if a.workload == "fgemm" else
+                   ("ffg_pluq_tile_recursive_u8 (host byte buffers)" if a.p <= 256
+                    else "ffg_pluq_tile_recursive (host buffers)"),
             "host_memory": "pinned"}
 
 

@@ -92,6 +92,12 @@ int ffg_pluq_tile_recursive(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, siz
                             size_t threshold, uint32_t *P, uint32_t *Q, size_t *rank);
 int ffg_pluq_tile_recursive_dev(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_t lda,
                                 size_t threshold, uint32_t *P, uint32_t *Q, size_t *rank);
+/* Byte storage for small fields (p <= 256, BASELINE config 5 "stored as uint8"): the same
+ * factorisation on a host matrix of uint8 residues (entries taken mod p; the packed L\U factors
+ * come back as bytes).  Not in the reference, whose storage is u32 only (field.hpp:15-17):
+ * PCIe traffic is a quarter of the u32 entry's.  FFG_ERR_CAPACITY when p > 256. */
+int ffg_pluq_tile_recursive_u8(ffg_ctx *ctx, uint64_t p, uint8_t *A, size_t m, size_t n, size_t lda,
+                               size_t threshold, uint32_t *P, uint32_t *Q, size_t *rank);
 int ffg_rr_base(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_t lda, uint32_t *P, uint32_t *Q,
                 size_t *rank);
 

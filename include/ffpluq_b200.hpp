@@ -145,6 +145,17 @@ inline PluqResult pluq_tile_recursive(MatView a, usize threshold = 8, Context& c
     return PluqResult{PermSeq::from_pivot_array(P), PermSeq::from_pivot_array(Q), r, true};
 }
 
+// Byte storage for p <= 256 (BASELINE config 5; an extension -- the reference stores u32 only)
+inline PluqResult pluq_tile_recursive_u8(std::uint8_t* data, usize rows, usize cols, usize stride, u32 p,
+                                         usize threshold = 8, Context& ctx = Context::global()) {
+    std::vector<u32> P(rows ? rows : 1), Q(cols ? cols : 1);
+    usize r = 0;
+    check(ffg_pluq_tile_recursive_u8(ctx.get(), p, data, rows, cols, stride, threshold, P.data(), Q.data(), &r));
+    P.resize(rows);
+    Q.resize(cols);
+    return PluqResult{PermSeq::from_pivot_array(P), PermSeq::from_pivot_array(Q), r, true};
+}
+
 // rankrev.hpp:29-78
 inline PluqResult rr_base(MatView a, Context& ctx = Context::global()) {
     std::vector<u32> P(a.rows ? a.rows : 1), Q(a.cols ? a.cols : 1);

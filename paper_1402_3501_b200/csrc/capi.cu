@@ -245,6 +245,17 @@ int ffg_pluq_tile_recursive(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, siz
     });
 }
 
+int ffg_pluq_tile_recursive_u8(ffg_ctx* ctx, uint64_t p, uint8_t* A, size_t m, size_t n, size_t lda,
+                               size_t threshold, uint32_t* P, uint32_t* Q, size_t* rank) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        if (lda < n) throw ffg::Error(FFG_ERR_INVALID_DIM, "pluq: lda < n");
+        size_t r = ffg::pluq_tile_recursive_host_u8(blas, A, m, n, lda, threshold, P, Q);
+        if (rank) *rank = r;
+    });
+}
+
 int ffg_rr_base(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, size_t n, size_t lda, uint32_t* P, uint32_t* Q,
                 size_t* rank) {
     return guarded(ctx, [&] {

@@ -228,4 +228,39 @@ void block_cols_perm_dev(const Blas& b, DView a, const uint32_t* q) {
     b.count();
 }
 
+// Byte storage of small-field matrices (p <= 256, BASELINE config 5 "stored as uint8"): the
+// host entry moves bytes over PCIe and widens / narrows them to the u32 working layout in HBM.
+__global__ void widen_u8_kernel(const uint8_t* __restrict__ S, uint64_t lds, uint32_t* __restrict__ D, uint64_t ldd,
+                                uint32_t rows, uint32_t cols, uint32_t p) {
+    const uint64_t total = (uint64_t)rows * cols;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = t / cols, c = t % cols;
+        const uint32_t v = S[r * lds + c];
+        D[r * ldd + c] = v < p ? v : v % p;
+    }
+}
+__global__ void narrow_u8_kernel(const uint32_t* __restrict__ S, uint64_t lds, uint8_t* __restrict__ D, uint64_t ldd,
+                                 uint32_t rows, uint32_t cols) {
+    const uint64_t total = (uint64_t)rows * cols;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = t / cols, c = t % cols;
+        D[r * ldd + c] = (uint8_t)S[r * lds + c];
+    }
+}
+
+void widen_u8_dev(const Blas& b, const uint8_t* src, size_t lds, DView dst) {
+    if (dst.empty()) return;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div((uint64_t)dst.rows * dst.cols, 256), 148 * 8);
+    widen_u8_kernel<<<grid, 256, 0, b.st>>>(src, lds, dst.d, dst.ld, (uint32_t)dst.rows, (uint32_t)dst.cols, b.F.p);
+    FFG_CUDA(cudaGetLastError());
+    b.count();
+}
+void narrow_u8_dev(const Blas& b, DView src, uint8_t* dst, size_t ldd) {
+    if (src.empty()) return;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div((uint64_t)src.rows * src.cols, 256), 148 * 8);
+    narrow_u8_kernel<<<grid, 256, 0, b.st>>>(src.d, src.ld, dst, ldd, (uint32_t)src.rows, (uint32_t)src.cols);
+    FFG_CUDA(cudaGetLastError());
+    b.count();
+}
+
 }  // namespace ffg

@@ -1245,6 +1245,43 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     return rank;
 }
 
+size_t pluq_tile_recursive_host_u8(const Blas& b, uint8_t* host, size_t m, size_t n, size_t lda, size_t threshold,
+                                   uint32_t* P, uint32_t* Q) {
+    if (b.F.p > 256) throw Error(FFG_ERR_CAPACITY, "byte storage needs p <= 256");
+    if (m == 0 || n == 0) return pluq_tile_recursive_dev(b, DView{nullptr, m, n, std::max<size_t>(n, 1)}, threshold, P, Q);
+    cudaStream_t cs = b.ws.stream(300, 0);  // copy stream
+    uint32_t* d = nullptr;
+    uint8_t* s8 = nullptr;
+    FFG_CUDA(cudaMallocAsync(&d, m * n * 4, b.st));
+    FFG_CUDA(cudaMallocAsync(&s8, m * n, b.st));
+    b.ws.reset_events();
+    auto mark = [&](cudaStream_t st) {
+        cudaEvent_t e = b.ws.event();
+        FFG_CUDA(cudaEventRecord(e, st));
+        return e;
+    };
+    FFG_CUDA(cudaStreamWaitEvent(cs, mark(b.st), 0));
+    const size_t chunk = std::max<size_t>(1, (size_t(32) << 20) / n);  // ~32 MB of bytes per copy
+    for (size_t r0 = 0; r0 < m; r0 += chunk) {  // upload chunk i while chunk i-1 widens
+        const size_t rows = std::min(chunk, m - r0);
+        FFG_CUDA(cudaMemcpy2DAsync(s8 + r0 * n, n, host + r0 * lda, lda, n, rows, cudaMemcpyHostToDevice, cs));
+        FFG_CUDA(cudaStreamWaitEvent(b.st, mark(cs), 0));
+        widen_u8_dev(b, s8 + r0 * n, n, DView{d + r0 * n, rows, n, n});
+    }
+    const size_t rank = pluq_tile_recursive_dev(b, DView{d, m, n, n}, threshold, P, Q);
+    for (size_t r0 = 0; r0 < m; r0 += chunk) {  // narrow chunk i while chunk i-1 downloads
+        const size_t rows = std::min(chunk, m - r0);
+        narrow_u8_dev(b, DView{d + r0 * n, rows, n, n}, s8 + r0 * n, n);
+        FFG_CUDA(cudaStreamWaitEvent(cs, mark(b.st), 0));
+        FFG_CUDA(cudaMemcpy2DAsync(host + r0 * lda, lda, s8 + r0 * n, n, n, rows, cudaMemcpyDeviceToHost, cs));
+    }
+    FFG_CUDA(cudaStreamWaitEvent(b.st, mark(cs), 0));
+    FFG_CUDA(cudaFreeAsync(s8, b.st));
+    FFG_CUDA(cudaFreeAsync(d, b.st));
+    FFG_CUDA(cudaStreamSynchronize(b.st));
+    return rank;
+}
+
 size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q) {
     Driver drv(b, SIZE_MAX, a.rows, a.cols);
     NodeRes res = drv.rec(a);

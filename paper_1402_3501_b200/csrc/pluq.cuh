@@ -45,6 +45,13 @@ void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv,
 size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t n, size_t lda, size_t threshold,
                                 uint32_t* P, uint32_t* Q);
 
+// The same on a host matrix of bytes (p <= 256; entries taken mod p): bytes cross PCIe in row
+// chunks, widened to u32 in HBM, factored, narrowed back.
+size_t pluq_tile_recursive_host_u8(const Blas& b, uint8_t* host, size_t m, size_t n, size_t lda, size_t threshold,
+                                   uint32_t* P, uint32_t* Q);
+void widen_u8_dev(const Blas& b, const uint8_t* src, size_t lds, DView dst);
+void narrow_u8_dev(const Blas& b, DView src, uint8_t* dst, size_t ldd);
+
 // rr_base (rankrev.hpp:29-78) on a device block; P/Q host arrays (to_array semantics).
 size_t rr_base_dev(const Blas& b, DView a, uint32_t* P, uint32_t* Q);
 

@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
         pluq_args = [vp, u64, vp, sz, sz, sz, sz, vp, vp, C.POINTER(sz)]
         L.ffg_pluq_tile_recursive.argtypes = pluq_args
         L.ffg_pluq_tile_recursive_dev.argtypes = pluq_args
+        L.ffg_pluq_tile_recursive_u8.argtypes = pluq_args
         L.ffg_rr_base.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
         L.ffg_field_info.argtypes = [u64, C.POINTER(C.c_int), C.POINTER(u64), C.POINTER(C.c_int)]
         L.ffg_apply_perm_dev.argtypes = [vp, vp, sz, sz, sz, C.c_int, C.c_int, vp]
@@ -338,6 +339,14 @@ def pluq_tile_recursive(p: int, A, threshold: int = 8, ctx: Context | None = Non
     Q = np.zeros(max(n, 1), np.uint32)
     r = C.c_size_t(0)
     dev = _is_torch(A)
+    if not dev and np.asarray(A).dtype == np.uint8:  # byte storage (p <= 256): ffg_pluq_tile_recursive_u8
+        A = np.asarray(A)
+        if A.ndim != 2 or (A.size and A.strides[1] != 1):
+            raise ValueError("row-major 2-D uint8 array with unit column stride required")
+        ld = int(A.strides[0]) if m > 0 else max(n, 1)
+        _check(lib().ffg_pluq_tile_recursive_u8(ctx.handle, p, A.ctypes.data, m, n, ld, threshold, P.ctypes.data,
+                                                Q.ctypes.data, C.byref(r)))
+        return PluqResult(P[:m], Q[:n], int(r.value))
     if not dev:
         A = _host(A)
     fn = lib().ffg_pluq_tile_recursive_dev if dev else lib().ffg_pluq_tile_recursive

@@ -415,3 +415,28 @@ def test_panel_column_pivots_match_oracle(gpu, oracle_lib, ks, n):
             assert np.array_equal(got, a_o), entry
         finally:
             ctx.close()
+
+
+@pytest.mark.parametrize("p,m,n", [(251, 300, 300), (251, 1000, 1000), (251, 333, 700), (2, 257, 190), (5, 64, 64),
+                                   (251, 0, 5)])
+def test_u8_host_entry_matches_oracle(gpu, oracle_lib, p, m, n):
+    """Byte storage (p <= 256, BASELINE config 5's "stored as uint8"): the same outputs as the
+    oracle on the u32 matrix, with a padded leading dimension left untouched."""
+    G, ctx = gpu
+    O = oracle_lib
+    A = O.random_mat(p, m, n, 11 + m + n) if m and n else np.zeros((m, n), np.uint32)
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 64)
+    buf = np.full((m, n + 9), 0xAB, np.uint8)
+    buf[:, :n] = A.astype(np.uint8)
+    view = buf[:, :n]
+    res = G.pluq_tile_recursive(p, view, 64, ctx=ctx)
+    assert res.rank == r_o
+    assert np.array_equal(res.P, P_o[:m]) and np.array_equal(res.Q, Q_o[:n])
+    assert np.array_equal(view.astype(np.uint32), a_o)
+    assert np.all(buf[:, n:] == 0xAB)
+
+
+def test_u8_host_entry_rejects_large_p(gpu):
+    G, ctx = gpu
+    with pytest.raises(Exception):
+        G.pluq_tile_recursive(131071, np.zeros((4, 4), np.uint8), 64, ctx=ctx)
