@@ -607,8 +607,55 @@ struct Driver {
         if (!bands.on) return;
         while (bands.next_down < bands.end.size() && bands.end[bands.next_down] <= hi) {
             wait(bands.down, mark_event(b.st));
+            for (cudaEvent_t e : deferred) wait(bands.down, e);
             band_copy(bands.next_down++, true, bands.down);
         }
+    }
+
+    // ---- deferred wide work (panel schedule): the last leaf of a subtree solves only the next
+    // thr columns / rows of its panels on the critical stream and leaves the rest, and a node of
+    // size <= corner_max updates only the first block of R on the critical stream (the corner) and
+    // leaves its wide GEMMs -- on side streams.  Their events are waited for right after the next
+    // base case and its inverses (flush_deferred), before anything that reads wide regions.
+    std::vector<cudaEvent_t> deferred;
+    size_t corner_max = 0;
+    void flush_deferred() {
+        for (cudaEvent_t e : deferred) wait(b.st, e);
+        deferred.clear();
+    }
+    cudaStream_t side_stream(int k) { return b.ws.stream(sid(slot, 400 + k), 0); }
+    // the leaf's right panel (rows of blk, columns beyond `beyond_c`) and bottom panel (rows beyond
+    // `beyond_r`, columns of blk): the first thr columns / rows on the critical stream, the rest
+    // on the side streams sa / sb (deferred)
+    void leaf_panels_split(DView blk, size_t r0, size_t c0, size_t beyond_r, size_t beyond_c, const uint32_t* inv,
+                           const uint32_t* q, int depth, const Blas& sa, const Blas& sb) {
+        const size_t t = blk.rows;
+        const size_t wr = pcols - beyond_c, hb = prows - beyond_r;
+        const size_t mr = std::min(thr, wr), mb = std::min(thr, hb);
+        DView rmini = at(r0, beyond_c, t, mr), bmini = at(beyond_r, c0, mb, t);
+        DView rrest = at(r0, beyond_c + mr, t, wr - mr), brest = at(beyond_r + mb, c0, hb - mb, t);
+        const bool both = !rmini.empty() && !bmini.empty();
+        const Blas side = both ? on(twin(depth)) : b;
+        const cudaEvent_t f = mark_event(b.st);
+        if (both) wait(side.st, f);
+        panel_apply_dev(b, 0, inv, t, rmini);
+        panel_apply_dev(side, 1, inv, t, bmini, q);
+        if (both) wait(b.st, mark_event(side.st));
+        if (!rrest.empty()) {
+            wait(sa.st, f);
+            panel_apply_dev(sa, 0, inv, t, rrest);
+            deferred.push_back(mark_event(sa.st));
+        }
+        if (!brest.empty()) {
+            wait(sb.st, f);
+            panel_apply_dev(sb, 1, inv, t, brest, q);
+            deferred.push_back(mark_event(sb.st));
+        }
+    }
+    // size of the first base case of a node of size s
+    size_t first_leaf(size_t s) const {
+        while (s > thr) s = (s + 1) / 2;
+        return s;
     }
 
     // Two-leaf node (A1, R both base cases): R's base case waits only for a one-CTA corner update
@@ -628,9 +675,10 @@ struct Driver {
         uint32_t* inv1 = inv_slot();
         leaves.push_back({c0, t1});
         panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
+        flush_deferred();  // the node's rows / columns carry every earlier update
         panel_corner_dev(b, a, t1, inv1, q1);
         const cudaEvent_t f = mark_event(b.st);
-        const Blas sa = on(b.ws.stream(sid(slot, 400), 0)), sb = on(b.ws.stream(sid(slot, 401), 0));
+        const Blas sa = on(side_stream(0)), sb = on(side_stream(1));
         wait(sa.st, f);
         wait(sb.st, f);
         DView rightA{a.d + m, t1, pcols - (c0 + m), pld};       // A1 rows, columns beyond the node
@@ -653,14 +701,18 @@ struct Driver {
         panel_inverses_dev(b, Rb, inv2);
         wait(b.st, ea);
         wait(b.st, eb);
-        DView rightR{Rb.d + t2, t2, pcols - (c0 + m), pld};
-        DView bottomR{Rb.d + t2 * pld, prows - (r0 + m), t2, pld};
-        const bool both = !rightR.empty() && !bottomR.empty();
-        const Blas side = both ? on(twin(depth)) : b;
-        if (both) wait(side.st, mark_event(b.st));
-        panel_apply_dev(b, 0, inv2, t2, rightR);
-        panel_apply_dev(side, 1, inv2, t2, bottomR, gq ? gq + c0 + t1 : nullptr);
-        if (both) wait(b.st, mark_event(side.st));
+        if (corner_max) {
+            leaf_panels_split(Rb, r0 + t1, c0 + t1, r0 + m, c0 + m, inv2, gq ? gq + c0 + t1 : nullptr, depth, sa, sb);
+        } else {
+            DView rightR{Rb.d + t2, t2, pcols - (c0 + m), pld};
+            DView bottomR{Rb.d + t2 * pld, prows - (r0 + m), t2, pld};
+            const bool both = !rightR.empty() && !bottomR.empty();
+            const Blas side = both ? on(twin(depth)) : b;
+            if (both) wait(side.st, mark_event(b.st));
+            panel_apply_dev(b, 0, inv2, t2, rightR);
+            panel_apply_dev(side, 1, inv2, t2, bottomR, gq ? gq + c0 + t1 : nullptr);
+            if (both) wait(b.st, mark_event(side.st));
+        }
         band_done(r0 + m);
         res.rank = m;
         res.pr = Range{};
@@ -687,10 +739,12 @@ struct Driver {
                 // inverses once, then every strip of both panels only applies them
                 uint32_t* inv = inv_slot();
                 panel_inverses_dev(b, a, inv);
+                flush_deferred();
                 if (both) wait(side.st, mark_event(b.st));
                 panel_apply_dev(b, 0, inv, m, right);
                 panel_apply_dev(side, 1, inv, m, bottom, gq ? gq + c0 : nullptr);
             } else {
+                flush_deferred();
                 if (both) wait(side.st, mark_event(b.st));
                 if (!right.empty()) ftrsm_dev(b, 0, 0, 0, a, right, false);
                 if (!bottom.empty()) ftrsm_dev(side, 1, 1, 1, a, bottom, false);
@@ -718,7 +772,26 @@ struct Driver {
         DView BP{a.d + m * pld + n1, prows - (r0 + m), n - n1, pld};          // below the node, R cols
         const bool both = !BP.empty();
         const Blas side = both ? on(twin(depth)) : b;
-        if (la_min && m >= la_min && m - m1 > thr) {
+        if (corner_max && m <= corner_max && m - m1 > thr) {
+            // corner: R's first base block gets its update now; the wide GEMMs of the node are
+            // deferred to side streams (after the last leaf's deferred panels)
+            const size_t A = r0 + m1, f = first_leaf(m - m1), E = r0 + m;
+            need(b.st, E);
+            const cudaEvent_t forked = mark_event(b.st);
+            gemm_sub(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
+            const Blas sc = on(side_stream(2)), sd = on(side_stream(3));
+            for (const Blas* sx : {&sc, &sd}) {
+                wait(sx->st, forked);
+                for (cudaEvent_t e : deferred) wait(sx->st, e);
+            }
+            deferred.clear();
+            if (pcols > A + f) gemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
+            if (E > A + f) gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
+            if (prows > E) gemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
+            deferred.push_back(mark_event(sc.st));
+            deferred.push_back(mark_event(sd.st));
+        } else if (la_min && m >= la_min && m - m1 > thr) {
+            flush_deferred();
             const size_t A = r0 + m1, E = r0 + m;  // R's rows / columns
             const size_t e1 = A + thr;
             need(b.st, e1);
@@ -738,6 +811,7 @@ struct Driver {
             }
         } else {
             need(b.st, r0 + m);
+            flush_deferred();
             if (both) wait(side.st, mark_event(b.st));
             if (!HR.empty()) gemm_sub(b, Fb, Dx, HR);
             if (both) gemm_sub(side, Fbelow, Dn, BP);
@@ -992,6 +1066,13 @@ static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
 
 // panel-mode nodes of at least this size cut their trailing update into look-ahead pieces
 // (FFG_PANEL_LA, read per call so tests can sweep it; 0 = off)
+// panel-mode nodes up to this size update only R's first block on the critical stream and defer
+// their wide GEMMs (FFG_CORNER_MAX, read per call; 0 = off)
+static size_t panel_corner_max() {
+    const char* e = getenv("FFG_CORNER_MAX");
+    return e ? (size_t)atoll(e) : 1024;
+}
+
 static size_t panel_lookahead_min() {
     const char* e = getenv("FFG_PANEL_LA");
     return e ? (size_t)atoll(e) : 0;
@@ -1024,6 +1105,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
         drv.panel = true;
         drv.la_min = panel_lookahead_min();
+        drv.corner_max = panel_corner_max();
         drv.proot = d;
         drv.pld = n;
         drv.prows = n;
@@ -1049,6 +1131,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         }
         try {
             NodeRes res = drv.rec_panel(DView{d, n, n, n}, 0);
+            drv.flush_deferred();
             drv.need(drv.b.st, n);  // every band backed up before the call returns
             drv.finish();
             FFG_CUDA(cudaStreamSynchronize(down));
@@ -1093,6 +1176,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
             drv.panel = !no_panel && m == n && std::min(m, n) > 0 && drv.use_streams;
             drv.la_min = panel_lookahead_min();
+            drv.corner_max = panel_corner_max();
             drv.proot = a.d;
             drv.pld = a.ld;
             drv.prows = m;
@@ -1100,6 +1184,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             if (drv.panel) drv.alloc_panel_inv();
             try {
                 NodeRes res = drv.panel ? drv.rec_panel(a, 0) : drv.rec(a);
+                drv.flush_deferred();
                 drv.finish();
                 if (drv.panel)
                     drv.panel_finish(P, Q, nullptr);  // synchronizes: every base kernel has reported

@@ -341,62 +341,82 @@ __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restr
                                                          uint32_t p, uint64_t mu, const uint32_t* __restrict__ qp) {
     __shared__ __align__(16) uint32_t Ct[LA][LAS];  // Ct[k][i] = coefficient of x_k in output i
     __shared__ __align__(16) uint32_t Bs[LA][LAS];  // Bs[k][v] = element k of vector v (later outputs)
-    const uint32_t tid = threadIdx.x, v0 = blockIdx.x * LA;
-    const uint32_t nv = min((uint32_t)LA, nvec - v0);
-    ptx::pdl_enter();
-    // all 32 loads of a thread in flight at once (a rolled loop serialises their latencies)
+    const uint32_t tid = threadIdx.x;
     constexpr int PER = LA * LA / 256;
-    uint32_t rc[PER], rb[PER];
+    uint32_t rb[PER];
+    // the strip's loads, all in flight at once (a rolled loop serialises their latencies)
+    auto load = [&](uint32_t v0) {
+        const uint32_t nv = min((uint32_t)LA, nvec - v0);
 #pragma unroll
-    for (int r = 0; r < PER; ++r) {
-        const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
-        rc[r] = (lo < d && hi < d) ? (SIDE == 0 ? inv[lo * d + hi] : inv[hi * d + lo]) : 0u;
-        if (SIDE == 0)  // hi = k, lo = v
-            rb[r] = (hi < d && lo < nv) ? B[(uint64_t)hi * ldb + v0 + lo] : 0u;
-        else  // hi = v, lo = k
-            rb[r] = (lo < d && hi < nv) ? B[(uint64_t)(v0 + hi) * ldb + (qp ? qp[lo] : lo)] : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < PER; ++r) {
-        const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
-        Ct[hi][lo] = rc[r];
-        if (SIDE == 0)
-            Bs[hi][lo] = rb[r];
-        else
-            Bs[lo][hi] = rb[r];
-    }
-    __syncthreads();
-    const uint32_t ti = tid / 16, tv = tid % 16;
-    uint64_t acc[4][4] = {};
-    for (uint32_t k = 0; k < d; ++k) {
-        const uint4 c = *reinterpret_cast<const uint4*>(&Ct[k][ti * 4]);
-        const uint4 x = *reinterpret_cast<const uint4*>(&Bs[k][tv * 4]);
-        const uint32_t cc[4] = {c.x, c.y, c.z, c.w}, xx[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[a][q] += (uint64_t)cc[a] * xx[q];
-    }
-    __syncthreads();  // every thread is done reading Bs: reuse it for the outputs Os[i][v]
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        uint4 o;
-        o.x = mod_u64(acc[a][0], p, mu);
-        o.y = mod_u64(acc[a][1], p, mu);
-        o.z = mod_u64(acc[a][2], p, mu);
-        o.w = mod_u64(acc[a][3], p, mu);
-        *reinterpret_cast<uint4*>(&Bs[ti * 4 + a][tv * 4]) = o;
-    }
-    __syncthreads();
-    if (SIDE == 0) {
-        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
-            const uint32_t i = idx / LA, v = idx % LA;
-            if (i < d && v < nv) B[(uint64_t)i * ldb + v0 + v] = Bs[i][v];
+        for (int r = 0; r < PER; ++r) {
+            const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
+            if (SIDE == 0)  // hi = k, lo = v
+                rb[r] = (hi < d && lo < nv) ? B[(uint64_t)hi * ldb + v0 + lo] : 0u;
+            else  // hi = v, lo = k
+                rb[r] = (lo < d && hi < nv) ? B[(uint64_t)(v0 + hi) * ldb + (qp ? qp[lo] : lo)] : 0u;
         }
-    } else {
-        for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
-            const uint32_t v = idx / LA, i = idx % LA;
-            if (i < d && v < nv) B[(uint64_t)(v0 + v) * ldb + i] = Bs[i][v];
+    };
+    ptx::pdl_enter();
+    {
+        uint32_t rc[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
+            rc[r] = (lo < d && hi < d) ? (SIDE == 0 ? inv[lo * d + hi] : inv[hi * d + lo]) : 0u;
+        }
+        if (blockIdx.x * LA < nvec) load(blockIdx.x * LA);
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const uint32_t idx = tid + 256 * r;
+            Ct[idx / LA][idx % LA] = rc[r];
+        }
+    }
+    // strips blockIdx.x, blockIdx.x + gridDim.x, ...: the next strip's loads fly during this one's math
+    for (uint32_t v0 = blockIdx.x * LA; v0 < nvec; v0 += gridDim.x * LA) {
+        const uint32_t nv = min((uint32_t)LA, nvec - v0);
+        __syncthreads();  // the previous strip's outputs are written out
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
+            if (SIDE == 0)
+                Bs[hi][lo] = rb[r];
+            else
+                Bs[lo][hi] = rb[r];
+        }
+        __syncthreads();
+        if (v0 + gridDim.x * LA < nvec) load(v0 + gridDim.x * LA);
+        const uint32_t ti = tid / 16, tv = tid % 16;
+        uint64_t acc[4][4] = {};
+        for (uint32_t k = 0; k < d; ++k) {
+            const uint4 c = *reinterpret_cast<const uint4*>(&Ct[k][ti * 4]);
+            const uint4 x = *reinterpret_cast<const uint4*>(&Bs[k][tv * 4]);
+            const uint32_t cc[4] = {c.x, c.y, c.z, c.w}, xx[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[a][q] += (uint64_t)cc[a] * xx[q];
+        }
+        __syncthreads();  // every thread is done reading Bs: reuse it for the outputs Os[i][v]
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            uint4 o;
+            o.x = mod_u64(acc[a][0], p, mu);
+            o.y = mod_u64(acc[a][1], p, mu);
+            o.z = mod_u64(acc[a][2], p, mu);
+            o.w = mod_u64(acc[a][3], p, mu);
+            *reinterpret_cast<uint4*>(&Bs[ti * 4 + a][tv * 4]) = o;
+        }
+        __syncthreads();
+        if (SIDE == 0) {
+            for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+                const uint32_t i = idx / LA, v = idx % LA;
+                if (i < d && v < nv) B[(uint64_t)i * ldb + v0 + v] = Bs[i][v];
+            }
+        } else {
+            for (uint32_t idx = tid; idx < LA * LA; idx += 256) {
+                const uint32_t v = idx / LA, i = idx % LA;
+                if (i < d && v < nv) B[(uint64_t)(v0 + v) * ldb + i] = Bs[i][v];
+            }
         }
     }
 }
@@ -555,17 +575,25 @@ void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
     b.count();
 }
 
+// CTAs of a panel apply: one per strip up to FFG_APPLY_CTAS (default: no cap); fewer CTAs loop
+// over strips and leave SMs to concurrent work
+static unsigned apply_grid(size_t nvec) {
+    const char* e = getenv("FFG_APPLY_CTAS");
+    const size_t cap = e ? (size_t)std::max(1, atoi(e)) : (size_t)1 << 30;
+    return (unsigned)std::min(ceil_div(nvec, (size_t)LA), cap);
+}
+
 // side 0: B <- inv(L) B; side 1: B <- B inv(U), with the inverses of panel_inverses_dev
 void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B, const uint32_t* qperm) {
     if (B.empty()) return;
     const size_t nvec = side == 0 ? B.cols : B.rows;
     b.ws.prof.begin(b.st);
     if (side == 0)
-        launch_k(leaf_apply_kernel<0>, dim3((unsigned)ceil_div(nvec, LA)), dim3(256), 0, b.st, inv, (uint32_t)t, B.d,
-                 B.ld, (uint32_t)nvec, b.F.p, b.F.mu, (const uint32_t*)nullptr);
+        launch_k(leaf_apply_kernel<0>, dim3(apply_grid(nvec)), dim3(256), 0, b.st, inv, (uint32_t)t, B.d, B.ld,
+                 (uint32_t)nvec, b.F.p, b.F.mu, (const uint32_t*)nullptr);
     else
-        launch_k(leaf_apply_kernel<1>, dim3((unsigned)ceil_div(nvec, LA)), dim3(256), 0, b.st, inv + t * t,
-                 (uint32_t)t, B.d, B.ld, (uint32_t)nvec, b.F.p, b.F.mu, qperm);
+        launch_k(leaf_apply_kernel<1>, dim3(apply_grid(nvec)), dim3(256), 0, b.st, inv + t * t, (uint32_t)t, B.d,
+                 B.ld, (uint32_t)nvec, b.F.p, b.F.mu, qperm);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)t * nvec);
     b.count();
