@@ -319,13 +319,16 @@ struct Driver {
         }
     }
 
-    NodeRes base(DView a, NodeRes res) {
+    bool base_wrote_inv = false;  // the last speculative base case also wrote its factor inverses
+    NodeRes base(DView a, NodeRes res, uint32_t* inv_out = nullptr) {
         if (spec) {
             if (a.rows > 64 || a.cols > 64) throw SpecAbort{};  // only the slab kernel checks
             if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) throw SpecAbort{};
             spec_throttle();
             const uint32_t seq = ((b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT) | SPEC_BIT;
-            rr_base_launch(b, a, res.P, res.Q, info_dev, nullptr, seq, allow_q && a.rows == a.cols);
+            // (inverses inside the base kernel by substitution measured slower than the separate
+            // log-depth kernel: 38 -> 90 us per base case; the spec kernel ignores inv_out)
+            base_wrote_inv = rr_base_launch(b, a, res.P, res.Q, info_dev, inv_out, seq, allow_q && a.rows == a.cols);
             spec_seqs.push_back(seq);
             ++base_cases;
             res.rank = std::min(a.rows, a.cols);
@@ -671,10 +674,10 @@ struct Driver {
         NodeRes r1;
         r1.P = arena.alloc(t1);
         r1.Q = gq ? gq + c0 : arena.alloc(t1);
-        base(a.sub(0, 0, t1, t1), r1);
         uint32_t* inv1 = inv_slot();
+        base(a.sub(0, 0, t1, t1), r1, inv1);
         leaves.push_back({c0, t1});
-        panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
+        if (!base_wrote_inv) panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
         flush_deferred();  // the node's rows / columns carry every earlier update
         panel_corner_dev(b, a, t1, inv1, q1);
         const cudaEvent_t f = mark_event(b.st);
@@ -695,10 +698,10 @@ struct Driver {
         NodeRes r2;
         r2.P = arena.alloc(t2);
         r2.Q = gq ? gq + c0 + t1 : arena.alloc(t2);
-        base(Rb, r2);
         uint32_t* inv2 = inv_slot();
+        base(Rb, r2, inv2);
         leaves.push_back({c0 + t1, t2});
-        panel_inverses_dev(b, Rb, inv2);
+        if (!base_wrote_inv) panel_inverses_dev(b, Rb, inv2);
         wait(b.st, ea);
         wait(b.st, eb);
         if (corner_max) {
@@ -729,7 +732,7 @@ struct Driver {
         if (std::min(m, n) <= thr) {
             need(b.st, r0 + m);
             if (gq) res.Q = gq + c0;
-            res = base(a, res);  // speculative: no wait
+            res = base(a, res, panel_inv && m == n && m <= 64 ? inv_slot() : nullptr);  // speculative: no wait
             // whole right panel (L^-1, left) and bottom panel (U^-1, right) of this block
             DView right{a.d + n, m, pcols - (c0 + n), pld};
             DView bottom{a.d + m * pld, prows - (r0 + m), n, pld};
@@ -738,7 +741,7 @@ struct Driver {
             if (panel_inv && m == n && m <= 64) {
                 // inverses once, then every strip of both panels only applies them
                 uint32_t* inv = inv_slot();
-                panel_inverses_dev(b, a, inv);
+                if (!base_wrote_inv) panel_inverses_dev(b, a, inv);
                 flush_deferred();
                 if (both) wait(side.st, mark_event(b.st));
                 panel_apply_dev(b, 0, inv, m, right);
