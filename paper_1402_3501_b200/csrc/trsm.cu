@@ -387,7 +387,9 @@ __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restr
         if (v0 + gridDim.x * LA < nvec) load(v0 + gridDim.x * LA);
         const uint32_t ti = tid / 16, tv = tid % 16;
         uint64_t acc[4][4] = {};
-        for (uint32_t k = 0; k < d; ++k) {
+        // both inverses are triangular in the output index: output i only takes k <= i
+        const uint32_t kend = min(d, ti * 4 + 4);
+        for (uint32_t k = 0; k < kend; ++k) {
             const uint4 c = *reinterpret_cast<const uint4*>(&Ct[k][ti * 4]);
             const uint4 x = *reinterpret_cast<const uint4*>(&Bs[k][tv * 4]);
             const uint32_t cc[4] = {c.x, c.y, c.z, c.w}, xx[4] = {x.x, x.y, x.z, x.w};
@@ -605,11 +607,11 @@ void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DVi
 // so R's base case can start before the wide panels of A1 and their updates are done.
 // One CTA, 512 threads, each owning a 2 x 4 tile of every 64 x 64 product (exact u64 sums).
 constexpr int CS = 68;
-__device__ __forceinline__ void mm64_tile(const uint32_t* Am, const uint32_t* Bm, uint32_t kn, uint32_t i0,
-                                          uint32_t v0, uint64_t acc[2][4]) {
-    // acc[a][q] += sum_k Am[(i0+a)][k] * Bm[k][v0+q]   (row-major, stride CS)
+__device__ __forceinline__ void mm64_tile(const uint32_t* Am, const uint32_t* Bm, uint32_t k0, uint32_t kn,
+                                          uint32_t i0, uint32_t v0, uint64_t acc[2][4]) {
+    // acc[a][q] += sum_{k0 <= k < kn} Am[(i0+a)][k] * Bm[k][v0+q]   (row-major, stride CS)
 #pragma unroll 4
-    for (uint32_t k = 0; k < kn; ++k) {
+    for (uint32_t k = k0; k < kn; ++k) {
         const uint4 x = *reinterpret_cast<const uint4*>(&Bm[k * CS + v0]);
         const uint32_t a0 = Am[i0 * CS + k], a1 = Am[(i0 + 1) * CS + k];
         const uint32_t xx[4] = {x.x, x.y, x.z, x.w};
@@ -644,8 +646,8 @@ __global__ void __launch_bounds__(512) panel_corner_kernel(uint32_t* __restrict_
     __syncthreads();
     const uint32_t i0 = (tid / 16) * 2, v0 = (tid % 16) * 4;
     uint64_t ax[2][4] = {}, ay[2][4] = {};
-    mm64_tile(Li, B1, t1, i0, v0, ax);  // X = inv(L1) B1
-    mm64_tile(B2, Ui, t1, i0, v0, ay);  // Y = B2 inv(U1)
+    mm64_tile(Li, B1, 0, min(t1, i0 + 2), i0, v0, ax);  // X = inv(L1) B1 (inv(L1) lower: k <= i)
+    mm64_tile(B2, Ui, 0, min(t1, v0 + 4), i0, v0, ay);  // Y = B2 inv(U1) (inv(U1) upper: k <= v)
     __syncthreads();  // B1 / B2 fully read
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(512) panel_corner_kernel(uint32_t* __restrict_
         }
     __syncthreads();
     uint64_t ac[2][4] = {};
-    mm64_tile(B2, B1, t1, i0, v0, ac);  // Y X
+    mm64_tile(B2, B1, 0, t1, i0, v0, ac);  // Y X
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
