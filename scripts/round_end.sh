@@ -13,6 +13,14 @@ python scripts/trace_pluq.py --n 16384 --json gpurun_out/trace_n16384.json > gpu
 # fgemm 8192^3: one full ncu capture of the tcgen05 kernel
 python scripts/prof_gemm.py > gpurun_out/prof_gemm_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:modgemm -s 1 -c 1 -o gpurun_out/gemm_full python scripts/prof_gemm.py > gpurun_out/ncu_gemm.log 2>&1
+python scripts/ncu_summary.py gpurun_out/gemm_full.ncu-rep --label "fgemm 8192^3 C <- C - A*B mod 131071 (config 2)" \
+  > gpurun_out/ncu_gemm_summary.json 2>/dev/null
+# the panel schedule's latency-bound kernels in the middle of an n = 16384 PLUQ
+python scripts/prof_pluq.py --n 16384 > gpurun_out/prof_pluq_plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"leaf_apply|panel_inv|panel_corner|rr_base_spec" \
+    -s 400 -c 8 -o gpurun_out/panel_full python scripts/prof_pluq.py --n 16384 > gpurun_out/ncu_panel.log 2>&1
+python scripts/ncu_summary.py gpurun_out/panel_full.ncu-rep --label "panel kernels inside an n = 16384 PLUQ (config 3)" \
+  > gpurun_out/ncu_panel_summary.json 2>/dev/null
 # launch list of one bench step (durations only)
 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/bench_small.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/ncu_bench.log 2>&1
