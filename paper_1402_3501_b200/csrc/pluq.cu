@@ -228,8 +228,9 @@ struct Driver {
     Blas on(cudaStream_t st) const { return Blas{b.F, b.ws, st, b.launches}; }
     // a second critical-path stream per recursion depth (the node's independent TRSM), and a
     // low-priority stream per depth for the look-ahead part of the trailing update
-    cudaStream_t twin(int depth) { return b.ws.stream(sid(slot, 100 + depth), 0); }
-    cudaStream_t lookahead(int depth) { return b.ws.stream(sid(slot, 200 + depth), 1); }
+    // (one stream when partitioned: every rank must issue its collectives in the same order)
+    cudaStream_t twin(int depth) { return use_streams ? b.ws.stream(sid(slot, 100 + depth), 0) : b.st; }
+    cudaStream_t lookahead(int depth) { return use_streams ? b.ws.stream(sid(slot, 200 + depth), 1) : b.st; }
 
     // ---- concurrent subtrees: G's recursion (rankrev.hpp:123) is independent of E's (:119) --
     // disjoint blocks, results combined only afterwards -- so a large G runs in a child driver
@@ -246,8 +247,10 @@ struct Driver {
             getenv("FFG_SUBTREE_THREADS")
                 ? atoi(getenv("FFG_SUBTREE_THREADS"))
                 : std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2));
+        static const size_t gmin = getenv("FFG_FORK_MIN") ? (size_t)atoll(getenv("FFG_FORK_MIN")) : 0;
+        const size_t gm = gmin ? gmin : 2 * thr;  // smallest G worth a host thread
         return max_threads > 0 && !spec && use_streams && !b.ws.prof.on && !use_factors && !E.empty() && !G.empty() &&
-               std::min(G.rows, G.cols) > 2 * thr && std::min(E.rows, E.cols) > thr &&
+               std::min(G.rows, G.cols) > gm && std::min(E.rows, E.cols) > thr &&
                active_children().load() < max_threads;
     }
     cudaEvent_t mark_event(cudaStream_t st) {
@@ -323,8 +326,10 @@ struct Driver {
     NodeRes base(DView a, NodeRes res, uint32_t* inv_out = nullptr) {
         if (spec) {
             if (a.rows > 64 || a.cols > 64) throw SpecAbort{};  // only the slab kernel checks
-            if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) throw SpecAbort{};
-            spec_throttle();
+            if (!b.ws.dist.active()) {  // partitioned: every rank enqueues the whole recursion
+                if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) throw SpecAbort{};
+                spec_throttle();
+            }
             const uint32_t seq = ((b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT) | SPEC_BIT;
             // (inverses inside the base kernel by substitution measured slower than the separate
             // log-depth kernel: 38 -> 90 us per base case; the spec kernel ignores inv_out)
@@ -626,7 +631,7 @@ struct Driver {
         for (cudaEvent_t e : deferred) wait(b.st, e);
         deferred.clear();
     }
-    cudaStream_t side_stream(int k) { return b.ws.stream(sid(slot, 400 + k), 0); }
+    cudaStream_t side_stream(int k) { return use_streams ? b.ws.stream(sid(slot, 400 + k), 0) : b.st; }
     // the leaf's right panel (rows of blk, columns beyond `beyond_c`) and bottom panel (rows beyond
     // `beyond_r`, columns of blk): the first thr columns / rows on the critical stream, the rest
     // on the side streams sa / sb (deferred)
@@ -788,9 +793,9 @@ struct Driver {
                 for (cudaEvent_t e : deferred) wait(sx->st, e);
             }
             deferred.clear();
-            if (pcols > A + f) gemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
-            if (E > A + f) gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
-            if (prows > E) gemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
+            if (pcols > A + f) pgemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
+            if (E > A + f) pgemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
+            if (prows > E) pgemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
             deferred.push_back(mark_event(sc.st));
             deferred.push_back(mark_event(sd.st));
         } else if (la_min && m >= la_min && m - m1 > thr) {
@@ -816,8 +821,8 @@ struct Driver {
             need(b.st, r0 + m);
             flush_deferred();
             if (both) wait(side.st, mark_event(b.st));
-            if (!HR.empty()) gemm_sub(b, Fb, Dx, HR);
-            if (both) gemm_sub(side, Fbelow, Dn, BP);
+            if (!HR.empty()) pgemm_sub(b, Fb, Dx, HR);  // split over the ranks when partitioned
+            if (both) pgemm_sub(side, Fbelow, Dn, BP);
             if (both) wait(b.st, mark_event(side.st));
         }
         rec_panel(a.sub(m1, n1, m - m1, n - n1), depth + 1);
@@ -1052,7 +1057,7 @@ void base_dbg_dump();
 // this context (then it rests for a few calls: rank-deficient workloads pay one failed try).
 static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
     static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
-    if (off || b.ws.dist.active() || a.rows == 0 || a.cols == 0) return false;
+    if (off || a.rows == 0 || a.cols == 0) return false;
     // A base block of i.i.d. residues is rank deficient with probability ~1/p: with
     // min(m, n) / thr blocks the guess holds with probability ~exp(-blocks / p).  Do not
     // speculate where it is likely to fail (small fields: config 5's GF(251) at n = 32768 has
@@ -1177,7 +1182,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             drv.spec = true;
             *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
             const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
-            drv.panel = !no_panel && m == n && std::min(m, n) > 0 && drv.use_streams;
+            drv.panel = !no_panel && m == n && std::min(m, n) > 0;
             drv.la_min = panel_lookahead_min();
             drv.corner_max = panel_corner_max();
             drv.proot = a.d;

@@ -91,3 +91,35 @@ def test_world_one_is_plain(gpu, oracle_lib):
         ctx.dist_finalize()
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("world,loopback", [(2, True), (4, False), (8, True)])
+@pytest.mark.parametrize("n,ks", [(1024, []), (2048, [100, 700]), (1500, [5, 64, 1400])])
+def test_virtual_world_panel_schedule(gpu, oracle_lib, world, loopback, n, ks):
+    """Square full-rank input on a partitioned context: the speculative panel schedule runs on
+    one stream, its large node GEMMs split over the (virtual) ranks and all-gathered, column
+    pivots included -- bit-exact against the oracle through the device and host entries."""
+    import torch
+
+    from test_gpu_parity import _zero_schur_pivot
+
+    G, _ = gpu
+    O = oracle_lib
+    p = 131071
+    A = _zero_schur_pivot(O.random_mat(p, n, n, 21 + n), p, [k for k in ks if k < n])
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 64)
+    ctx = _ctx(G, world, loopback, 1 << 20)
+    try:
+        d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+        res = G.pluq_tile_recursive(p, d, 64, ctx=ctx)
+        ctx.synchronize()
+        assert res.rank == r_o
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), a_o)
+        h = A.copy()
+        res = G.pluq_tile_recursive(p, h, 64, ctx=ctx)
+        assert res.rank == r_o and np.array_equal(h, a_o)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert ctx.dist_info()["exchanges"] > 0 or not loopback
+    finally:
+        ctx.close()
