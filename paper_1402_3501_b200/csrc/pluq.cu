@@ -620,6 +620,40 @@ struct Driver {
         }
     }
 
+    // ---- progressive trailing updates (panel schedule): a node Y of size >= prog_min does not
+    // wait for its whole first half A1 before its trailing update H -= L(., A1) U(A1, .): the
+    // update is applied in K-chunks, each as soon as the chunk's sub-nodes of A1 are done, on a
+    // low-priority SM-capped stream while A1's chain goes on.  Y's [H | right panel] and bottom
+    // panel of R's columns are untouched by A1's processing, and chunks commute (exact
+    // arithmetic), so only the last chunk is left when A1 finishes.
+    struct Prog {
+        size_t o, m, m1, next_k, chunk;
+        int depth;
+        cudaEvent_t last;
+    };
+    std::vector<Prog> progs;
+    size_t prog_min = 0, prog_nchunks = 4;
+    int prog_sms = 0;
+    void prog_update(Prog& g, size_t k0, size_t k1) {
+        Blas la = on(lookahead(g.depth));
+        la.sm_cap = prog_sms;
+        const size_t A = g.o + g.m1, E = g.o + g.m;  // R's rows / columns
+        need(la.st, E);
+        wait(la.st, mark_event(b.st));
+        for (cudaEvent_t e : deferred) wait(la.st, e);
+        if (E > A && pcols > A) gemm_sub(la, at(A, k0, E - A, k1 - k0), at(k0, A, k1 - k0, pcols - A), at(A, A, E - A, pcols - A));
+        if (prows > E) gemm_sub(la, at(E, k0, prows - E, k1 - k0), at(k0, A, k1 - k0, E - A), at(E, A, prows - E, E - A));
+        g.last = mark_event(la.st);
+        g.next_k = k1;
+    }
+    // every operation on rows / columns < done is enqueued: start the chunks that became ready
+    void prog_progress(size_t done) {
+        for (auto& g : progs) {
+            const size_t lim = std::min(done, g.o + g.m1);
+            if (lim > g.next_k && lim - g.next_k >= g.chunk) prog_update(g, g.next_k, lim);
+        }
+    }
+
     // ---- deferred wide work (panel schedule): the last leaf of a subtree solves only the next
     // thr columns / rows of its panels on the critical stream and leaves the rest, and a node of
     // size <= corner_max updates only the first block of R on the critical stream (the corner) and
@@ -722,6 +756,7 @@ struct Driver {
             if (both) wait(b.st, mark_event(side.st));
         }
         band_done(r0 + m);
+        prog_progress(r0 + m);
         res.rank = m;
         res.pr = Range{};
         res.qr = Range{};
@@ -760,6 +795,7 @@ struct Driver {
             if (both) wait(b.st, mark_event(side.st));
             leaves.push_back({c0, n});
             band_done(r0 + m);
+            prog_progress(r0 + m);
             return res;
         }
         const size_t mark = arena.mark();
@@ -770,6 +806,8 @@ struct Driver {
             arena.reset(mark);
             return res;
         }
+        const bool prog = prog_min && m >= prog_min && use_streams && m == n && m - m1 > thr;
+        if (prog) progs.push_back(Prog{r0, m, m1, r0, std::max(thr, m1 / prog_nchunks), depth, nullptr});
         rec_panel(a.sub(0, 0, m1, n1), depth + 1);
         // A1's panels solved D and Fb (and the parts of A1's rows / columns beyond this node)
         DView Fb = a.sub(m1, 0, m - m1, n1);                                  // rows of R, cols of A1
@@ -780,7 +818,14 @@ struct Driver {
         DView BP{a.d + m * pld + n1, prows - (r0 + m), n - n1, pld};          // below the node, R cols
         const bool both = !BP.empty();
         const Blas side = both ? on(twin(depth)) : b;
-        if (corner_max && m <= corner_max && m - m1 > thr) {
+        if (prog) {
+            Prog g = progs.back();
+            progs.pop_back();
+            if (g.next_k < r0 + m1) prog_update(g, g.next_k, r0 + m1);  // the last chunk
+            need(b.st, r0 + m);
+            flush_deferred();
+            wait(b.st, g.last);  // [H | right panel] and the bottom panel are complete
+        } else if (corner_max && m <= corner_max && m - m1 > thr) {
             // corner: R's first base block gets its update now; the wide GEMMs of the node are
             // deferred to side streams (after the last leaf's deferred panels)
             const size_t A = r0 + m1, f = first_leaf(m - m1), E = r0 + m;
@@ -827,6 +872,7 @@ struct Driver {
         }
         rec_panel(a.sub(m1, n1, m - m1, n - n1), depth + 1);
         band_done(r0 + m);
+        prog_progress(r0 + m);
         res.rank = std::min(m, n);
         res.pr = Range{};
         res.qr = Range{};
@@ -1081,6 +1127,17 @@ static size_t panel_corner_max() {
     return e ? (size_t)atoll(e) : 1024;
 }
 
+// panel-mode nodes of at least this size apply their trailing update progressively in K-chunks
+// (FFG_PROG_MIN, read per call; 0 = off); FFG_PROG_CHUNKS chunks per node, FFG_PROG_SMS SM cap
+static size_t panel_prog_min() {
+    const char* e = getenv("FFG_PROG_MIN");
+    return e ? (size_t)atoll(e) : 0;
+}
+static size_t prog_chunks() {
+    const char* e = getenv("FFG_PROG_CHUNKS");
+    return e ? std::max<size_t>(1, (size_t)atoll(e)) : 4;
+}
+
 static size_t panel_lookahead_min() {
     const char* e = getenv("FFG_PANEL_LA");
     return e ? (size_t)atoll(e) : 0;
@@ -1114,6 +1171,9 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         drv.panel = true;
         drv.la_min = panel_lookahead_min();
         drv.corner_max = panel_corner_max();
+        drv.prog_min = panel_prog_min();
+        drv.prog_nchunks = prog_chunks();
+        drv.prog_sms = getenv("FFG_PROG_SMS") ? atoi(getenv("FFG_PROG_SMS")) : drv.lookahead_sms;
         drv.proot = d;
         drv.pld = n;
         drv.prows = n;
@@ -1185,6 +1245,9 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             drv.panel = !no_panel && m == n && std::min(m, n) > 0;
             drv.la_min = panel_lookahead_min();
             drv.corner_max = panel_corner_max();
+            drv.prog_min = panel_prog_min();
+            drv.prog_nchunks = prog_chunks();
+            drv.prog_sms = getenv("FFG_PROG_SMS") ? atoi(getenv("FFG_PROG_SMS")) : drv.lookahead_sms;
             drv.proot = a.d;
             drv.pld = a.ld;
             drv.prows = m;
