@@ -40,30 +40,6 @@ constexpr uint32_t INV_MAX = 64;  // largest base-case rank whose factor inverse
 
 __device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
 
-// binary extended Euclid for odd p (no divisions); p == 2 -> the only unit is 1
-__device__ __forceinline__ uint32_t inv_mod_bin(uint32_t a, uint32_t p) {
-    if (p == 2) return 1;
-    uint32_t u = a, v = p, x1 = 1, x2 = 0;  // a*x1 = u, a*x2 = v (mod p)
-    while (u != 1 && v != 1) {
-        while ((u & 1) == 0) {
-            u >>= 1;
-            x1 = (x1 & 1) ? (x1 + p) >> 1 : x1 >> 1;
-        }
-        while ((v & 1) == 0) {
-            v >>= 1;
-            x2 = (x2 & 1) ? (x2 + p) >> 1 : x2 >> 1;
-        }
-        if (u >= v) {
-            u -= v;
-            x1 = x1 >= x2 ? x1 - x2 : x1 + p - x2;
-        } else {
-            v -= u;
-            x2 = x2 >= x1 ? x2 - x1 : x2 + p - x1;
-        }
-    }
-    return u == 1 ? x1 : x2;
-}
-
 // diagnostics (FFG_BASE_DBG): per launch {clock64, globaltimer} at entry, end of pivoting, exit
 __device__ unsigned long long* g_base_dbg = nullptr;
 __device__ unsigned int g_base_dbg_n = 0;

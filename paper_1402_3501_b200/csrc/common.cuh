@@ -61,6 +61,34 @@ __host__ __device__ __forceinline__ uint32_t mod_u64(uint64_t x, uint32_t p, uin
     return (uint32_t)r;
 }
 
+// binary extended Euclid for odd p (no divisions): a^-1 mod p for a != 0 mod p; p == 2 -> 1
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t inv_mod_bin(uint32_t a, uint32_t p) {
+    if (p == 2) return 1;
+    a %= p;
+    if (a == 0) return 0;  // no inverse; callers on a failed speculative path get garbage, not a hang
+    uint32_t u = a, v = p, x1 = 1, x2 = 0;  // a*x1 = u, a*x2 = v (mod p)
+    while (u != 1 && v != 1) {
+        while ((u & 1) == 0) {
+            u >>= 1;
+            x1 = (x1 & 1) ? (x1 + p) >> 1 : x1 >> 1;
+        }
+        while ((v & 1) == 0) {
+            v >>= 1;
+            x2 = (x2 & 1) ? (x2 + p) >> 1 : x2 >> 1;
+        }
+        if (u >= v) {
+            u -= v;
+            x1 = x1 >= x2 ? x1 - x2 : x1 + p - x2;
+        } else {
+            v -= u;
+            x2 = x2 >= x1 ? x2 - x1 : x2 + p - x1;
+        }
+    }
+    return u == 1 ? x1 : x2;
+}
+#endif
+
 __host__ __device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, uint32_t p, uint64_t mu) {
     return mod_u64((uint64_t)a * b, p, mu);
 }

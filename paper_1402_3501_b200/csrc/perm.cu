@@ -7,6 +7,7 @@
 // gather over the moved range only: HBM traffic = 2 reads + 2 writes of the
 // rows/columns that actually move, nothing for the rest.
 #include <algorithm>
+#include <mutex>
 
 #include "pluq.cuh"
 #include "ptx.cuh"
@@ -63,9 +64,65 @@ __global__ void iota_kernel(uint32_t* a, uint32_t len) {
     if (t < len) a[t] = t;
 }
 
+// In-place gathers in one launch for the common small ranges (every permutation of the
+// rank-deficient recursion): a CTA stages its slice of the moved block in shared memory and
+// writes it back permuted -- rows: a column slice of all moved rows; columns: a row slice of all
+// moved columns.  Larger ranges take the two-pass gather through a temporary.
+constexpr size_t PERM_SMEM = 96 * 1024;
+__global__ void __launch_bounds__(256) rows_perm_inplace_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows,
+                                                                uint32_t ncols, uint32_t w, PermSrc src) {
+    extern __shared__ uint32_t sbuf[];
+    ptx::pdl_enter();
+    const uint32_t c0 = blockIdx.x * w, cw = min(w, ncols - c0), tot = nrows * cw;
+    for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        const uint32_t r = idx / cw, c = idx % cw;
+        sbuf[idx] = A[(uint64_t)r * lda + c0 + c];
+    }
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        const uint32_t t = idx / cw, c = idx % cw;
+        A[(uint64_t)t * lda + c0 + c] = sbuf[src.at(t) * cw + c];
+    }
+}
+__global__ void __launch_bounds__(256) cols_perm_inplace_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t nrows,
+                                                                uint32_t ncols, uint32_t h, PermSrc src) {
+    extern __shared__ uint32_t sbuf[];
+    uint32_t* sidx = sbuf + (size_t)h * ncols;  // src.at(u) for every column
+    ptx::pdl_enter();
+    const uint32_t r0 = blockIdx.x * h, rh = min(h, nrows - r0), tot = rh * ncols;
+    for (uint32_t u = threadIdx.x; u < ncols; u += blockDim.x) sidx[u] = src.at(u);
+    for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        const uint32_t r = idx / ncols, c = idx % ncols;
+        sbuf[idx] = A[(uint64_t)(r0 + r) * lda + c];
+    }
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+        const uint32_t r = idx / ncols, u = idx % ncols;
+        A[(uint64_t)(r0 + r) * lda + u] = sbuf[r * ncols + sidx[u]];
+    }
+}
+
 namespace {
+void perm_smem_attr() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        FFG_CUDA(cudaFuncSetAttribute(rows_perm_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PERM_SMEM));
+        FFG_CUDA(cudaFuncSetAttribute(cols_perm_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PERM_SMEM));
+    });
+}
 void gather_rows(const Blas& b, DView a, PermSrc src) {
     if (a.empty()) return;
+    if (a.rows * 4 * 32 <= PERM_SMEM) {  // at least 32 columns per CTA
+        perm_smem_attr();
+        const size_t w = std::min<size_t>(a.cols, std::min<size_t>(512, PERM_SMEM / (a.rows * 4)));
+        b.ws.prof.begin(b.st);
+        launch_k(rows_perm_inplace_kernel, dim3((unsigned)ceil_div(a.cols, w)), dim3(256), a.rows * w * 4, b.st, a.d,
+                 a.ld, (uint32_t)a.rows, (uint32_t)a.cols, (uint32_t)w, src);
+        b.ws.prof.end(b.st, PROF_PERM, 16.0 * a.rows * a.cols);
+        FFG_CUDA(cudaGetLastError());
+        b.count();
+        return;
+    }
     uint32_t* tmp = nullptr;
     FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
     dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
@@ -79,6 +136,17 @@ void gather_rows(const Blas& b, DView a, PermSrc src) {
 }
 void gather_cols(const Blas& b, DView a, PermSrc src) {
     if (a.empty()) return;
+    if ((a.cols * 4 + a.cols * 4) * 4 <= PERM_SMEM) {  // at least 4 rows per CTA
+        perm_smem_attr();
+        const size_t h = std::min<size_t>(a.rows, std::min<size_t>(64, (PERM_SMEM - a.cols * 4) / (a.cols * 4)));
+        b.ws.prof.begin(b.st);
+        launch_k(cols_perm_inplace_kernel, dim3((unsigned)ceil_div(a.rows, h)), dim3(256), (h + 1) * a.cols * 4, b.st,
+                 a.d, a.ld, (uint32_t)a.rows, (uint32_t)a.cols, (uint32_t)h, src);
+        b.ws.prof.end(b.st, PROF_PERM, 16.0 * a.rows * a.cols);
+        FFG_CUDA(cudaGetLastError());
+        b.count();
+        return;
+    }
     uint32_t* tmp = nullptr;
     FFG_CUDA(cudaMallocAsync(&tmp, a.rows * a.cols * 4, b.st));
     dim3 g((unsigned)ceil_div(a.cols, 256), (unsigned)a.rows);
