@@ -131,6 +131,7 @@ struct Driver {
     // slot: 0 for the root driver of a call; a concurrent subtree (E || G) gets its own slot =
     // its own streams (ids slot*1000 + ...) and base-case mailbox
     int slot = 0;
+    bool owns_slot = true;  // false for a node-level speculative sub-driver sharing its parent's slot
     int device = 0;
     static int sid(int slot, int k) { return slot * 1000 + k; }
 
@@ -217,7 +218,7 @@ struct Driver {
         if (gq) cudaFreeAsync(gq, b.st);
         if (panel_inv) cudaFreeAsync(panel_inv, b.st);
         if (inv_arena) cudaFreeAsync(inv_arena, b.st);
-        b.ws.release_slot(slot);
+        if (owns_slot) b.ws.release_slot(slot);
     }
     // join the critical stream back into the caller's stream
     void finish() {
@@ -880,12 +881,80 @@ struct Driver {
         return res;
     }
 
+    // ---- node-level speculation (exact recursion on small fields): where a whole-matrix guess
+    // is likely to fail (config 5: GF(251), ~2 rank-deficient blocks per matrix), a square node
+    // of <= node_spec_max is still likely full rank; it runs the speculative panel schedule
+    // restricted to itself (a sub-driver whose "matrix" is the node), backed up in HBM and
+    // rerun exactly when its guess fails.  A full-rank node's result is the unique one (P the
+    // identity, Q its blocks' column pivots), so the exact parent continues unchanged.
+    size_t node_spec_max = 0;
+    int node_spec_fails = 0;  // consecutive failures: stop trying after 3
+    bool try_node_spec(DView a, int depth, NodeRes& res) {
+        const size_t m = a.rows;
+        uint32_t* bk = nullptr;
+        FFG_CUDA(cudaMallocAsync(&bk, m * m * 4, b.st));
+        copy_block_dev(b, a, DView{bk, m, m, m});
+        std::vector<uint32_t> qh(m);
+        bool ok = false;
+        {
+            Driver sub(b, thr, m, m, /*keep_events=*/true, slot);
+            sub.owns_slot = false;
+            sub.spec = true;
+            *reinterpret_cast<volatile uint32_t*>(&sub.info_host->spec_fail) = 0u;
+            sub.panel = true;
+            sub.proot = a.d;
+            sub.pld = a.ld;
+            sub.prows = m;
+            sub.pcols = m;
+            sub.corner_max = corner_max;
+            sub.alloc_panel_inv();
+            try {
+                sub.rec_panel(a, depth);
+                sub.flush_deferred();
+                sub.finish();
+                sub.panel_finish(nullptr, qh.data(), nullptr);  // synchronizes
+                ok = *reinterpret_cast<volatile uint32_t*>(&sub.info_host->spec_fail) == 0u;
+            } catch (const SpecAbort&) {
+                ok = false;
+            }
+            if (!ok) FFG_CUDA(cudaDeviceSynchronize());
+        }
+        if (!ok) {
+            copy_block_dev(b, DView{bk, m, m, m}, a);
+            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            ++node_spec_fails;
+            return false;
+        }
+        FFG_CUDA(cudaFreeAsync(bk, b.st));
+        node_spec_fails = 0;
+        size_t lo = m, hi = 0;
+        for (size_t j = 0; j < m; ++j)
+            if (qh[j] != j) {
+                lo = std::min(lo, j);
+                hi = j + 1;
+            }
+        res.rank = m;
+        res.pr = Range{};
+        res.qr = Range{};
+        if (hi > lo) {
+            FFG_CUDA(cudaMemcpyAsync(res.Q + lo, qh.data() + lo, (hi - lo) * 4, cudaMemcpyHostToDevice, b.st));
+            FFG_CUDA(cudaStreamSynchronize(b.st));  // qh is a local buffer
+            res.qr = Range{lo, hi};
+        }
+        return true;
+    }
+
     NodeRes rec(DView a, int depth = 0, cudaEvent_t pending = nullptr, bool rspine = false) {
         const size_t m = a.rows, n = a.cols;
         NodeRes res;
         res.P = arena.alloc(std::max<size_t>(m, 1));
         res.Q = arena.alloc(std::max<size_t>(n, 1));
         if (m == 0 || n == 0) return res;                        // rankrev.hpp:91
+        if (node_spec_max && m == n && m > thr && m <= node_spec_max && node_spec_fails < 3 && thr <= 64 &&
+            !spine_root && !early.armed) {
+            wait(b.st, pending);
+            if (try_node_spec(a, depth, res)) return res;
+        }
         if (std::min(m, n) <= thr) {                             // :92
             wait(b.st, pending);
             if (level_timing) {
@@ -1143,6 +1212,21 @@ static size_t panel_lookahead_min() {
     return e ? (size_t)atoll(e) : 0;
 }
 
+// Node-level speculation of the exact recursion (FFG_NODE_SPEC = largest node, 0 = off): only
+// where the whole-matrix guess was skipped for a small field, nodes whose guess holds with
+// probability >= ~90% (blocks per node <= p / 10), single stream drivers excluded.
+static size_t node_spec_max(const Blas& b, const DView& a, size_t thr, const Driver& drv) {
+    static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
+    const char* e = getenv("FFG_NODE_SPEC");
+    size_t s = e ? (size_t)atoll(e) : 1024;
+    if (off || s == 0 || !drv.use_streams || b.ws.dist.active() || thr > 64) return 0;
+    const double blocks_all = (double)std::min(a.rows, a.cols) / (double)std::max<size_t>(thr, 1);
+    if (blocks_all <= 0.25 * (double)b.F.p) return 0;  // the whole-matrix guess was tried instead
+    static const double risk = getenv("FFG_NODE_SPEC_RISK") ? atof(getenv("FFG_NODE_SPEC_RISK")) : 0.1;
+    while (s > thr && (double)s / (double)thr > risk * (double)b.F.p) s /= 2;
+    return s > 2 * thr ? s : 0;
+}
+
 // band ends for the streamed host entry: the recursion's nodes of size <= min(T, max(Tmin, o)) in
 // order -- finer at the start, where the factorisation waits for each band
 static void band_bounds(size_t o, size_t s, size_t thr, size_t T, size_t Tmin, std::vector<size_t>& out) {
@@ -1281,6 +1365,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
     }
     Driver drv(b, threshold, a.rows, a.cols);
     drv.level_timing = getenv("FFG_LEVEL_TIMING") != nullptr;
+    drv.node_spec_max = node_spec_max(b, a, threshold, drv);
     NodeRes res = drv.rec(a);
     drv.level_report();
     drv.finish();

@@ -440,3 +440,52 @@ def test_u8_host_entry_rejects_large_p(gpu):
     G, ctx = gpu
     with pytest.raises(Exception):
         G.pluq_tile_recursive(131071, np.zeros((4, 4), np.uint8), 64, ctx=ctx)
+
+
+@pytest.mark.parametrize("n,thr,seed", [(1100, 16, 1), (1100, 16, 2), (1300, 16, 3)])
+def test_node_level_speculation_small_field(gpu, oracle_lib, n, thr, seed):
+    """GF(251) with many blocks: the whole-matrix guess is skipped, square nodes of the exact
+    recursion try the speculative panel schedule on their own (some fail and rerun exactly)
+    -- bit-exact against the oracle."""
+    import torch
+
+    G, _ = gpu
+    O = oracle_lib
+    p = 251
+    A = O.random_mat(p, n, n, seed)
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+    ctx = G.Context(0)
+    try:
+        d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+        res = G.pluq_tile_recursive(p, d, thr, ctx=ctx)
+        ctx.synchronize()
+        assert res.rank == r_o
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), a_o)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.slow
+def test_node_level_speculation_matches_exact_at_config5_blocks(gpu, monkeypatch):
+    """n = 4096, GF(251), thr 64 (config 5's block size): node-level speculation on vs off,
+    bit for bit."""
+    import torch
+
+    G, _ = gpu
+    p, n = 251, 4096
+    outs = []
+    for ns in ("1024", "0"):
+        monkeypatch.setenv("FFG_NODE_SPEC", ns)
+        ctx = G.Context(0)
+        try:
+            d = torch.empty((n, n), dtype=torch.int32, device="cuda")
+            G.random_mat_dev(p, d, 5, ctx=ctx)
+            res = G.pluq_tile_recursive(p, d, 64, ctx=ctx)
+            ctx.synchronize()
+            outs.append((res.rank, res.P.copy(), res.Q.copy(), d.cpu().numpy().copy()))
+        finally:
+            ctx.close()
+    assert outs[0][0] == outs[1][0]
+    for i in (1, 2, 3):
+        assert np.array_equal(outs[0][i], outs[1][i])
