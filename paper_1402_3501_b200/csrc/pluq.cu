@@ -95,7 +95,8 @@ struct Driver {
     size_t inv_cap = 0, inv_top = 0;
     bool use_factors = true;
 
-    bool use_streams = true;
+    bool use_streams = true;     // exact recursion: side streams (off when partitioned)
+    bool panel_streams = true;   // panel schedule: side streams (collectives stay on the critical one)
     int lookahead_sms = 0;  // SM cap of the look-ahead GEMMs (FFG_LOOKAHEAD_SMS, default SMs - 32)
 
     // host-pipelined entry (pluq_tile_recursive_host): the top-left spine of the recursion
@@ -150,6 +151,7 @@ struct Driver {
         // partitioned (multi-GPU) runs keep one stream: every rank must issue its NCCL
         // exchanges in the same order, and the replicated control flow guarantees that
         use_streams = !no_streams && !bl.ws.dist.active();
+        panel_streams = !no_streams;
         {
             static int sms = -1;
             if (sms < 0) {
@@ -230,8 +232,9 @@ struct Driver {
     // a second critical-path stream per recursion depth (the node's independent TRSM), and a
     // low-priority stream per depth for the look-ahead part of the trailing update
     // (one stream when partitioned: every rank must issue its collectives in the same order)
-    cudaStream_t twin(int depth) { return use_streams ? b.ws.stream(sid(slot, 100 + depth), 0) : b.st; }
-    cudaStream_t lookahead(int depth) { return use_streams ? b.ws.stream(sid(slot, 200 + depth), 1) : b.st; }
+    bool multi() const { return use_streams || (panel && panel_streams); }
+    cudaStream_t twin(int depth) { return multi() ? b.ws.stream(sid(slot, 100 + depth), 0) : b.st; }
+    cudaStream_t lookahead(int depth) { return multi() ? b.ws.stream(sid(slot, 200 + depth), 1) : b.st; }
 
     // ---- concurrent subtrees: G's recursion (rankrev.hpp:123) is independent of E's (:119) --
     // disjoint blocks, results combined only afterwards -- so a large G runs in a child driver
@@ -666,7 +669,7 @@ struct Driver {
         for (cudaEvent_t e : deferred) wait(b.st, e);
         deferred.clear();
     }
-    cudaStream_t side_stream(int k) { return use_streams ? b.ws.stream(sid(slot, 400 + k), 0) : b.st; }
+    cudaStream_t side_stream(int k) { return multi() ? b.ws.stream(sid(slot, 400 + k), 0) : b.st; }
     // the leaf's right panel (rows of blk, columns beyond `beyond_c`) and bottom panel (rows beyond
     // `beyond_r`, columns of blk): the first thr columns / rows on the critical stream, the rest
     // on the side streams sa / sb (deferred)
@@ -839,9 +842,10 @@ struct Driver {
                 for (cudaEvent_t e : deferred) wait(sx->st, e);
             }
             deferred.clear();
-            if (pcols > A + f) pgemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
-            if (E > A + f) pgemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
-            if (prows > E) pgemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
+            // (replicated when partitioned: only the critical stream issues collectives)
+            if (pcols > A + f) gemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
+            if (E > A + f) gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
+            if (prows > E) gemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
             deferred.push_back(mark_event(sc.st));
             deferred.push_back(mark_event(sd.st));
         } else if (la_min && m >= la_min && m - m1 > thr) {
@@ -866,10 +870,12 @@ struct Driver {
         } else {
             need(b.st, r0 + m);
             flush_deferred();
-            if (both) wait(side.st, mark_event(b.st));
-            if (!HR.empty()) pgemm_sub(b, Fb, Dx, HR);  // split over the ranks when partitioned
-            if (both) pgemm_sub(side, Fbelow, Dn, BP);
-            if (both) wait(b.st, mark_event(side.st));
+            // partitioned: both split over the ranks, on the critical stream (one collective order)
+            const Blas bside = b.ws.dist.active() ? b : side;
+            if (both) wait(bside.st, mark_event(b.st));
+            if (!HR.empty()) pgemm_sub(b, Fb, Dx, HR);
+            if (both) pgemm_sub(bside, Fbelow, Dn, BP);
+            if (both) wait(b.st, mark_event(bside.st));
         }
         rec_panel(a.sub(m1, n1, m - m1, n - n1), depth + 1);
         band_done(r0 + m);

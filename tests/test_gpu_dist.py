@@ -95,7 +95,7 @@ def test_world_one_is_plain(gpu, oracle_lib):
 
 @pytest.mark.parametrize("world,loopback", [(2, True), (4, False), (8, True)])
 @pytest.mark.parametrize("n,ks", [(1024, []), (2048, [100, 700]), (1500, [5, 64, 1400])])
-def test_virtual_world_panel_schedule(gpu, oracle_lib, world, loopback, n, ks):
+def test_virtual_world_panel_schedule(gpu, oracle_lib, world, loopback, n, ks, monkeypatch):
     """Square full-rank input on a partitioned context: the speculative panel schedule runs on
     one stream, its large node GEMMs split over the (virtual) ranks and all-gathered, column
     pivots included -- bit-exact against the oracle through the device and host entries."""
@@ -108,6 +108,10 @@ def test_virtual_world_panel_schedule(gpu, oracle_lib, world, loopback, n, ks):
     p = 131071
     A = _zero_schur_pivot(O.random_mat(p, n, n, 21 + n), p, [k for k in ks if k < n])
     a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 64)
+    # nodes above 256 take the generic node branch, whose GEMMs are split (corner nodes stay
+    # replicated: their wide GEMMs run on side streams, and only the critical stream may
+    # issue collectives)
+    monkeypatch.setenv("FFG_CORNER_MAX", "256")
     ctx = _ctx(G, world, loopback, 1 << 20)
     try:
         d = torch.from_numpy(A.view(np.int32).copy()).cuda()
