@@ -489,3 +489,35 @@ def test_node_level_speculation_matches_exact_at_config5_blocks(gpu, monkeypatch
     assert outs[0][0] == outs[1][0]
     for i in (1, 2, 3):
         assert np.array_equal(outs[0][i], outs[1][i])
+
+
+@pytest.mark.parametrize("trial", range(40))
+def test_panel_schedule_random_sweep(gpu, oracle_lib, trial):
+    """Random square sizes, thresholds (odd leaf sizes, two-leaf nodes of unequal leaves),
+    primes up to 2^26 and injected zero Schur diagonals through the speculative schedules
+    (device and host entries), against the oracle."""
+    import torch
+
+    G, _ = gpu
+    O = oracle_lib
+    rng = np.random.default_rng(1000 + trial)
+    p = int(rng.choice([65521, 131071, 16777213, 67108859]))
+    thr = int(rng.choice([8, 16, 33, 48, 64]))
+    n = int(rng.integers(150, 900))
+    ks = sorted(set(int(k) for k in rng.integers(0, n - 1, size=int(rng.integers(0, 4)))))
+    A = _zero_schur_pivot(O.random_mat(p, n, n, 77 * trial + 1), p, ks)
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+    ctx = G.Context(0)
+    try:
+        d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+        res = G.pluq_tile_recursive(p, d, thr, ctx=ctx)
+        ctx.synchronize()
+        assert res.rank == r_o, (p, thr, n, ks)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o), (p, thr, n, ks)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), a_o), (p, thr, n, ks)
+        h = A.copy()
+        res = G.pluq_tile_recursive(p, h, thr, ctx=ctx)
+        assert res.rank == r_o and np.array_equal(h, a_o), (p, thr, n, ks)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o), (p, thr, n, ks)
+    finally:
+        ctx.close()
