@@ -804,7 +804,7 @@ struct Driver {
         }
         const size_t mark = arena.mark();
         const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;
-        static const bool no_corner = getenv("FFG_NO_CORNER") && atoi(getenv("FFG_NO_CORNER")) != 0;
+        const bool no_corner = getenv("FFG_NO_CORNER") && atoi(getenv("FFG_NO_CORNER")) != 0;  // per call: tests
         if (!no_corner && panel_inv && m == n && m1 <= thr && m1 <= 64 && m - m1 > 0) {
             two_leaf(a, depth, res);
             arena.reset(mark);

@@ -35,6 +35,7 @@ __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, ui
             if (!UPPER) {  // W = L21 X11 (X11 lower: k >= c); rows/cols >= t contribute nothing
                 const uint32_t row0 = ob + h + i0;
                 const uint32_t kend = t > ob ? min(h, t - ob) : 0u;
+#pragma unroll 4
                 for (uint32_t k = c; k < kend; ++k) {
                     const uint64_t xk = X[(ob + k) * xs + ob + c];
 #pragma unroll
@@ -45,6 +46,7 @@ __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, ui
             } else {  // W = U12 X22 (X22 upper: k <= c)
                 const uint32_t row0 = ob + i0;
                 const uint32_t kend = t > ob + h ? min(c + 1, t - ob - h) : 0u;
+#pragma unroll 4
                 for (uint32_t k = 0; k < kend; ++k) {
                     const uint64_t xk = X[(ob + h + k) * xs + ob + h + c];
 #pragma unroll
@@ -60,6 +62,7 @@ __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, ui
             const uint32_t* w = W + blk * h * h;
             uint64_t s[4] = {0, 0, 0, 0};
             if (!UPPER) {  // X21 = -X22 W (X22 lower: k <= i; the zeros above its diagonal pad)
+#pragma unroll 4
                 for (uint32_t k = 0; k < i0 + 4; ++k) {
                     const uint64_t wk = w[k * h + c];
 #pragma unroll
@@ -71,6 +74,7 @@ __device__ __forceinline__ void tri_inverse_levels(const uint32_t* S, int ss, ui
                     X[(ob + h + i0 + a) * xs + ob + c] = v ? p - v : 0u;
                 }
             } else {  // X12 = -X11 W (X11 upper: k >= i)
+#pragma unroll 4
                 for (uint32_t k = i0; k < h; ++k) {
                     const uint64_t wk = w[k * h + c];
 #pragma unroll
@@ -97,7 +101,7 @@ __device__ void tri_inverse_part(const uint32_t* S, int ss, uint32_t* X, int xs,
     constexpr int LEAF = 8;
     for (uint32_t idx = tid; idx < (uint32_t)R * R; idx += nth) X[(idx / R) * xs + idx % R] = 0u;
     for (uint32_t i = tid; i < (uint32_t)R; i += nth)
-        dinv[i] = (!UPPER || i >= t) ? 1u : inv_mod32(S[i * ss + i], p);
+        dinv[i] = (!UPPER || i >= t) ? 1u : inv_mod_bin(S[i * ss + i], p);  // no 64-bit divisions
     tri_bar(bar, nth);
     if (tid < (uint32_t)R) {  // leaves: thread per (leaf block, column)
         const uint32_t base = (tid / LEAF) * LEAF, j = tid % LEAF;

@@ -521,3 +521,29 @@ def test_panel_schedule_random_sweep(gpu, oracle_lib, trial):
         assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o), (p, thr, n, ks)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("knobs", [{"FFG_PROG_MIN": "256"}, {"FFG_PROG_MIN": "512", "FFG_PROG_CHUNKS": "2"},
+                                   {"FFG_CORNER_MAX": "0"}, {"FFG_NO_CORNER": "1"}, {"FFG_APPLY_CTAS": "7"}])
+def test_panel_schedule_variants_match_oracle(gpu, oracle_lib, knobs, monkeypatch):
+    """The panel schedule's off-by-default variants (progressive K-chunked trailing updates,
+    no corner deferral, no two-leaf corner, capped strip-looping applies) stay bit-exact."""
+    import torch
+
+    G, _ = gpu
+    O = oracle_lib
+    p, n = 131071, 1300
+    A = _zero_schur_pivot(O.random_mat(p, n, n, 606), p, [40, 700])
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, 64)
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    ctx = G.Context(0)
+    try:
+        d = torch.from_numpy(A.view(np.int32).copy()).cuda()
+        res = G.pluq_tile_recursive(p, d, 64, ctx=ctx)
+        ctx.synchronize()
+        assert res.rank == r_o
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), a_o)
+    finally:
+        ctx.close()
