@@ -547,3 +547,31 @@ def test_panel_schedule_variants_match_oracle(gpu, oracle_lib, knobs, monkeypatc
         assert np.array_equal(d.cpu().numpy().view(np.uint32), a_o)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("n,thr,seed,lead", [(1100, 16, 4, 0), (1300, 16, 5, 7), (1200, 8, 6, 3)])
+def test_small_field_host_pipeline_matches_oracle(gpu, oracle_lib, n, thr, seed, lead):
+    """GF(251) with many blocks through the host entries: u32 (the pipelined exact recursion:
+    spine uploads, right-spine early downloads) and bytes (widened / narrowed in HBM, node-level
+    speculation inside) -- bit-exact against the oracle, padding untouched."""
+    G, _ = gpu
+    O = oracle_lib
+    p = 251
+    A = O.random_mat(p, n, n, seed)
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+    ctx = G.Context(0)
+    try:
+        buf = np.full((n, n + lead), 0xCD, np.uint32)
+        buf[:, :n] = A
+        res = G.pluq_tile_recursive(p, buf[:, :n], thr, ctx=ctx)
+        assert res.rank == r_o and np.array_equal(buf[:, :n], a_o)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.all(buf[:, n:] == 0xCD)
+        b8 = np.full((n, n + lead), 0xEE, np.uint8)
+        b8[:, :n] = A.astype(np.uint8)
+        res = G.pluq_tile_recursive(p, b8[:, :n], thr, ctx=ctx)
+        assert res.rank == r_o and np.array_equal(b8[:, :n].astype(np.uint32), a_o)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+        assert np.all(b8[:, n:] == 0xEE)
+    finally:
+        ctx.close()
