@@ -838,7 +838,19 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
             pcol[k] = c;
         }
         const uint32_t nxt = k + 1;
-        if (diag) {  // uniform: the pivot is (k, k)
+        if (diag && k >= 32) {  // uniform: pivot (k, k) in the second column half; the first half is final
+#pragma unroll
+            for (int j = 0; j < SP_RPW; ++j) {
+                const uint32_t i = warp + SP_WARPS * j;
+                if (i > k && i < m) {  // warp-uniform
+                    const uint32_t numer = red4p(__shfl_sync(FULL, x[j][1], k & 31), p);
+                    const uint32_t u1 = (x[j][1] * pv - __umulhi(x[j][1], pvp) * p) + 2 * p -
+                                        (numer * b1 - __umulhi(numer, f1) * p);
+                    x[j][1] = lane + 32 > k ? u1 : (lane + 32 == k ? numer : x[j][1]);
+                    if (i == nxt && nxt < r) publish(x[j][0], x[j][1], buf[nxt & 1]);
+                }
+            }
+        } else if (diag) {  // uniform: the pivot is (k, k)
 #pragma unroll
             for (int j = 0; j < SP_RPW; ++j) {
                 const uint32_t i = warp + SP_WARPS * j;
