@@ -639,6 +639,7 @@ struct SplitArgs {
     uint8_t* outB;
     int L, NT;
     uint32_t a_blocks, b_kblocks;
+    uint32_t a_vec;  // A rows 16-byte aligned (A and lda multiples of 4 words): vector loads
 };
 
 
@@ -646,39 +647,66 @@ __global__ void __launch_bounds__(256) split_kernel(const SplitArgs a) {
     __shared__ uint32_t tile[64][65];
     ptx::pdl_enter();
     if (blockIdx.x < a.a_blocks) {
-        const uint32_t kq_per_row = a.Kp >> 2;
-        for (uint32_t it = 0; it < 4; ++it) {
-            const uint64_t item = ((uint64_t)blockIdx.x * 4 + it) * 256 + threadIdx.x;
-            const uint32_t m = (uint32_t)(item / kq_per_row), kq = (uint32_t)(item % kq_per_row);
-            if (m >= a.Mp) return;
-            const uint32_t k = kq * 4;
-            uint32_t v[4];
-            const uint32_t* row = a.A + (uint64_t)m * a.lda;
+        // 16 consecutive k of one row per thread: four 16-byte loads in flight, one 16-byte store
+        // per limb plane
+        const uint32_t kh_per_row = a.Kp >> 4;
+        const uint64_t item = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+        const uint32_t m = (uint32_t)(item / kh_per_row), kh = (uint32_t)(item % kh_per_row), k = kh * 16;
+        if (m >= a.Mp) return;
+        uint4 v[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) v[t] = (m < a.M && k + t < a.K) ? row[k + t] : 0u;
-            for (int l = 0; l < a.L; ++l)
-                reinterpret_cast<uint32_t*>(a.outA + ((uint64_t)l * a.Mp + m) * a.Kp)[kq] =
-                    pack_limb(v[0], v[1], v[2], v[3], 8 * l);
+        for (int q = 0; q < 4; ++q) {
+            v[q] = make_uint4(0, 0, 0, 0);
+            const uint32_t kk = k + 4 * q;
+            if (m < a.M) {
+                const uint32_t* row = a.A + (uint64_t)m * a.lda + kk;
+                if (a.a_vec && kk + 3 < a.K) {
+                    v[q] = *reinterpret_cast<const uint4*>(row);
+                } else {
+                    v[q].x = kk < a.K ? row[0] : 0u;
+                    v[q].y = kk + 1 < a.K ? row[1] : 0u;
+                    v[q].z = kk + 2 < a.K ? row[2] : 0u;
+                    v[q].w = kk + 3 < a.K ? row[3] : 0u;
+                }
+            }
+        }
+        for (int l = 0; l < a.L; ++l) {
+            uint4 o;
+            o.x = pack_limb(v[0].x, v[0].y, v[0].z, v[0].w, 8 * l);
+            o.y = pack_limb(v[1].x, v[1].y, v[1].z, v[1].w, 8 * l);
+            o.z = pack_limb(v[2].x, v[2].y, v[2].z, v[2].w, 8 * l);
+            o.w = pack_limb(v[3].x, v[3].y, v[3].z, v[3].w, 8 * l);
+            *reinterpret_cast<uint4*>(a.outA + ((uint64_t)l * a.Mp + m) * a.Kp + k) = o;
         }
         return;
     }
     const uint32_t bid = blockIdx.x - a.a_blocks;
     const uint32_t k0 = (bid % a.b_kblocks) * 64, n0 = (bid / a.b_kblocks) * 64;
     const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-    for (uint32_t r = ty; r < 64; r += 4) {
-        const uint32_t k = k0 + r, n = n0 + tx;
-        tile[r][tx] = (k < a.K && n < a.N) ? a.B[(uint64_t)k * a.ldb + n] : 0u;
+    {
+        uint32_t v[16];  // all 16 loads of the thread in flight
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const uint32_t k = k0 + ty + 4 * q, n = n0 + tx;
+            v[q] = (k < a.K && n < a.N) ? a.B[(uint64_t)k * a.ldb + n] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) tile[ty + 4 * q][tx] = v[q];
     }
     __syncthreads();
-    for (uint32_t idx = threadIdx.x; idx < 64u * 16u * (uint32_t)a.L; idx += blockDim.x) {
-        const uint32_t wq = idx & 15, nn = (idx >> 4) & 63, l = idx >> 10;
-        const uint32_t n = n0 + nn;
-        const uint32_t kw = (k0 >> 2) + wq;
-        if (n >= a.Np || kw * 4 >= a.Kp) continue;
-        const uint32_t packed =
-            pack_limb(tile[wq * 4 + 0][nn], tile[wq * 4 + 1][nn], tile[wq * 4 + 2][nn], tile[wq * 4 + 3][nn], 8 * l);
+    // each item: 16 consecutive k of one column n, one limb plane -> one 16-byte store
+    for (uint32_t idx = threadIdx.x; idx < 64u * 4u * (uint32_t)a.L; idx += blockDim.x) {
+        const uint32_t g = idx & 3, nn = (idx >> 2) & 63, l = idx >> 8;
+        const uint32_t n = n0 + nn, kb = k0 + 16 * g;
+        if (n >= a.Np || kb >= a.Kp) continue;
+        uint4 o;
+        const uint32_t r0 = 16 * g;
+        o.x = pack_limb(tile[r0 + 0][nn], tile[r0 + 1][nn], tile[r0 + 2][nn], tile[r0 + 3][nn], 8 * l);
+        o.y = pack_limb(tile[r0 + 4][nn], tile[r0 + 5][nn], tile[r0 + 6][nn], tile[r0 + 7][nn], 8 * l);
+        o.z = pack_limb(tile[r0 + 8][nn], tile[r0 + 9][nn], tile[r0 + 10][nn], tile[r0 + 11][nn], 8 * l);
+        o.w = pack_limb(tile[r0 + 12][nn], tile[r0 + 13][nn], tile[r0 + 14][nn], tile[r0 + 15][nn], 8 * l);
         const uint64_t orow = (uint64_t)(n / a.NT) * a.L * a.NT + (uint64_t)l * a.NT + (n % a.NT);
-        reinterpret_cast<uint32_t*>(a.outB + orow * a.Kp)[kw] = packed;
+        *reinterpret_cast<uint4*>(a.outB + orow * a.Kp + kb) = o;
     }
 }
 
@@ -1020,7 +1048,8 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
             sa.outB = Bp;
             sa.L = L;
             sa.NT = NT;
-            sa.a_blocks = (uint32_t)ceil_div(Mp * (Kp / 4), 1024);
+            sa.a_blocks = (uint32_t)ceil_div(Mp * (Kp / 16), 256);
+            sa.a_vec = ((reinterpret_cast<uintptr_t>(sa.A) & 15) == 0 && (A.ld & 3) == 0) ? 1u : 0u;
             sa.b_kblocks = (uint32_t)ceil_div(Kp, 64);
             const size_t nblk = sa.a_blocks + (size_t)sa.b_kblocks * ceil_div(Np, 64);
             launch_k(split_kernel, dim3((unsigned)nblk), dim3(256), 0, st, sa);

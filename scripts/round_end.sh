@@ -15,6 +15,11 @@ python scripts/prof_gemm.py > gpurun_out/prof_gemm_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:modgemm -s 1 -c 1 -o gpurun_out/gemm_full python scripts/prof_gemm.py > gpurun_out/ncu_gemm.log 2>&1
 python scripts/ncu_summary.py gpurun_out/gemm_full.ncu-rep --label "fgemm 8192^3 C <- C - A*B mod 131071 (config 2)" \
   > gpurun_out/ncu_gemm_summary.json 2>/dev/null
+# the limb split (HBM-bound) of the 8192^3 fgemm operands
+ncu --set full --clock-control none -k regex:split_kernel -c 2 -o gpurun_out/split_full python scripts/prof_gemm.py \
+  > gpurun_out/ncu_split.log 2>&1
+python scripts/ncu_summary.py gpurun_out/split_full.ncu-rep --label "split_kernel: limb planes of the 8192^3 fgemm operands" \
+  > gpurun_out/ncu_split_summary.json 2>/dev/null
 # the panel schedule's latency-bound kernels in the middle of an n = 16384 PLUQ
 python scripts/prof_pluq.py --n 16384 > gpurun_out/prof_pluq_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"leaf_apply|panel_inv|panel_corner|rr_base_spec" \
