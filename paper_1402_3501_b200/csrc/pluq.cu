@@ -616,7 +616,7 @@ struct Driver {
     }
     // every operation on rows / columns < hi is enqueued (and joined into the critical stream)
     void band_done(size_t hi) {
-        if (!bands.on) return;
+        if (!bands.on || !bands.host) return;  // the device entry uses bands for lazy backups only
         while (bands.next_down < bands.end.size() && bands.end[bands.next_down] <= hi) {
             wait(bands.down, mark_event(b.st));
             for (cudaEvent_t e : deferred) wait(bands.down, e);
@@ -1075,8 +1075,7 @@ struct Driver {
         DView J = I;
         if (r3 > 0 && !I.empty()) {                              // :146, J = L3^-1 I into a temporary
             FFG_CUDA(cudaMallocAsync(&jbuf, I.rows * I.cols * 4, b.st));
-            FFG_CUDA(cudaMemcpy2DAsync(jbuf, I.cols * 4, I.d, I.ld * 4, I.cols * 4, I.rows, cudaMemcpyDeviceToDevice,
-                                       b.st));
+            copy_block_dev(b, I, DView{jbuf, I.rows, I.cols, I.cols});  // kernel: a DMA copy costs more latency
             J = DView{jbuf, I.rows, I.cols, I.cols};
             ptrsm(b, 0, r3s, L3, J);
         }
@@ -1310,7 +1309,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
     }
     if (!ok) {
-        FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, bk, n * 4, n * 4, n, cudaMemcpyDeviceToDevice, b.st));
+        copy_block_dev(b, DView{bk, n, n, n}, DView{d, n, n, n});
         b.ws.spec_failed();
     } else {
         b.ws.spec_fails = 0;
@@ -1322,17 +1321,22 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
     if (threshold <= 64 && spec_allowed(b, a, threshold)) {
         const size_t m = a.rows, n = a.cols;
+        const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
+        const bool panel = !no_panel && m == n;
+        // backup of the input for a failed guess: the panel schedule backs each band up lazily
+        // on a side stream right before its first use (bands, as the host entry); otherwise
+        // one copy up front
         uint32_t* bk = nullptr;
-        FFG_CUDA(cudaMallocAsync(&bk, m * n * 4, b.st));
-        FFG_CUDA(cudaMemcpy2DAsync(bk, n * 4, a.d, a.ld * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
+        const size_t ldb = panel ? a.ld : n;
+        FFG_CUDA(cudaMallocAsync(&bk, m * ldb * 4, b.st));
+        if (!panel) copy_block_dev(b, a, DView{bk, m, n, ldb});
         bool ok = false;
         size_t rank = 0;
         {
             Driver drv(b, threshold, m, n);
             drv.spec = true;
             *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
-            const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
-            drv.panel = !no_panel && m == n && std::min(m, n) > 0;
+            drv.panel = panel;
             drv.la_min = panel_lookahead_min();
             drv.corner_max = panel_corner_max();
             drv.prog_min = panel_prog_min();
@@ -1342,7 +1346,16 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             drv.pld = a.ld;
             drv.prows = m;
             drv.pcols = n;
-            if (drv.panel) drv.alloc_panel_inv();
+            if (drv.panel) {
+                drv.alloc_panel_inv();
+                const size_t T = std::max<size_t>(256, n / 16);
+                band_bounds(0, n, drv.thr, T, 256, drv.bands.end);
+                const cudaEvent_t start = drv.mark_event(b.st);  // the input is in place
+                drv.bands.uploaded.assign(drv.bands.end.size(), start);
+                drv.bands.backup = bk;
+                drv.bands.bks = b.ws.stream(302, 0);
+                drv.bands.on = true;
+            }
             try {
                 NodeRes res = drv.panel ? drv.rec_panel(a, 0) : drv.rec(a);
                 drv.flush_deferred();
@@ -1356,6 +1369,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             } catch (const Driver::SpecAbort&) {
                 ok = false;
             }
+            if (!ok && drv.panel) drv.need(drv.b.st, n);  // bands nothing touched yet are still pristine
             if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // all speculative work retired
         }
         static const bool log = getenv("FFG_SPEC_LOG") != nullptr;
@@ -1365,7 +1379,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             FFG_CUDA(cudaFreeAsync(bk, b.st));
             return rank;
         }
-        FFG_CUDA(cudaMemcpy2DAsync(a.d, a.ld * 4, bk, n * 4, n * 4, m, cudaMemcpyDeviceToDevice, b.st));
+        copy_block_dev(b, DView{bk, m, n, ldb}, a);  // a copy kernel: the DMA engines are far slower HBM to HBM
         FFG_CUDA(cudaFreeAsync(bk, b.st));
         b.ws.spec_failed();
     }
