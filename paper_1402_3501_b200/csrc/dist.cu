@@ -139,9 +139,9 @@ void dist_allgather(Dist& d, uint32_t* C, size_t rows, size_t cols, size_t ld, i
         const size_t w = axis == 0 ? cols : s.hi - s.lo, h = axis == 0 ? s.hi - s.lo : rows;
         const size_t pitch = axis == 0 ? cols : chunk;
         if (pack)
-            FFG_CUDA(cudaMemcpy2DAsync(buf, pitch * 4, win, ld * 4, w * 4, h, cudaMemcpyDeviceToDevice, st));
+            copy_2d_dev(win, ld, buf, pitch, h, w, st);
         else
-            FFG_CUDA(cudaMemcpy2DAsync(win, ld * 4, buf, pitch * 4, w * 4, h, cudaMemcpyDeviceToDevice, st));
+            copy_2d_dev(buf, pitch, win, ld, h, w, st);
     };
     if (d.virt) {
         // loopback: the same pack / unpack through the stage with the window wiped in between,

@@ -21,6 +21,10 @@
 
 namespace ffg {
 
+// rows x cols u32 copy between device buffers with leading dimensions (perm.cu: a copy kernel)
+void copy_2d_dev(const uint32_t* src, size_t lds, uint32_t* dst, size_t ldd, size_t rows, size_t cols,
+                 cudaStream_t st);
+
 struct Slice {
     size_t lo = 0, hi = 0;
 };

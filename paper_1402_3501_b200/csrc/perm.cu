@@ -258,6 +258,17 @@ __global__ void copy_block_kernel(const uint32_t* __restrict__ S, uint64_t lds, 
     }
 }
 
+void copy_2d_dev(const uint32_t* src, size_t lds, uint32_t* dst, size_t ldd, size_t rows, size_t cols,
+                 cudaStream_t st) {
+    if (!rows || !cols) return;
+    const bool vec = cols % 4 == 0 && lds % 4 == 0 && ldd % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    const uint64_t items = (uint64_t)rows * (vec ? cols / 4 : cols);
+    const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(items, 256), (uint64_t)148 * 4);
+    copy_block_kernel<<<grid, 256, 0, st>>>(src, lds, dst, ldd, (uint32_t)rows, (uint32_t)cols, vec ? 1u : 0u);
+    FFG_CUDA(cudaGetLastError());
+}
+
 void copy_block_dev(const Blas& b, DView src, DView dst) {
     if (src.empty()) return;
     const bool vec = src.cols % 4 == 0 && src.ld % 4 == 0 && dst.ld % 4 == 0 &&

@@ -807,8 +807,7 @@ void trsm_rec(const TrsmCtx& c, size_t o, size_t t, DView B) {
             FFG_CUDA(cudaMallocAsync(&tmp, B.rows * B.cols * 4, c.b.st));
             DView X{tmp, B.rows, B.cols, B.cols};
             c.b.gemm(1, B, inv, 0, X);
-            FFG_CUDA(cudaMemcpy2DAsync(B.d, B.ld * 4, tmp, B.cols * 4, B.cols * 4, B.rows, cudaMemcpyDeviceToDevice,
-                                       c.b.st));
+            copy_block_dev(c.b, X, B);
             FFG_CUDA(cudaFreeAsync(tmp, c.b.st));
         }
         return;
