@@ -1272,10 +1272,12 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         cudaEvent_t start = drv.b.ws.event();  // d and bk are allocated on the caller's stream
         FFG_CUDA(cudaEventRecord(start, b.st));
         for (cudaStream_t st : {up, down, bks}) drv.wait(st, start);
-        const size_t T = std::max<size_t>(256, n / 16);
+        static const size_t T_env = getenv("FFG_BAND_MAX") ? (size_t)atoll(getenv("FFG_BAND_MAX")) : 0;
+        static const size_t Tmin_env = getenv("FFG_BAND_MIN") ? (size_t)atoll(getenv("FFG_BAND_MIN")) : 256;
+        const size_t T = T_env ? T_env : std::max<size_t>(256, n / 16);
         // bands of 256 rows first (a narrower band's column strip is a 2-D copy of short rows,
         // which the copy engines move slowly: 128-row bands measured slower)
-        band_bounds(0, n, thr, T, 256, drv.bands.end);
+        band_bounds(0, n, thr, T, Tmin_env, drv.bands.end);
         drv.bands.on = true;
         drv.bands.host = host;
         drv.bands.ldh = lda;
