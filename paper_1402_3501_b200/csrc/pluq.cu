@@ -680,13 +680,18 @@ struct Driver {
         const size_t mr = std::min(thr, wr), mb = std::min(thr, hb);
         DView rmini = at(r0, beyond_c, t, mr), bmini = at(beyond_r, c0, mb, t);
         DView rrest = at(r0, beyond_c + mr, t, wr - mr), brest = at(beyond_r + mb, c0, hb - mb, t);
-        const bool both = !rmini.empty() && !bmini.empty();
-        const Blas side = both ? on(twin(depth)) : b;
         const cudaEvent_t f = mark_event(b.st);
-        if (both) wait(side.st, f);
-        panel_apply_dev(b, 0, inv, t, rmini);
-        panel_apply_dev(side, 1, inv, t, bmini, q);
-        if (both) wait(b.st, mark_event(side.st));
+        static const bool two = getenv("FFG_MINI_TWO") && atoi(getenv("FFG_MINI_TWO")) != 0;
+        if (two) {  // diagnostics: the two strip applies on two streams
+            const bool both = !rmini.empty() && !bmini.empty();
+            const Blas side = both ? on(twin(depth)) : b;
+            if (both) wait(side.st, f);
+            panel_apply_dev(b, 0, inv, t, rmini);
+            panel_apply_dev(side, 1, inv, t, bmini, q);
+            if (both) wait(b.st, mark_event(side.st));
+        } else {
+            panel_mini_dev(b, inv, t, rmini, bmini, q);  // one launch of small CTAs
+        }
         if (!rrest.empty()) {
             wait(sa.st, f);
             panel_apply_dev(sa, 0, inv, t, rrest);
@@ -722,7 +727,13 @@ struct Driver {
         leaves.push_back({c0, t1});
         if (!base_wrote_inv) panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
         flush_deferred();  // the node's rows / columns carry every earlier update
-        panel_corner_dev(b, a, t1, inv1, q1);
+        static const bool one_cta = getenv("FFG_CORNER_ONE") && atoi(getenv("FFG_CORNER_ONE")) != 0;
+        if (one_cta) {  // diagnostics: the one-CTA corner kernel
+            panel_corner_dev(b, a, t1, inv1, q1);
+        } else {  // A1's panel blocks inside the node, then R's update, each in small CTAs
+            panel_mini_dev(b, inv1, t1, a.sub(0, t1, t1, t2), a.sub(t1, 0, t2, t1), q1);
+            panel_update_dev(b, a.sub(t1, 0, t2, t1), a.sub(0, t1, t1, t2), a.sub(t1, t1, t2, t2));
+        }
         const cudaEvent_t f = mark_event(b.st);
         const Blas sa = on(side_stream(0)), sb = on(side_stream(1));
         wait(sa.st, f);

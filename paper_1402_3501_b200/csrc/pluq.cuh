@@ -36,6 +36,12 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
 void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv);
 void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DView B, const uint32_t* qperm = nullptr);
 
+// a leaf's next-block panels in one launch: X <- inv(L) X (t x w), Y <- Y[:, q] inv(U) (h x t)
+void panel_mini_dev(const Blas& b, const uint32_t* inv, size_t t, DView X, DView Y, const uint32_t* qperm);
+
+// C -= Y X for blocks <= 64 (small CTAs, 16 columns each)
+void panel_update_dev(const Blas& b, DView Y, DView X, DView C);
+
 // two-leaf node of the panel schedule: A1's panel blocks inside the node and R's update (see trsm.cu)
 void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv, const uint32_t* q);
 

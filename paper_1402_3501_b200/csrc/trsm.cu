@@ -601,6 +601,152 @@ void panel_apply_dev(const Blas& b, int side, const uint32_t* inv, size_t t, DVi
     b.count();
 }
 
+// The next block's columns and rows of a leaf's panels (X = inv(L) X, t x w and Y = Y[:, q] inv(U),
+// h x t; w, h <= 64) in one launch, 16 vectors per CTA: the right side's strips first, then the
+// bottom side's.  A thread owns one output row x 4 vectors; both inverses are triangular in the
+// output index (k <= i).  Small CTAs: this sits on the critical path between two base cases.
+constexpr int MV = 16;
+__global__ void __launch_bounds__(256) panel_mini_kernel(const uint32_t* __restrict__ inv, uint32_t d,
+                                                         uint32_t* __restrict__ X, uint64_t ldx, uint32_t w,
+                                                         uint32_t* __restrict__ Y, uint64_t ldy, uint32_t h,
+                                                         const uint32_t* __restrict__ qp, uint32_t p, uint64_t mu) {
+    __shared__ __align__(16) uint32_t Ct[64][68];  // Ct[k][i] = coefficient of x_k in output i
+    __shared__ __align__(16) uint32_t Bs[64][MV];  // Bs[k][v]
+    const uint32_t tid = threadIdx.x, nr = (w + MV - 1) / MV;
+    const bool right = blockIdx.x < nr;
+    const uint32_t v0 = (right ? blockIdx.x : blockIdx.x - nr) * MV, nvec = right ? w : h;
+    const uint32_t nv = min((uint32_t)MV, nvec - v0);
+    const uint32_t* invp = right ? inv : inv + d * d;
+    ptx::pdl_enter();
+    uint32_t rc[16], rb[4];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const uint32_t idx = tid + 256 * r, k = idx / 64, i = idx % 64;
+        rc[r] = (i < d && k < d) ? (right ? invp[i * d + k] : invp[k * d + i]) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t idx = tid + 256 * r, k = idx / MV, v = idx % MV;
+        rb[r] = 0u;
+        if (k < d && v < nv)
+            rb[r] = right ? X[(uint64_t)k * ldx + v0 + v] : Y[(uint64_t)(v0 + v) * ldy + (qp ? qp[k] : k)];
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const uint32_t idx = tid + 256 * r;
+        Ct[idx / 64][idx % 64] = rc[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t idx = tid + 256 * r;
+        Bs[idx / MV][idx % MV] = rb[r];
+    }
+    __syncthreads();
+    const uint32_t i = tid >> 2, vg = (tid & 3) * 4;
+    uint64_t acc[4] = {0, 0, 0, 0};
+    const uint32_t kend = min(d, i + 1);
+#pragma unroll 4
+    for (uint32_t k = 0; k < kend; ++k) {
+        const uint64_t c = Ct[k][i];
+        const uint4 x = *reinterpret_cast<const uint4*>(&Bs[k][vg]);
+        acc[0] += c * x.x;
+        acc[1] += c * x.y;
+        acc[2] += c * x.z;
+        acc[3] += c * x.w;
+    }
+    if (i < d) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t v = vg + q;
+            if (v >= nv) continue;
+            const uint32_t val = mod_u64(acc[q], p, mu);
+            if (right)
+                X[(uint64_t)i * ldx + v0 + v] = val;
+            else
+                Y[(uint64_t)(v0 + v) * ldy + i] = val;
+        }
+    }
+}
+
+void panel_mini_dev(const Blas& b, const uint32_t* inv, size_t t, DView X, DView Y, const uint32_t* qperm) {
+    const size_t w = X.empty() ? 0 : X.cols, h = Y.empty() ? 0 : Y.rows;
+    if (!w && !h) return;
+    if (t > 64 || w > 64 || h > 64) throw Error(FFG_ERR_INTERNAL, "panel_mini: blocks wider than 64");
+    const unsigned grid = (unsigned)(ceil_div(w, (size_t)MV) + ceil_div(h, (size_t)MV));
+    b.ws.prof.begin(b.st);
+    launch_k(panel_mini_kernel, dim3(grid), dim3(256), 0, b.st, inv, (uint32_t)t, X.d, X.ld, (uint32_t)w, Y.d, Y.ld,
+             (uint32_t)h, qperm, b.F.p, b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)t * (w + h));
+    b.count();
+}
+
+// C -= Y X (C h x w, Y h x t, X t x w; all <= 64), 16 columns of C per CTA: R's update inside a
+// two-leaf node, right after A1's panel blocks (panel_mini_kernel), in small CTAs.
+__global__ void __launch_bounds__(256) panel_update_kernel(const uint32_t* __restrict__ Y, uint64_t ldy,
+                                                           const uint32_t* __restrict__ X, uint64_t ldx,
+                                                           uint32_t* __restrict__ C, uint64_t ldc, uint32_t h,
+                                                           uint32_t t, uint32_t w, uint32_t p, uint64_t mu) {
+    __shared__ __align__(16) uint32_t Ys[64][65];  // Ys[i][k]
+    __shared__ __align__(16) uint32_t Xs[64][MV];  // Xs[k][v]
+    const uint32_t tid = threadIdx.x, v0 = blockIdx.x * MV, nv = min((uint32_t)MV, w - v0);
+    ptx::pdl_enter();
+    uint32_t ry[16], rx[4];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const uint32_t idx = tid + 256 * r, i = idx / 64, k = idx % 64;
+        ry[r] = (i < h && k < t) ? Y[(uint64_t)i * ldy + k] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t idx = tid + 256 * r, k = idx / MV, v = idx % MV;
+        rx[r] = (k < t && v < nv) ? X[(uint64_t)k * ldx + v0 + v] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const uint32_t idx = tid + 256 * r;
+        Ys[idx / 64][idx % 64] = ry[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t idx = tid + 256 * r;
+        Xs[idx / MV][idx % MV] = rx[r];
+    }
+    __syncthreads();
+    const uint32_t i = tid >> 2, vg = (tid & 3) * 4;
+    if (i >= h) return;
+    uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll 4
+    for (uint32_t k = 0; k < t; ++k) {
+        const uint64_t y = Ys[i][k];
+        const uint4 x = *reinterpret_cast<const uint4*>(&Xs[k][vg]);
+        acc[0] += y * x.x;
+        acc[1] += y * x.y;
+        acc[2] += y * x.z;
+        acc[3] += y * x.w;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t v = vg + q;
+        if (v >= nv) continue;
+        uint32_t* c = C + (uint64_t)i * ldc + v0 + v;
+        const uint32_t yx = mod_u64(acc[q], p, mu), cv = *c;
+        *c = cv >= yx ? cv - yx : cv + p - yx;
+    }
+}
+
+void panel_update_dev(const Blas& b, DView Y, DView X, DView C) {
+    if (C.empty() || Y.cols == 0) return;
+    if (C.rows > 64 || C.cols > 64 || Y.cols > 64 || Y.rows != C.rows || X.cols != C.cols || X.rows != Y.cols)
+        throw Error(FFG_ERR_INTERNAL, "panel_update: bad shapes");
+    b.ws.prof.begin(b.st);
+    launch_k(panel_update_kernel, dim3((unsigned)ceil_div(C.cols, (size_t)MV)), dim3(256), 0, b.st, Y.d, Y.ld, X.d,
+             X.ld, C.d, C.ld, (uint32_t)C.rows, (uint32_t)Y.cols, (uint32_t)C.cols, b.F.p, b.F.mu);
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * 64 * 64);
+    b.count();
+}
+
 // Corner of a two-leaf node of the panel schedule (A1 = rows/cols [0, t1), R = [t1, t1 + t2),
 // t1, t2 <= 64, A1 factored, its inverses in inv): X = inv(L1) A(A1, R) and Y = A(R, A1) inv(U1)
 // (A(R, A1) read through A1's column pivots q, may be null) are written back, and A(R, R) -= Y X,
