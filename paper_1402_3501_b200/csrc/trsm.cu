@@ -554,6 +554,19 @@ __global__ void __launch_bounds__(512) panel_inv_kernel(const uint32_t* __restri
         }
     }
     __syncthreads();
+    if (gridDim.x == 2) {  // one triangle per CTA, all 512 threads on it
+        uint32_t* Xc = Ts + 64 * PI_RS;
+        uint32_t* Wc = Xc + 64 * PI_RS;
+        uint32_t* dvc = Wc + 32 * 32;
+        if (blockIdx.x == 0)
+            tri_inverse_smem<false, 64>(Ts, PI_RS, Xc, PI_RS, Wc, dvc, t, p, mu);
+        else
+            tri_inverse_smem<true, 64>(Ts, PI_RS, Xc, PI_RS, Wc, dvc, t, p, mu);
+        __syncthreads();
+        uint32_t* out = inv + (size_t)blockIdx.x * t * t;
+        for (uint32_t idx = tid; idx < t * t; idx += 512) out[idx] = Xc[(idx / t) * PI_RS + idx % t];
+        return;
+    }
     if (half == 0)
         tri_inverse_part<false, 64>(Ts, PI_RS, X, PI_RS, W, dv, t, p, mu, lt, 256, 1);
     else
@@ -571,7 +584,8 @@ void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
         FFG_CUDA(cudaFuncSetAttribute(panel_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     b.ws.prof.begin(b.st);
-    launch_k(panel_inv_kernel, dim3(1), dim3(512), smem, b.st, T.d, T.ld, t, inv, b.F.p, b.F.mu);
+    static const bool one = getenv("FFG_INV_ONE_CTA") && atoi(getenv("FFG_INV_ONE_CTA")) != 0;
+    launch_k(panel_inv_kernel, dim3(one ? 1 : 2), dim3(512), smem, b.st, T.d, T.ld, t, inv, b.F.p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * t * t);
     b.count();
