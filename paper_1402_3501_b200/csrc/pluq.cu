@@ -846,7 +846,11 @@ struct Driver {
             const size_t A = r0 + m1, f = first_leaf(m - m1), E = r0 + m;
             need(b.st, E);
             const cudaEvent_t forked = mark_event(b.st);
-            gemm_sub(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
+            static const bool tc_corner = getenv("FFG_CORNER_TC") && atoi(getenv("FFG_CORNER_TC")) != 0;
+            if (tc_corner)
+                gemm_sub(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
+            else  // f x f x m1 in small CUDA-core CTAs: shorter than a tensor-core launch at this size
+                panel_update_dev(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
             const Blas sc = on(side_stream(2)), sd = on(side_stream(3));
             for (const Blas* sx : {&sc, &sd}) {
                 wait(sx->st, forked);

@@ -695,50 +695,55 @@ void panel_mini_dev(const Blas& b, const uint32_t* inv, size_t t, DView X, DView
     b.count();
 }
 
-// C -= Y X (C h x w, Y h x t, X t x w; all <= 64), 16 columns of C per CTA: R's update inside a
-// two-leaf node, right after A1's panel blocks (panel_mini_kernel), in small CTAs.
+// C -= Y X (C h x w with h, w <= 64; Y h x t, X t x w, any t: 64-deep chunks through shared
+// memory, one exact u64 sum per entry -- t <= 2^13 keeps it below 2^64 for p < 2^26), 16 columns
+// of C per CTA: R's update inside a two-leaf node and the corner of larger nodes, in small CTAs.
 __global__ void __launch_bounds__(256) panel_update_kernel(const uint32_t* __restrict__ Y, uint64_t ldy,
                                                            const uint32_t* __restrict__ X, uint64_t ldx,
                                                            uint32_t* __restrict__ C, uint64_t ldc, uint32_t h,
                                                            uint32_t t, uint32_t w, uint32_t p, uint64_t mu) {
-    __shared__ __align__(16) uint32_t Ys[64][65];  // Ys[i][k]
+    __shared__ __align__(16) uint32_t Ys[64][65];  // Ys[i][k] of the current chunk
     __shared__ __align__(16) uint32_t Xs[64][MV];  // Xs[k][v]
     const uint32_t tid = threadIdx.x, v0 = blockIdx.x * MV, nv = min((uint32_t)MV, w - v0);
-    ptx::pdl_enter();
-    uint32_t ry[16], rx[4];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const uint32_t idx = tid + 256 * r, i = idx / 64, k = idx % 64;
-        ry[r] = (i < h && k < t) ? Y[(uint64_t)i * ldy + k] : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const uint32_t idx = tid + 256 * r, k = idx / MV, v = idx % MV;
-        rx[r] = (k < t && v < nv) ? X[(uint64_t)k * ldx + v0 + v] : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        const uint32_t idx = tid + 256 * r;
-        Ys[idx / 64][idx % 64] = ry[r];
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const uint32_t idx = tid + 256 * r;
-        Xs[idx / MV][idx % MV] = rx[r];
-    }
-    __syncthreads();
     const uint32_t i = tid >> 2, vg = (tid & 3) * 4;
-    if (i >= h) return;
+    ptx::pdl_enter();
     uint64_t acc[4] = {0, 0, 0, 0};
+    for (uint32_t kc = 0; kc < t; kc += 64) {
+        const uint32_t kn = min(64u, t - kc);
+        uint32_t ry[16], rx[4];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t idx = tid + 256 * r, ii = idx / 64, k = idx % 64;
+            ry[r] = (ii < h && k < kn) ? Y[(uint64_t)ii * ldy + kc + k] : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t idx = tid + 256 * r, k = idx / MV, v = idx % MV;
+            rx[r] = (k < kn && v < nv) ? X[(uint64_t)(kc + k) * ldx + v0 + v] : 0u;
+        }
+        if (kc) __syncthreads();  // the previous chunk is consumed
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint32_t idx = tid + 256 * r;
+            Ys[idx / 64][idx % 64] = ry[r];
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t idx = tid + 256 * r;
+            Xs[idx / MV][idx % MV] = rx[r];
+        }
+        __syncthreads();
 #pragma unroll 4
-    for (uint32_t k = 0; k < t; ++k) {
-        const uint64_t y = Ys[i][k];
-        const uint4 x = *reinterpret_cast<const uint4*>(&Xs[k][vg]);
-        acc[0] += y * x.x;
-        acc[1] += y * x.y;
-        acc[2] += y * x.z;
-        acc[3] += y * x.w;
+        for (uint32_t k = 0; k < kn; ++k) {
+            const uint64_t y = Ys[i][k];
+            const uint4 x = *reinterpret_cast<const uint4*>(&Xs[k][vg]);
+            acc[0] += y * x.x;
+            acc[1] += y * x.y;
+            acc[2] += y * x.z;
+            acc[3] += y * x.w;
+        }
     }
+    if (i >= h) return;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = vg + q;
@@ -751,13 +756,13 @@ __global__ void __launch_bounds__(256) panel_update_kernel(const uint32_t* __res
 
 void panel_update_dev(const Blas& b, DView Y, DView X, DView C) {
     if (C.empty() || Y.cols == 0) return;
-    if (C.rows > 64 || C.cols > 64 || Y.cols > 64 || Y.rows != C.rows || X.cols != C.cols || X.rows != Y.cols)
+    if (C.rows > 64 || C.cols > 64 || Y.cols > 8192 || Y.rows != C.rows || X.cols != C.cols || X.rows != Y.cols)
         throw Error(FFG_ERR_INTERNAL, "panel_update: bad shapes");
     b.ws.prof.begin(b.st);
     launch_k(panel_update_kernel, dim3((unsigned)ceil_div(C.cols, (size_t)MV)), dim3(256), 0, b.st, Y.d, Y.ld, X.d,
              X.ld, C.d, C.ld, (uint32_t)C.rows, (uint32_t)Y.cols, (uint32_t)C.cols, b.F.p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
-    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * 64 * 64);
+    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * C.rows * C.cols * (double)Y.cols);
     b.count();
 }
 
