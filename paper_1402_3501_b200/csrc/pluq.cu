@@ -858,8 +858,21 @@ struct Driver {
             }
             deferred.clear();
             // (replicated when partitioned: only the critical stream issues collectives)
-            if (pcols > A + f) gemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
-            if (E > A + f) gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
+            // R's rows right of the corner in one GEMM (full row tiles), then the block below the
+            // corner (rows A+f..E, columns A..A+f)
+            static const bool split_hr = getenv("FFG_SPLIT_HR") && atoi(getenv("FFG_SPLIT_HR")) != 0;
+            if (split_hr) {
+                if (pcols > A + f) gemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
+                if (E > A + f) gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
+            } else {
+                if (pcols > A + f) gemm_sub(sc, at(A, c0, E - A, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, E - A, pcols - (A + f)));
+                if (E > A + f) {
+                    if (E - (A + f) <= 64)
+                        panel_update_dev(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, f), at(A + f, A, E - (A + f), f));
+                    else
+                        gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, f), at(A + f, A, E - (A + f), f));
+                }
+            }
             if (prows > E) gemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
             deferred.push_back(mark_event(sc.st));
             deferred.push_back(mark_event(sd.st));
