@@ -695,7 +695,7 @@ void panel_mini_dev(const Blas& b, const uint32_t* inv, size_t t, DView X, DView
     b.count();
 }
 
-// C -= Y X (C h x w with h, w <= 64; Y h x t, X t x w, any t: 64-deep chunks through shared
+// C -= Y X (C h x w with h <= 64, any w; Y h x t, X t x w, any t: 64-deep chunks through shared
 // memory, one exact u64 sum per entry -- t <= 2^13 keeps it below 2^64 for p < 2^26), 16 columns
 // of C per CTA: R's update inside a two-leaf node and the corner of larger nodes, in small CTAs.
 __global__ void __launch_bounds__(256) panel_update_kernel(const uint32_t* __restrict__ Y, uint64_t ldy,
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(256) panel_update_kernel(const uint32_t* __res
 
 void panel_update_dev(const Blas& b, DView Y, DView X, DView C) {
     if (C.empty() || Y.cols == 0) return;
-    if (C.rows > 64 || C.cols > 64 || Y.cols > 8192 || Y.rows != C.rows || X.cols != C.cols || X.rows != Y.cols)
+    if (C.rows > 64 || Y.cols > 8192 || Y.rows != C.rows || X.cols != C.cols || X.rows != Y.cols)
         throw Error(FFG_ERR_INTERNAL, "panel_update: bad shapes");
     b.ws.prof.begin(b.st);
     launch_k(panel_update_kernel, dim3((unsigned)ceil_div(C.cols, (size_t)MV)), dim3(256), 0, b.st, Y.d, Y.ld, X.d,
