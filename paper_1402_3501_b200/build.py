@@ -21,7 +21,7 @@ LIB = os.path.join(PKG, "libffg_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")] + os.environ.get("FFG_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -766,7 +766,10 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
 // column k).  Rows stay in registers (warp w owns rows w, w+16, w+32, w+48; lane l columns l and
 // l+32); the owner of row k+1 publishes it (reduced, with Shoup factors) right after its step-k
 // update into a double-buffered slot -- one barrier per pivot, no slab phases.
-constexpr int SP_WARPS = 16;
+#ifndef FFG_SP_WARPS
+#define FFG_SP_WARPS 16
+#endif
+constexpr int SP_WARPS = FFG_SP_WARPS;
 constexpr int SP_THREADS = SP_WARPS * 32;
 constexpr int SP_RPW = 64 / SP_WARPS;  // rows per warp
 
