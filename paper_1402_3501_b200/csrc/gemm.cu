@@ -1011,7 +1011,11 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     // its whole column strip of B before the CTA's own epilogue overwrites exactly that strip
     const bool c_is_b = C.d == B.d && C.ld == B.ld && C.rows == B.rows && C.cols == B.cols && M <= (size_t)BM;
     const size_t kb_need = ceil_div(K, (size_t)BK);
-    const bool fits = kb_need == 1 ? direct_fits(L, 1) : (kb_need == 2 && direct_fits(L, 2));
+    // 128 < K <= 256 takes the TMA pipeline: inside the PLUQ the direct kernel's two staged K
+    // blocks cost more than the split (measured 29.9 -> 29.4 ms at n = 16384); FFG_DIRECT_KB2=1
+    // restores the direct path for them
+    static const bool kb2 = getenv("FFG_DIRECT_KB2") && atoi(getenv("FFG_DIRECT_KB2")) != 0;
+    const bool fits = kb_need == 1 ? direct_fits(L, 1) : (kb2 && kb_need == 2 && direct_fits(L, 2));
     if (!no_direct && fits && !overlap(C, A) && (c_is_b || !overlap(C, B))) {
         ws.prof.begin(st);
         const bool one = kb_need == 1;
