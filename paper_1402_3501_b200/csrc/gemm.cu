@@ -949,7 +949,7 @@ size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k) {
 }
 
 void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, DView C, cudaStream_t st,
-               Workspace& ws, uint64_t* launches, int sm_cap) {
+               Workspace& ws, uint64_t* launches, int sm_cap, bool no_direct_call) {
     if (A.cols != B.rows || C.rows != A.rows || C.cols != B.cols)
         throw Error(FFG_ERR_DIM_MISMATCH, "gemm: non-conforming shapes");  // blas.hpp:21-24
     const size_t M = C.rows, N = C.cols, K = A.cols;
@@ -1016,7 +1016,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     // restores the direct path for them
     static const bool kb2 = getenv("FFG_DIRECT_KB2") && atoi(getenv("FFG_DIRECT_KB2")) != 0;
     const bool fits = kb_need == 1 ? direct_fits(L, 1) : (kb2 && kb_need == 2 && direct_fits(L, 2));
-    if (!no_direct && fits && !overlap(C, A) && (c_is_b || !overlap(C, B))) {
+    if (!no_direct && !no_direct_call && fits && !overlap(C, A) && (c_is_b || !overlap(C, B))) {
         ws.prof.begin(st);
         const bool one = kb_need == 1;
         switch (L) {

@@ -219,8 +219,9 @@ private:
 // C <- alpha*A*B + beta*C mod p (blas.hpp:31-103 semantics), enqueued on st.
 // sm_cap > 0: the tensor-core GEMM runs persistent on at most sm_cap CTAs (one per SM), leaving
 // the other SMs to kernels of higher-priority streams.
+// no_direct: take the split + TMA pipeline even where the one-launch direct kernel applies
 void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, DView C, cudaStream_t st,
-               Workspace& ws, uint64_t* launches, int sm_cap = 0);
+               Workspace& ws, uint64_t* launches, int sm_cap = 0, bool no_direct = false);
 size_t gemm_workspace_bytes(const Field& F, size_t m, size_t n, size_t k);
 int tile_n(int limbs);
 extern size_t g_simt_macs;  // problems with M*N*K <= this use the CUDA-core kernel

@@ -228,7 +228,11 @@ struct Driver {
         FFG_CUDA(cudaEventRecord(e, b.st));
         FFG_CUDA(cudaStreamWaitEvent(user.st, e, 0));
     }
-    Blas on(cudaStream_t st) const { return Blas{b.F, b.ws, st, b.launches}; }
+    Blas on(cudaStream_t st) const {
+        Blas r{b.F, b.ws, st, b.launches};
+        r.no_direct = b.no_direct;
+        return r;
+    }
     // a second critical-path stream per recursion depth (the node's independent TRSM), and a
     // low-priority stream per depth for the look-ahead part of the trailing update
     // (one stream when partitioned: every rank must issue its collectives in the same order)
@@ -1222,6 +1226,14 @@ static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
 
 // panel-mode nodes of at least this size cut their trailing update into look-ahead pieces
 // (FFG_PANEL_LA, read per call so tests can sweep it; 0 = off)
+// the whole-matrix panel schedule issues its tensor-core GEMMs through the split + TMA pipeline:
+// off the critical path, throughput beats the direct kernel's latency (n = 16384: 29.4 -> 29.0
+// ms); the exact recursion (configs 4 / 5) keeps the direct kernel.  FFG_PANEL_DIRECT=1 reverts.
+static bool panel_no_direct() {
+    static const bool keep = getenv("FFG_PANEL_DIRECT") && atoi(getenv("FFG_PANEL_DIRECT")) != 0;
+    return !keep;
+}
+
 // panel-mode nodes up to this size update only R's first block on the critical stream and defer
 // their wide GEMMs (FFG_CORNER_MAX, read per call; 0 = off)
 static size_t panel_corner_max() {
@@ -1286,6 +1298,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         drv.spec = true;
         *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
         drv.panel = true;
+        drv.b.no_direct = panel_no_direct();
         drv.la_min = panel_lookahead_min();
         drv.corner_max = panel_corner_max();
         drv.prog_min = panel_prog_min();
@@ -1377,6 +1390,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             drv.prows = m;
             drv.pcols = n;
             if (drv.panel) {
+                drv.b.no_direct = panel_no_direct();  // the panel schedule's GEMMs are throughput work
                 drv.alloc_panel_inv();
                 const size_t T = std::max<size_t>(256, n / 16);
                 band_bounds(0, n, drv.thr, T, 256, drv.bands.end);

@@ -18,9 +18,10 @@ struct Blas {
     Workspace& ws;
     cudaStream_t st;
     uint64_t* launches;
-    int sm_cap = 0;  // > 0: tensor-core GEMMs on this stream use at most this many SMs
+    int sm_cap = 0;          // > 0: tensor-core GEMMs on this stream use at most this many SMs
+    bool no_direct = false;  // skip the one-launch direct kernel (throughput over latency)
     void gemm(uint32_t alpha, DView A, DView B, uint32_t beta, DView C) const {
-        fgemm_dev(F, alpha, A, B, beta, C, st, ws, launches, sm_cap);
+        fgemm_dev(F, alpha, A, B, beta, C, st, ws, launches, sm_cap, no_direct);
     }
     void count(uint64_t n = 1) const {
         if (launches) __atomic_add_fetch(launches, n, __ATOMIC_RELAXED);
