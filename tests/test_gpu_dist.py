@@ -45,13 +45,15 @@ def test_virtual_world_matches_oracle(gpu, oracle_lib, world, loopback):
 
 
 @pytest.mark.parametrize("p", [251, 131071])
-def test_virtual_world_matches_single_gpu_large(gpu, p):
+def test_virtual_world_matches_single_gpu_large(gpu, p, monkeypatch):
     """n = 2048 rank-deficient and full-rank inputs: partitioned (4 virtual ranks, loopback,
     default min_work and a small one) vs the single-GPU path, bit for bit."""
     import torch
 
     G, ctx1 = gpu
     n = 2048
+    # generic (split) node GEMMs above 256: corner nodes' deferred GEMMs stay replicated
+    monkeypatch.setenv("FFG_CORNER_MAX", "256")
     for gen in ("iid", "lru"):
         d = torch.empty((n, n), dtype=torch.int32, device="cuda")
         if gen == "iid":
