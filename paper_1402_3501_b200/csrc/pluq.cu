@@ -1240,6 +1240,12 @@ static size_t panel_corner_max() {
     const char* e = getenv("FFG_CORNER_MAX");
     return e ? (size_t)atoll(e) : 4096;  // 1024 / 2048 / 4096 / 8192: 29.1 / 28.7 / 28.7 / 28.7 ms
 }
+// partitioned runs split the generic nodes' GEMMs over the ranks and keep the corner nodes'
+// deferred GEMMs replicated: keep more nodes generic there
+static size_t panel_corner_max(const Blas& b) {
+    const size_t c = panel_corner_max();
+    return (b.ws.dist.active() && !getenv("FFG_CORNER_MAX")) ? std::min<size_t>(c, 1024) : c;
+}
 
 // panel-mode nodes of at least this size apply their trailing update progressively in K-chunks
 // (FFG_PROG_MIN, read per call; 0 = off); FFG_PROG_CHUNKS chunks per node, FFG_PROG_SMS SM cap
@@ -1300,7 +1306,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         drv.panel = true;
         drv.b.no_direct = panel_no_direct();
         drv.la_min = panel_lookahead_min();
-        drv.corner_max = panel_corner_max();
+        drv.corner_max = panel_corner_max(b);
         drv.prog_min = panel_prog_min();
         drv.prog_nchunks = prog_chunks();
         drv.prog_sms = getenv("FFG_PROG_SMS") ? atoi(getenv("FFG_PROG_SMS")) : drv.lookahead_sms;
@@ -1381,7 +1387,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             *reinterpret_cast<volatile uint32_t*>(&drv.info_host->spec_fail) = 0u;
             drv.panel = panel;
             drv.la_min = panel_lookahead_min();
-            drv.corner_max = panel_corner_max();
+            drv.corner_max = panel_corner_max(b);
             drv.prog_min = panel_prog_min();
             drv.prog_nchunks = prog_chunks();
             drv.prog_sms = getenv("FFG_PROG_SMS") ? atoi(getenv("FFG_PROG_SMS")) : drv.lookahead_sms;
