@@ -161,6 +161,10 @@ struct Driver {
             }
             static const char* env = getenv("FFG_LOOKAHEAD_SMS");
             lookahead_sms = env ? atoi(env) : std::max(1, sms - 32);
+            static const char* ed = getenv("FFG_DEFER_SMS");
+            static const char* es = getenv("FFG_SIDE_SMS");
+            defer_sms = ed ? atoi(ed) : std::max(1, sms - 4);
+            side_sms = es ? atoi(es) : std::max(1, sms - 4);
         }
         uint32_t* dev = nullptr;
         // the base kernel writes rank + moved ranges straight into host-mapped memory
@@ -668,6 +672,10 @@ struct Driver {
     // leaves its wide GEMMs -- on side streams.  Their events are waited for right after the next
     // base case and its inverses (flush_deferred), before anything that reads wide regions.
     std::vector<cudaEvent_t> deferred;
+    // SM caps of the side streams' tensor-core GEMMs (persistent grids): the corner nodes'
+    // deferred GEMMs (FFG_DEFER_SMS) and a two-leaf node's wide updates (FFG_SIDE_SMS); 0 = none
+    // (persistent grids leaving 4 SMs free measured 28.7 -> 28.1 ms at n = 16384; 8 or 28 free: 28.2 / 29.2)
+    int defer_sms = -1, side_sms = -1;  // resolved in the constructor
     size_t corner_max = 0;
     void flush_deferred() {
         for (cudaEvent_t e : deferred) wait(b.st, e);
@@ -739,7 +747,8 @@ struct Driver {
             panel_update_dev(b, a.sub(t1, 0, t2, t1), a.sub(0, t1, t1, t2), a.sub(t1, t1, t2, t2));
         }
         const cudaEvent_t f = mark_event(b.st);
-        const Blas sa = on(side_stream(0)), sb = on(side_stream(1));
+        Blas sa = on(side_stream(0)), sb = on(side_stream(1));
+        sa.sm_cap = sb.sm_cap = side_sms;
         wait(sa.st, f);
         wait(sb.st, f);
         DView rightA{a.d + m, t1, pcols - (c0 + m), pld};       // A1 rows, columns beyond the node
@@ -855,7 +864,8 @@ struct Driver {
                 gemm_sub(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
             else  // f x f x m1 in small CUDA-core CTAs: shorter than a tensor-core launch at this size
                 panel_update_dev(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
-            const Blas sc = on(side_stream(2)), sd = on(side_stream(3));
+            Blas sc = on(side_stream(2)), sd = on(side_stream(3));
+            sc.sm_cap = sd.sm_cap = defer_sms;  // leave SMs for the critical stream's small kernels
             for (const Blas* sx : {&sc, &sd}) {
                 wait(sx->st, forked);
                 for (cudaEvent_t e : deferred) wait(sx->st, e);
