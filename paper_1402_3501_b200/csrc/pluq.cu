@@ -571,6 +571,10 @@ struct Driver {
     };
     std::vector<Piece> pieces;
     size_t la_min = 0;  // 0: off
+    size_t la_end = SIZE_MAX;  // ... and only for nodes ending at or before la_end
+    bool la_here(size_t r0, size_t m, size_t m1) const {
+        return la_min && m >= la_min && m - m1 > thr && r0 + m <= la_end;
+    }
     DView at(size_t r, size_t c, size_t rows, size_t cols) const {
         return DView{const_cast<uint32_t*>(proot) + r * pld + c, rows, cols, pld};
     }
@@ -853,7 +857,7 @@ struct Driver {
             need(b.st, r0 + m);
             flush_deferred();
             wait(b.st, g.last);  // [H | right panel] and the bottom panel are complete
-        } else if (corner_max && m <= corner_max && m - m1 > thr) {
+        } else if (corner_max && m <= corner_max && m - m1 > thr && !la_here(r0, m, m1)) {
             // corner: R's first base block gets its update now; the wide GEMMs of the node are
             // deferred to side streams (after the last leaf's deferred panels)
             const size_t A = r0 + m1, f = first_leaf(m - m1), E = r0 + m;
@@ -890,7 +894,7 @@ struct Driver {
             if (prows > E) gemm_sub(sd, at(E, c0, prows - E, n1), at(r0, A, m1, E - A), at(E, A, prows - E, E - A));
             deferred.push_back(mark_event(sc.st));
             deferred.push_back(mark_event(sd.st));
-        } else if (la_min && m >= la_min && m - m1 > thr) {
+        } else if (la_here(r0, m, m1)) {
             flush_deferred();
             const size_t A = r0 + m1, E = r0 + m;  // R's rows / columns
             const size_t e1 = A + thr;
@@ -898,13 +902,15 @@ struct Driver {
             cudaEvent_t forked = mark_event(b.st);
             Blas la = on(lookahead(depth));
             la.sm_cap = lookahead_sms;  // keep SMs free for the critical path
-            need(la.st, E);             // older pieces overlapping R
             wait(la.st, forked);
             wait(side.st, forked);
             piece(b, side, r0, m1, A, e1);
             wait(b.st, mark_event(side.st));
             for (size_t x = e1; x < E;) {
                 const size_t e = std::min(E, x + std::max(thr, x - A));
+                // the bands and older pieces this piece touches only: in the host entry later
+                // bands are still on their way over PCIe
+                need(la.st, e);
                 piece(la, la, r0, m1, x, e);
                 pieces.push_back(Piece{x, mark_event(la.st)});
                 x = e;
@@ -1316,6 +1322,18 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         drv.panel = true;
         drv.b.no_direct = panel_no_direct();
         drv.la_min = panel_lookahead_min();
+        {
+            // look-ahead pieces in the first half of the matrix, where the factorisation waits for
+            // the bands still crossing PCIe: R's first band starts as soon as it has arrived
+            // (n = 16384: e2e 42.4 -> 39.6 ms with nodes >= n/4 ending in the first half)
+            const char* e = getenv("FFG_HOST_LA");
+            const char* ee = getenv("FFG_HOST_LA_END");
+            const size_t hl = e ? (size_t)atoll(e) : (n / 4 >= 2048 ? n / 4 : 0);
+            if (hl && !drv.la_min) {  // an explicit FFG_PANEL_LA wins
+                drv.la_min = hl;
+                drv.la_end = ee ? (size_t)(atof(ee) * (double)n) : n / 2;
+            }
+        }
         drv.corner_max = panel_corner_max(b);
         drv.prog_min = panel_prog_min();
         drv.prog_nchunks = prog_chunks();
@@ -1329,8 +1347,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         cudaEvent_t start = drv.b.ws.event();  // d and bk are allocated on the caller's stream
         FFG_CUDA(cudaEventRecord(start, b.st));
         for (cudaStream_t st : {up, down, bks}) drv.wait(st, start);
-        static const size_t T_env = getenv("FFG_BAND_MAX") ? (size_t)atoll(getenv("FFG_BAND_MAX")) : 0;
-        static const size_t Tmin_env = getenv("FFG_BAND_MIN") ? (size_t)atoll(getenv("FFG_BAND_MIN")) : 256;
+        const size_t T_env = getenv("FFG_BAND_MAX") ? (size_t)atoll(getenv("FFG_BAND_MAX")) : 0;
+        const size_t Tmin_env = getenv("FFG_BAND_MIN") ? (size_t)atoll(getenv("FFG_BAND_MIN")) : 256;
         const size_t T = T_env ? T_env : std::max<size_t>(256, n / 16);
         // bands of 256 rows first (a narrower band's column strip is a 2-D copy of short rows,
         // which the copy engines move slowly: 128-row bands measured slower)

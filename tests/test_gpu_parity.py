@@ -369,6 +369,32 @@ def test_panel_lookahead_pieces_match_oracle(gpu, oracle_lib, la, n, thr, monkey
         ctx.close()
 
 
+@pytest.mark.parametrize("la,end", [("256", "0.5"), ("512", "1"), ("1024", "0.5")])
+@pytest.mark.parametrize("n,pivots", [(2048, False), (1537, False), (2048, True)])
+def test_host_entry_lookahead_matches_oracle(gpu, oracle_lib, la, end, n, pivots, monkeypatch):
+    """Streamed host entry with look-ahead pieces in the nodes of >= FFG_HOST_LA ending before
+    FFG_HOST_LA_END * n (each piece waits only for the bands it touches): bit-exact against the
+    oracle, column pivots inside and at the end of blocks included."""
+    G, _ = gpu
+    O = oracle_lib
+    p, thr = 131071, 64
+    A = O.random_mat(p, n, n, 31 + n)
+    if pivots:
+        A = _zero_schur_pivot(A, p, [70, 300, 700, 1100, 1400])
+    a_o, P_o, Q_o, r_o = O.pluq_tile_recursive(p, A, thr)
+    monkeypatch.setenv("FFG_HOST_LA", la)
+    monkeypatch.setenv("FFG_HOST_LA_END", end)
+    monkeypatch.setenv("FFG_BAND_MAX", "256")
+    ctx = G.Context(0)
+    try:
+        h = A.copy()
+        res = G.pluq_tile_recursive(p, h, thr, ctx=ctx)
+        assert res.rank == r_o and np.array_equal(h, a_o)
+        assert np.array_equal(res.P, P_o) and np.array_equal(res.Q, Q_o)
+    finally:
+        ctx.close()
+
+
 def _zero_schur_pivot(A, p, ks, seed=5):
     """Row k's first k+1 entries become a combination of rows 0..k-1 (the rest stays random): the
     Schur diagonal at k is zero and row k pivots on a later column -- a column rotation inside its
