@@ -778,8 +778,11 @@ constexpr int SP_RPW = 64 / SP_WARPS;  // rows per warp
 // columns not yet chosen (rr_base's rotations keep the remaining columns in original order), so
 // the kernel tracks physical pivot columns c_k and writes the block in logical (rotated) order,
 // with Q[t] = c_t.  Full rank implies P = identity.  Without allow_q any c_k != k fails the guess.
+// FULLB: a 64 x 64 block (every base case of a square matrix whose order is a multiple of 64):
+// the bounds checks fold away.
+template <bool FULLB>
 __global__ void __launch_bounds__(SP_THREADS, 1)
-    rr_base_spec_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t m, uint32_t n, uint32_t* __restrict__ Pd,
+    rr_base_spec_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t m_, uint32_t n_, uint32_t* __restrict__ Pd,
                         uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t p, uint64_t mu,
                         uint32_t seq, uint32_t allow_q) {
     __shared__ __align__(16) uint32_t buf[2][128];  // published pivot row: 64 values, 64 Shoup factors
@@ -790,6 +793,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
     __shared__ uint32_t fail;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t m = FULLB ? 64u : m_, n = FULLB ? 64u : n_;
     const uint32_t r = min(m, n);
     ptx::pdl_enter();
 
@@ -1047,8 +1051,12 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const bool no_slab = !spec && e_slab && atoi(e_slab) != 0;
     const char* e_spec = getenv("FFG_SPEC_SLAB");  // diagnostics: speculative launches on the slab kernel
     if (spec && lay.m <= 64 && lay.n <= 64 && !(e_spec && atoi(e_spec) != 0)) {
-        launch_k(rr_base_spec_kernel, dim3(1), dim3(SP_THREADS), 0, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd, info,
-                 b.F.p, b.F.mu, seq, (uint32_t)(allow_q && lay.m == lay.n));
+        if (lay.m == 64 && lay.n == 64)
+            launch_k(rr_base_spec_kernel<true>, dim3(1), dim3(SP_THREADS), 0, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd,
+                     info, b.F.p, b.F.mu, seq, (uint32_t)allow_q);
+        else
+            launch_k(rr_base_spec_kernel<false>, dim3(1), dim3(SP_THREADS), 0, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd,
+                     info, b.F.p, b.F.mu, seq, (uint32_t)(allow_q && lay.m == lay.n));
         FFG_CUDA(cudaGetLastError());
         b.ws.prof.end(b.st, PROF_BASE, 2.0 * lay.m * lay.n * 4, 2.0 * lay.rmax * (double)lay.m * lay.n);
         b.count();

@@ -1325,7 +1325,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         {
             // look-ahead pieces in the first half of the matrix, where the factorisation waits for
             // the bands still crossing PCIe: R's first band starts as soon as it has arrived
-            // (n = 16384: e2e 42.4 -> 39.6 ms with nodes >= n/4 ending in the first half)
+            // (n = 16384: e2e 42.4 -> 39.6 ms with nodes >= n/4 ending in the first half; the root
+            // included: 40.3 ms)
             const char* e = getenv("FFG_HOST_LA");
             const char* ee = getenv("FFG_HOST_LA_END");
             const size_t hl = e ? (size_t)atoll(e) : (n / 4 >= 2048 ? n / 4 : 0);
