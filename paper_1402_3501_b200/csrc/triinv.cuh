@@ -100,8 +100,43 @@ __device__ void tri_inverse_part(const uint32_t* S, int ss, uint32_t* X, int xs,
                                  uint32_t t, uint32_t p, uint64_t mu, uint32_t tid, uint32_t nth, uint32_t bar) {
     constexpr int LEAF = 8;
     for (uint32_t idx = tid; idx < (uint32_t)R * R; idx += nth) X[(idx / R) * xs + idx % R] = 0u;
-    for (uint32_t i = tid; i < (uint32_t)R; i += nth)
-        dinv[i] = (!UPPER || i >= t) ? 1u : inv_mod_bin(S[i * ss + i], p);  // no 64-bit divisions
+    if (!UPPER) {
+        for (uint32_t i = tid; i < (uint32_t)R; i += nth) dinv[i] = 1u;
+    } else if (tid < 32) {
+        // batch inversion of the diagonal in one warp, 64 entries (two per lane) per round:
+        // prefix products D_e = prod_{j<e} d_j, one inverse of the total, 1/d_e = D_e / D_{e+1} --
+        // one extended Euclid per 64 entries instead of 64 divergent ones
+        const uint32_t FULL = 0xffffffffu, lane = tid;
+        for (uint32_t o = 0; o < (uint32_t)R; o += 64) {
+            const uint32_t e0 = o + 2 * lane, e1 = e0 + 1;
+            const uint32_t v0 = (e0 < t && e0 < (uint32_t)R) ? S[e0 * ss + e0] : 1u % p;
+            const uint32_t v1 = (e1 < t && e1 < (uint32_t)R) ? S[e1 * ss + e1] : 1u % p;
+            uint32_t inc = mul_mod(v0, v1, p, mu);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t u = __shfl_up_sync(FULL, inc, off);
+                if (lane >= (uint32_t)off) inc = mul_mod(inc, u, p, mu);
+            }
+            uint32_t D0 = __shfl_up_sync(FULL, inc, 1);
+            if (lane == 0) D0 = 1u % p;
+            const uint32_t D1 = mul_mod(D0, v0, p, mu);
+            const uint32_t total = __shfl_sync(FULL, inc, 31);
+            const uint32_t tinv = __shfl_sync(FULL, lane == 0 ? inv_mod_bin(total, p) : 0u, 0);
+            uint32_t suf = mul_mod(v0, v1, p, mu);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t u = __shfl_down_sync(FULL, suf, off);
+                if (lane + off < 32) suf = mul_mod(suf, u, p, mu);
+            }
+            const uint32_t sufx = __shfl_down_sync(FULL, suf, 1);
+            const uint32_t iD2 = mul_mod(tinv, lane == 31 ? 1u % p : sufx, p, mu);  // 1 / D_{e0 + 2}
+            const uint32_t iD1 = mul_mod(iD2, v1, p, mu);                           // 1 / D_{e0 + 1}
+            // a zero diagonal entry (singular input; uniform) keeps the per-entry inverses (0 for it)
+            const bool sing = total == 0u;
+            if (e0 < (uint32_t)R) dinv[e0] = e0 >= t ? 1u : (sing ? inv_mod_bin(v0, p) : mul_mod(D0, iD1, p, mu));
+            if (e1 < (uint32_t)R) dinv[e1] = e1 >= t ? 1u : (sing ? inv_mod_bin(v1, p) : mul_mod(D1, iD2, p, mu));
+        }
+    }
     tri_bar(bar, nth);
     if (tid < (uint32_t)R) {  // leaves: thread per (leaf block, column)
         const uint32_t base = (tid / LEAF) * LEAF, j = tid % LEAF;
