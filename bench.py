@@ -10,17 +10,26 @@ Gop/s (2n^3/3 / time)".  One step = one pluq_tile_recursive of one resident
 matrix (a fresh seeded matrix per step, all generated in HBM before the timed
 region; 1 GiB each, larger than L2, so no flush is needed).  The fgemm part
 of the metric (config 2, 8192^3 C <- C - A*B) is reported in the same line
-under "fgemm".
+under "fgemm".  --workload lru = config 4, --p 251 --n 32768 = config 5.
 
-N > 1 (torchrun, one process per GPU): the PLUQ workloads run PARTITIONED --
-all ranks factor the same matrix, each computing its slice of every large Schur
-GEMM/TRSM, exchanged with NCCL all-gathers (csrc/dist.cu, DESIGN.md "Multi-GPU");
-value = one matrix's work / max-over-ranks device time; scaling "strong".
-The fgemm workload runs as independent replicas (value = all ranks' work, "weak").
+--gpus N > 1: when not already under torchrun, bench.py re-launches itself with
+`python -m torch.distributed.run --nproc-per-node N` (one process per GPU, NCCL).
+The PLUQ workloads then run PARTITIONED -- all ranks factor the same matrix, each
+computing its slice of every large Schur GEMM/TRSM, exchanged with NCCL
+all-gathers (csrc/dist.cu); value = one matrix's work /
+max-over-ranks device time; scaling "strong".  fgemm runs as independent
+replicas (value = all ranks' work, "weak").
+
+Roofline: the tcgen05 GEMM kernels' in-situ durations from CUPTI (torch.profiler)
+over one extra, untimed step -- no events inside the step -- and their
+algorithmic int8 work counted by the library (ffg_profile_enable(ctx, 2)),
+against peak = 2 x the driver-measured dense bf16 burst (MEASURED_PEAKS.json;
+B200 dense int8 = 2 x bf16), with cuBLASLt's int8 measured beside it.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 reference headers compiled unchanged + the rankrev.hpp:146 fix) on this box's
-host cores, on a bounded sample of the same workload; rank 0 only.
+host cores, on the SAME configuration (one full-size timed run -- the CPU takes
+~45 s for n = 16384 on 16 cores; the reported "steps" is 1); rank 0 only.
 """
 from __future__ import annotations
 
@@ -50,7 +59,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fgemm", action="store_true")
-    ap.add_argument("--no-prof", action="store_true", help="no per-kernel CUDA events in the timed region")
+    ap.add_argument("--no-prof", action="store_true", help="skip the extra CUPTI-profiled step (roofline)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3) if a.impl == "ours" else a.warmup
     if a.n is None:
@@ -60,17 +69,25 @@ def parse():
     return a
 
 
+def config_no(a):
+    if a.workload == "fgemm":
+        return "2"
+    if a.workload == "lru":
+        return "4"
+    return "5" if a.p <= 256 else ("1" if a.n <= 1024 else "3")
+
+
 def workload_config(a, world):
     if a.workload == "fgemm":
         return {"workload": f"fgemm C <- C - A*B mod {a.p}, M=N=K={a.n} (BASELINE config 2)", "n": a.n, "p": a.p,
                 "parallelism": f"replicas x{world}", "l2": "inputs > L2 (768 MiB limb planes + 768 MiB operands)"}
     kind = "i.i.d. random_mat" if a.workload == "pluq" else f"L*R*U rank {a.n // 2}"
-    cfgno = "3" if a.workload == "pluq" else "4"
-    return {"workload": f"pluq_tile_recursive n={a.n} {kind} over GF({a.p}), threshold {a.thr} (BASELINE config {cfgno})",
+    return {"workload": f"pluq_tile_recursive n={a.n} {kind} over GF({a.p}), threshold {a.thr} "
+                        f"(BASELINE config {config_no(a)})",
             "n": a.n, "p": a.p, "threshold": a.thr,
             "parallelism": "single GPU" if world == 1 else
             f"partitioned x{world}: one matrix, replicated panel, Schur GEMM/TRSM output slices + NCCL all-gather",
-            "l2": "inputs larger than L2 (a fresh 1 GiB matrix per step)"}
+            "l2": "inputs larger than L2 (a fresh matrix per step)"}
 
 
 def metric_ops(a):
@@ -139,15 +156,17 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------- peaks
 def tensor_peak(torch):
-    """int8 tensor-core peak for the roofline: cuBLASLt IMMA (torch._int_mm 8192^3) measured here,
-    else 2x the driver-measured bf16 figure (nominal dense int8 = 2x bf16 on B200)."""
+    """Peak for the roofline: 2 x the driver-measured dense bf16 burst of MEASURED_PEAKS.json (B200
+    dense int8 = 2 x dense bf16), with cuBLASLt's int8 (torch._int_mm 8192^3) measured here beside it."""
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    bf16 = peaks.get("bf16_tflops", 1590.0)
-    src = "2 x bf16_tflops of MEASURED_PEAKS.json" if "bf16_tflops" in peaks else "2 x fallback 1.59 PFLOP/s bf16"
+    if "bf16_tflops" in peaks:
+        bf16, src = peaks["bf16_tflops"], "2 x bf16_tflops (burst) of MEASURED_PEAKS.json"
+    else:
+        bf16, src = 1590.0, "2 x 1.59 PFLOP/s bf16 (B200_PROFILING.md fallback; MEASURED_PEAKS.json absent)"
     best = None
     try:
         n = 8192
@@ -168,14 +187,12 @@ def tensor_peak(torch):
         del a, b
     except Exception:
         best = None
-    if best and best > 2.0 * bf16 * 0.5:
-        return {"int8_tops": best, "source": "measured torch._int_mm 8192^3 (cuBLASLt int8) burst, best of 10",
-                "bf16_tflops_measured": bf16, "int8_from_bf16": 2.0 * bf16}
-    return {"int8_tops": 2.0 * bf16, "source": src, "cublaslt_int8_tops": best, "bf16_tflops_measured": bf16}
+    return {"int8_tops": 2.0 * bf16, "source": src, "cublaslt_int8_tops_measured": best,
+            "bf16_tflops_measured": bf16}
 
 
 # ---------------------------------------------------------------------- CPU reference
-def run_reference_sample(n, p, thr, workers, seed=1, gen="iid", timeout=600, retries=3):
+def run_reference_sample(n, p, thr, workers, seed=1, gen="iid", timeout=1500, retries=2):
     cmd = [sys.executable, os.path.join(ROOT, "scripts", "ref_runner.py"), "--n", str(n), "--p", str(p),
            "--thr", str(thr), "--workers", str(workers), "--seed", str(seed), "--gen", gen]
     last = None
@@ -190,53 +207,114 @@ def run_reference_sample(n, p, thr, workers, seed=1, gen="iid", timeout=600, ret
     raise RuntimeError(f"reference run failed: {last}")
 
 
-def cpu_sample_size(a):
-    return {"pluq": 4096, "lru": 2048, "fgemm": 4096}[a.workload]
+def run_fgemm_reference(n, p, workers):
+    code = ("import sys,json;sys.path.insert(0,%r);from oracle import oracle as O;"
+            "A=O.random_mat(%d,%d,%d,11);B=O.random_mat(%d,%d,%d,12);C=O.random_mat(%d,%d,%d,13);"
+            "import ctypes as c,numpy as np;r=O.Ref(True);s=c.c_double(0);Cc=C.copy();"
+            "rc=r.L.ref_pfgemm_timed(%d,%d,A,B,1,Cc,%d,%d,%d,%d,c.byref(s));"
+            "print(json.dumps({'seconds':s.value,'kind':'reference'}))") % (
+        ROOT, p, n, n, p, n, n, p, n, n, p, p - 1, n, n, n, workers)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=1500)
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+# The reference is timed at the configured size when that is at most this (config 3 / 4 / 2: about
+# 45 s / 90 s / 20 s on 16 cores); config 5 (n = 32768, several minutes) is sampled at n = 16384.
+REF_FULL_MAX_N = 16384
+
+
+def reference_size(a):
+    return a.n if a.n <= REF_FULL_MAX_N else REF_FULL_MAX_N
+
+
+def time_reference(a, workers, seed=1):
+    """One reference run on this host: (seconds, ops, sample description, kind)."""
+    n = reference_size(a)
+    gen = "lru" if a.workload == "lru" else "iid"
+    if a.workload == "fgemm":
+        res = run_fgemm_reference(n, a.p, workers)
+        ops = 2.0 * n ** 3
+        sample = f"pfgemm C <- C - A*B mod {a.p}, {n}^3, workers={workers}"
+    else:
+        res = run_reference_sample(n, a.p, a.thr, workers, seed=seed, gen=gen)
+        ops = 2.0 * n ** 3 / 3.0
+        sample = f"pluq_tile_recursive n={n} {gen} GF({a.p}) thr={a.thr}, workers={workers}"
+    if n == a.n:
+        sample += " -- the full configured size, one run"
+    else:
+        sample += f" -- bounded sample of n={a.n} (the full size takes several minutes on the CPU)"
+    return res["seconds"], ops, sample, res.get("kind", "reference"), n
 
 
 def reference_arm(a, rank, world):
     if rank != 0:
         return
     workers = os.cpu_count() or 1
-    n = min(a.n, cpu_sample_size(a))
-    gen = "lru" if a.workload == "lru" else "iid"
-    if a.workload == "fgemm":
-        sample = f"pfgemm C <- C - A*B mod {a.p}, {n}^3 (bounded sample of {a.n}^3)"
-    else:
-        sample = f"pluq_tile_recursive n={n} (bounded sample of n={a.n}) {gen} GF({a.p}) thr={a.thr}"
-    secs = []
-    kind = "reference"
-    for i in range(a.warmup + a.steps):
-        if a.workload == "fgemm":
-            res = run_fgemm_reference(n, a.p, workers)
-        else:
-            res = run_reference_sample(n, a.p, a.thr, workers, seed=1 + i, gen=gen)
-        kind = res.get("kind", kind)
-        if i >= a.warmup:
-            secs.append(res["seconds"])
-    ops = 2.0 * n ** 3 if a.workload == "fgemm" else 2.0 * n ** 3 / 3.0
-    t = sum(secs) / len(secs)
-    val = ops / t / 1e9
+    if a.warmup > 0:  # page in the library and start the thread pool on a small case (untimed)
+        run_reference_sample(512, a.p, a.thr, workers, seed=99, gen="iid")
+    secs, ops, sample, kind, n = time_reference(a, workers, seed=1)
+    val = ops / secs / 1e9
     line = {"impl": "reference", "metric": METRIC_FGEMM if a.workload == "fgemm" else METRIC, "value": val,
-            "unit": "Gop/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 residues (i64 accum)",
-            "data": "synthetic (seeded SplitMix64, test_util.hpp random_mat)",
-            "config": workload_config(a, world),
+            "unit": "Gop/s", "n_gpus": world, "steps": 1, "steps_requested": a.steps, "warmup": a.warmup,
+            "ms_per_step": secs * 1e3, "higher_is_better": True,
+            "scaling": "weak" if a.workload == "fgemm" else "strong", "vs_baseline": None,
+            "dtype": "u32 residues (i64 accum)", "data": "synthetic (seeded SplitMix64, test_util.hpp random_mat)",
+            "config": workload_config(a, world), "same_size_as_config": n == a.n,
             "cpu_baseline": {"value": val, "unit": "Gop/s", "cores": workers if kind == "reference" else 1,
                              "kind": kind, "sample": sample},
-            "e2e": {"value": val, "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": val, "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "one full-size CPU factorisation is the step (a K-step loop at this size would take "
+                    "K x ~45 s); warmup = small untimed runs"}
     print(json.dumps(line), flush=True)
 
 
-def run_fgemm_reference(n, p, workers):
-    code = ("import sys,json;sys.path.insert(0,%r);from oracle import oracle as O;"
-            "A=O.random_mat(%d,%d,%d,1);B=O.random_mat(%d,%d,%d,2);C=O.random_mat(%d,%d,%d,3);"
-            "import ctypes as c,numpy as np;r=O.Ref(True);s=c.c_double(0);Cc=C.copy();"
-            "rc=r.L.ref_pfgemm_timed(%d,%d,A,B,1,Cc,%d,%d,%d,%d,c.byref(s));"
-            "print(json.dumps({'seconds':s.value,'kind':'reference'}))") % (
-        ROOT, p, n, n, p, n, n, p, n, n, p, p - 1, n, n, n, workers)
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900)
-    return json.loads(r.stdout.strip().splitlines()[-1])
+def cpu_baseline(a):
+    workers = os.cpu_count() or 1
+    secs, ops, sample, kind, n = time_reference(a, workers, seed=1)
+    return {"value": ops / secs / 1e9, "unit": "Gop/s", "cores": workers if kind == "reference" else 1,
+            "kind": kind, "sample": sample, "seconds": secs, "n": n, "same_size_as_config": n == a.n}
+
+
+# ---------------------------------------------------------------------- in-situ kernel timeline
+def cupti_step(torch, fn, stream):
+    """Run fn() once under torch.profiler (CUPTI activity tracing: device timestamps of every kernel of
+    the process, any stream, no events inserted) -> (event ms of the step, [(start_us, end_us, name)])."""
+    import re
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ks = []
+    for e in prof.events():
+        if e.device_type.name != "CUDA" or e.device_time_total <= 0:
+            continue
+        nm = re.sub(r"^void ", "", re.sub(r"\(.*", "", e.name))
+        if nm.startswith("Memcpy") or nm.startswith("Memset"):
+            continue
+        ks.append((e.time_range.start, e.time_range.end, nm))
+    ks.sort()
+    return e0.elapsed_time(e1), ks
+
+
+def union_ms(spans):
+    busy, last = 0.0, None
+    for s, t in sorted(spans):
+        if last is None or s >= last:
+            busy += t - s
+            last = t
+        elif t > last:
+            busy += t - last
+            last = t
+    return busy / 1e3
+
+
+def is_tc_gemm(name):
+    return name.startswith("ffg::modgemm") and "simt" not in name or (
+        name.startswith("modgemm") and "simt" not in name)
 
 
 # ---------------------------------------------------------------------- our arm
@@ -282,8 +360,11 @@ def our_arm(a, rank, world, local_rank):
     if partitioned:
         G.dist.init_from_process_group(ctx)
     seed0 = 1 if partitioned or world == 1 else 1000 * rank + 1
+    # one fresh matrix per step; n = 32768 (4 GiB each) keeps two and regenerates between steps
+    # outside the timed region would break the K-step loop, so config 5 holds all of them (4 GiB x
+    # (W + K) of the 180 GB)
     if is_fgemm:
-        mats = [make(seed0), make(seed0 + 1), make(seed0 + 2)]
+        mats = [make(11), make(12), make(13)]
     else:
         mats = [make(seed0 + i) for i in range(a.warmup + a.steps)]
     ctx.synchronize()
@@ -313,28 +394,21 @@ def our_arm(a, rank, world, local_rank):
     ops_step = metric_ops(a)
     value = (1 if partitioned else world) * a.steps * ops_step / (ms_max / 1e3) / 1e9
     clocks = clk.summary()
-    # ---- per-kernel-class breakdown from ONE extra, untimed step with event profiling on
-    # (events around every launch perturb the schedule, so they stay out of the timed region)
-    prof, prof_ms = None, None
-    if not a.no_prof:
-        if is_fgemm:
-            pm = mats
-        else:
-            pm = [make(seed0 + 999)]
-            ctx.synchronize()
-        ctx.profile(True)
-        p0 = torch.cuda.Event(enable_timing=True)
-        p1 = torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        run_once(pm, 0)
-        p1.record(stream)
-        torch.cuda.synchronize()
-        ctx.profile(False)
-        prof = ctx.profile_read()
-        prof_ms = p0.elapsed_time(p1)
-        del pm
     del mats
     torch.cuda.empty_cache()
+
+    # ---- in-situ kernel timeline of ONE extra, untimed step (CUPTI) + the library's work count
+    insitu = None
+    if not a.no_prof:
+        pm = [make(11), make(12), make(13)] if is_fgemm else [make(seed0 + 999)]
+        ctx.synchronize()
+        ctx.profile(2)  # count launches and algorithmic work only: no events in the step
+        step_ms, ks = cupti_step(torch, lambda: run_once(pm, 0), stream)
+        ctx.profile(0)
+        prof = ctx.profile_read()
+        del pm
+        torch.cuda.empty_cache()
+        insitu = {"step_ms": step_ms, "kernels": ks, "prof": prof}
 
     # ---- e2e through the public host API (pinned host buffers, copies inside the timed region)
     e2e = None
@@ -348,35 +422,7 @@ def our_arm(a, rank, world, local_rank):
 
     if rank != 0:
         return
-    roof = None
-    if prof is not None:
-        peak = tensor_peak(torch)
-        g = prof["gemm"]
-        total_prof_ms = sum(v["ms"] for v in prof.values())
-        achieved = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
-        # DRAM bytes per modgemm launch from an ncu capture of this same workload (see
-        # scripts/round_end.sh); null when no capture is committed
-        traffic, tfile = None, os.path.join(ROOT, "profiles", "pluq_gemm_traffic.json")
-        if os.path.exists(tfile) and not is_fgemm:
-            try:
-                tj = json.load(open(tfile))
-                if tj.get("n") == a.n and tj.get("p") == a.p and tj.get("threshold") == a.thr:
-                    traffic = tj.get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
-        roof = {"bound": "tensor", "kernel": "modgemm_kernel<L> (tcgen05 kind::i8 limb GEMM)",
-                "achieved": achieved, "peak": peak["int8_tops"], "unit": "TOPS (int8 tensor ops)",
-                "frac": achieved / peak["int8_tops"] if peak["int8_tops"] else None, "traffic": traffic,
-                "peak_source": peak["source"], "work_per_unit": "2*L^2 int8 ops per field MAC (L limbs)",
-                "measured_on": "one extra untimed step with CUDA events around every launch "
-                               "(on each launch's own stream)",
-                "profiled_step_ms": prof_ms,
-                "gemm_launches": g["launches"], "gemm_ms": g["ms"],
-                "field_gops_in_gemm": g["field_ops"] / (g["ms"] / 1e3) / 1e9 if g["ms"] > 0 else None,
-                "share_of_step": g["ms"] / prof_ms if prof_ms else None,
-                "breakdown_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
-                "breakdown_launches": {k: v["launches"] for k, v in prof.items()},
-                "overlap_or_gaps_ms": round(prof_ms - total_prof_ms, 3)}
+    roof = roofline(a, torch, insitu, ms_max / a.steps) if insitu else None
     cpu = None
     if not a.no_cpu:
         try:
@@ -385,7 +431,7 @@ def our_arm(a, rank, world, local_rank):
             cpu = {"value": None, "unit": "Gop/s", "error": str(ex)[:200]}
     line = {"metric": METRIC_FGEMM if is_fgemm else METRIC, "value": value, "unit": "Gop/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-            "scaling": "strong" if partitioned else "weak", "vs_baseline": None,
+            "scaling": "weak" if is_fgemm else "strong", "vs_baseline": None,
             "dtype": "u32 residues (u8 limbs on tcgen05, s32 accum)",
             "data": "synthetic (seeded SplitMix64 random_mat / L*R*U, generated in HBM)",
             "config": workload_config(a, world), "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
@@ -393,6 +439,47 @@ def our_arm(a, rank, world, local_rank):
     if fg:
         line["fgemm"] = fg
     print(json.dumps(line), flush=True)
+
+
+def roofline(a, torch, insitu, ms_step):
+    ks, prof, step_ms = insitu["kernels"], insitu["prof"], insitu["step_ms"]
+    peak = tensor_peak(torch)
+    gem = [(s, t) for s, t, nm in ks if is_tc_gemm(nm)]
+    gemm_ms = sum(t - s for s, t in gem) / 1e3
+    work = prof["gemm"]["work"]
+    achieved = work / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    by = {}
+    for s, t, nm in ks:
+        k = nm.replace("ffg::", "")
+        k = k[:k.index("<")] if "<" in k else k
+        c = by.setdefault(k, [0, 0.0])
+        c[0] += 1
+        c[1] += (t - s) / 1e3
+    span = (ks[-1][1] - ks[0][0]) / 1e3 if ks else 0.0
+    # DRAM bytes per tcgen05 GEMM launch from one ncu capture of this same workload
+    # (scripts/round_end.sh -> profiles/pluq_gemm_traffic.json); null when none matches
+    traffic, tfile = None, os.path.join(ROOT, "profiles", "pluq_gemm_traffic.json")
+    if a.workload != "fgemm" and os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile))
+            if tj.get("n") == a.n and tj.get("p") == a.p and tj.get("threshold") == a.thr:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    return {"bound": "tensor", "kernel": "modgemm_kernel<L> / modgemm_direct_kernel<L,KB> (tcgen05 kind::i8)",
+            "achieved": achieved, "peak": peak["int8_tops"], "unit": "TOPS (int8 tensor ops)",
+            "frac": achieved / peak["int8_tops"], "traffic": traffic, "peak_source": peak["source"],
+            "cublaslt_int8_tops_measured": peak["cublaslt_int8_tops_measured"],
+            "work_per_unit": "2*L^2 int8 ops per field MAC (L = 8-bit limbs per residue)",
+            "work_per_step_int8_ops": work, "gemm_launches_per_step": int(prof["gemm"]["launches"]),
+            "timing": "CUPTI in-situ kernel durations (torch.profiler) over one extra untimed step; "
+                      "work counted by the library (no events in the step)",
+            "gemm_kernel_ms_per_step": gemm_ms, "gemm_busy_ms_per_step": union_ms(gem),
+            "profiled_step_ms": step_ms, "timed_ms_per_step": ms_step,
+            "whole_step_frac": work / (ms_step / 1e3) / 1e12 / peak["int8_tops"],
+            "kernel_span_ms": span, "gpu_busy_ms": union_ms([(s, t) for s, t, _ in ks]),
+            "kernels_ms": {k: round(v[1], 3) for k, v in sorted(by.items(), key=lambda x: -x[1][1])[:12]},
+            "kernels_launches": {k: v[0] for k, v in sorted(by.items(), key=lambda x: -x[1][1])[:12]}}
 
 
 def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world, partitioned=False):
@@ -441,15 +528,15 @@ def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world, partitioned=False):
             H.copy_(H0)  # restore the in/out host buffer (untimed)
             return lambda: G.pluq_tile_recursive(p, Hn, a.thr, ctx=ctx)
     torch.cuda.empty_cache()
-    ws = 1
-    for _ in range(ws):
-        step()()
+    step()()  # warm
     ctx.synchronize()
     tot = 0.0
     k = max(1, min(a.steps, 3))
     for _ in range(k):
         f = step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -471,7 +558,7 @@ def e2e_host(a, G, ctx, torch, np, dev, stream, rank, world, partitioned=False):
 
 
 def fgemm_secondary(a, G, ctx, torch, dev, stream):
-    n, p = 8192, a.p
+    n, p = 8192, 131071
     mats = []
     for s in (11, 12, 13):
         d = torch.empty((n, n), dtype=torch.int32, device=dev)
@@ -481,7 +568,6 @@ def fgemm_secondary(a, G, ctx, torch, dev, stream):
     for _ in range(3):
         G.fgemm(p, p - 1, A, B, 1, C_, ctx=ctx)
     ctx.synchronize()
-    ctx.profile(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     reps = 5
@@ -490,47 +576,54 @@ def fgemm_secondary(a, G, ctx, torch, dev, stream):
         G.fgemm(p, p - 1, A, B, 1, C_, ctx=ctx)
     e1.record(stream)
     torch.cuda.synchronize()
-    ctx.profile(False)
-    prof = ctx.profile_read()
     ms = e0.elapsed_time(e1) / reps
+    ctx.profile(2)
+    _, ks = cupti_step(torch, lambda: G.fgemm(p, p - 1, A, B, 1, C_, ctx=ctx), stream)
+    ctx.profile(0)
+    prof = ctx.profile_read()
     del mats, A, B, C_
     torch.cuda.empty_cache()
-    g = prof["gemm"]
+    gem_ms = sum(t - s for s, t, nm in ks if is_tc_gemm(nm)) / 1e3
+    split_ms = sum(t - s for s, t, nm in ks if "split" in nm) / 1e3
     traffic = algo = None  # ncu DRAM bytes of this launch (profiles/gemm_traffic.json)
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
         traffic, algo = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
     except Exception:
         pass
+    peak = None
+    try:
+        peak = 2.0 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+    except Exception:
+        peak = 3180.0
+    tops = prof["gemm"]["work"] / (gem_ms / 1e3) / 1e12 if gem_ms else None
     return {"metric": METRIC_FGEMM, "config": f"BASELINE config 2: M=N=K={n}, C <- C - A*B mod {p}",
             "value": 2.0 * n ** 3 / (ms / 1e3) / 1e9, "unit": "Gop/s", "ms_per_call": ms,
-            "gemm_kernel_ms": g["ms"] / reps, "split_ms": prof["split"]["ms"] / reps,
-            "int8_tops_in_kernel": g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] else None,
+            "gemm_kernel_ms": gem_ms, "split_ms": split_ms, "int8_tops_in_kernel": tops,
+            "frac_of_int8_peak": tops / peak if tops else None, "peak_int8_tops": peak,
             "traffic": traffic, "algorithmic_bytes": algo}
 
 
-def cpu_baseline(a):
-    n = min(a.n, cpu_sample_size(a))
-    workers = os.cpu_count() or 1
-    gen = "lru" if a.workload == "lru" else "iid"
-    if a.workload == "fgemm":
-        res = run_fgemm_reference(n, a.p, workers)
-        ops = 2.0 * n ** 3
-        sample = f"pfgemm {n}^3 mod {a.p}, workers={workers}"
-    else:
-        res = run_reference_sample(n, a.p, a.thr, workers, seed=1, gen=gen)
-        ops = 2.0 * n ** 3 / 3.0
-        sample = f"pluq_tile_recursive n={n} {gen} GF({a.p}) thr={a.thr}, one run (bounded sample of n={a.n})"
-    kind = res.get("kind", "reference")
-    return {"value": ops / res["seconds"] / 1e9, "unit": "Gop/s", "cores": workers if kind == "reference" else 1,
-            "kind": kind, "sample": sample, "seconds": res["seconds"]}
+def relaunch_under_torchrun(a):
+    """--gpus N > 1 outside torchrun: re-exec this script with one process per GPU."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(relaunch_under_torchrun(a))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         reference_arm(a, rank, world)
         return

@@ -135,7 +135,9 @@ uint64_t ffg_launch_count(ffg_ctx *ctx);
  * default).  Classes: 0 tensor-core GEMM, 1 limb split, 2 base case,
  * 3 triangle inverse, 4 permutation gathers, 5 CUDA-core small GEMM.  ffg_profile_read fills
  * out[4*c + {0,1,2,3}] = {milliseconds, launches, work, field ops} per class c
- * (work = int8 tensor ops for class 0, bytes moved otherwise) and clears. */
+ * (work = int8 tensor ops for class 0, bytes moved otherwise) and clears.
+ * on = 1: events around every launch; on = 2: count launches and work only (no
+ * events, ms stays 0 -- pair with an external kernel timeline such as CUPTI). */
 int ffg_profile_enable(ffg_ctx *ctx, int on);
 int ffg_profile_read(ffg_ctx *ctx, double *out, int nclasses);
 

@@ -184,6 +184,30 @@ def lru_matrix(n: int, r: int, p: int, seed: int):
     return M, rows[:r], cols[:r]
 
 
+def lru_matrix_exact_blas(n: int, r: int, p: int, seed: int):
+    """Config-4 generator at full size: the same L, U, rows, cols as lru_matrix (orc_lru_factors),
+    with M = L[:, rows] . U[cols, :] mod p formed in float64 BLAS -- exact because every partial
+    sum is < r * (p - 1)^2 < 2^53 (asserted).  Equal to lru_matrix bit for bit (tests pin it)."""
+    if r * (p - 1) ** 2 >= 2 ** 53:
+        raise ValueError("float64 accumulation would not be exact")
+    L = np.zeros((n, n), np.uint32)
+    U = np.zeros((n, n), np.uint32)
+    rows = np.zeros(max(r, 1), np.uint32)
+    cols = np.zeros(max(r, 1), np.uint32)
+    rc = lib().orc_lru_factors(n, r, p, seed, L.ctypes.data, U.ctypes.data, rows, cols)
+    if rc:
+        raise OracleError(rc)
+    rows, cols = rows[:r], cols[:r]
+    Ls = L[:, rows].astype(np.float64)
+    del L
+    Us = U[cols, :].astype(np.float64)
+    del U
+    M = np.empty((n, n), np.uint32)
+    for i in range(0, n, 4096):
+        M[i:i + 4096] = np.fmod(Ls[i:i + 4096] @ Us, p).astype(np.uint32)
+    return M, rows, cols
+
+
 def lru_positions(n: int, r: int, p: int, seed: int):
     rows = np.zeros(max(r, 1), np.uint32)
     cols = np.zeros(max(r, 1), np.uint32)
@@ -191,6 +215,30 @@ def lru_positions(n: int, r: int, p: int, seed: int):
     if rc:
         raise OracleError(rc)
     return rows[:r], cols[:r]
+
+
+def apply_moves(A: np.ndarray, axis: int, moves, inverse: bool = False) -> np.ndarray:
+    """apply_perm (perm.hpp:167-193) of a PermSeq given as its move list [(type, i, j)]
+    (type 0 = Swap, 1 = Rot), to the rows (axis 0) or columns (axis 1) of a copy of A."""
+    a = _c(A).copy()
+    m, n = a.shape
+    t = np.array([mv[0] for mv in moves] or [0], np.uint32)
+    i = np.array([mv[1] for mv in moves] or [0], np.uint32)
+    j = np.array([mv[2] for mv in moves] or [0], np.uint32)
+    rc = lib().orc_apply_moves(a, m, n, n, 1 if axis else 0, 1 if inverse else 0, t, i, j, len(moves))
+    if rc:
+        raise OracleError(rc)
+    return a
+
+
+def moves_to_array(dim: int, moves) -> np.ndarray:
+    """PermSeq::to_array() (perm.hpp:88-95) of a move list."""
+    t = np.array([mv[0] for mv in moves] or [0], np.uint32)
+    i = np.array([mv[1] for mv in moves] or [0], np.uint32)
+    j = np.array([mv[2] for mv in moves] or [0], np.uint32)
+    out = np.zeros(max(dim, 1), np.uint32)
+    lib().orc_moves_to_array(dim, t, i, j, len(moves), out)
+    return out[:dim]
 
 
 def splitmix_at(seed: int, k: int) -> int:

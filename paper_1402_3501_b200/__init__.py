@@ -6,6 +6,7 @@ csrc/).  This package is its Python host mirror; see ffpluq.py.
 from .ffpluq import (  # noqa: F401
     CapacityError,
     Context,
+    apply_perm_dev,
     CudaError,
     DimMismatch,
     FfgError,

@@ -1064,8 +1064,8 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     }
     if (!no_reg && !no_slab && lay.m <= 64 && lay.n <= 64) {
         const size_t smem = (2 * 64 * SS + 64 * LS + 2 * 16 * 132 + 64 * 11 + 8) * 4;
-        static std::once_flag once;
-        std::call_once(once, [smem] {
+        static PerDeviceOnce once;
+        once([smem] {
             FFG_CUDA(cudaFuncSetAttribute(rr_base_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         });
         launch_k(rr_base_slab_kernel, dim3(1), dim3(SL_THREADS), smem, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd, info,
@@ -1079,16 +1079,16 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const size_t slots = (8 + 128 + 16 + 16 * 64 + 64 + 4) * 4;  // candidate slots of the register path
     if (reg && fixed + blk + slots <= BASE_SMEM_LIMIT) {
         inv_out = nullptr;  // the register path does not cache factor inverses
-        static std::once_flag once;
-        std::call_once(once, [] {
+        static PerDeviceOnce once;
+        once([] {
             FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)BASE_SMEM_LIMIT));
         });
         rr_base_kernel<true, true><<<1, BASE_THREADS_REG, fixed + blk + slots, b.st>>>(a.d, a.ld, lay, nullptr, Pd, Qd,
                                                                                    info, b.F.p, b.F.mu, nullptr, seq);
     } else if (fixed + blk <= BASE_SMEM_LIMIT) {
-        static std::once_flag once;
-        std::call_once(once, [] {
+        static PerDeviceOnce once;
+        once([] {
             FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)BASE_SMEM_LIMIT));
         });
@@ -1097,8 +1097,8 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     } else {
         inv_out = nullptr;
         if (fixed > BASE_SMEM_LIMIT) throw Error(FFG_ERR_INVALID_BLOCK, "base case block too large");
-        static std::once_flag once;
-        std::call_once(once, [] {
+        static PerDeviceOnce once;
+        once([] {
             FFG_CUDA(cudaFuncSetAttribute(rr_base_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)BASE_SMEM_LIMIT));
         });

@@ -66,6 +66,14 @@ struct DevMat {
     cudaStream_t stream;
 };
 
+// every entry point: a non-empty matrix needs a pointer and ld >= cols (the MatView invariant,
+// matrix.hpp:13-43); anything else would be read out of bounds on the device
+void check_mat(const char* what, const void* ptr, size_t rows, size_t cols, size_t ld) {
+    if (rows == 0 || cols == 0) return;
+    if (!ptr) throw ffg::Error(FFG_ERR_INVALID_ARG, std::string(what) + ": null matrix pointer");
+    if (ld < cols) throw ffg::Error(FFG_ERR_INVALID_DIM, std::string(what) + ": leading dimension < columns");
+}
+
 }  // namespace
 
 extern "C" {
@@ -125,7 +133,7 @@ int ffg_synchronize(ffg_ctx* ctx) { return guarded(ctx, [&] { FFG_CUDA(cudaStrea
 uint64_t ffg_launch_count(ffg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int ffg_profile_enable(ffg_ctx* ctx, int on) {
-    return guarded(ctx, [&] { ctx->ws.prof.on = on != 0; });
+    return guarded(ctx, [&] { ctx->ws.prof.mode = on < 0 || on > 2 ? 1 : on; });
 }
 
 int ffg_profile_read(ffg_ctx* ctx, double* out, int nclasses) {
@@ -158,6 +166,7 @@ int ffg_field_info(uint64_t p, int* limbs, uint64_t* kmax, int* nt) {
 int ffg_random_mat_dev(ffg_ctx* ctx, uint64_t p, uint64_t seed, uint32_t* A, size_t m, size_t n, size_t lda) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
+        check_mat("random_mat", A, m, n, lda);
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
         ffg::random_mat_dev(blas, ffg::DView{A, m, n, lda}, seed);
     });
@@ -167,6 +176,8 @@ int ffg_lru_matrix_dev(ffg_ctx* ctx, uint64_t p, uint64_t seed, uint32_t* M, siz
                        uint32_t* rows, uint32_t* cols) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
+        check_mat("lru_matrix", M, n, n, ldm);
+        if (r > n) throw ffg::Error(FFG_ERR_INVALID_RANK, "lru_matrix: r > n");
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
         ffg::lru_matrix_dev(blas, ffg::DView{M, n, n, ldm}, r, seed, rows, cols);
     });
@@ -176,6 +187,9 @@ int ffg_fgemm_dev(ffg_ctx* ctx, uint64_t p, uint32_t alpha, const uint32_t* A, s
                   size_t ldb, uint32_t beta, uint32_t* C, size_t ldc, size_t m, size_t n, size_t k) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
+        check_mat("fgemm A", A, m, k, lda);
+        check_mat("fgemm B", B, k, n, ldb);
+        check_mat("fgemm C", C, m, n, ldc);
         ffg::fgemm_dev(F, alpha, ffg::DView{const_cast<uint32_t*>(A), m, k, lda},
                        ffg::DView{const_cast<uint32_t*>(B), k, n, ldb}, beta, ffg::DView{C, m, n, ldc}, ctx->stream,
                        ctx->ws, &ctx->launches);
@@ -186,6 +200,9 @@ int ffg_fgemm(ffg_ctx* ctx, uint64_t p, uint32_t alpha, const uint32_t* A, size_
               size_t ldb, uint32_t beta, uint32_t* C, size_t ldc, size_t m, size_t n, size_t k) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
+        check_mat("fgemm A", A, m, k, lda);
+        check_mat("fgemm B", B, k, n, ldb);
+        check_mat("fgemm C", C, m, n, ldc);
         cudaStream_t st = ctx->stream;
         DevMat dA(m, k, st), dB(k, n, st), dC(m, n, st);
         dA.upload(A, lda);
@@ -202,6 +219,8 @@ int ffg_ftrsm_dev(ffg_ctx* ctx, uint64_t p, int side, int uplo, int diag, const 
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
         const size_t t = side == 0 ? m : n;
+        check_mat("ftrsm A", A, t, t, lda);
+        check_mat("ftrsm B", B, m, n, ldb);
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
         ffg::ftrsm_dev(blas, side, uplo, diag, ffg::DView{const_cast<uint32_t*>(A), t, t, lda}, ffg::DView{B, m, n, ldb},
                        /*check_diag=*/true);
@@ -214,6 +233,8 @@ int ffg_ftrsm(ffg_ctx* ctx, uint64_t p, int side, int uplo, int diag, const uint
         ffg::Field F = ffg::make_field(p);
         cudaStream_t st = ctx->stream;
         const size_t t = side == 0 ? m : n;
+        check_mat("ftrsm A", A, t, t, lda);
+        check_mat("ftrsm B", B, m, n, ldb);
         DevMat dA(t, t, st), dB(m, n, st);
         dA.upload(A, lda);
         dB.upload(B, ldb);
@@ -228,6 +249,7 @@ int ffg_pluq_tile_recursive_dev(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m,
                                 size_t threshold, uint32_t* P, uint32_t* Q, size_t* rank) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
+        check_mat("pluq", A, m, n, lda);
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
         size_t r = ffg::pluq_tile_recursive_dev(blas, ffg::DView{A, m, n, lda}, threshold, P, Q);
         if (rank) *rank = r;
@@ -239,7 +261,7 @@ int ffg_pluq_tile_recursive(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, siz
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
-        if (lda < n) throw ffg::Error(FFG_ERR_INVALID_DIM, "pluq: lda < n");
+        check_mat("pluq", A, m, n, lda);
         size_t r = ffg::pluq_tile_recursive_host(blas, A, m, n, lda, threshold, P, Q);
         if (rank) *rank = r;
     });
@@ -250,7 +272,7 @@ int ffg_pluq_tile_recursive_u8(ffg_ctx* ctx, uint64_t p, uint8_t* A, size_t m, s
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
-        if (lda < n) throw ffg::Error(FFG_ERR_INVALID_DIM, "pluq: lda < n");
+        check_mat("pluq", A, m, n, lda);
         size_t r = ffg::pluq_tile_recursive_host_u8(blas, A, m, n, lda, threshold, P, Q);
         if (rank) *rank = r;
     });
@@ -260,6 +282,7 @@ int ffg_rr_base(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, size_t n, size_
                 size_t* rank) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(p);
+        check_mat("rr_base", A, m, n, lda);
         cudaStream_t st = ctx->stream;
         DevMat dA(m, n, st);
         dA.upload(A, lda);
@@ -275,6 +298,9 @@ int ffg_apply_perm_dev(ffg_ctx* ctx, uint32_t* A, size_t m, size_t n, size_t lda
                        const uint32_t* perm) {
     return guarded(ctx, [&] {
         ffg::Field F = ffg::make_field(2);
+        check_mat("apply_perm", A, m, n, lda);
+        if (axis != 0 && axis != 1) throw ffg::Error(FFG_ERR_INVALID_ARG, "apply_perm: axis must be 0 or 1");
+        if (!perm && (axis == 0 ? m : n) > 0) throw ffg::Error(FFG_ERR_INVALID_ARG, "apply_perm: null perm");
         ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
         ffg::apply_perm_dev(blas, ffg::DView{A, m, n, lda}, axis, inverse, perm);
     });

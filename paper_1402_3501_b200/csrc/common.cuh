@@ -2,7 +2,9 @@
 #pragma once
 
 #include <cstddef>
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <cstdlib>
 #include <utility>
 #include <cuda_runtime.h>
@@ -12,6 +14,28 @@
 #include "../../include/ffg.h"
 
 namespace ffg {
+
+// One-time per-device setup (cudaFuncSetAttribute is a per-device property: a process with
+// contexts on several GPUs must set it on each).  Thread-safe; devices 0..63.
+class PerDeviceOnce {
+public:
+    template <class Fn>
+    void operator()(Fn&& fn) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = 1ull << (dev & 63);
+        if (mask_.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> g(mu_);
+        if (mask_.load(std::memory_order_relaxed) & bit) return;
+        fn();
+        mask_.fetch_or(bit, std::memory_order_release);
+    }
+
+private:
+    std::atomic<uint64_t> mask_{0};
+    std::mutex mu_;
+};
+
 
 // A non-owning row-major window of u32 residues in device memory (the
 // device-side twin of MatView, matrix.hpp:13-43).

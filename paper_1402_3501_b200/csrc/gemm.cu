@@ -847,11 +847,8 @@ template <int L>
 void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t* Ap, const uint8_t* Bp, size_t Mp,
                     size_t Np, size_t Kp, DView C, cudaStream_t st, int sm_cap) {
     using S = Smem<L>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        FFG_CUDA(cudaFuncSetAttribute(modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
-        attr_set = true;
-    }
+    static PerDeviceOnce once;
+    once([] { FFG_CUDA(cudaFuncSetAttribute(modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL)); });
     CUtensorMap ma = make_map(Ap, Kp, (uint64_t)L * Mp, BM);
     CUtensorMap mb = make_map(Bp, Kp, (uint64_t)(Np / S::NT) * L * S::NT, L * S::NT);
     EpiParams ep = make_ep(F, alpha, beta, C);
@@ -884,8 +881,8 @@ void launch_direct(const Field& F, uint32_t alpha, uint32_t beta, DView A, DView
     if constexpr (!S::FITS) {
         throw Error(FFG_ERR_INTERNAL, "direct GEMM tile does not fit shared memory");
     } else {
-    static std::once_flag once;
-    std::call_once(once, [] {
+    static PerDeviceOnce once;
+    once([] {
         FFG_CUDA(cudaFuncSetAttribute(modgemm_direct_kernel<L, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       S::TOTAL));
     });

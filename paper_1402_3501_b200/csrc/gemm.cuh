@@ -31,27 +31,37 @@ enum ProfKind {
 
 class Profiler {
 public:
-    bool on = false;
+    // 0 off, 1 CUDA events around every launch, 2 count launches and work only (no events: the
+    // schedule is not perturbed; bench.py pairs it with CUPTI kernel durations)
+    int mode = 0;
     ~Profiler() { clear(true); }
     void begin(cudaStream_t st) {
-        if (!on) return;
+        if (mode != 1) return;
+        std::lock_guard<std::mutex> g(mu_);
         cur_a_ = take();
         cudaEventRecord(cur_a_, st);
     }
     // work = algorithmic units of this launch (int8 tensor ops for GEMM, bytes for others)
     void end(cudaStream_t st, int kind, double work, double field_ops = 0) {
-        if (!on) return;
-        cudaEvent_t b = take();
-        cudaEventRecord(b, st);
-        recs_.push_back(Rec{cur_a_, b, kind, work, field_ops});
+        if (mode == 0) return;
+        std::lock_guard<std::mutex> g(mu_);
+        cudaEvent_t b = nullptr;
+        if (mode == 1) {
+            b = take();
+            cudaEventRecord(b, st);
+        }
+        recs_.push_back(Rec{mode == 1 ? cur_a_ : nullptr, b, kind, work, field_ops});
     }
     // totals per kind: ms, launches, work, field_ops (synchronizes the recorded events)
     void read(double* ms, double* launches, double* work, double* field_ops) {
+        std::lock_guard<std::mutex> g(mu_);
         for (int k = 0; k < PROF_NKINDS; ++k) ms[k] = launches[k] = work[k] = field_ops[k] = 0;
         for (auto& r : recs_) {
-            cudaEventSynchronize(r.b);
             float t = 0;
-            cudaEventElapsedTime(&t, r.a, r.b);
+            if (r.a && r.b) {
+                cudaEventSynchronize(r.b);
+                cudaEventElapsedTime(&t, r.a, r.b);
+            }
             ms[r.kind] += t;
             launches[r.kind] += 1;
             work[r.kind] += r.work;
@@ -59,9 +69,10 @@ public:
         }
     }
     void clear(bool destroy = false) {
+        std::lock_guard<std::mutex> g(mu_);
         for (auto& r : recs_) {
-            free_.push_back(r.a);
-            free_.push_back(r.b);
+            if (r.a) free_.push_back(r.a);
+            if (r.b) free_.push_back(r.b);
         }
         recs_.clear();
         if (destroy) {
@@ -86,6 +97,7 @@ private:
         cudaEventCreate(&e);
         return e;
     }
+    std::mutex mu_;
     cudaEvent_t cur_a_ = nullptr;
     std::vector<Rec> recs_;
     std::vector<cudaEvent_t> free_;

@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(256) cols_perm_inplace_kernel(uint32_t* __rest
 
 namespace {
 void perm_smem_attr() {
-    static std::once_flag once;
-    std::call_once(once, [] {
+    static PerDeviceOnce once;
+    once([] {
         FFG_CUDA(cudaFuncSetAttribute(rows_perm_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PERM_SMEM));
         FFG_CUDA(cudaFuncSetAttribute(cols_perm_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PERM_SMEM));
     });
@@ -183,11 +183,10 @@ static void array_gather(const Blas& b, uint32_t* a, size_t len, PermSrc src) {
     if (len == 0) return;
     const size_t bytes = len * 4;
     if (bytes <= 200 * 1024) {
-        static bool set = false;
-        if (!set) {
+        static PerDeviceOnce once;
+        once([] {
             FFG_CUDA(cudaFuncSetAttribute(array_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            set = true;
-        }
+        });
         launch_k(array_gather_kernel, dim3(1), dim3(1024), bytes, b.st, a, (uint32_t)len, src);
         b.count();
     } else {

@@ -261,7 +261,7 @@ struct Driver {
                 : std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2));
         static const size_t gmin = getenv("FFG_FORK_MIN") ? (size_t)atoll(getenv("FFG_FORK_MIN")) : 0;
         const size_t gm = gmin ? gmin : 2 * thr;  // smallest G worth a host thread
-        return max_threads > 0 && !spec && use_streams && !b.ws.prof.on && !use_factors && !E.empty() && !G.empty() &&
+        return max_threads > 0 && !spec && use_streams && b.ws.prof.mode != 1 && !use_factors && !E.empty() && !G.empty() &&
                std::min(G.rows, G.cols) > gm && std::min(E.rows, E.cols) > thr &&
                active_children().load() < max_threads;
     }

@@ -510,8 +510,8 @@ void trsm_fused_launch(const Blas& b, int side, int upper, int unit, DView T, DV
     using K = void (*)(const uint32_t*, uint64_t, uint32_t, uint32_t*, uint64_t, uint32_t, uint32_t, uint64_t);
     // tile_rec pairs: (left, lower, unit) and (right, upper, nonunit); others use the generic path
     K k = side == 0 ? trsm_fused_kernel<0, false, true, R> : trsm_fused_kernel<1, true, false, R>;
-    static std::once_flag once;
-    std::call_once(once, [&] {
+    static PerDeviceOnce once;
+    once([&] {
         FFG_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<0, false, true, R>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         FFG_CUDA(cudaFuncSetAttribute(trsm_fused_kernel<1, true, false, R>,
@@ -579,8 +579,8 @@ void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
     const uint32_t t = (uint32_t)T.rows;
     if (t == 0 || t > 64 || T.cols != T.rows) throw Error(FFG_ERR_INTERNAL, "panel_inverses: block must be square <= 64");
     const size_t smem = (64 * PI_RS + 2 * (64 * PI_RS + 32 * 32 + 64)) * 4;
-    static std::once_flag once;
-    std::call_once(once, [smem] {
+    static PerDeviceOnce once;
+    once([smem] {
         FFG_CUDA(cudaFuncSetAttribute(panel_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     b.ws.prof.begin(b.st);
@@ -847,8 +847,8 @@ void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv,
         throw Error(FFG_ERR_INTERNAL, "panel_corner: node must be square with two leaves <= 64");
     if (t2 == 0) return;
     const size_t smem = 5 * 64 * CS * 4;
-    static std::once_flag once;
-    std::call_once(once, [smem] {
+    static PerDeviceOnce once;
+    once([smem] {
         FFG_CUDA(cudaFuncSetAttribute(panel_corner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     b.ws.prof.begin(b.st);
@@ -939,8 +939,8 @@ void trsm_small(const Blas& b, int side, int upper, int unit, DView T, DView B) 
                          trsm_small_kernel<0, true, false>,  trsm_small_kernel<0, true, true>,
                          trsm_small_kernel<1, false, false>, trsm_small_kernel<1, false, true>,
                          trsm_small_kernel<1, true, false>,  trsm_small_kernel<1, true, true>};
-    static std::once_flag once;
-    std::call_once(once, [&] {
+    static PerDeviceOnce once;
+    once([&] {
         for (auto k : kerns) FFG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     // forward order: left lower / right upper; reversed: left upper / right lower
@@ -1045,8 +1045,8 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     b.ws.prof.begin(b.st);
     if (column_inverse) {  // per-column substitution (kept for A/B comparison)
         const size_t smem = (TB * TSTR + 2 * TB) * sizeof(uint32_t);
-        static std::once_flag once;
-        std::call_once(once, [&] {
+        static PerDeviceOnce once;
+        once([&] {
             FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             FFG_CUDA(cudaFuncSetAttribute(tri_inv_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1057,8 +1057,8 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
         kern<<<(unsigned)(nblk * (TB / TRI_COLS)), TRI_COLS * 32, smem, b.st>>>(A.d, A.ld, (uint32_t)t, Tinv, p, b.F.mu);
     } else {
         const size_t smem = (2 * TB * TSTR + (TB / 2) * (TB / 2 + 1) + TB) * sizeof(uint32_t);
-        static std::once_flag once2;
-        std::call_once(once2, [&] {
+        static PerDeviceOnce once2;
+        once2([&] {
             FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             FFG_CUDA(cudaFuncSetAttribute(tri_inv_rec_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

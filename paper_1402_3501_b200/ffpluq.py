@@ -159,8 +159,9 @@ class Context:
 
     PROFILE_CLASSES = ("gemm", "split", "base", "trinv", "perm", "simt")
 
-    def profile(self, on: bool) -> None:
-        _check(lib().ffg_profile_enable(self._h, 1 if on else 0))
+    def profile(self, on) -> None:
+        """False/0 off, True/1 CUDA events around every launch, 2 count launches and work only."""
+        _check(lib().ffg_profile_enable(self._h, int(on)))
 
     def profile_read(self) -> dict:
         """{class: {ms, launches, work, field_ops}} since the last read (CUDA-event timed)."""
@@ -284,6 +285,18 @@ def _host(a) -> np.ndarray:
     return a
 
 
+def _dev(t, what: str = "matrix"):
+    """A torch tensor handed to a _dev entry: CUDA, 32-bit residues, 2-D, unit column stride."""
+    import torch
+    if not t.is_cuda:
+        raise TypeError(f"{what}: torch tensors must live on a CUDA device (host data: pass numpy arrays)")
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise TypeError(f"{what}: torch tensors must be int32/uint32 residues, got {t.dtype}")
+    if t.dim() != 2 or (t.numel() and t.stride(1) != 1):
+        raise ValueError(f"{what}: row-major 2-D tensor with unit column stride required")
+    return t
+
+
 def _ld(a) -> int:
     if _is_torch(a):
         return int(a.stride(0)) if a.dim() == 2 and a.shape[0] > 0 else max(int(a.shape[-1]), 1)
@@ -307,6 +320,8 @@ def fgemm(p: int, alpha: int, A, B, beta: int, Cm, ctx: Context | None = None):
         if not Cm.flags.writeable:
             raise ValueError("C must be writeable")
         _host(Cm)
+    else:
+        _dev(A, "A"), _dev(B, "B"), _dev(Cm, "C")
     if B.shape[0] != k or tuple(Cm.shape) != (m, n):
         raise DimMismatch("gemm: non-conforming shapes")
     fn = lib().ffg_fgemm_dev if dev else lib().ffg_fgemm
@@ -326,6 +341,8 @@ def ftrsm(p: int, side: int, uplo: int, diag: int, A, B, ctx: Context | None = N
     dev = _is_torch(B)
     if not dev:
         A, B = _host(A), _host(B)
+    else:
+        _dev(A, "A"), _dev(B, "B")
     fn = lib().ffg_ftrsm_dev if dev else lib().ffg_ftrsm
     _check(fn(ctx.handle, p, side, uplo, diag, _ptr(A), _ld(A), _ptr(B), _ld(B), m, n))
     return B
@@ -349,6 +366,8 @@ def pluq_tile_recursive(p: int, A, threshold: int = 8, ctx: Context | None = Non
         return PluqResult(P[:m], Q[:n], int(r.value))
     if not dev:
         A = _host(A)
+    else:
+        _dev(A, "A")
     fn = lib().ffg_pluq_tile_recursive_dev if dev else lib().ffg_pluq_tile_recursive
     _check(fn(ctx.handle, p, _ptr(A), m, n, _ld(A), threshold, P.ctypes.data, Q.ctypes.data, C.byref(r)))
     return PluqResult(P[:m], Q[:n], int(r.value))
@@ -366,9 +385,24 @@ def rr_base(p: int, A, ctx: Context | None = None) -> PluqResult:
     return PluqResult(P[:m], Q[:n], int(r.value))
 
 
+def apply_perm_dev(A, axis: int, perm, inverse: bool = False, ctx: Context | None = None):
+    """apply_perm (perm.hpp:167-193) of a PermSeq given by its to_array() index array `perm` (CUDA
+    int32/uint32 tensor) to the rows (axis 0) or columns (axis 1) of the CUDA matrix A, in place:
+    forward moves position perm[t] to t; inverse undoes it."""
+    ctx = ctx or default_context()
+    _dev(A, "A")
+    m, n = A.shape
+    dim = m if axis == 0 else n
+    if not _is_torch(perm) or not perm.is_cuda or perm.numel() != dim:
+        raise DimMismatch("permutation does not match matrix dimension")
+    _check(lib().ffg_apply_perm_dev(ctx.handle, _ptr(A), m, n, _ld(A), axis, 1 if inverse else 0, _ptr(perm)))
+    return A
+
+
 def random_mat_dev(p: int, A, seed: int, ctx: Context | None = None):
     """Fill a device matrix with the reference's random_mat (test_util.hpp:22-28)."""
     ctx = ctx or default_context()
+    _dev(A, "A")
     m, n = A.shape
     _check(lib().ffg_random_mat_dev(ctx.handle, p, seed, _ptr(A), m, n, _ld(A)))
     return A
@@ -377,6 +411,7 @@ def random_mat_dev(p: int, A, seed: int, ctx: Context | None = None):
 def lru_matrix_dev(p: int, M, r: int, seed: int, ctx: Context | None = None):
     """Fill a square device matrix with the config-4 input L*R*U; returns (rows, cols) of R's ones."""
     ctx = ctx or default_context()
+    _dev(M, "M")
     n = M.shape[0]
     rows = np.zeros(max(r, 1), np.uint32)
     cols = np.zeros(max(r, 1), np.uint32)

@@ -32,7 +32,7 @@ def main():
     if a.gen == "iid":
         A = O.random_mat(a.p, a.n, a.n, a.seed)
     else:
-        A, _, _ = O.lru_matrix(a.n, a.n // 2, a.p, a.seed)
+        A, _, _ = O.lru_matrix_exact_blas(a.n, a.n // 2, a.p, a.seed)
     if a.lib == "fixed" and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libffref_fixed.so")):
         ref = O.Ref(fixed=True)
         out, P, Q, r, sec = ref.pluq_tile_recursive(a.p, A, a.thr, a.workers)
