@@ -1038,6 +1038,13 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     const size_t fixed = ((size_t)5 * lay.rmax + 2 * ((size_t)lay.m + lay.n) + 4) * 4;
     const size_t blk = ((size_t)lay.m * lay.ns + (size_t)lay.m * lay.rmax) * 4;
     BaseInfo* info = static_cast<BaseInfo*>(info_dev);
+    // panel schedule: square speculative block with an inverse slot -> the fused base + inverses
+    // kernel (baseinv.cu), which also writes inv(L) and inv(U) into inv_out
+    static const bool no_fused_inv = getenv("FFG_BASE_INV") && atoi(getenv("FFG_BASE_INV")) == 0;
+    if ((seq & SPEC_BIT) && inv_out && !no_fused_inv && lay.m == lay.n && lay.m <= 64 && lay.m > 0) {
+        rr_base_inv_launch(b, a, Pd, Qd, info, inv_out, seq, allow_q);
+        return true;
+    }
     // room for the factor inverses (two INV_MAX frames + workspace), only for ranks <= INV_MAX
     const size_t inv_bytes = (2 * INV_MAX * (INV_MAX + 1) + (INV_MAX / 2) * (INV_MAX / 2) + INV_MAX + 8) * 4;
     if (inv_out && (fixed + blk + inv_bytes > BASE_SMEM_LIMIT)) inv_out = nullptr;

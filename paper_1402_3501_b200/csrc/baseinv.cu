@@ -1,0 +1,477 @@
+// baseinv.cu -- the panel schedule's speculative base case that also produces both factor inverses.
+//
+// The panel schedule (pluq.cu, rec_panel / two_leaf) factors each t x t diagonal block (t <= 64,
+// full rank guessed: P = identity, Q = the block's column pivots, rankrev.hpp:29-78 restated) and
+// then needs inv(L) and inv(U) of the block for its panel solves.  Here both come out of the same
+// 64-step elimination chain as L and U, as a cluster of two independent CTAs:
+//
+//   CTA 0 eliminates [A | I] row-wise:          [A | I]    ->  [D_i U_i | D_i inv(L)_i]
+//   CTA 1 eliminates [A^T | I] (same pivots):   [A^T | I]  ->  row i of its I part = D_i pv_i U^-1[:, i]^T
+//
+// (fraction-free: row_i <- pv_k row_i - x_ik row_k keeps row_i = D_k x the exact Schur row,
+// D_k = pv_0 ... pv_{k-1}; one modular inverse at the end recovers 1/D_k and 1/pv_k.)
+// The augmentation costs no extra arithmetic: the I part of a row is nonzero only in columns <= k
+// and the A part is live only in columns > k, so lane column j carries ONE live value -- the A part
+// while j > k, the I part after -- plus the frozen L numerator of column j.  Each CTA runs exactly
+// the work of a plain 64 x 64 elimination; the two run side by side on two SMs.
+//
+// Chain.  Warp w (of 16) holds the 4-row block b = 15 - w in registers (lane l: columns l, l + 32)
+// as a shift register: slot 0 is always the warp's next pivot row.  Pivot row k is published into
+// its own slot of a 64-slot ring in shared memory (values + Shoup factors) and announced on its own
+// mbarrier: warps run decoupled, the owner of row k + 1 updates it first, publishes it, then its
+// other rows; the next three pivots stay in the same warp (forwarded in registers).  Early blocks
+// sit in high warp ids: the SMSP arbiter issues highest-id-first, so the warp producing the next
+// pivot wins its SMSP over the warps still catching up.
+//
+// Instruction fetch.  Two CTAs on two SMs that ran other kernels a moment ago start with cold
+// instruction caches; every straight-line instruction executed once costs an L2 fetch (measured
+// ~25-40 cycles each on B200, against ~8 once warm).  So this kernel is written small: the pivot
+// loop is one body of four row updates (fits the ~6 KB L0 cache) and every other phase is a rolled
+// loop.  (An unrolled version of the same arithmetic measured 2.5x slower.)
+//
+// A zero Schur diagonal (column pivot, ~1/p per pivot) switches both CTAs, at that step, to a plain
+// shared-memory elimination with explicit A and I parts (CTA 0: first nonzero unused column of the
+// pivot row, rr_base's choice; CTA 1: the matching row of A^T).  A rank-deficient block raises the
+// speculation-failed flag exactly like rr_base_spec_kernel (base.cu); its outputs are then unused.
+#include "pluq.cuh"
+#include "ptx.cuh"
+
+namespace ffg {
+
+namespace {
+
+constexpr int BI_WARPS = 16;
+constexpr int BI_THREADS = BI_WARPS * 32;
+constexpr int BI_SS = 65;  // row stride of the shared-memory matrices
+constexpr uint32_t BI_FULL = 0xffffffffu;
+
+struct BiSmem {
+    uint32_t pub[64][64];    // published pivot row k (fraction-free; cols < k: I part, > k: A part,
+                             // [k][k] = 1, see the I-part scaling note); after the loop: the final
+                             // rows in logical order
+    uint32_t pf[64][64];     // Shoup factors of pub
+    uint32_t Ln[64][64];     // L numerators of row i (columns < i), saved when row i is published
+    uint32_t S[64][BI_SS];   // block staging / slow path: A part / epilogue transpose
+    uint32_t I[64][BI_SS];   // slow path: I part
+    uint32_t pv[64], pvf[64], D[64];
+    uint32_t invd[64], invdf[64], invp[64], invpf[64], Dd[64], Ddf[64];
+    uint32_t pcol[64];       // CTA 0: physical column of pivot t; CTA 1: physical row of pivot t
+    uint64_t full[64];       // pivot row k published
+    uint32_t fail, k0;
+};
+
+__device__ __forceinline__ uint32_t bi_red4p(uint32_t x, uint32_t p) {  // [0, 4p) -> [0, p)
+    x = min(x, x - 2 * p);
+    return min(x, x - p);
+}
+
+__device__ __forceinline__ uint32_t bi_sub(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
+
+__device__ __forceinline__ void bi_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// a * b mod p for a, b < p < 2^26 in double precision (the epilogue's short serial chains): the product
+// is exact (< 2^52), the quotient estimate is off by at most one, corrected once each way
+__device__ __forceinline__ uint32_t bi_mulmod(uint32_t a, uint32_t b, double pd, double pinv) {
+    const double ab = (double)a * (double)b;
+    const double q = floor(ab * pinv);
+    double r = fma(-q, pd, ab);
+    r = r < 0.0 ? r + pd : r;
+    r = r >= pd ? r - pd : r;
+    return (uint32_t)r;
+}
+
+// x * w - (x * w div p) * p with w's Shoup factor wf: in [0, 2p) for any 32-bit x
+__device__ __forceinline__ uint32_t bi_shoup_lazy(uint32_t x, uint32_t w, uint32_t wf, uint32_t p) {
+    return x * w - __umulhi(x, wf) * p;
+}
+
+// per-step values every row update of step k uses
+struct BiStep {
+    uint32_t kh, kl, pv, pvp, b0, b1, f0, f1, p;
+    bool dk0, dk1;
+};
+
+// one row's step-k update (fast path): numer = its live value in column k (frozen as the L
+// numerator there), every lane column then takes new = pv * live - numer * b  (lazy, [0, 4p));
+// in column k the I part starts from zero
+__device__ __forceinline__ void bi_row(uint32_t (&lv)[2], uint32_t (&fz)[2], const BiStep& q) {
+    const uint32_t numer = __shfl_sync(BI_FULL, q.kh ? lv[1] : lv[0], q.kl);
+    const uint32_t t10 = bi_shoup_lazy(lv[0], q.pv, q.pvp, q.p), t11 = bi_shoup_lazy(lv[1], q.pv, q.pvp, q.p);
+    const uint32_t t20 = bi_shoup_lazy(numer, q.b0, q.f0, q.p), t21 = bi_shoup_lazy(numer, q.b1, q.f1, q.p);
+    lv[0] = (q.dk0 ? 0u : t10) + 2 * q.p - t20;
+    lv[1] = (q.dk1 ? 0u : t11) + 2 * q.p - t21;
+    fz[0] = q.dk0 ? numer : fz[0];
+    fz[1] = q.dk1 ? numer : fz[1];
+}
+
+}  // namespace
+
+// I-part scaling: the I part of column j starts at step j from the pivot row's entry there, which
+// is D_j in the plain fraction-free form; it is published as 1 instead (no product on the serial
+// path), which scales the whole I column j by 1/D_j -- undone in the epilogue.
+//
+// grid = 2 CTAs (CTA 0: A, CTA 1: A^T, one cluster), BI_THREADS threads, sizeof(BiSmem) dynamic
+// shared memory.  Outputs (CTA 0): the packed block (logical column order), Pd = identity, Qd =
+// column pivots, inv[0, t^2) = inv(L); (CTA 1): inv[t^2, 2 t^2) = inv(U), both row-major with ld t;
+// info as rr_base_spec_kernel.  allow_q = 0: any column pivot fails the guess.
+__global__ void __launch_bounds__(BI_THREADS, 1)
+    rr_base_inv_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t t, uint32_t* __restrict__ Pd,
+                       uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t* __restrict__ inv, uint32_t p,
+                       uint64_t mu, uint32_t seq, uint32_t allow_q) {
+    extern __shared__ __align__(16) unsigned char bi_raw[];
+    BiSmem& sm = *reinterpret_cast<BiSmem*>(bi_raw);
+    const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const bool tr = blockIdx.x == 1;
+    if (tid < 64) ptx::mbar_init(&sm.full[tid], 32);
+    if (tid == 0) {
+        sm.fail = 0u;
+        sm.k0 = t;
+    }
+    ptx::fence_mbar_init();
+    ptx::pdl_enter();
+    // stage the block (coalesced), zero-padded to 64 x 64
+#pragma unroll 1
+    for (uint32_t idx = tid; idx < 64 * 64; idx += 4 * BI_THREADS) {
+        uint32_t r[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t x = idx + q * BI_THREADS, i = x >> 6, j = x & 63;
+            r[q] = (i < t && j < t) ? A[(uint64_t)i * lda + j] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t x = idx + q * BI_THREADS;
+            sm.S[x >> 6][x & 63] = r[q];
+        }
+    }
+    // both CTAs hold the input before CTA 0 may overwrite it (a 2-CTA cluster: co-scheduled)
+    bi_cluster_sync();
+    // this warp's block: rows r0 .. r0 + 3, slot 0 = the next one to become a pivot
+    const uint32_t r0 = 4 * (BI_WARPS - 1 - w);
+    uint32_t nxt = r0, left = r0 < t ? min(4u, t - r0) : 0u;
+    uint32_t lv[4][2], fz[4][2];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const uint32_t i = r0 + s;
+        lv[s][0] = tr ? sm.S[lane][i] : sm.S[i][lane];
+        lv[s][1] = tr ? sm.S[lane + 32][i] : sm.S[i][lane + 32];
+        fz[s][0] = fz[s][1] = 0u;
+    }
+    // forwarded pivot (the warp's own last publish) and the publish itself
+    bool fwd = false;
+    uint32_t fpv = 0, fpvp = 0, fb0 = 0, fb1 = 0, ff0 = 0, ff1 = 0;
+    auto publish = [&](uint32_t kn) {  // slot 0 (row kn, updated through pivot kn - 1) -> ring slot kn
+        const uint32_t a0 = bi_red4p(lv[0][0], p), a1 = bi_red4p(lv[0][1], p);
+        const uint32_t pvn = __shfl_sync(BI_FULL, kn >= 32 ? a1 : a0, kn & 31);
+        const uint32_t v0 = lane == kn ? 1u : a0, v1 = lane + 32 == kn ? 1u : a1;
+        const uint32_t g0 = shoup_pre(v0, p, mu), g1 = shoup_pre(v1, p, mu), pvnf = shoup_pre(pvn, p, mu);
+        sm.pub[kn][lane] = v0;
+        sm.pub[kn][lane + 32] = v1;
+        sm.pf[kn][lane] = g0;
+        sm.pf[kn][lane + 32] = g1;
+        if (lane == 0) {
+            sm.pv[kn] = pvn;
+            sm.pvf[kn] = pvnf;
+        }
+        ptx::mbar_arrive(&sm.full[kn]);
+        fwd = true;
+        fpv = pvn;
+        fpvp = pvnf;
+        fb0 = v0;
+        fb1 = v1;
+        ff0 = g0;
+        ff1 = g1;
+        // its L numerators (columns < kn) -- then the shift register moves on
+        sm.Ln[kn][lane] = bi_red4p(fz[0][0], p);
+        sm.Ln[kn][lane + 32] = bi_red4p(fz[0][1], p);
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            lv[s][0] = lv[s + 1][0];
+            lv[s][1] = lv[s + 1][1];
+            fz[s][0] = fz[s + 1][0];
+            fz[s][1] = fz[s + 1][1];
+        }
+        ++nxt;
+        --left;
+    };
+    if (left && nxt == 0) publish(0);  // row 0: I part [0][0] = 1, pivot = A[0][0]
+#pragma unroll 1
+    for (uint32_t k = 0; k < t && left; ++k) {
+        BiStep q;
+        if (fwd) {
+            q.pv = fpv;
+            q.pvp = fpvp;
+            q.b0 = fb0;
+            q.b1 = fb1;
+            q.f0 = ff0;
+            q.f1 = ff1;
+        } else {
+            ptx::mbar_wait(&sm.full[k], 0);
+            q.pv = sm.pv[k];
+            q.pvp = sm.pvf[k];
+            q.b0 = sm.pub[k][lane];
+            q.b1 = sm.pub[k][lane + 32];
+            q.f0 = sm.pf[k][lane];
+            q.f1 = sm.pf[k][lane + 32];
+        }
+        fwd = false;
+        if (q.pv == 0u) {  // zero Schur diagonal: every warp still holding rows leaves at this step
+            sm.k0 = k;
+            break;
+        }
+        q.p = p;
+        q.kh = k >> 5;
+        q.kl = k & 31;
+        q.dk0 = lane == k;
+        q.dk1 = lane + 32 == k;
+        const bool owner = nxt == k + 1;  // slot 0 is the next pivot row
+        if (owner) {
+            bi_row(lv[0], fz[0], q);
+            publish(k + 1);  // shifts: the rows after it move down one slot
+            bi_row(lv[0], fz[0], q);
+            bi_row(lv[1], fz[1], q);
+            bi_row(lv[2], fz[2], q);
+        } else {
+            bi_row(lv[0], fz[0], q);
+            bi_row(lv[1], fz[1], q);
+            bi_row(lv[2], fz[2], q);
+            bi_row(lv[3], fz[3], q);
+        }
+    }
+    __syncthreads();
+    // the last pivot row is published but never consumed inside the loop: check its diagonal here
+    if (tid == 0 && sm.k0 == t && t > 0 && sm.pv[t - 1] == 0u) sm.k0 = t - 1;
+    __syncthreads();
+    const uint32_t k0 = sm.k0;
+    if (k0 < t) {
+        // ---- slow path from step k0: rows >= k0 (still in registers) into S / I with explicit A / I
+        // parts, every I column rescaled to the plain fraction-free form (x D_j)
+        if (tid == 0) {
+            uint32_t d = 1u;
+            for (uint32_t k = 0; k <= k0 && k < 64; ++k) {
+                sm.D[k] = d;
+                if (k < k0) d = mul_mod(d, sm.pv[k], p, mu);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if ((uint32_t)s >= left) break;
+            const uint32_t i = nxt + s;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t j = lane + 32 * h;
+                const uint32_t f = bi_red4p(fz[s][h], p), l = bi_red4p(lv[s][h], p);
+                sm.S[i][j] = j < k0 ? f : l;
+                sm.I[i][j] = j < k0 ? mul_mod(l, sm.D[j], p, mu) : 0u;
+            }
+        }
+        if (w == 0) {  // row k0 was published (its zero diagonal stopped the fast path): back into S / I
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t j = lane + 32 * h;
+                const uint32_t v = sm.pub[k0][j];
+                sm.S[k0][j] = j < k0 ? sm.Ln[k0][j] : (j == k0 ? sm.pv[k0] : v);
+                sm.I[k0][j] = j < k0 ? mul_mod(v, sm.D[j], p, mu) : 0u;
+            }
+        }
+        for (uint32_t idx = tid; idx < k0 * 64; idx += BI_THREADS) {  // the published rows' I parts
+            const uint32_t i = idx >> 6, j = idx & 63;
+            if (j <= i) sm.pub[i][j] = mul_mod(sm.pub[i][j], sm.D[j], p, mu);
+        }
+        uint64_t used = k0 ? (~0ull >> (64 - k0)) : 0ull;  // CTA 0: pivot columns; CTA 1: pivot rows
+        if (tid < k0) sm.pcol[tid] = tid;
+        __syncthreads();
+        for (uint32_t k = k0; k < t; ++k) {
+            if (w == 0) {
+                uint32_t c;
+                if (!tr) {  // first nonzero unused column of pivot row k
+                    const bool z0 = lane < t && !((used >> lane) & 1u) && sm.S[k][lane] != 0u;
+                    const bool z1 = lane + 32 < t && !((used >> (lane + 32)) & 1u) && sm.S[k][lane + 32] != 0u;
+                    const uint32_t m0 = __ballot_sync(BI_FULL, z0), m1 = __ballot_sync(BI_FULL, z1);
+                    c = m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : 64u);
+                } else {  // first unused row of A^T with a nonzero in column k
+                    const bool z0 = lane < t && !((used >> lane) & 1u) && sm.S[lane][k] != 0u;
+                    const bool z1 = lane + 32 < t && !((used >> (lane + 32)) & 1u) && sm.S[lane + 32][k] != 0u;
+                    const uint32_t m0 = __ballot_sync(BI_FULL, z0), m1 = __ballot_sync(BI_FULL, z1);
+                    c = m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : 64u);
+                }
+                if (lane == 0) {
+                    if (c == 64u || (!allow_q && c != k)) {
+                        sm.fail = 1u;
+                        // keep going on a harmless choice (the outputs are discarded): any unused index
+                        for (uint32_t r = 0; r < 64; ++r)
+                            if (!((used >> r) & 1u)) {
+                                c = r;
+                                break;
+                            }
+                    }
+                    sm.pcol[k] = c;
+                    const uint32_t pvk = tr ? sm.S[c][k] : sm.S[k][c];
+                    sm.pv[k] = pvk;
+                    if (k + 1 < 64) sm.D[k + 1] = mul_mod(sm.D[k], pvk, p, mu);
+                    sm.I[tr ? c : k][k] = sm.D[k];  // the pivot row's own I part in column k
+                }
+            }
+            __syncthreads();
+            const uint32_t c = sm.pcol[k], pvk = sm.pv[k];
+            const uint32_t prow = tr ? c : k;
+            used |= 1ull << c;
+            // rows not yet pivots: CTA 0 rows > k; CTA 1 unused rows
+            for (uint32_t idx = tid; idx < 64 * 64; idx += BI_THREADS) {
+                const uint32_t i = idx >> 6, j = idx & 63;
+                const bool active = tr ? (i < t && !((used >> i) & 1u)) : (i > k && i < t);
+                if (!active) continue;
+                const uint32_t pc = tr ? k : c;  // pivot column (physical)
+                const uint32_t numer = sm.S[i][pc];
+                // A part: columns not yet pivots (CTA 0: unused columns; CTA 1: columns > k)
+                const bool live_a = tr ? (j > k) : !((used >> j) & 1u);
+                if (live_a && j < t)
+                    sm.S[i][j] = bi_sub(mul_mod(sm.S[i][j], pvk, p, mu), mul_mod(numer, sm.S[prow][j], p, mu), p);
+                if (j <= k)
+                    sm.I[i][j] = bi_sub(mul_mod(sm.I[i][j], pvk, p, mu), mul_mod(numer, sm.I[prow][j], p, mu), p);
+            }
+            __syncthreads();
+        }
+        // final rows in logical order into pub (pivot rows k >= k0) and L numerators into Ln; the
+        // rows pivoted before k0 take the later column pivots too (rr_base rotates whole columns)
+        if (!tr) {
+            for (uint32_t idx = tid; idx < k0 * 64; idx += BI_THREADS) sm.S[idx >> 6][idx & 63] = sm.pub[idx >> 6][idx & 63];
+            __syncthreads();
+            for (uint32_t idx = tid; idx < k0 * 64; idx += BI_THREADS) {
+                const uint32_t kk = idx >> 6, j = idx & 63;
+                if (j >= k0 && j < t) sm.pub[kk][j] = sm.S[kk][sm.pcol[j]];
+            }
+            __syncthreads();
+        }
+        for (uint32_t idx = tid; idx < 64 * 64; idx += BI_THREADS) {
+            const uint32_t kk = idx >> 6, j = idx & 63;
+            if (kk < k0 || kk >= t) continue;
+            const uint32_t prow = tr ? sm.pcol[kk] : kk;
+            if (j <= kk)
+                sm.pub[kk][j] = sm.I[prow][j];
+            else if (j < t)
+                sm.pub[kk][j] = tr ? sm.S[prow][j] : sm.S[prow][sm.pcol[j]];
+            if (!tr && j < kk && j < t) sm.Ln[kk][j] = sm.S[kk][sm.pcol[j]];  // frozen numerators
+        }
+    } else if (tid < 64) {
+        sm.pcol[tid] = tid;
+    }
+    __syncthreads();
+    // ---- one inverse: D_k = prod_{j<k} pv_j -> 1/D_k and 1/pv_k = D_k / D_{k+1}; plus the I-column
+    // scales Dd_j (= D_j on the fast path, 1 after the slow path rescaled them).  Branch-free scans.
+    if (w == 0) {
+        const double pd = (double)p, pinv = (double)mu * 5.421010862427522e-20;  // mu / 2^64 ~ 1 / p
+        const uint32_t e0 = 2 * lane, e1 = 2 * lane + 1;
+        const uint32_t v0 = (e0 < t && sm.pv[e0]) ? sm.pv[e0] : 1u, v1 = (e1 < t && sm.pv[e1]) ? sm.pv[e1] : 1u;
+        uint32_t inc = bi_mulmod(v0, v1, pd, pinv), suf = inc;
+#pragma unroll 1
+        for (uint32_t off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(BI_FULL, inc, off), u = __shfl_down_sync(BI_FULL, suf, off);
+            const uint32_t mi = bi_mulmod(inc, o, pd, pinv), ms = bi_mulmod(suf, u, pd, pinv);
+            inc = lane >= off ? mi : inc;
+            suf = lane + off < 32 ? ms : suf;
+        }
+        uint32_t exc = __shfl_up_sync(BI_FULL, inc, 1);
+        if (lane == 0) exc = 1u;
+        const uint32_t D0 = exc, D1 = bi_mulmod(exc, v0, pd, pinv);
+        const uint32_t total = __shfl_sync(BI_FULL, inc, 31);
+        const uint32_t tinv = inv_mod_bin(total, p);  // every lane, same input: a uniform loop
+        const uint32_t iD0 = bi_mulmod(tinv, suf, pd, pinv);
+        const uint32_t sufx = __shfl_down_sync(BI_FULL, suf, 1);
+        const uint32_t iD2 = bi_mulmod(tinv, lane == 31 ? 1u : sufx, pd, pinv);
+        const uint32_t iD1 = bi_mulmod(iD2, v1, pd, pinv);
+        const uint32_t ip0 = bi_mulmod(D0, iD1, pd, pinv), ip1 = bi_mulmod(D1, iD2, pd, pinv);
+        const uint32_t s0 = k0 < t ? 1u : D0, s1 = k0 < t ? 1u : D1;
+        sm.invd[e0] = iD0;
+        sm.invp[e0] = ip0;
+        sm.Dd[e0] = s0;
+        sm.invd[e1] = iD1;
+        sm.invp[e1] = ip1;
+        sm.Dd[e1] = s1;
+    }
+    __syncthreads();
+    if (tid < 3 * 64) {  // Shoup factors of the three scale vectors, one per thread
+        uint32_t* v = tid < 64 ? sm.invd : (tid < 128 ? sm.invp : sm.Dd);
+        uint32_t* f = tid < 64 ? sm.invdf : (tid < 128 ? sm.invpf : sm.Ddf);
+        f[tid & 63] = shoup_pre(v[tid & 63], p, mu);
+    }
+    __syncthreads();
+    if (!tr) {
+        // packed L \ U (logical columns) and inv(L)[i][j] = I[i][j] D_j / D_i
+#pragma unroll 1
+        for (uint32_t idx = tid; idx < t * t; idx += BI_THREADS) {
+            const uint32_t i = idx / t, j = idx - i * t;
+            const bool lo = j < i, dg = j == i;
+            const uint32_t x = lo ? sm.Ln[i][j] : (dg ? sm.pv[i] : sm.pub[i][j]);
+            const uint32_t m = lo ? sm.invp[j] : sm.invd[i], mf = lo ? sm.invpf[j] : sm.invdf[i];
+            A[(uint64_t)i * lda + j] = shoup_mul(x, m, mf, p);
+            const uint32_t y = shoup_mul(sm.pub[i][j], sm.Dd[j], sm.Ddf[j], p);
+            inv[idx] = j <= i ? shoup_mul(y, sm.invd[i], sm.invdf[i], p) : 0u;
+        }
+        for (uint32_t i = tid; i < t; i += BI_THREADS) {
+            Pd[i] = i;
+            Qd[i] = sm.pcol[i];
+        }
+    } else {
+        // inv(U)[s][q] = I1[q][s] D_s / pv_q (s <= q): transposed through S, then coalesced stores
+#pragma unroll 1
+        for (uint32_t idx = tid; idx < 64 * 64; idx += BI_THREADS) {
+            const uint32_t q = idx >> 6, s = idx & 63;
+            const uint32_t y = shoup_mul(sm.pub[q][s], sm.Dd[s], sm.Ddf[s], p);
+            sm.S[s][q] = s <= q ? shoup_mul(y, sm.invp[q], sm.invpf[q], p) : 0u;
+        }
+        __syncthreads();
+        uint32_t* invU = inv + (size_t)t * t;
+#pragma unroll 1
+        for (uint32_t idx = tid; idx < t * t; idx += BI_THREADS) {
+            const uint32_t s = idx / t, q = idx - s * t;
+            invU[idx] = sm.S[s][q];
+        }
+    }
+    __syncthreads();
+    if (!tr && tid == 0) {
+        info->rank = t;
+        info->plo = info->phi = info->qlo = info->qhi = 0;
+        info->cached = 0;
+        if ((seq & SPEC_BIT) && sm.fail) *reinterpret_cast<volatile uint32_t*>(&info->spec_fail) = 1u;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+    }
+}
+
+void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv,
+                        uint32_t seq, bool allow_q) {
+    const uint32_t t = (uint32_t)a.rows;
+    if (t == 0 || t > 64 || a.cols != a.rows) throw Error(FFG_ERR_INTERNAL, "rr_base_inv: block must be square <= 64");
+    const size_t smem = sizeof(BiSmem);
+    static PerDeviceOnce once;
+    once([smem] {
+        FFG_CUDA(cudaFuncSetAttribute(rr_base_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    });
+    BaseInfo* info = static_cast<BaseInfo*>(info_dev);
+    b.ws.prof.begin(b.st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(BI_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = b.st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    FFG_CUDA(cudaLaunchKernelEx(&cfg, rr_base_inv_kernel, a.d, (uint64_t)a.ld, t, Pd, Qd, info, inv, b.F.p, b.F.mu,
+                                seq, (uint32_t)allow_q));
+    FFG_CUDA(cudaGetLastError());
+    b.ws.prof.end(b.st, PROF_BASE, 2.0 * t * t * 4, 2.0 * t * (double)t * t);
+    b.count();
+}
+
+}  // namespace ffg

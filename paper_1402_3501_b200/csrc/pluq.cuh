@@ -81,6 +81,10 @@ constexpr uint32_t SPEC_BIT = 0x80000000u;
 // allowed (Qd receives them; P is then the identity)
 bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev,
                     uint32_t* inv_out = nullptr, uint32_t seq = 0, bool allow_q = false);
+// speculative square block (t <= 64) of the panel schedule + both factor inverses in one launch
+// (baseinv.cu): inv[0, t^2) = inv(L), inv[t^2, 2 t^2) = inv(U), row-major ld t
+void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv,
+                        uint32_t seq, bool allow_q);
 
 // Structure of a node's leading r x r factor (tile_rec pivot gather order A1, E, G, R):
 // block triangular with the children's leading factors on the diagonal.  Leaves are base
