@@ -744,8 +744,11 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
     if (tid == 0) {
         info->cached = 0;
         // speculative launch (top bit of seq): the host assumed full rank and identity P, Q
-        if ((seq & SPEC_BIT) && (r != min(m, n) || misc[5] || misc[6]))
-            *reinterpret_cast<volatile uint32_t*>(&info->spec_fail) = 1u;
+        if ((seq & SPEC_BIT) && (r != min(m, n) || misc[5] || misc[6])) {
+            volatile uint32_t* sf = &info->spec_fail;
+            if (!*sf) *reinterpret_cast<volatile uint32_t*>(&info->fail_seq) = seq;  // the first failure
+            *sf = 1u;
+        }
         __threadfence_system();
         *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
     }
@@ -973,7 +976,11 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
         info->rank = r;
         info->plo = info->phi = info->qlo = info->qhi = 0;
         info->cached = 0;
-        if ((seq & SPEC_BIT) && fail) *reinterpret_cast<volatile uint32_t*>(&info->spec_fail) = 1u;
+        if ((seq & SPEC_BIT) && fail) {
+            volatile uint32_t* sf = &info->spec_fail;
+            if (!*sf) *reinterpret_cast<volatile uint32_t*>(&info->fail_seq) = seq;  // the first failure
+            *sf = 1u;
+        }
         __threadfence_system();
         *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
     }

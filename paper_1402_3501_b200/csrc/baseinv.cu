@@ -108,6 +108,15 @@ __device__ __forceinline__ void bi_row(uint32_t (&lv)[2], uint32_t (&fz)[2], con
 
 }  // namespace
 
+// diagnostics (-DBI_DBG builds, FFG_BI_DBG=1): clock64 at phase boundaries of CTA 0
+__device__ long long* g_bi_dbg = nullptr;
+#ifdef BI_DBG
+#define BI_STAMP(i) \
+    if (!tr && tid == 0 && g_bi_dbg) g_bi_dbg[i] = clock64();
+#else
+#define BI_STAMP(i)
+#endif
+
 // I-part scaling: the I part of column j starts at step j from the pivot row's entry there, which
 // is D_j in the plain fraction-free form; it is published as 1 instead (no product on the serial
 // path), which scales the whole I column j by 1/D_j -- undone in the epilogue.
@@ -130,7 +139,9 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         sm.k0 = t;
     }
     ptx::fence_mbar_init();
+    BI_STAMP(0);
     ptx::pdl_enter();
+    BI_STAMP(1);
     // stage the block (coalesced), zero-padded to 64 x 64
 #pragma unroll 1
     for (uint32_t idx = tid; idx < 64 * 64; idx += 4 * BI_THREADS) {
@@ -148,6 +159,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     }
     // both CTAs hold the input before CTA 0 may overwrite it (a 2-CTA cluster: co-scheduled)
     bi_cluster_sync();
+    BI_STAMP(2);
     // this warp's block: rows r0 .. r0 + 3, slot 0 = the next one to become a pivot
     const uint32_t r0 = 4 * (BI_WARPS - 1 - w);
     uint32_t nxt = r0, left = r0 < t ? min(4u, t - r0) : 0u;
@@ -244,6 +256,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     // the last pivot row is published but never consumed inside the loop: check its diagonal here
     if (tid == 0 && sm.k0 == t && t > 0 && sm.pv[t - 1] == 0u) sm.k0 = t - 1;
     __syncthreads();
+    BI_STAMP(3);
     const uint32_t k0 = sm.k0;
     if (k0 < t) {
         // ---- slow path from step k0: rows >= k0 (still in registers) into S / I with explicit A / I
@@ -393,6 +406,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         sm.Dd[e1] = s1;
     }
     __syncthreads();
+    BI_STAMP(4);
     if (tid < 3 * 64) {  // Shoup factors of the three scale vectors, one per thread
         uint32_t* v = tid < 64 ? sm.invd : (tid < 128 ? sm.invp : sm.Dd);
         uint32_t* f = tid < 64 ? sm.invdf : (tid < 128 ? sm.invpf : sm.Ddf);
@@ -432,14 +446,34 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         }
     }
     __syncthreads();
+    BI_STAMP(5);
     if (!tr && tid == 0) {
         info->rank = t;
         info->plo = info->phi = info->qlo = info->qhi = 0;
         info->cached = 0;
-        if ((seq & SPEC_BIT) && sm.fail) *reinterpret_cast<volatile uint32_t*>(&info->spec_fail) = 1u;
+        if ((seq & SPEC_BIT) && sm.fail) {
+            volatile uint32_t* sf = &info->spec_fail;
+            if (!*sf) *reinterpret_cast<volatile uint32_t*>(&info->fail_seq) = seq;  // the first failure
+            *sf = 1u;
+        }
         __threadfence_system();
         *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
     }
+}
+
+static void bi_dbg_dump(cudaStream_t st) {
+    static long long* buf = nullptr;
+    if (!buf) {
+        FFG_CUDA(cudaMalloc(&buf, 8 * 8));
+        FFG_CUDA(cudaMemset(buf, 0, 8 * 8));
+        FFG_CUDA(cudaMemcpyToSymbol(g_bi_dbg, &buf, sizeof(buf)));
+        return;
+    }
+    long long h[8];
+    FFG_CUDA(cudaStreamSynchronize(st));
+    FFG_CUDA(cudaMemcpy(h, buf, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "BI_DBG cycles: pdl wait %lld, staging+cluster %lld, pivot loop %lld, scan %lld, outputs %lld\n",
+            h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3], h[5] - h[4]);
 }
 
 void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv,
@@ -467,6 +501,8 @@ void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    static const bool dbg = getenv("FFG_BI_DBG") != nullptr;
+    if (dbg) bi_dbg_dump(b.st);
     FFG_CUDA(cudaLaunchKernelEx(&cfg, rr_base_inv_kernel, a.d, (uint64_t)a.ld, t, Pd, Qd, info, inv, b.F.p, b.F.mu,
                                 seq, (uint32_t)allow_q));
     FFG_CUDA(cudaGetLastError());

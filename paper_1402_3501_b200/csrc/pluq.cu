@@ -314,6 +314,31 @@ struct Driver {
     // noticed (and the queue drained) within a few steps instead of after the whole recursion
     size_t spec_window = 32;
     std::vector<uint32_t> spec_seqs;
+    std::vector<size_t> spec_pos;  // panel schedule: diagonal offset of each speculative base case
+    // the offset of the base case whose guess failed first (after a drain); false if unknown
+    bool failed_at(size_t& off) const {
+        if (!*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) return false;
+        const uint32_t fs = *reinterpret_cast<volatile uint32_t*>(&info_host->fail_seq);
+        for (size_t i = 0; i < spec_seqs.size(); ++i)
+            if (spec_seqs[i] == fs && spec_pos[i] != SIZE_MAX) {
+                off = spec_pos[i];
+                return true;
+            }
+        return false;
+    }
+    // the schedule's prefix before `off`: block-local column pivots and base cases (call after a drain)
+    void prefix_of(size_t off, std::vector<uint32_t>& gqh, std::vector<std::pair<size_t, size_t>>& lv) const {
+        gqh.assign(off, 0u);
+        lv.clear();
+        for (const auto& lf : leaves)
+            if (lf.first + lf.second <= off) lv.push_back(lf);
+        if (gq && off) {
+            FFG_CUDA(cudaMemcpy(gqh.data(), gq, off * 4, cudaMemcpyDeviceToHost));
+        } else {
+            for (const auto& lf : lv)
+                for (size_t i = 0; i < lf.second; ++i) gqh[lf.first + i] = (uint32_t)i;  // no column pivots
+        }
+    }
     void spec_throttle() {
         if (spec_seqs.size() < spec_window) return;
         const uint32_t target = spec_seqs[spec_seqs.size() - spec_window] & ~SPEC_BIT;
@@ -347,6 +372,7 @@ struct Driver {
             // log-depth kernel: 38 -> 90 us per base case; the spec kernel ignores inv_out)
             base_wrote_inv = rr_base_launch(b, a, res.P, res.Q, info_dev, inv_out, seq, allow_q && a.rows == a.cols);
             spec_seqs.push_back(seq);
+            spec_pos.push_back(proot ? (size_t)(a.d - proot) / pld : SIZE_MAX);
             ++base_cases;
             res.rank = std::min(a.rows, a.cols);
             res.pr = Range{};
@@ -949,7 +975,9 @@ struct Driver {
         FFG_CUDA(cudaMallocAsync(&bk, m * m * 4, b.st));
         copy_block_dev(b, a, DView{bk, m, m, m});
         std::vector<uint32_t> qh(m);
-        bool ok = false;
+        bool ok = false, resumable = false;
+        size_t fail_off = 0;
+        Prefix px;
         {
             Driver sub(b, thr, m, m, /*keep_events=*/true, slot);
             sub.owns_slot = false;
@@ -971,7 +999,22 @@ struct Driver {
             } catch (const SpecAbort&) {
                 ok = false;
             }
-            if (!ok) FFG_CUDA(cudaDeviceSynchronize());
+            if (!ok) {
+                FFG_CUDA(cudaDeviceSynchronize());
+                if (sub.failed_at(fail_off)) {
+                    sub.prefix_of(fail_off, px.gq, px.leaves);
+                    resumable = true;
+                }
+            }
+        }
+        if (!ok && resumable) {
+            // keep the prefix the schedule finished; recompute the rest of the node from its backup
+            node_spec_fails = fail_off == 0 ? node_spec_fails + 1 : 0;
+            px.root = a.d;
+            px.ld = a.ld;
+            res = recover(a, depth, fail_off, bk, m, px);
+            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            return true;
         }
         if (!ok) {
             copy_block_dev(b, DView{bk, m, m, m}, a);
@@ -1072,6 +1115,18 @@ struct Driver {
             }
         }
 
+        return rec_tail(a, depth, res, mark, r1s, pending_r, rspine, LR);
+    }
+
+    // tile_rec after its first child and the Schur updates that child feeds (rankrev.hpp:119-183):
+    // E and G, the I / K / N / R updates, R, the permutations and the pivot gather
+    NodeRes rec_tail(DView a, int depth, NodeRes& res, size_t mark, const NodeRes& r1s, cudaEvent_t pending_r,
+                     bool rspine, LevelRec& LR) {
+        const size_t m = a.rows, n = a.cols;
+        const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;
+        const size_t r1 = r1s.rank;
+        DView E = a.sub(r1, n1, m1 - r1, n - n1);
+        DView G = a.sub(m1, r1, m - m1, n1 - r1);
         NodeRes r2s, r3s;                                        // :119-125 (E, G independent)
         std::unique_ptr<Driver> child;
         int cslot = can_fork(E, G) ? b.ws.acquire_slot() : -1;
@@ -1189,7 +1244,7 @@ struct Driver {
         res.rank = r1 + r2 + r3 + r4;
         if (use_factors) {  // leading factor = children's factors in gather order
             res.fac = new_factor(res.rank);
-            for (const NodeRes* c : {&r1s, &r2s, &r3s, &r4s})
+            for (const NodeRes* c : std::initializer_list<const NodeRes*>{&r1s, &r2s, &r3s, &r4s})
                 if (c->rank > 0) res.fac->kids.push_back(c->fac);
         }
         arena.reset(mark);  // children consumed (stream order protects the pending kernels)
@@ -1198,6 +1253,134 @@ struct Driver {
             levels.push_back(LR);
         }
         return res;
+    }
+
+    // ---- resume after a failed whole-matrix guess.  The speculative panel
+    // schedule failed at the base case starting at global offset pre_a; every pivot before it is
+    // final (the schedule solved its row panel, its column panel and -- recomputed from the backup by
+    // the caller -- its whole contribution to the trailing square).  resume(node, pre) evaluates
+    // tile_rec (rankrev.hpp:85-183) on a square node whose first `pre` rows / columns are that
+    // prefix: a first child wholly inside the prefix is taken as factored (full rank, P the identity,
+    // Q its blocks' column pivots); otherwise the path to the failed block recurses, and the node's
+    // TRSMs / GEMMs after it touch only the non-prefix parts (the prefix parts of D, Fb, E, G, H
+    // were applied by the schedule).  The prefix's column pivots reach the rows above their blocks
+    // once, at the end (block_cols_perm, as panel_finish does), never through the recursion.
+    struct Prefix {
+        const uint32_t* root = nullptr;                 // the matrix the offsets refer to
+        size_t ld = 0;
+        std::vector<uint32_t> gq;                       // block-local column pivot of each prefix column
+        std::vector<std::pair<size_t, size_t>> leaves;  // prefix base cases (offset, size)
+    };
+    NodeRes prefix_res(size_t o, size_t s, const Prefix& px) {
+        NodeRes r;
+        r.P = arena.alloc(std::max<size_t>(s, 1));
+        r.Q = arena.alloc(std::max<size_t>(s, 1));
+        r.rank = s;
+        std::vector<uint32_t> q(s);
+        for (size_t t = 0; t < s; ++t) q[t] = (uint32_t)t;
+        size_t lo = s, hi = 0;
+        for (const auto& lf : px.leaves) {
+            if (lf.first < o || lf.first + lf.second > o + s) continue;
+            for (size_t i = 0; i < lf.second; ++i) {
+                const size_t t = lf.first - o + i;
+                q[t] = (uint32_t)(lf.first - o + px.gq[lf.first + i]);
+                if (q[t] != t) {
+                    lo = std::min(lo, t);
+                    hi = std::max(hi, t + 1);
+                }
+            }
+        }
+        if (hi > lo) {
+            FFG_CUDA(cudaMemcpyAsync(r.Q + lo, q.data() + lo, (hi - lo) * 4, cudaMemcpyHostToDevice, b.st));
+            FFG_CUDA(cudaStreamSynchronize(b.st));  // q is a local buffer
+            r.qr = Range{lo, hi};
+        }
+        return r;
+    }
+    // a child's column permutation applied only past the prefix (its prefix part is applied later)
+    void apply_cols_from(const NodeRes& c, DView v, size_t from) {
+        Range r = c.qr;
+        r.lo = std::max(r.lo, from);
+        if (r.empty() || v.empty()) return;
+        perm_apply_range(b, v, 1, c.Q, r.lo, r.hi);
+    }
+    // After a failed guess on the square region a (speculative schedule drained): restore its
+    // trailing square [off, s) x [off, s) from the backup bk (ld ldb, same shape as a) and subtract
+    // the prefix pivots' whole contribution, L(rows >= off, prefix) U(prefix, cols >= off) -- the
+    // schedule's row and column panels of the prefix are final -- then resume tile_rec on a and
+    // apply the prefix blocks' column pivots to the rows above them inside a.
+    NodeRes recover(DView a, int depth, size_t off, const uint32_t* bk, size_t ldb, const Prefix& px) {
+        const size_t s = a.rows;
+        copy_block_dev(b, DView{const_cast<uint32_t*>(bk) + off * ldb + off, s - off, s - off, ldb},
+                       a.sub(off, off, s - off, s - off));
+        if (off > 0) pgemm_sub(b, a.sub(off, 0, s - off, off), a.sub(0, off, off, s - off), a.sub(off, off, s - off, s - off));
+        NodeRes res = resume(a, depth, off, px);
+        // prefix column pivots -> the rows above each block (panel_finish's block_cols_perm)
+        uint32_t* dq = nullptr;
+        for (const auto& lf : px.leaves) {
+            bool id = true;
+            for (size_t i = 0; i < lf.second; ++i) id = id && px.gq[lf.first + i] == i;
+            if (id || lf.first == 0) continue;
+            if (!dq) {
+                dq = arena.alloc(std::max<size_t>(off, 1));
+                FFG_CUDA(cudaMemcpyAsync(dq, px.gq.data(), off * 4, cudaMemcpyHostToDevice, b.st));
+                FFG_CUDA(cudaStreamSynchronize(b.st));
+            }
+            block_cols_perm_dev(b, a.sub(0, lf.first, lf.first, lf.second), dq + lf.first);
+        }
+        return res;
+    }
+
+    NodeRes resume(DView a, int depth, size_t pre, const Prefix& px) {
+        const size_t m = a.rows, n = a.cols;  // square, diagonal
+        if (pre == 0) return rec(a, depth);
+        if (m <= thr || pre >= m) throw Error(FFG_ERR_INTERNAL, "resume: prefix does not end at a base case");
+        NodeRes res;
+        res.P = arena.alloc(m);
+        res.Q = arena.alloc(n);
+        LevelRec LR{depth, false, {nullptr, nullptr, nullptr, nullptr}};
+        const size_t mark = arena.mark();
+        const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;
+        if (pre >= m1) {  // the failed block lies in R: A1 is a full-rank prefix node
+            const NodeRes r1s = prefix_res((size_t)(a.d - px.root) / px.ld, m1, px);
+            const size_t r1 = m1;
+            // D, Fb solved, E and G empty, H updated: the schedule did all of it
+            NodeRes r4s = resume(a.sub(m1, n1, m - m1, n - n1), depth + 1, pre - m1, px);
+            const size_t r4 = r4s.rank;
+            apply(r4s, 0, a.sub(m1, 0, m - m1, r1));                      // rankrev.hpp:156
+            apply_cols_from(r4s, a.sub(0, n1, r1, n - n1), pre - m1);     // :158
+            bool pinit = false, qinit = false;                            // :163-170 (r2 = r3 = 0)
+            compose(res.P, pinit, m, res.pr, 0, r1s.P, r1s.pr);
+            compose(res.P, pinit, m, res.pr, m1, r4s.P, r4s.pr);
+            compose(res.Q, qinit, n, res.qr, 0, r1s.Q, r1s.qr);
+            compose(res.Q, qinit, n, res.qr, n1, r4s.Q, r4s.qr);
+            // :174-179: every gather rotation is empty (r1 = m1 = n1, r2 = r3 = 0)
+            res.rank = r1 + r4;
+            arena.reset(mark);
+            return res;
+        }
+        // the failed block lies in A1
+        NodeRes r1s = resume(a.sub(0, 0, m1, n1), depth + 1, pre, px);  // :97
+        const size_t r1 = r1s.rank;
+        apply(r1s, 0, a.sub(0, n1, m1, n - n1));                        // :99 (never moves prefix rows)
+        apply_cols_from(r1s, a.sub(m1, 0, m - m1, n1), pre);            // :100
+        if (r1 > pre) {                                                 // :111-117, past the prefix
+            const size_t q = r1 - pre;
+            DView Lr = a.sub(pre, pre, q, q);  // trailing part of L1 \ U1
+            DView Dr = a.sub(pre, n1, q, n - n1);
+            DView M1r = a.sub(r1, pre, m1 - r1, q);
+            DView E = a.sub(r1, n1, m1 - r1, n - n1);
+            DView Fbr = a.sub(m1, pre, m - m1, q);
+            DView V1r = a.sub(pre, r1, q, n1 - r1);
+            DView G = a.sub(m1, r1, m - m1, n1 - r1);
+            DView H = a.sub(m1, n1, m - m1, n - n1);
+            if (!Dr.empty()) ptrsm(b, 0, r1s, Lr, Dr);
+            if (!E.empty() && !M1r.empty()) pgemm_sub(b, M1r, Dr, E);
+            if (!Fbr.empty()) ptrsm(b, 1, r1s, Lr, Fbr);
+            if (!G.empty() && !V1r.empty()) pgemm_sub(b, Fbr, V1r, G);
+            if (!H.empty()) pgemm_sub(b, Fbr, Dr, H);
+        }
+        return rec_tail(a, depth, res, mark, r1s, nullptr, false, LR);
     }
 
     void download(const NodeRes& res, size_t m, size_t n, uint32_t* P, uint32_t* Q) {
@@ -1226,13 +1409,12 @@ void base_dbg_dump();
 static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
     static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
     if (off || a.rows == 0 || a.cols == 0) return false;
-    // A base block of i.i.d. residues is rank deficient with probability ~1/p: with
-    // min(m, n) / thr blocks the guess holds with probability ~exp(-blocks / p).  Do not
-    // speculate where it is likely to fail (small fields: config 5's GF(251) at n = 32768 has
-    // ~2 rank-deficient blocks per matrix on average); FFG_SPEC_FORCE=1 overrides.
-    static const bool force = getenv("FFG_SPEC_FORCE") && atoi(getenv("FFG_SPEC_FORCE")) != 0;
+    // A base block of i.i.d. residues is rank deficient with probability ~1/p (config 5's GF(251)
+    // at n = 32768: ~2 such blocks per matrix).  A failed guess costs little on square input: the
+    // schedule's prefix is kept and tile_rec resumes at the failed block (Driver::recover).
+    // Non-square input reruns from scratch: skip the guess there when it is likely to fail.
     const double blocks = (double)std::min(a.rows, a.cols) / (double)std::max<size_t>(thr, 1);
-    if (!force && blocks > 0.25 * (double)b.F.p) return false;
+    if (a.rows != a.cols && blocks > 0.25 * (double)b.F.p) return false;
     if (b.ws.spec_rest > 0) {
         --b.ws.spec_rest;
         return false;
@@ -1314,7 +1496,9 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
                                uint32_t* P, uint32_t* Q, size_t& rank) {
     uint32_t* bk = nullptr;
     FFG_CUDA(cudaMallocAsync(&bk, n * n * 4, b.st));
-    bool ok = false;
+    bool ok = false, resumable = false;
+    size_t fail_off = 0;
+    Driver::Prefix px;
     {
         Driver drv(b, thr, n, n);
         drv.spec = true;
@@ -1384,7 +1568,32 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             ok = false;
             drv.need(drv.b.st, n);  // bands no operation touched yet are still pristine: back them up too
         }
-        if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
+        if (!ok) {
+            FFG_CUDA(cudaDeviceSynchronize());  // every speculative kernel and copy retired
+            if (drv.failed_at(fail_off)) {
+                drv.prefix_of(fail_off, px.gq, px.leaves);
+                resumable = true;
+            }
+        }
+    }
+    if (!ok && resumable) {
+        // resume tile_rec at the failed block on the device copy (every band is uploaded and backed
+        // up by now), then bring the whole matrix back
+        Driver rdrv(b, thr, n, n);
+        rdrv.node_spec_max = n;
+        px.root = d;
+        px.ld = n;
+        NodeRes res = rdrv.recover(DView{d, n, n, n}, 0, fail_off, bk, n, px);
+        rdrv.finish();
+        FFG_CUDA(cudaMemcpy2DAsync(host, lda * 4, d, n * 4, n * 4, n, cudaMemcpyDeviceToHost, rdrv.b.st));
+        rdrv.download(res, n, n, P, Q);  // synchronizes
+        rank = res.rank;
+        if (fail_off == 0)
+            b.ws.spec_failed();
+        else
+            b.ws.spec_fails = 0;
+        FFG_CUDA(cudaFreeAsync(bk, b.st));
+        return true;
     }
     if (!ok) {
         copy_block_dev(b, DView{bk, n, n, n}, DView{d, n, n, n});
@@ -1408,8 +1617,9 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
         const size_t ldb = panel ? a.ld : n;
         FFG_CUDA(cudaMallocAsync(&bk, m * ldb * 4, b.st));
         if (!panel) copy_block_dev(b, a, DView{bk, m, n, ldb});
-        bool ok = false;
-        size_t rank = 0;
+        bool ok = false, resumable = false;
+        size_t rank = 0, fail_off = 0;
+        Driver::Prefix px;
         {
             Driver drv(b, threshold, m, n);
             drv.spec = true;
@@ -1450,6 +1660,10 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             }
             if (!ok && drv.panel) drv.need(drv.b.st, n);  // bands nothing touched yet are still pristine
             if (!ok) FFG_CUDA(cudaDeviceSynchronize());  // all speculative work retired
+            if (!ok && drv.panel && drv.failed_at(fail_off)) {
+                drv.prefix_of(fail_off, px.gq, px.leaves);
+                resumable = true;
+            }
         }
         static const bool log = getenv("FFG_SPEC_LOG") != nullptr;
         if (log) fprintf(stderr, "SPEC %s (panel %d, %zu base cases enqueued)\n", ok ? "ok" : "failed", (int)(m == n), (size_t)b.ws.base_seq.load());
@@ -1457,6 +1671,26 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             b.ws.spec_fails = 0;
             FFG_CUDA(cudaFreeAsync(bk, b.st));
             return rank;
+        }
+        if (resumable) {
+            // the pivots before the failed block are final: resume tile_rec from there (the rest of
+            // the matrix is recomputed from the backup), node-level guesses again on fresh subproblems
+            Driver rdrv(b, threshold, m, n);
+            rdrv.node_spec_max = std::min(m, n);
+            Driver::Prefix& rx = px;
+            rx.root = a.d;
+            rx.ld = a.ld;
+            NodeRes res = rdrv.recover(a, 0, fail_off, bk, ldb, rx);
+            rdrv.finish();
+            rdrv.download(res, m, n, P, Q);
+            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            if (fail_off == 0)
+                b.ws.spec_failed();  // the very first block: likely deficient everywhere, rest a few calls
+            else
+                b.ws.spec_fails = 0;
+            static const bool log2 = getenv("FFG_SPEC_LOG") != nullptr;
+            if (log2) fprintf(stderr, "SPEC resumed at offset %zu of %zu\n", fail_off, m);
+            return res.rank;
         }
         copy_block_dev(b, DView{bk, m, n, ldb}, a);  // a copy kernel: the DMA engines are far slower HBM to HBM
         FFG_CUDA(cudaFreeAsync(bk, b.st));

@@ -72,6 +72,7 @@ struct BaseInfo {
     uint32_t seq;        // written last: the launch's sequence number (host spins on it)
     uint32_t spec_fail;  // sticky: a speculative launch (seq & SPEC_BIT) did not see full rank +
                          // identity permutations
+    uint32_t fail_seq;   // the sequence number of the first launch that raised spec_fail
 };
 constexpr uint32_t SPEC_BIT = 0x80000000u;
 // one-CTA rr_base kernel: writes the permuted packed block, P/Q index arrays and info; with
