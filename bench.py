@@ -60,7 +60,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fgemm", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="skip the extra CUPTI-profiled step (roofline)")
-    a = ap.parse_args()
+    # under the self-relaunch (--gpus N outside torchrun) the arguments travel in the environment:
+    # torchrun's own parser would otherwise claim abbreviations such as --n
+    argv = json.loads(os.environ["FFG_BENCH_ARGV"]) if "FFG_BENCH_ARGV" in os.environ else None
+    a = ap.parse_args(argv)
     a.warmup = max(a.warmup, 3) if a.impl == "ours" else a.warmup
     if a.n is None:
         a.n = 8192 if a.workload == "fgemm" else 16384
@@ -611,8 +614,9 @@ def relaunch_under_torchrun(a):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+    env = dict(os.environ, FFG_BENCH_ARGV=json.dumps(sys.argv[1:]))
+    return subprocess.call(cmd, env=env)
 
 
 def main():

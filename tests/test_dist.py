@@ -9,6 +9,8 @@ import pytest
 
 import paper_1402_3501_b200 as G
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 def test_partition_covers_disjoint_aligned():
     for world in (1, 2, 3, 4, 5, 8):
@@ -119,3 +121,30 @@ def test_two_rank_gloo_decomposition(oracle_lib):
 
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     mp.spawn(_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+def test_bench_relaunches_itself_under_torchrun_for_gpus_n():
+    """`bench.py --gpus 2` outside torchrun re-executes itself with one process per rank (CPU check
+    through the reference arm: rank 0 prints the line, rank 1 exits cleanly)."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--n", "256", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["same_size_as_config"] is True
+
+
+def test_bench_rejects_world_mismatch():
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--n", "256"], capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)
