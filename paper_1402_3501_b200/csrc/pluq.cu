@@ -148,9 +148,10 @@ struct Driver {
         FFG_CUDA(cudaEventRecord(e, user.st));
         FFG_CUDA(cudaStreamWaitEvent(b.st, e, 0));
         static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
-        // partitioned (multi-GPU) runs keep one stream: every rank must issue its NCCL
-        // exchanges in the same order, and the replicated control flow guarantees that
-        use_streams = !no_streams && !bl.ws.dist.active();
+        // partitioned (multi-GPU) runs keep their side streams: every split operation (the only ones
+        // with a collective) is moved onto the critical stream (pgemm_sub / ptrsm), so all ranks issue
+        // their collectives in one stream and one order
+        use_streams = !no_streams;
         panel_streams = !no_streams;
         {
             static int sms = -1;
@@ -261,7 +262,8 @@ struct Driver {
                 : std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2));
         static const size_t gmin = getenv("FFG_FORK_MIN") ? (size_t)atoll(getenv("FFG_FORK_MIN")) : 0;
         const size_t gm = gmin ? gmin : 2 * thr;  // smallest G worth a host thread
-        return max_threads > 0 && !spec && use_streams && b.ws.prof.mode != 1 && !use_factors && !E.empty() && !G.empty() &&
+        return max_threads > 0 && !spec && use_streams && !b.ws.dist.active() && b.ws.prof.mode != 1 && !use_factors &&
+               !E.empty() && !G.empty() &&
                std::min(G.rows, G.cols) > gm && std::min(E.rows, E.cols) > thr &&
                active_children().load() < max_threads;
     }
@@ -359,13 +361,43 @@ struct Driver {
         }
     }
 
+    // Partitioned runs abort a failed guess only at deterministic points: wait for the base case
+    // spec_window launches back to complete and abort iff the FIRST failure (its sequence number,
+    // which every rank computes identically) is at or before it -- whatever else any rank's device
+    // has reached by then -- so every rank stops after the same launch and issues the same
+    // collectives.
+    void spec_throttle_det() {
+        if (spec_seqs.size() < spec_window) return;
+        const uint32_t target = spec_seqs[spec_seqs.size() - spec_window] & ~SPEC_BIT;
+        volatile uint32_t* sq = &info_host->seq;
+        auto at_or_after = [](uint32_t x, uint32_t y) { return ((x - y) & ~SPEC_BIT) < 0x40000000u; };
+        for (uint64_t it = 0;; ++it) {
+            const uint32_t cur = *sq & ~SPEC_BIT;
+            if (at_or_after(cur, target)) break;
+            if (it > (1u << 24)) {
+                FFG_CUDA(cudaStreamSynchronize(b.st));
+                break;
+            }
+#if defined(__x86_64__) || defined(__i386__)
+            __builtin_ia32_pause();
+#endif
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) {
+            const uint32_t fs = *reinterpret_cast<volatile uint32_t*>(&info_host->fail_seq) & ~SPEC_BIT;
+            if (at_or_after(target, fs)) throw SpecAbort{};
+        }
+    }
+
     bool base_wrote_inv = false;  // the last speculative base case also wrote its factor inverses
     NodeRes base(DView a, NodeRes res, uint32_t* inv_out = nullptr) {
         if (spec) {
             if (a.rows > 64 || a.cols > 64) throw SpecAbort{};  // only the slab kernel checks
-            if (!b.ws.dist.active()) {  // partitioned: every rank enqueues the whole recursion
+            if (!b.ws.dist.active()) {
                 if (*reinterpret_cast<volatile uint32_t*>(&info_host->spec_fail)) throw SpecAbort{};
                 spec_throttle();
+            } else {
+                spec_throttle_det();  // partitioned: abort at the same point on every rank
             }
             const uint32_t seq = ((b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT) | SPEC_BIT;
             // (inverses inside the base kernel by substitution measured slower than the separate
@@ -437,9 +469,24 @@ struct Driver {
         }
     }
     // C -= A B, split along C's longer side
+    // a split operation requested on a side stream runs on the critical stream (joined both ways)
+    template <class Fn>
+    void on_critical(const Blas& bb, Fn&& fn) {
+        if (bb.st == b.st) {
+            fn(b);
+            return;
+        }
+        wait(b.st, mark_event(bb.st));
+        fn(b);
+        wait(bb.st, mark_event(b.st));
+    }
     void pgemm_sub(const Blas& bb, DView A, DView B, DView C) {
         if (!split((double)C.rows * C.cols * A.cols)) {
             gemm_sub(bb, A, B, C);
+            return;
+        }
+        if (bb.st != b.st) {
+            on_critical(bb, [&](const Blas& c) { pgemm_sub(c, A, B, C); });
             return;
         }
         const int axis = C.rows >= C.cols ? 0 : 1;
@@ -464,6 +511,10 @@ struct Driver {
         const double w = side == 0 ? (double)B.cols : (double)B.rows;
         if (!split(0.5 * (double)T.rows * T.rows * w)) {
             one(B);
+            return;
+        }
+        if (bb.st != b.st) {
+            on_critical(bb, [&](const Blas& cb) { ptrsm(cb, side, c, T, B); });
             return;
         }
         if (side == 0)
@@ -1100,7 +1151,7 @@ struct Driver {
                 // top-left quadrant; update that first on the critical stream, the rest on a
                 // low-priority stream that R waits for only after its first child
                 const size_t hm1 = (H.rows + 1) / 2, hn1 = (H.cols + 1) / 2;
-                if (use_streams && E.empty() && G.empty() && std::min(H.rows, H.cols) > thr) {
+                if (use_streams && !b.ws.dist.active() && E.empty() && G.empty() && std::min(H.rows, H.cols) > thr) {
                     gemm_sub(b, Fb.sub(0, 0, hm1, r1), D.sub(0, 0, r1, hn1), H.sub(0, 0, hm1, hn1));
                     Blas la = on(lookahead(depth));
                     la.sm_cap = lookahead_sms;  // keep SMs free for the critical path
@@ -1468,7 +1519,7 @@ static size_t node_spec_max(const Blas& b, const DView& a, size_t thr, const Dri
     static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
     const char* e = getenv("FFG_NODE_SPEC");
     size_t s = e ? (size_t)atoll(e) : 1024;
-    if (off || s == 0 || !drv.use_streams || b.ws.dist.active() || thr > 64) return 0;
+    if (off || s == 0 || !drv.use_streams || thr > 64) return 0;
     const double blocks_all = (double)std::min(a.rows, a.cols) / (double)std::max<size_t>(thr, 1);
     if (blocks_all <= 0.25 * (double)b.F.p) return 0;  // the whole-matrix guess was tried instead
     static const double risk = getenv("FFG_NODE_SPEC_RISK") ? atof(getenv("FFG_NODE_SPEC_RISK")) : 0.1;
