@@ -242,9 +242,11 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         if (owner) {
             bi_row(lv[0], fz[0], q);
             publish(k + 1);  // shifts: the rows after it move down one slot
-            bi_row(lv[0], fz[0], q);
-            bi_row(lv[1], fz[1], q);
+#ifndef BI_CHAIN_ONLY
+            bi_row(lv[0], fz[0], q);  // (rows past the block's last are stale copies: updating them
+            bi_row(lv[1], fz[1], q);  //  unconditionally measured faster than branching around them)
             bi_row(lv[2], fz[2], q);
+#endif
         } else {
             bi_row(lv[0], fz[0], q);
             bi_row(lv[1], fz[1], q);
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         // packed L \ U (logical columns) and inv(L)[i][j] = I[i][j] D_j / D_i
 #pragma unroll 1
         for (uint32_t idx = tid; idx < t * t; idx += BI_THREADS) {
-            const uint32_t i = idx / t, j = idx - i * t;
+            const uint32_t i = t == 64 ? idx >> 6 : idx / t, j = idx - i * t;
             const bool lo = j < i, dg = j == i;
             const uint32_t x = lo ? sm.Ln[i][j] : (dg ? sm.pv[i] : sm.pub[i][j]);
             const uint32_t m = lo ? sm.invp[j] : sm.invd[i], mf = lo ? sm.invpf[j] : sm.invdf[i];
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         uint32_t* invU = inv + (size_t)t * t;
 #pragma unroll 1
         for (uint32_t idx = tid; idx < t * t; idx += BI_THREADS) {
-            const uint32_t s = idx / t, q = idx - s * t;
+            const uint32_t s = t == 64 ? idx >> 6 : idx / t, q = idx - s * t;
             invU[idx] = sm.S[s][q];
         }
     }

@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-rm -f paper_1402_3501_b200/build/baseinv.o
-FFG_NVCC_EXTRA="-DBI_DBG" python -m paper_1402_3501_b200.build > /dev/null 2>&1
-FFG_BI_DBG=1 python scripts/base_micro.py --reps 3 2>&1 | grep BI_DBG | tail -2
+ncu --set full --import-source on -k regex:rr_base_inv -s 5 -c 1 -o gpurun_out/bi_src python scripts/base_micro.py --reps 3 > gpurun_out/ncu_bi.log 2>&1
+ncu -i gpurun_out/bi_src.ncu-rep --page source --csv --print-source sass > gpurun_out/bi_sass.csv 2>&1
+ncu -i gpurun_out/bi_src.ncu-rep --page raw --csv > gpurun_out/bi_raw.csv 2>&1
+ls -la gpurun_out/bi_*
