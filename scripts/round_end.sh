@@ -1,34 +1,29 @@
 #!/bin/bash
 # Round-end style evidence run on one B200 (writes gpurun_out/*); every ncu pass runs only
 # after the same command exited 0 without ncu.
-set -x
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "ref rc=$?"
-python bench.py --workload lru --steps 1 --warmup 1 --no-cpu --no-fgemm > gpurun_out/bench_config4.json 2> gpurun_out/bench_config4.err
-python bench.py --p 251 --n 32768 --steps 2 --warmup 1 --no-cpu --no-fgemm > gpurun_out/bench_config5.json 2> gpurun_out/bench_config5.err
+python bench.py --workload lru --steps 2 --warmup 3 --no-cpu --no-fgemm > gpurun_out/bench_config4.json 2> gpurun_out/bench_config4.err
+python bench.py --p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-fgemm > gpurun_out/bench_config5.json 2> gpurun_out/bench_config5.err
 python scripts/trace_pluq.py --n 16384 --json gpurun_out/trace_n16384.json > gpurun_out/trace_n16384.txt 2>&1
+# launch list of one bench step (durations only)
+python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/bench_small.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file gpurun_out/launches_bench.csv \
+    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/ncu_bench.log 2>&1
+# the fused base case + inverses inside an n = 16384 PLUQ (full set, with source)
+python scripts/prof_pluq.py --n 16384 > gpurun_out/prof_pluq_plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"rr_base_inv|leaf_apply|panel_update|panel_mini" \
+    -s 200 -c 8 -o gpurun_out/panel_full python scripts/prof_pluq.py --n 16384 > gpurun_out/ncu_panel.log 2>&1
+python scripts/ncu_summary.py gpurun_out/panel_full.ncu-rep --label "panel-chain kernels inside an n = 16384 PLUQ (config 3)" \
+  > gpurun_out/ncu_panel_summary.json 2>/dev/null
 # fgemm 8192^3: one full ncu capture of the tcgen05 kernel
 python scripts/prof_gemm.py > gpurun_out/prof_gemm_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:modgemm -s 1 -c 1 -o gpurun_out/gemm_full python scripts/prof_gemm.py > gpurun_out/ncu_gemm.log 2>&1
 python scripts/ncu_summary.py gpurun_out/gemm_full.ncu-rep --label "fgemm 8192^3 C <- C - A*B mod 131071 (config 2)" \
   > gpurun_out/ncu_gemm_summary.json 2>/dev/null
-# the limb split (HBM-bound) of the 8192^3 fgemm operands
-ncu --set full --clock-control none -k regex:split_kernel -c 2 -o gpurun_out/split_full python scripts/prof_gemm.py \
-  > gpurun_out/ncu_split.log 2>&1
-python scripts/ncu_summary.py gpurun_out/split_full.ncu-rep --label "split_kernel: limb planes of the 8192^3 fgemm operands" \
-  > gpurun_out/ncu_split_summary.json 2>/dev/null
-# the panel schedule's latency-bound kernels in the middle of an n = 16384 PLUQ
-python scripts/prof_pluq.py --n 16384 > gpurun_out/prof_pluq_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"leaf_apply|panel_inv|panel_corner|rr_base_spec" \
-    -s 400 -c 8 -o gpurun_out/panel_full python scripts/prof_pluq.py --n 16384 > gpurun_out/ncu_panel.log 2>&1
-python scripts/ncu_summary.py gpurun_out/panel_full.ncu-rep --label "panel kernels inside an n = 16384 PLUQ (config 3)" \
-  > gpurun_out/ncu_panel_summary.json 2>/dev/null
-# launch list of one bench step (durations only)
-python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/bench_small.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/ncu_bench.log 2>&1
 # DRAM traffic of every tensor-core GEMM launch inside one n = 16384 PLUQ
 FFG_GEMM_LOG=1 python scripts/gemm_shapes.py --run --n 16384 2> gpurun_out/shapes.log && \
   FFG_GEMM_LOG=1 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
