@@ -55,9 +55,10 @@ struct BiSmem {
     uint32_t I[64][BI_SS];   // slow path: I part
     uint32_t pv[64], pvf[64], D[64];
     uint32_t invd[64], invdf[64], invp[64], invpf[64], Dd[64], Ddf[64];
-    uint32_t pcol[64];       // CTA 0: physical column of pivot t; CTA 1: physical row of pivot t
+    uint32_t pcol[64];       // physical column of logical column t (the block's Q)
+    uint32_t perm[64];       // current logical -> physical column order (CTA 1: rows of A^T)
     uint64_t full[64];       // pivot row k published
-    uint32_t fail, k0;
+    uint32_t fail, k0, cmin;
 };
 
 __device__ __forceinline__ uint32_t bi_red4p(uint32_t x, uint32_t p) {  // [0, 4p) -> [0, p)
@@ -133,10 +134,14 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     BiSmem& sm = *reinterpret_cast<BiSmem*>(bi_raw);
     const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const bool tr = blockIdx.x == 1;
-    if (tid < 64) ptx::mbar_init(&sm.full[tid], 32);
+    if (tid < 64) {
+        ptx::mbar_init(&sm.full[tid], 32);
+        sm.perm[tid] = tid;
+    }
     if (tid == 0) {
         sm.fail = 0u;
         sm.k0 = t;
+        sm.cmin = 64u;
     }
     ptx::fence_mbar_init();
     BI_STAMP(0);
@@ -160,16 +165,32 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     // both CTAs hold the input before CTA 0 may overwrite it (a 2-CTA cluster: co-scheduled)
     bi_cluster_sync();
     BI_STAMP(2);
+    // A zero Schur diagonal at step k0 with a nonzero further right in row k0 (a column pivot,
+    // ~1/p per step): rr_base takes the first such column (rankrev.hpp:29-78, columns rotated so
+    // the ones not yet pivots stay in ascending order), so the elimination restarts on the block
+    // with that logical column order -- the steps before k0 repeat unchanged.  No such column: the
+    // block is rank deficient and the guess fails.
+    uint32_t passes = 0;
+    uint64_t ph = 0;  // bit k: parity of the phase pivot row k's mbarrier is in (flips per publish)
+#pragma unroll 1
+    for (;;) {
+    ++passes;
+#ifdef BI_RESTART_DBG
+    if (tid == 0) printf("cta %d start pass %u\n", (int)tr, passes);
+#endif
     // this warp's block: rows r0 .. r0 + 3, slot 0 = the next one to become a pivot
     const uint32_t r0 = 4 * (BI_WARPS - 1 - w);
     uint32_t nxt = r0, left = r0 < t ? min(4u, t - r0) : 0u;
     uint32_t lv[4][2], fz[4][2];
+    {
+        const uint32_t c0 = sm.perm[lane], c1 = sm.perm[lane + 32];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        const uint32_t i = r0 + s;
-        lv[s][0] = tr ? sm.S[lane][i] : sm.S[i][lane];
-        lv[s][1] = tr ? sm.S[lane + 32][i] : sm.S[i][lane + 32];
-        fz[s][0] = fz[s][1] = 0u;
+        for (int s = 0; s < 4; ++s) {
+            const uint32_t i = r0 + s, ci = sm.perm[i];
+            lv[s][0] = tr ? sm.S[lane][ci] : sm.S[i][c0];
+            lv[s][1] = tr ? sm.S[lane + 32][ci] : sm.S[i][c1];
+            fz[s][0] = fz[s][1] = 0u;
+        }
     }
     // forwarded pivot (the warp's own last publish) and the publish itself
     bool fwd = false;
@@ -220,7 +241,17 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
             q.f0 = ff0;
             q.f1 = ff1;
         } else {
-            ptx::mbar_wait(&sm.full[k], 0);
+#ifdef BI_RESTART_DBG
+            {
+                uint32_t it = 0;
+                while (!ptx::mbar_try_wait(&sm.full[k], (uint32_t)(ph >> k) & 1u)) {
+                    if (++it == (1u << 22) && lane == 0)
+                        printf("HANG cta %d pass %u warp %u step %u nxt %u left %u\n", (int)tr, passes, w, k, nxt, left);
+                }
+            }
+#else
+            ptx::mbar_wait(&sm.full[k], (uint32_t)(ph >> k) & 1u);
+#endif
             q.pv = sm.pv[k];
             q.pvp = sm.pvf[k];
             q.b0 = sm.pub[k][lane];
@@ -258,122 +289,49 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     // the last pivot row is published but never consumed inside the loop: check its diagonal here
     if (tid == 0 && sm.k0 == t && t > 0 && sm.pv[t - 1] == 0u) sm.k0 = t - 1;
     __syncthreads();
-    BI_STAMP(3);
     const uint32_t k0 = sm.k0;
-    if (k0 < t) {
-        // ---- slow path from step k0: rows >= k0 (still in registers) into S / I with explicit A / I
-        // parts, every I column rescaled to the plain fraction-free form (x D_j)
-        if (tid == 0) {
-            uint32_t d = 1u;
-            for (uint32_t k = 0; k <= k0 && k < 64; ++k) {
-                sm.D[k] = d;
-                if (k < k0) d = mul_mod(d, sm.pv[k], p, mu);
-            }
+    if (k0 >= t) break;
+    // the first logical column c > k0 whose entry in the reduced row k0 is nonzero -- CTA 0 reads
+    // the published row k0, CTA 1 the column-k0 entries of its unpublished rows (= the same row of
+    // the transposed Schur complement, times the same D_k0)
+    if (!tr) {
+        if (w == 0) {
+            const bool z0 = lane > k0 && lane < t && sm.pub[k0][lane] != 0u;
+            const bool z1 = lane + 32 > k0 && lane + 32 < t && sm.pub[k0][lane + 32] != 0u;
+            const uint32_t m0 = __ballot_sync(BI_FULL, z0), m1 = __ballot_sync(BI_FULL, z1);
+            if (lane == 0) sm.cmin = m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : 64u);
         }
-        __syncthreads();
+    } else {
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
             if ((uint32_t)s >= left) break;
+            const uint32_t x = bi_red4p(__shfl_sync(BI_FULL, (k0 >> 5) ? lv[s][1] : lv[s][0], k0 & 31), p);
             const uint32_t i = nxt + s;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t j = lane + 32 * h;
-                const uint32_t f = bi_red4p(fz[s][h], p), l = bi_red4p(lv[s][h], p);
-                sm.S[i][j] = j < k0 ? f : l;
-                sm.I[i][j] = j < k0 ? mul_mod(l, sm.D[j], p, mu) : 0u;
-            }
+            if (lane == 0 && x != 0u && i > k0 && i < t) atomicMin(&sm.cmin, i);
         }
-        if (w == 0) {  // row k0 was published (its zero diagonal stopped the fast path): back into S / I
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t j = lane + 32 * h;
-                const uint32_t v = sm.pub[k0][j];
-                sm.S[k0][j] = j < k0 ? sm.Ln[k0][j] : (j == k0 ? sm.pv[k0] : v);
-                sm.I[k0][j] = j < k0 ? mul_mod(v, sm.D[j], p, mu) : 0u;
-            }
-        }
-        for (uint32_t idx = tid; idx < k0 * 64; idx += BI_THREADS) {  // the published rows' I parts
-            const uint32_t i = idx >> 6, j = idx & 63;
-            if (j <= i) sm.pub[i][j] = mul_mod(sm.pub[i][j], sm.D[j], p, mu);
-        }
-        uint64_t used = k0 ? (~0ull >> (64 - k0)) : 0ull;  // CTA 0: pivot columns; CTA 1: pivot rows
-        if (tid < k0) sm.pcol[tid] = tid;
-        __syncthreads();
-        for (uint32_t k = k0; k < t; ++k) {
-            if (w == 0) {
-                uint32_t c;
-                if (!tr) {  // first nonzero unused column of pivot row k
-                    const bool z0 = lane < t && !((used >> lane) & 1u) && sm.S[k][lane] != 0u;
-                    const bool z1 = lane + 32 < t && !((used >> (lane + 32)) & 1u) && sm.S[k][lane + 32] != 0u;
-                    const uint32_t m0 = __ballot_sync(BI_FULL, z0), m1 = __ballot_sync(BI_FULL, z1);
-                    c = m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : 64u);
-                } else {  // first unused row of A^T with a nonzero in column k
-                    const bool z0 = lane < t && !((used >> lane) & 1u) && sm.S[lane][k] != 0u;
-                    const bool z1 = lane + 32 < t && !((used >> (lane + 32)) & 1u) && sm.S[lane + 32][k] != 0u;
-                    const uint32_t m0 = __ballot_sync(BI_FULL, z0), m1 = __ballot_sync(BI_FULL, z1);
-                    c = m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : 64u);
-                }
-                if (lane == 0) {
-                    if (c == 64u || (!allow_q && c != k)) {
-                        sm.fail = 1u;
-                        // keep going on a harmless choice (the outputs are discarded): any unused index
-                        for (uint32_t r = 0; r < 64; ++r)
-                            if (!((used >> r) & 1u)) {
-                                c = r;
-                                break;
-                            }
-                    }
-                    sm.pcol[k] = c;
-                    const uint32_t pvk = tr ? sm.S[c][k] : sm.S[k][c];
-                    sm.pv[k] = pvk;
-                    if (k + 1 < 64) sm.D[k + 1] = mul_mod(sm.D[k], pvk, p, mu);
-                    sm.I[tr ? c : k][k] = sm.D[k];  // the pivot row's own I part in column k
-                }
-            }
-            __syncthreads();
-            const uint32_t c = sm.pcol[k], pvk = sm.pv[k];
-            const uint32_t prow = tr ? c : k;
-            used |= 1ull << c;
-            // rows not yet pivots: CTA 0 rows > k; CTA 1 unused rows
-            for (uint32_t idx = tid; idx < 64 * 64; idx += BI_THREADS) {
-                const uint32_t i = idx >> 6, j = idx & 63;
-                const bool active = tr ? (i < t && !((used >> i) & 1u)) : (i > k && i < t);
-                if (!active) continue;
-                const uint32_t pc = tr ? k : c;  // pivot column (physical)
-                const uint32_t numer = sm.S[i][pc];
-                // A part: columns not yet pivots (CTA 0: unused columns; CTA 1: columns > k)
-                const bool live_a = tr ? (j > k) : !((used >> j) & 1u);
-                if (live_a && j < t)
-                    sm.S[i][j] = bi_sub(mul_mod(sm.S[i][j], pvk, p, mu), mul_mod(numer, sm.S[prow][j], p, mu), p);
-                if (j <= k)
-                    sm.I[i][j] = bi_sub(mul_mod(sm.I[i][j], pvk, p, mu), mul_mod(numer, sm.I[prow][j], p, mu), p);
-            }
-            __syncthreads();
-        }
-        // final rows in logical order into pub (pivot rows k >= k0) and L numerators into Ln; the
-        // rows pivoted before k0 take the later column pivots too (rr_base rotates whole columns)
-        if (!tr) {
-            for (uint32_t idx = tid; idx < k0 * 64; idx += BI_THREADS) sm.S[idx >> 6][idx & 63] = sm.pub[idx >> 6][idx & 63];
-            __syncthreads();
-            for (uint32_t idx = tid; idx < k0 * 64; idx += BI_THREADS) {
-                const uint32_t kk = idx >> 6, j = idx & 63;
-                if (j >= k0 && j < t) sm.pub[kk][j] = sm.S[kk][sm.pcol[j]];
-            }
-            __syncthreads();
-        }
-        for (uint32_t idx = tid; idx < 64 * 64; idx += BI_THREADS) {
-            const uint32_t kk = idx >> 6, j = idx & 63;
-            if (kk < k0 || kk >= t) continue;
-            const uint32_t prow = tr ? sm.pcol[kk] : kk;
-            if (j <= kk)
-                sm.pub[kk][j] = sm.I[prow][j];
-            else if (j < t)
-                sm.pub[kk][j] = tr ? sm.S[prow][j] : sm.S[prow][sm.pcol[j]];
-            if (!tr && j < kk && j < t) sm.Ln[kk][j] = sm.S[kk][sm.pcol[j]];  // frozen numerators
-        }
-    } else if (tid < 64) {
-        sm.pcol[tid] = tid;
     }
+    __syncthreads();
+    const uint32_t c = sm.cmin;
+#ifdef BI_RESTART_DBG
+    if (tid == 0) printf("cta %d pass %u k0 %u c %u t %u allow %u\n", (int)tr, passes, k0, c, t, allow_q);
+#endif
+    if (c >= t || !allow_q || passes > 64) {  // rank deficient (or no column pivots allowed): the guess fails
+        if (tid == 0) sm.fail = 1u;
+        break;
+    }
+    __syncthreads();  // every thread has read k0 and c
+    if (tid == 0) {   // rotate logical columns k0..c: c moves to k0, the rest keeps its order
+        const uint32_t pc = sm.perm[c];
+        for (uint32_t j = c; j > k0; --j) sm.perm[j] = sm.perm[j - 1];
+        sm.perm[k0] = pc;
+        sm.k0 = t;
+        sm.cmin = 64u;
+    }
+    ph ^= (2ull << k0) - 1ull;  // rows 0..k0 were published in this pass (k0 = 63: all bits)
+    __syncthreads();
+    }  // restart
+    BI_STAMP(3);
+    if (tid < 64) sm.pcol[tid] = sm.perm[tid];
     __syncthreads();
     // ---- one inverse: D_k = prod_{j<k} pv_j -> 1/D_k and 1/pv_k = D_k / D_{k+1}; plus the I-column
     // scales Dd_j (= D_j on the fast path, 1 after the slow path rescaled them).  Branch-free scans.
@@ -399,7 +357,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         const uint32_t iD2 = bi_mulmod(tinv, lane == 31 ? 1u : sufx, pd, pinv);
         const uint32_t iD1 = bi_mulmod(iD2, v1, pd, pinv);
         const uint32_t ip0 = bi_mulmod(D0, iD1, pd, pinv), ip1 = bi_mulmod(D1, iD2, pd, pinv);
-        const uint32_t s0 = k0 < t ? 1u : D0, s1 = k0 < t ? 1u : D1;
+        const uint32_t s0 = D0, s1 = D1;
         sm.invd[e0] = iD0;
         sm.invp[e0] = ip0;
         sm.Dd[e0] = s0;

@@ -18,6 +18,8 @@
 // "O = N - J*V2" describes.  Outputs equal the fixed reference everywhere and
 // the unmodified reference wherever r2 == 0 or r3 == 0 (all full-rank input).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cstring>
 #include <deque>
@@ -29,6 +31,8 @@
 #include "pluq.cuh"
 
 namespace ffg {
+
+static bool panel_no_direct();
 
 namespace {
 
@@ -830,6 +834,8 @@ struct Driver {
         const cudaEvent_t f = mark_event(b.st);
         Blas sa = on(side_stream(0)), sb = on(side_stream(1));
         sa.sm_cap = sb.sm_cap = side_sms;
+        static const bool side_direct = getenv("FFG_SIDE_DIRECT") && atoi(getenv("FFG_SIDE_DIRECT")) != 0;
+        if (side_direct) sa.no_direct = sb.no_direct = false;
         wait(sa.st, f);
         wait(sb.st, f);
         DView rightA{a.d + m, t1, pcols - (c0 + m), pld};       // A1 rows, columns beyond the node
@@ -947,6 +953,10 @@ struct Driver {
                 panel_update_dev(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
             Blas sc = on(side_stream(2)), sd = on(side_stream(3));
             sc.sm_cap = sd.sm_cap = defer_sms;  // leave SMs for the critical stream's small kernels
+            // these GEMMs gate the next two-leaf node (flush_deferred): FFG_DEFER_DIRECT=1 lets the
+            // single-launch direct kernel take the ones with K <= 128 (no limb split round trip)
+            static const bool defer_direct = getenv("FFG_DEFER_DIRECT") && atoi(getenv("FFG_DEFER_DIRECT")) != 0;
+            if (defer_direct) sc.no_direct = sd.no_direct = false;
             for (const Blas* sx : {&sc, &sd}) {
                 wait(sx->st, forked);
                 for (cudaEvent_t e : deferred) wait(sx->st, e);
@@ -1019,9 +1029,17 @@ struct Driver {
     // rerun exactly when its guess fails.  A full-rank node's result is the unique one (P the
     // identity, Q its blocks' column pivots), so the exact parent continues unchanged.
     size_t node_spec_max = 0;
-    int node_spec_fails = 0;  // consecutive failures: stop trying after 3
+    int node_spec_fails = 0;  // consecutive failures at a node's first block: stop trying after 3
+    const uint32_t* spec_dead = nullptr;  // origin of the last node whose first block failed
+    static double host_ms() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+    static inline const uint32_t* g_log_root = nullptr;  // FFG_NODE_LOG: offsets relative to the entry's matrix
+    static inline size_t g_log_ld = 1;
     bool try_node_spec(DView a, int depth, NodeRes& res) {
         const size_t m = a.rows;
+        static const bool nlog = getenv("FFG_NODE_LOG") != nullptr;
+        const double t0 = nlog ? host_ms() : 0.0;
         uint32_t* bk = nullptr;
         FFG_CUDA(cudaMallocAsync(&bk, m * m * 4, b.st));
         copy_block_dev(b, a, DView{bk, m, m, m});
@@ -1040,6 +1058,7 @@ struct Driver {
             sub.prows = m;
             sub.pcols = m;
             sub.corner_max = corner_max;
+            sub.b.no_direct = panel_no_direct();  // throughput GEMMs, as the whole-matrix schedule
             sub.alloc_panel_inv();
             try {
                 sub.rec_panel(a, depth);
@@ -1058,9 +1077,12 @@ struct Driver {
                 }
             }
         }
-        if (!ok && resumable) {
+        if (nlog)
+            fprintf(stderr, "[node] depth %d m %zu at %td: %s fail_off %zu, %.2f ms host\n", depth, m,
+                    g_log_root ? (a.d - g_log_root) / (ptrdiff_t)g_log_ld : -1, ok ? "ok" : (resumable ? "resume" : "fail"), fail_off, host_ms() - t0);
+        if (!ok && resumable && fail_off > 0) {
             // keep the prefix the schedule finished; recompute the rest of the node from its backup
-            node_spec_fails = fail_off == 0 ? node_spec_fails + 1 : 0;
+            node_spec_fails = 0;
             px.root = a.d;
             px.ld = a.ld;
             res = recover(a, depth, fail_off, bk, m, px);
@@ -1068,9 +1090,12 @@ struct Driver {
             return true;
         }
         if (!ok) {
+            // the node's first block is deficient: every node on its left spine would fail there
+            // too, so the exact recursion descends that spine without guessing (spec_dead)
             copy_block_dev(b, DView{bk, m, m, m}, a);
             FFG_CUDA(cudaFreeAsync(bk, b.st));
             ++node_spec_fails;
+            spec_dead = a.d;
             return false;
         }
         FFG_CUDA(cudaFreeAsync(bk, b.st));
@@ -1099,7 +1124,7 @@ struct Driver {
         res.Q = arena.alloc(std::max<size_t>(n, 1));
         if (m == 0 || n == 0) return res;                        // rankrev.hpp:91
         if (node_spec_max && m == n && m > thr && m <= node_spec_max && node_spec_fails < 3 && thr <= 64 &&
-            !spine_root && !early.armed) {
+            !spine_root && !early.armed && a.d != spec_dead) {
             wait(b.st, pending);
             if (try_node_spec(a, depth, res)) return res;
         }
@@ -1729,6 +1754,8 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             Driver rdrv(b, threshold, m, n);
             rdrv.node_spec_max = std::min(m, n);
             Driver::Prefix& rx = px;
+            Driver::g_log_root = a.d;
+            Driver::g_log_ld = a.ld;
             rx.root = a.d;
             rx.ld = a.ld;
             NodeRes res = rdrv.recover(a, 0, fail_off, bk, ldb, rx);

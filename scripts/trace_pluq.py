@@ -109,3 +109,30 @@ if len(bases) > 2:
         for s, t_, nm in ks:
             if b0 <= s < bases[i + 1][0] + 1:
                 print(f"   +{(s - b0) / 1e3 * 1e3:8.1f} us  {((t_ - s) / 1e3) * 1e3:7.1f} us  {nm}")
+
+# ---- long gaps between consecutive base cases (resumes, top-level GEMMs, host round trips)
+if len(bases) > 2:
+    print("long base-to-base gaps (> 150 us): base index, start ms, gap us, idle us, top kernels in the gap")
+    t00 = ks[0][0]
+    nlong = 0
+    tot_long = 0.0
+    for i in range(len(bases) - 1):
+        s0, s1 = bases[i][0], bases[i + 1][0]
+        gap = (s1 - s0) / 1e3
+        if gap * 1e3 <= 150:
+            continue
+        nlong += 1
+        tot_long += gap
+        inside = [(s, t_, nm) for s, t_, nm in ks if s0 <= s < s1]
+        by = collections.defaultdict(float)
+        for s, t_, nm in inside:
+            by[nm] += (t_ - s) / 1e3
+        # idle: parts of the gap with no kernel running
+        cov, last = 0.0, s0
+        for s, t_, _ in sorted(inside):
+            if t_ > last:
+                cov += (t_ - max(s, last)) / 1e3
+                last = t_
+        top = ", ".join(f"{k.split('::')[-1][:22]} {1e3 * v:.0f}" for k, v in sorted(by.items(), key=lambda x: -x[1])[:4])
+        print(f"  base {i:5d} at {(s0 - t00) / 1e3:8.2f} ms: gap {1e3 * gap:8.1f} us, idle {1e3 * (gap - cov):7.1f} us | {top}")
+    print(f"  {nlong} long gaps, {tot_long:.2f} ms total")
