@@ -117,6 +117,16 @@ int ffg_apply_perm_dev(ffg_ctx *ctx, uint32_t *A, size_t m, size_t n, size_t lda
  * Pure host function (no device needed). */
 int ffg_field_info(uint64_t p, int *limbs, uint64_t *kmax, int *nt);
 
+/* ---- rank profile matrix -> tile_rec permutations (host) ---------------
+ * tile_rec's P and Q depend only on the rank profile matrix R_A (the pivots
+ * (prow[k], pcol[k]), k < rank, in any order), m, n and the threshold: this
+ * evaluates pluq_tile_recursive's permutation logic (rankrev.hpp:85-183) on
+ * R_A itself, where every TRSM/GEMM is a no-op.  P (m words) and Q (n words)
+ * receive the to_array() forms.  Pure host function (no device needed); the
+ * profile-first exact path of ffg_pluq_tile_recursive[_dev] uses it. */
+int ffg_tile_rec_perms(size_t m, size_t n, size_t threshold, size_t rank, const uint32_t *prow,
+                       const uint32_t *pcol, uint32_t *P, uint32_t *Q);
+
 /* ---- seeded inputs on the device (generate.hpp / test_util.hpp) --------
  * ffg_random_mat_dev: A[i][j] = output i*n+j of SplitMix64(seed) mod p -- the
  *   reference's random_mat (test_util.hpp:22-28), bit for bit.

@@ -24,5 +24,6 @@ from .ffpluq import (  # noqa: F401
     random_mat_dev,
     pluq_tile_recursive,
     rr_base,
+    tile_rec_perms,
 )
 from . import dist  # noqa: F401,E402

@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "pluq.cuh"
+#include "profile.cuh"
 
 struct ffg_ctx {
     int device = 0;
@@ -160,6 +161,21 @@ int ffg_field_info(uint64_t p, int* limbs, uint64_t* kmax, int* nt) {
     } catch (const ffg::Error& e) {
         g_err = e.what();
         return e.code;
+    }
+}
+
+int ffg_tile_rec_perms(size_t m, size_t n, size_t threshold, size_t rank, const uint32_t* prow, const uint32_t* pcol,
+                       uint32_t* P, uint32_t* Q) {
+    try {
+        if ((rank && (!prow || !pcol)) || (m && !P) || (n && !Q)) throw ffg::Error(FFG_ERR_INVALID_ARG, "null array");
+        ffg::tile_rec_perms(m, n, threshold, rank, prow, pcol, P, Q);
+        return FFG_OK;
+    } catch (const ffg::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return FFG_ERR_NO_MEMORY;
     }
 }
 

@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
         L.ffg_pluq_tile_recursive_u8.argtypes = pluq_args
         L.ffg_rr_base.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
         L.ffg_field_info.argtypes = [u64, C.POINTER(C.c_int), C.POINTER(u64), C.POINTER(C.c_int)]
+        L.ffg_tile_rec_perms.argtypes = [sz, sz, sz, sz, vp, vp, vp, vp]
         L.ffg_apply_perm_dev.argtypes = [vp, vp, sz, sz, sz, C.c_int, C.c_int, vp]
         L.ffg_profile_enable.argtypes = [vp, C.c_int]
         L.ffg_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.c_int]
@@ -225,6 +226,20 @@ def field_info(p: int) -> dict:
     kmax = C.c_uint64(0)
     _check(lib().ffg_field_info(p, C.byref(limbs), C.byref(kmax), C.byref(nt)))
     return {"limbs": limbs.value, "kmax": kmax.value, "nt": nt.value}
+
+
+def tile_rec_perms(m: int, n: int, threshold: int, prow, pcol) -> tuple[np.ndarray, np.ndarray, int]:
+    """tile_rec's (P, Q, rank) from the rank profile matrix alone: pivots (prow[k], pcol[k]).
+    Host function (rpsim.cu); equals pluq_tile_recursive's P, Q on any matrix with that profile."""
+    prow = np.ascontiguousarray(prow, dtype=np.uint32)
+    pcol = np.ascontiguousarray(pcol, dtype=np.uint32)
+    if prow.shape != pcol.shape:
+        raise ValueError("prow and pcol differ in length")
+    P = np.zeros(max(m, 1), np.uint32)
+    Q = np.zeros(max(n, 1), np.uint32)
+    _check(lib().ffg_tile_rec_perms(m, n, threshold, prow.size, prow.ctypes.data, pcol.ctypes.data,
+                                    P.ctypes.data, Q.ctypes.data))
+    return P[:m], Q[:n], int(prow.size)
 
 
 def _nccl_hint() -> None:
