@@ -127,6 +127,20 @@ int ffg_field_info(uint64_t p, int *limbs, uint64_t *kmax, int *nt);
 int ffg_tile_rec_perms(size_t m, size_t n, size_t threshold, size_t rank, const uint32_t *prow,
                        const uint32_t *pcol, uint32_t *P, uint32_t *Q);
 
+/* ---- rank profile (device) --------------------------------------------
+ * ffg_rank_profile_dev: the rank profile matrix of a device matrix A (not
+ * modified): prow/pcol (host, min(m, n) words) receive the pivots in rr_base's
+ * discovery order -- rr_base's P[k], Q[k] for k < rank (rankrev.hpp:29-78) --
+ * computed by the blocked slab search of the profile-first path.
+ * ffg_pluq_from_profile_dev: pluq_tile_recursive's outputs on A (in place)
+ * given its rank profile (phases 2 and 3 of the profile-first path; the
+ * profile must be A's, e.g. from ffg_rank_profile_dev). */
+int ffg_rank_profile_dev(ffg_ctx *ctx, uint64_t p, const uint32_t *A, size_t m, size_t n, size_t lda,
+                         uint32_t *prow, uint32_t *pcol, size_t *rank);
+int ffg_pluq_from_profile_dev(ffg_ctx *ctx, uint64_t p, uint32_t *A, size_t m, size_t n, size_t lda,
+                              size_t threshold, size_t rank, const uint32_t *prow, const uint32_t *pcol,
+                              uint32_t *P, uint32_t *Q);
+
 /* ---- seeded inputs on the device (generate.hpp / test_util.hpp) --------
  * ffg_random_mat_dev: A[i][j] = output i*n+j of SplitMix64(seed) mod p -- the
  *   reference's random_mat (test_util.hpp:22-28), bit for bit.

@@ -22,7 +22,9 @@ from .ffpluq import (  # noqa: F401
     lib,
     lru_matrix_dev,
     random_mat_dev,
+    pluq_from_profile_dev,
     pluq_tile_recursive,
+    rank_profile_dev,
     rr_base,
     tile_rec_perms,
 )

@@ -1,5 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/ffg.h): context, status codes, host/device entry points.
+#include <algorithm>
 #include <cstdio>
+#include <vector>
 #include <cstring>
 #include <string>
 
@@ -177,6 +179,37 @@ int ffg_tile_rec_perms(size_t m, size_t n, size_t threshold, size_t rank, const 
         g_err = "host allocation failed";
         return FFG_ERR_NO_MEMORY;
     }
+}
+
+int ffg_rank_profile_dev(ffg_ctx* ctx, uint64_t p, const uint32_t* A, size_t m, size_t n, size_t lda, uint32_t* prow,
+                         uint32_t* pcol, size_t* rank) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        check_mat("rank_profile", A, m, n, lda);
+        if (std::min(m, n) && (!prow || !pcol)) throw ffg::Error(FFG_ERR_INVALID_ARG, "rank_profile: null output");
+        if (!ffg::profile_first_fits(n)) throw ffg::Error(FFG_ERR_INVALID_DIM, "rank_profile: too many columns");
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        DevMat W(m, n, ctx->stream);
+        if (m && n) ffg::copy_block_dev(blas, ffg::DView{const_cast<uint32_t*>(A), m, n, lda}, W.view());
+        std::vector<uint32_t> pr, pc;
+        const size_t r = ffg::rank_profile_dev(blas, W.view(), pr, pc);
+        std::copy(pr.begin(), pr.end(), prow);
+        std::copy(pc.begin(), pc.end(), pcol);
+        if (rank) *rank = r;
+    });
+}
+
+int ffg_pluq_from_profile_dev(ffg_ctx* ctx, uint64_t p, uint32_t* A, size_t m, size_t n, size_t lda, size_t threshold,
+                              size_t rank, const uint32_t* prow, const uint32_t* pcol, uint32_t* P, uint32_t* Q) {
+    return guarded(ctx, [&] {
+        ffg::Field F = ffg::make_field(p);
+        check_mat("pluq_from_profile", A, m, n, lda);
+        if ((rank && (!prow || !pcol)) || (m && !P) || (n && !Q)) throw ffg::Error(FFG_ERR_INVALID_ARG, "null array");
+        ffg::Blas blas{F, ctx->ws, ctx->stream, &ctx->launches};
+        DevMat W(m, n, ctx->stream);
+        ffg::pluq_from_profile_dev(blas, ffg::DView{A, m, n, lda}, threshold, rank, prow, pcol, P, Q, W.d);
+        FFG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
 }
 
 int ffg_random_mat_dev(ffg_ctx* ctx, uint64_t p, uint64_t seed, uint32_t* A, size_t m, size_t n, size_t lda) {

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "pluq.cuh"
+#include "profile.cuh"
 
 namespace ffg {
 
@@ -1564,6 +1565,22 @@ static void band_bounds(size_t o, size_t s, size_t thr, size_t T, size_t Tmin, s
     band_bounds(o + h, s - h, thr, T, Tmin, out);
 }
 
+// The profile-first exact path (profile.cu) replaces the exact recursion for rank-deficient input
+// of order >= 512: FFG_PROFILE_FIRST (read per call) 0 = never, 2 = always (whenever the slab kernel
+// takes the width; tests), default: when the whole-matrix guess failed in its first eighth -- the
+// matrix is deficient throughout -- or was not tried, on single-GPU runs (partitioned runs keep
+// the recursion, whose large operations split over the ranks).
+static int profile_first_mode() {
+    const char* e = getenv("FFG_PROFILE_FIRST");
+    return e ? atoi(e) : 1;
+}
+static bool profile_first_ok(const Blas& b, size_t m, size_t n) {
+    const int mode = profile_first_mode();
+    // (the path factors its generic leading block through pluq_tile_recursive_dev: never nested)
+    if (mode == 0 || profile_first_active() || b.ws.dist.active() || b.ws.prof.mode == 1 || !profile_first_fits(n)) return false;
+    return mode == 2 || std::min(m, n) >= 512;
+}
+
 // Streamed speculative attempt of the host entry (square input, panel mode): band c uploads on
 // one copy engine, is backed up in HBM by a copy kernel, factors, and downloads on the other copy
 // engine as soon as its last base case is done -- PCIe in both directions overlaps the
@@ -1652,6 +1669,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             }
         }
     }
+    if (!ok && resumable && fail_off < n / 8 && profile_first_ok(b, n, n)) resumable = false;  // profile-first
     if (!ok && resumable) {
         // resume tile_rec at the failed block on the device copy (every band is uploaded and backed
         // up by now), then bring the whole matrix back
@@ -1682,6 +1700,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
 }
 
 size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
+    if (profile_first_mode() == 2 && profile_first_ok(b, a.rows, a.cols))
+        return pluq_profile_first_dev(b, a, threshold, P, Q);
     if (threshold <= 64 && spec_allowed(b, a, threshold)) {
         const size_t m = a.rows, n = a.cols;
         const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
@@ -1748,6 +1768,13 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             FFG_CUDA(cudaFreeAsync(bk, b.st));
             return rank;
         }
+        if (resumable && fail_off < m / 8 && profile_first_ok(b, m, n)) {
+            // deficient from the start: the profile-first path on the restored input
+            copy_block_dev(b, DView{bk, m, n, ldb}, a);
+            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            if (fail_off == 0) b.ws.spec_failed();
+            return pluq_profile_first_dev(b, a, threshold, P, Q);
+        }
         if (resumable) {
             // the pivots before the failed block are final: resume tile_rec from there (the rest of
             // the matrix is recomputed from the backup), node-level guesses again on fresh subproblems
@@ -1774,6 +1801,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
         FFG_CUDA(cudaFreeAsync(bk, b.st));
         b.ws.spec_failed();
     }
+    if (profile_first_ok(b, a.rows, a.cols)) return pluq_profile_first_dev(b, a, threshold, P, Q);
     Driver drv(b, threshold, a.rows, a.cols);
     drv.level_timing = getenv("FFG_LEVEL_TIMING") != nullptr;
     drv.node_spec_max = node_spec_max(b, a, threshold, drv);
@@ -1810,6 +1838,15 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
             return rank;
         }
         restored = true;
+    }
+    if (profile_first_ok(b, m, n)) {  // rank-deficient input: upload, profile-first, download
+        if (!restored)
+            FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, host, lda * 4, n * 4, m, cudaMemcpyHostToDevice, b.st));
+        const size_t rank = pluq_profile_first_dev(b, DView{d, m, n, n}, thr, P, Q);
+        FFG_CUDA(cudaMemcpy2DAsync(host, lda * 4, d, n * 4, n * 4, m, cudaMemcpyDeviceToHost, b.st));
+        FFG_CUDA(cudaFreeAsync(d, b.st));
+        FFG_CUDA(cudaStreamSynchronize(b.st));
+        return rank;
     }
     // speculative full rank (see Driver::spec) is off here: its device backup would share the copy
     // stream with the spine uploads and delay them more than the saved rank round trips gain

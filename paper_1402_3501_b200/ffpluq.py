@@ -108,6 +108,8 @@ def lib() -> C.CDLL:
         L.ffg_rr_base.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
         L.ffg_field_info.argtypes = [u64, C.POINTER(C.c_int), C.POINTER(u64), C.POINTER(C.c_int)]
         L.ffg_tile_rec_perms.argtypes = [sz, sz, sz, sz, vp, vp, vp, vp]
+        L.ffg_rank_profile_dev.argtypes = [vp, u64, vp, sz, sz, sz, vp, vp, C.POINTER(sz)]
+        L.ffg_pluq_from_profile_dev.argtypes = [vp, u64, vp, sz, sz, sz, sz, sz, vp, vp, vp, vp]
         L.ffg_apply_perm_dev.argtypes = [vp, vp, sz, sz, sz, C.c_int, C.c_int, vp]
         L.ffg_profile_enable.argtypes = [vp, C.c_int]
         L.ffg_profile_read.argtypes = [vp, C.POINTER(C.c_double), C.c_int]
@@ -386,6 +388,34 @@ def pluq_tile_recursive(p: int, A, threshold: int = 8, ctx: Context | None = Non
     fn = lib().ffg_pluq_tile_recursive_dev if dev else lib().ffg_pluq_tile_recursive
     _check(fn(ctx.handle, p, _ptr(A), m, n, _ld(A), threshold, P.ctypes.data, Q.ctypes.data, C.byref(r)))
     return PluqResult(P[:m], Q[:n], int(r.value))
+
+
+def rank_profile_dev(p: int, A, ctx: Context | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Rank profile matrix of a device matrix (not modified): pivots (rows, cols) in rr_base's
+    discovery order (rankrev.hpp:40-57), i.e. rr_base's P[:r], Q[:r]."""
+    ctx = ctx or default_context()
+    _dev(A, "A")
+    m, n = A.shape
+    rows = np.zeros(max(min(m, n), 1), np.uint32)
+    cols = np.zeros(max(min(m, n), 1), np.uint32)
+    r = C.c_size_t(0)
+    _check(lib().ffg_rank_profile_dev(ctx.handle, p, _ptr(A), m, n, _ld(A), rows.ctypes.data, cols.ctypes.data,
+                                      C.byref(r)))
+    return rows[: r.value], cols[: r.value]
+
+
+def pluq_from_profile_dev(p: int, A, threshold: int, prow, pcol, ctx: Context | None = None) -> PluqResult:
+    """pluq_tile_recursive's outputs on a device matrix (in place) given its rank profile."""
+    ctx = ctx or default_context()
+    _dev(A, "A")
+    m, n = A.shape
+    prow = np.ascontiguousarray(prow, dtype=np.uint32)
+    pcol = np.ascontiguousarray(pcol, dtype=np.uint32)
+    P = np.zeros(max(m, 1), np.uint32)
+    Q = np.zeros(max(n, 1), np.uint32)
+    _check(lib().ffg_pluq_from_profile_dev(ctx.handle, p, _ptr(A), m, n, _ld(A), threshold, prow.size,
+                                           prow.ctypes.data, pcol.ctypes.data, P.ctypes.data, Q.ctypes.data))
+    return PluqResult(P[:m], Q[:n], int(prow.size))
 
 
 def rr_base(p: int, A, ctx: Context | None = None) -> PluqResult:
