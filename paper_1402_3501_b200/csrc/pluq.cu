@@ -1580,6 +1580,16 @@ static bool profile_first_ok(const Blas& b, size_t m, size_t n) {
     if (mode == 0 || profile_first_active() || b.ws.dist.active() || b.ws.prof.mode == 1 || !profile_first_fits(n)) return false;
     return mode == 2 || std::min(m, n) >= 512;
 }
+// after a failed whole-matrix guess at diagonal offset fail_off: the matrix counts as deficient
+// throughout when its very first block failed, or when it failed in the first eighth over a field
+// where a random singular block is not expected (blocks / p < 0.05; GF(251) at n = 32768 expects
+// two such blocks per matrix, and resuming there costs less than a second elimination)
+static bool profile_first_after_failure(const Blas& b, size_t fail_off, size_t m, size_t n, size_t thr) {
+    if (!profile_first_ok(b, m, n)) return false;
+    if (fail_off == 0) return true;
+    const double blocks = (double)std::min(m, n) / (double)std::max<size_t>(thr, 1);
+    return fail_off < std::min(m, n) / 8 && blocks < 0.05 * (double)b.F.p;
+}
 
 // Streamed speculative attempt of the host entry (square input, panel mode): band c uploads on
 // one copy engine, is backed up in HBM by a copy kernel, factors, and downloads on the other copy
@@ -1669,7 +1679,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             }
         }
     }
-    if (!ok && resumable && fail_off < n / 8 && profile_first_ok(b, n, n)) resumable = false;  // profile-first
+    if (!ok && resumable && profile_first_after_failure(b, fail_off, n, n, thr)) resumable = false;  // profile-first
     if (!ok && resumable) {
         // resume tile_rec at the failed block on the device copy (every band is uploaded and backed
         // up by now), then bring the whole matrix back
@@ -1768,7 +1778,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             FFG_CUDA(cudaFreeAsync(bk, b.st));
             return rank;
         }
-        if (resumable && fail_off < m / 8 && profile_first_ok(b, m, n)) {
+        if (resumable && profile_first_after_failure(b, fail_off, m, n, threshold)) {
             // deficient from the start: the profile-first path on the restored input
             copy_block_dev(b, DView{bk, m, n, ldb}, a);
             FFG_CUDA(cudaFreeAsync(bk, b.st));
