@@ -124,6 +124,7 @@ struct EpiParams {
     uint32_t w[8];
     uint32_t kblocks;
     uint32_t m_tiles, n_tiles;
+    uint32_t l2_hints;  // TMA loads carry L2 eviction policies (large problems: keep the A panel of a row group)
 };
 
 // --------------------------------------------------------------------------- epilogue
@@ -286,6 +287,11 @@ __global__ void __launch_bounds__(384, 1)
         // ---------------- TMA producer (runs ahead across tile boundaries)
         if (lane == 0) {
             uint32_t it = 0;
+            // a wave of CTAs covers GROUP_M row blocks x a few column blocks and the next wave moves
+            // on to the next column blocks: the row group's A panel is re-read by every wave of the
+            // group (keep it in L2), a B tile only inside its wave
+            const bool hints = ep.l2_hints != 0;
+            const uint64_t pol_a = hints ? ptx::l2_policy_evict_last() : 0, pol_b = hints ? ptx::l2_policy_evict_first() : 0;
             for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
                 uint32_t m_blk, n_blk;
                 tile_coords(tile, m_blk, n_blk);
@@ -296,10 +302,17 @@ __global__ void __launch_bounds__(384, 1)
                     ptx::mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * S::STAGE_BYTES;
                     ptx::mbar_expect_tx(&full[s], S::STAGE_BYTES);
-                    for (int i = 0; i < L; ++i)
-                        ptx::tma_load_2d(st + i * BM * BK, &mapA, &full[s], (int32_t)(kb * BK),
-                                         a_row0 + i * (int32_t)(ep.m_tiles * BM));
-                    ptx::tma_load_2d(st + S::A_BYTES, &mapB, &full[s], (int32_t)(kb * BK), b_row0);
+                    if (hints) {
+                        for (int i = 0; i < L; ++i)
+                            ptx::tma_load_2d_hint(st + i * BM * BK, &mapA, &full[s], (int32_t)(kb * BK),
+                                                  a_row0 + i * (int32_t)(ep.m_tiles * BM), pol_a);
+                        ptx::tma_load_2d_hint(st + S::A_BYTES, &mapB, &full[s], (int32_t)(kb * BK), b_row0, pol_b);
+                    } else {
+                        for (int i = 0; i < L; ++i)
+                            ptx::tma_load_2d(st + i * BM * BK, &mapA, &full[s], (int32_t)(kb * BK),
+                                             a_row0 + i * (int32_t)(ep.m_tiles * BM));
+                        ptx::tma_load_2d(st + S::A_BYTES, &mapB, &full[s], (int32_t)(kb * BK), b_row0);
+                    }
                 }
             }
         }
@@ -1042,7 +1055,7 @@ CUtensorMap make_map(const uint8_t* base, uint64_t inner_bytes, uint64_t rows, u
 }
 
 EpiParams make_ep(const Field& F, uint32_t alpha, uint32_t beta, DView C) {
-    EpiParams ep;
+    EpiParams ep{};
     ep.C = C.d;
     ep.ldc = C.ld;
     ep.M = (uint32_t)C.rows;
@@ -1072,6 +1085,9 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
     ep.kblocks = (uint32_t)(Kp / BK);
     ep.m_tiles = (uint32_t)(Mp / BM);
     ep.n_tiles = (uint32_t)(Np / S::NT);
+    // L2 eviction hints once the limb planes no longer fit in L2 beside C (FFG_GEMM_L2_HINTS=0/1 forces)
+    static const int hints_env = getenv("FFG_GEMM_L2_HINTS") ? atoi(getenv("FFG_GEMM_L2_HINTS")) : -1;
+    ep.l2_hints = hints_env >= 0 ? (uint32_t)hints_env : ((uint64_t)L * (Mp + Np) * Kp > (64ull << 20) ? 1u : 0u);
     const uint32_t tiles = ep.m_tiles * ep.n_tiles;
     dim3 grid(sm_cap > 0 ? std::min<uint32_t>(tiles, (uint32_t)sm_cap) : tiles);
     launch_k(modgemm_kernel<L>, grid, dim3(384), S::TOTAL, st, ma, mb, ep);

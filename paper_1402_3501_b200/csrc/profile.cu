@@ -19,6 +19,7 @@
 //            Schur complement, which is zero).
 // Every phase is exact integer arithmetic, so the outputs are bit-identical to the reference.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -34,6 +35,13 @@ constexpr uint32_t RP_THREADS = 512;
 constexpr uint32_t RP_KMAX = 32;        // slab rows
 constexpr uint32_t RP_SMEM_WORDS = 40960;  // slab values per CTA (160 KB)
 constexpr uint32_t NONE = 0xFFFFFFFFu;
+
+#ifdef RP_TIMING
+__device__ unsigned long long rp_clk[16];
+#define RP_T(k) do { unsigned long long t_ = clock64(); rp_acc[k] += t_ - rp_t0; rp_t0 = t_; } while (0)
+#else
+#define RP_T(k) do { } while (0)
+#endif
 
 struct RpPub {
     uint32_t row, col, pad0, pad1;
@@ -61,6 +69,63 @@ __device__ __forceinline__ uint32_t ld_cluster(const uint32_t* local, uint32_t c
     return v;
 }
 
+// The end phase of a slab search: the slab's pivot rows (shared memory S, kk x w per CTA) brought
+// to reduced echelon form V (V[t][c_t'] = delta_tt') by a column-parallel back substitution and
+// stored, the pivots and the slab's rank reported (CTA 0).
+struct RpEnd {
+    uint32_t pubT[RP_KMAX][RP_KMAX];
+    uint32_t Tn[RP_KMAX][RP_KMAX + 1];
+    uint32_t dinv[RP_KMAX];
+};
+__device__ __forceinline__ void rp_finish(uint32_t* S, RpEnd& E, const uint32_t* piv_row, const uint32_t* piv_col,
+                                          uint32_t rho, uint32_t w, uint32_t wv, uint32_t c0, uint32_t cta,
+                                          uint32_t row0, uint32_t* __restrict__ prow_out,
+                                          uint32_t* __restrict__ pcol_out, uint32_t* __restrict__ V, uint64_t ldv,
+                                          BaseInfo* __restrict__ info, uint32_t seq, uint32_t p, uint64_t mu) {
+    const uint32_t tid = threadIdx.x;
+    auto& pubT = E.pubT;
+    auto& Tn = E.Tn;
+    auto& dinv = E.dinv;
+    // reduced echelon form of the pivot rows: T[t][t'] = S[row_t][c_t'] (upper triangular in pivot
+    // order -- each pivot column is zero in every later pivot row), gathered from the columns' owners
+    for (uint32_t idx = tid; idx < rho * rho; idx += RP_THREADS) {
+        const uint32_t tc = idx / rho, t = idx % rho;
+        if (piv_col[tc] / w == cta) pubT[tc][t] = S[piv_row[t] * w + (piv_col[tc] - c0)];
+    }
+    cluster_sync_all();
+    for (uint32_t idx = tid; idx < rho * rho; idx += RP_THREADS) {
+        const uint32_t tc = idx / rho, t = idx % rho;
+        const uint32_t v = ld_cluster(&pubT[tc][t], piv_col[tc] / w);
+        Tn[t][tc] = v ? p - v : 0u;  // negated: the back substitution subtracts
+    }
+    __syncthreads();
+    if (tid < rho) dinv[tid] = inv_mod32(p - Tn[tid][tid], p);
+    __syncthreads();
+    for (uint32_t j = tid; j < w; j += RP_THREADS) {
+        for (int t = (int)rho - 1; t >= 0; --t) {
+            uint64_t acc = S[piv_row[t] * w + j];
+            for (uint32_t u = t + 1; u < rho; ++u) acc += (uint64_t)Tn[t][u] * S[piv_row[u] * w + j];
+            S[piv_row[t] * w + j] = mul_mod(mod_u64(acc, p, mu), dinv[t], p, mu);
+        }
+    }
+    __syncthreads();
+    for (uint32_t t = 0; t < rho; ++t)
+        for (uint32_t j = tid; j < wv; j += RP_THREADS) V[(uint64_t)t * ldv + c0 + j] = S[piv_row[t] * w + j];
+    if (cta == 0) {
+        if (tid < rho) {
+            prow_out[tid] = row0 + piv_row[tid];
+            pcol_out[tid] = piv_col[tid];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            *reinterpret_cast<volatile uint32_t*>(&info->rank) = rho;
+            __threadfence_system();
+            *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+        }
+    }
+}
+
 // One row slab (kk <= 32 rows starting at global row row0, already reduced by every earlier
 // pivot) searched the way rr_base searches (rankrev.hpp:40-57): the next pivot is the first row
 // with a nonzero Schur entry, at its first nonzero column.  Earlier pivot columns are exact zeros
@@ -82,9 +147,7 @@ __global__ void __launch_bounds__(RP_THREADS, 1)
     __shared__ uint32_t mneg[RP_KMAX], mnegsh[RP_KMAX];
     __shared__ uint32_t piv_row[RP_KMAX], piv_col[RP_KMAX];
     __shared__ uint32_t s_istar, s_piv, s_pivsh, s_done;
-    __shared__ uint32_t pubT[RP_KMAX][RP_KMAX];
-    __shared__ uint32_t Tn[RP_KMAX][RP_KMAX + 1];
-    __shared__ uint32_t dinv[RP_KMAX];
+    __shared__ RpEnd rpend;
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t cta = cluster_rank(), ncta = cluster_size();
@@ -171,45 +234,266 @@ __global__ void __launch_bounds__(RP_THREADS, 1)
         par ^= 1u;
     }
 
-    // reduced echelon form of the pivot rows: T[t][t'] = S[row_t][c_t'] (upper triangular in pivot
-    // order -- each pivot column is zero in every later pivot row), gathered from the columns' owners
-    for (uint32_t idx = tid; idx < rho * rho; idx += RP_THREADS) {
-        const uint32_t tc = idx / rho, t = idx % rho;
-        if (piv_col[tc] / w == cta) pubT[tc][t] = S[piv_row[t] * w + (piv_col[tc] - c0)];
-    }
-    cluster_sync_all();
-    for (uint32_t idx = tid; idx < rho * rho; idx += RP_THREADS) {
-        const uint32_t tc = idx / rho, t = idx % rho;
-        const uint32_t v = ld_cluster(&pubT[tc][t], piv_col[tc] / w);
-        Tn[t][tc] = v ? p - v : 0u;  // negated: the back substitution subtracts
-    }
-    __syncthreads();
-    if (tid < rho) dinv[tid] = inv_mod32(p - Tn[tid][tid], p);
-    __syncthreads();
-    for (uint32_t j = tid; j < w; j += RP_THREADS) {
-        for (int t = (int)rho - 1; t >= 0; --t) {
-            uint64_t acc = S[piv_row[t] * w + j];
-            for (uint32_t u = t + 1; u < rho; ++u) acc += (uint64_t)Tn[t][u] * S[piv_row[u] * w + j];
-            S[piv_row[t] * w + j] = mul_mod(mod_u64(acc, p, mu), dinv[t], p, mu);
+    rp_finish(S, rpend, piv_row, piv_col, rho, w, wv, c0, cta, row0, prow_out, pcol_out, V, ldv, info, seq, p, mu);
+    cluster_sync_all();  // no CTA leaves while another may still read its shared memory
+}
+
+// The same search with the slab in registers (w <= 512 * CPT columns per CTA, <= 32 rows): thread
+// tid owns columns tid + 512 q (q < CPT) of every row, so an elimination step is thread-local --
+// the pivot row's entry of a column sits in the column's own thread -- and needs only the rows'
+// multipliers (shared memory, broadcast).  Per step:
+//   * candidates only for the next RP_WIN rows after the last pivot (one ballot per row and
+//     warp; a window without any nonzero row slides on without an elimination);
+//   * every CTA PUSHES its candidate (row, column) and that column's 32 entries into its slot of
+//     every CTA's inbox (st.shared::cluster) before the one cluster barrier of the step, so the
+//     winner (lowest row, then lowest column) is picked from local shared memory;
+//   * the winner is eliminated from every other row, above and below (fraction-free
+//     Gauss-Jordan: S_i <- piv S_i - S_i[c*] S_i*), values kept lazily in [0, 2p): the pivot
+//     rows end in reduced echelon form up to their diagonal entries, tracked by warp 0 and
+//     divided out when the rows are stored -- no back substitution, no shared-memory slab;
+//   * the slab's rank goes to the host mailbox as soon as the search ends, before the rows are
+//     scaled and stored (the host enqueues the next launches meanwhile).
+struct RpMsg {
+    unsigned long long key;   // (row << 32) | column; ~0 = no candidate in the window
+    uint32_t vals[RP_KMAX];   // the candidate column's entries (rows 0..31, in [0, 2p))
+};
+constexpr int RP_WIN = 8;
+
+__device__ __forceinline__ uint32_t map_cluster(uint32_t local_addr, uint32_t cta) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(cta));
+    return ra;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t local_addr, uint32_t cta, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_cluster(local_addr, cta)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t local_addr, uint32_t cta, unsigned long long v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(map_cluster(local_addr, cta)), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_min_shared(uint32_t* a, uint32_t v) {
+    asm volatile("red.shared::cta.min.u32 [%0], %1;" ::"r"(ptx::smem_u32(a)), "r"(v) : "memory");
+}
+// x * w mod p up to one p: in [0, 2p) for any 32-bit x (w < p, wp = shoup_pre(w))
+__device__ __forceinline__ uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t wp, uint32_t p) {
+    return x * w - __umulhi(x, wp) * p;
+}
+
+template <int CPT>
+__global__ void __launch_bounds__(RP_THREADS, 1)
+    rp_slab_reg_kernel(const uint32_t* __restrict__ W, uint64_t ldw, uint32_t row0, uint32_t kk, uint32_t n, uint32_t w,
+                       uint32_t* __restrict__ prow_out, uint32_t* __restrict__ pcol_out, uint32_t* __restrict__ V,
+                       uint64_t ldv, BaseInfo* __restrict__ info, uint32_t seq, uint32_t p, uint64_t mu) {
+    constexpr int KK = (int)RP_KMAX;
+    __shared__ __align__(16) RpMsg inbox[2][16];
+    __shared__ uint32_t cand[2][RP_WIN];
+    __shared__ uint32_t stage[RP_KMAX];
+    __shared__ __align__(16) uint32_t mneg[RP_KMAX], mnegsh[RP_KMAX];
+    __shared__ uint32_t piv_row[RP_KMAX], piv_col[RP_KMAX];
+    __shared__ uint32_t dinvs[RP_KMAX], dinvsh[RP_KMAX];
+    __shared__ uint32_t s_mode, s_istar, s_piv, s_pivsh;
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t cta = cluster_rank(), ncta = cluster_size();
+    const uint32_t c0 = cta * w;
+    const uint32_t wv = c0 < n ? min(w, n - c0) : 0u;  // valid columns of this CTA
+    const uint32_t p2 = 2u * p;
+#ifdef RP_TIMING
+    unsigned long long rp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long rp_t0 = clock64();
+#endif
+
+    uint32_t s[KK][CPT];
+#pragma unroll
+    for (int i = 0; i < KK; ++i)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const uint32_t j = tid + RP_THREADS * q;
+            s[i][q] = ((uint32_t)i < kk && j < wv) ? W[(uint64_t)(row0 + i) * ldw + c0 + j] : 0u;
         }
+    uint32_t nz[CPT];  // bit i: s[i][q] is nonzero mod p
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+        nz[q] = 0u;
+#pragma unroll
+        for (int i = 0; i < KK; ++i) nz[q] |= (s[i][q] != 0u ? 1u : 0u) << i;
     }
+    if (tid < 2 * RP_WIN) (&cand[0][0])[tid] = NONE;
     __syncthreads();
-    for (uint32_t t = 0; t < rho; ++t)
-        for (uint32_t j = tid; j < wv; j += RP_THREADS) V[(uint64_t)t * ldv + c0 + j] = S[piv_row[t] * w + j];
-    if (cta == 0) {
-        if (tid < rho) {
-            prow_out[tid] = row0 + piv_row[tid];
-            pcol_out[tid] = piv_col[tid];
+    RP_T(0);
+
+    int iprev = -1;
+    uint32_t par = 0, rho = 0, pivmask = 0;
+    uint32_t dg = 1;  // warp 0, lane i: row i's entry at its own pivot column
+    for (;;) {
+        // offers: this warp's first window row with a nonzero entry, at its first nonzero column
+        // (the rows' nonzero patterns are kept as bit masks per column, so no register indexing)
+        {
+            const uint32_t sh = (uint32_t)(iprev + 1);
+#pragma unroll
+            for (int slot = 0; slot < RP_WIN; ++slot) {
+                const uint32_t r = sh + slot;
+                if (r >= (uint32_t)KK) break;
+                uint32_t bq[CPT];
+                uint32_t any = 0;
+#pragma unroll
+                for (int q = 0; q < CPT; ++q) {
+                    bq[q] = __ballot_sync(0xffffffffu, (nz[q] >> r) & 1u);
+                    any |= bq[q];
+                }
+                if (any) {
+                    if (lane == 0) {
+                        uint32_t first = 0;
+#pragma unroll
+                        for (int q = CPT - 1; q >= 0; --q)
+                            if (bq[q]) first = RP_THREADS * q + warp * 32 + __ffs(bq[q]) - 1;
+                        red_min_shared(&cand[par][slot], c0 + first);
+                    }
+                    break;  // the CTA's candidate row is this one or an earlier one
+                }
+            }
         }
         __syncthreads();
-        if (tid == 0) {
-            __threadfence_system();
-            *reinterpret_cast<volatile uint32_t*>(&info->rank) = rho;
-            __threadfence_system();
-            *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+        {   // this CTA's candidate (every warp works it out); the owner's warp pushes it
+            const uint32_t cm = lane < RP_WIN ? cand[par][lane] : NONE;
+            const uint32_t b = __ballot_sync(0xffffffffu, cm != NONE);
+            const uint32_t keyaddr = ptx::smem_u32(&inbox[par][cta].key);
+            if (b) {
+                const uint32_t slot = (uint32_t)(__ffs(b) - 1);
+                const uint32_t fr = (uint32_t)(iprev + 1) + slot;
+                const uint32_t fc = __shfl_sync(0xffffffffu, cm, slot);
+                const uint32_t jl = fc - c0;
+                if (warp == ((jl & (RP_THREADS - 1)) >> 5)) {
+                    if (lane == (jl & 31u)) {
+                        const uint32_t q = jl / RP_THREADS;
+#pragma unroll
+                        for (int i = 0; i < KK; ++i) {
+                            uint32_t v = s[i][0];
+#pragma unroll
+                            for (int qq = 1; qq < CPT; ++qq) v = q == (uint32_t)qq ? s[i][qq] : v;
+                            stage[i] = v;
+                        }
+                    }
+                    __syncwarp();
+                    const uint32_t myv = stage[lane];
+                    const uint32_t vaddr = ptx::smem_u32(&inbox[par][cta].vals[lane]);
+                    for (uint32_t d = 0; d < ncta; ++d) st_cluster_u32(vaddr, d, myv);
+                    if (lane < ncta) st_cluster_u64(keyaddr, lane, ((unsigned long long)fr << 32) | fc);
+                }
+            } else if (warp == 0 && lane < ncta) {
+                st_cluster_u64(keyaddr, lane, ~0ull);
+            }
+            if (tid < RP_WIN) cand[par ^ 1u][tid] = NONE;  // last read before the previous cluster barrier
+        }
+        RP_T(1);
+        cluster_sync_all();
+        RP_T(2);
+        if (warp == 0) {  // the cluster-wide winner: lowest row, then lowest column
+            const unsigned long long key = lane < ncta ? inbox[par][lane].key : ~0ull;
+            const uint32_t rowk = (uint32_t)(key >> 32);
+            const uint32_t rmin = __reduce_min_sync(0xffffffffu, rowk);
+            if (rmin == NONE) {
+                if (lane == 0) s_mode = (iprev + RP_WIN + 1 >= (int)kk) ? 2u : 1u;
+            } else {
+                const uint32_t colk = rowk == rmin ? (uint32_t)key : NONE;
+                const uint32_t cmin = __reduce_min_sync(0xffffffffu, colk);
+                const uint32_t owner = (uint32_t)(__ffs(__ballot_sync(0xffffffffu, colk == cmin && rowk == rmin)) - 1);
+                uint32_t v = inbox[par][owner].vals[lane];
+                v = v >= p ? v - p : v;
+                const uint32_t istar = rmin;
+                const uint32_t piv = __shfl_sync(0xffffffffu, v, istar);
+                const uint32_t mn = (lane != istar && v) ? p - v : 0u;  // rows beyond the slab are zero
+                mneg[lane] = mn;
+                mnegsh[lane] = shoup_pre(mn, p, mu);
+                if (lane == istar)
+                    dg = piv;
+                else if (mn)
+                    dg = mul_mod(dg, piv, p, mu);
+                if (lane == 0) {
+                    s_mode = 0;
+                    s_istar = istar;
+                    s_piv = piv;
+                    s_pivsh = shoup_pre(piv, p, mu);
+                    piv_row[rho] = istar;
+                    piv_col[rho] = cmin;
+                }
+            }
+        }
+        __syncthreads();
+        RP_T(3);
+        const uint32_t mode = s_mode;
+        if (mode == 2u) break;
+        par ^= 1u;
+        if (mode == 1u) {  // no nonzero row in the window
+            iprev += RP_WIN;
+            continue;
+        }
+        const uint32_t istar = s_istar, piv = s_piv, pivsh = s_pivsh;
+        uint32_t pr[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) pr[q] = 0u;
+#pragma unroll
+        for (int i = 0; i < KK; ++i)
+            if ((uint32_t)i == istar) {
+#pragma unroll
+                for (int q = 0; q < CPT; ++q) pr[q] = s[i][q];
+            }
+#pragma unroll
+        for (int g = 0; g < KK / 4; ++g) {
+            const uint4 m4 = reinterpret_cast<const uint4*>(mneg)[g];
+            const uint4 h4 = reinterpret_cast<const uint4*>(mnegsh)[g];
+            const uint32_t mm[4] = {m4.x, m4.y, m4.z, m4.w}, hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (mm[e] == 0u) continue;  // the pivot row itself, rows with a zero entry
+#pragma unroll
+                for (int q = 0; q < CPT; ++q) {
+                    const uint32_t x = shoup_lazy(s[4 * g + e][q], piv, pivsh, p) + shoup_lazy(pr[q], mm[e], hh[e], p);
+                    const uint32_t y = x >= p2 ? x - p2 : x;
+                    s[4 * g + e][q] = y;
+                    const uint32_t BIT = 1u << (4 * g + e);
+                    nz[q] = (y != 0u && y != p) ? (nz[q] | BIT) : (nz[q] & ~BIT);
+                }
+            }
+        }
+        iprev = (int)istar;
+        ++rho;
+        pivmask |= 1u << istar;
+        RP_T(4);
+    }
+    if (cta == 0 && tid == 0) {  // the rank first: the host's next launches queue up behind this kernel
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&info->rank) = rho;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(&info->seq) = seq;
+    }
+    RP_T(5);
+    if (warp == 0) {
+        const uint32_t di = (pivmask >> lane) & 1u ? inv_mod32(dg, p) : 0u;
+        dinvs[lane] = di;
+        dinvsh[lane] = shoup_pre(di, p, mu);
+    }
+    __syncthreads();
+    // pivot rows in discovery order = increasing row order: row i is pivot number popc(pivmask below i)
+#pragma unroll
+    for (int i = 0; i < KK; ++i) {
+        if (!((pivmask >> i) & 1u)) continue;
+        const uint32_t t = __popc(pivmask & ((1u << i) - 1u));
+        const uint32_t di = dinvs[i], dish = dinvsh[i];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const uint32_t j = tid + RP_THREADS * q;
+            if (j < wv) V[(uint64_t)t * ldv + c0 + j] = shoup_mul(s[i][q], di, dish, p);
         }
     }
-    cluster_sync_all();  // no CTA leaves while another may still read its shared memory
+    if (cta == 0 && tid < rho) {
+        prow_out[tid] = row0 + piv_row[tid];
+        pcol_out[tid] = piv_col[tid];
+    }
+    RP_T(6);
+#ifdef RP_TIMING
+    if (tid == 0 && cta == 0)
+        for (int k = 0; k < 8; ++k) rp_clk[k] += rp_acc[k];
+#endif
 }
 
 // X[i][t] = S[i][cols[t]]  (rows x nc)
@@ -269,6 +553,7 @@ struct RankProfile {
     BaseInfo* info_dev = nullptr;
     cudaStream_t side = nullptr;
     size_t leaves = 0;
+    bool reg_path = false;  // slab in registers (w <= 1024)
 
     RankProfile(const Blas& bb, DView w_, uint32_t* vb, uint32_t* pr, uint32_t* pc) : b(bb), W(w_), VB(vb), PR(pr), PC(pc) {}
 
@@ -287,7 +572,7 @@ struct RankProfile {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(ncta);
         cfg.blockDim = dim3(RP_THREADS);
-        cfg.dynamicSmemBytes = (size_t)kk * w * 4;
+        cfg.dynamicSmemBytes = reg_path ? 0 : (size_t)kk * w * 4;
         cfg.stream = b.st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -297,7 +582,9 @@ struct RankProfile {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         b.ws.prof.begin(b.st);
-        FFG_CUDA(cudaLaunchKernelEx(&cfg, rp_slab_kernel, (const uint32_t*)W.d, (uint64_t)W.ld, (uint32_t)a,
+        auto kern = rp_slab_kernel;
+        if (reg_path) kern = w <= RP_THREADS ? rp_slab_reg_kernel<1> : rp_slab_reg_kernel<2>;
+        FFG_CUDA(cudaLaunchKernelEx(&cfg, kern, (const uint32_t*)W.d, (uint64_t)W.ld, (uint32_t)a,
                                     (uint32_t)rows, (uint32_t)W.cols, w, PR + total, PC + total,
                                     VB + total * W.cols, (uint64_t)W.cols, info_dev, seq, b.F.p, b.F.mu));
         b.ws.prof.end(b.st, PROF_BASE, 2.0 * rows * W.cols * 4, 0.0);
@@ -388,6 +675,8 @@ size_t rank_profile_dev(const Blas& b, DView W, std::vector<uint32_t>& prow, std
         FFG_CUDA(cudaFuncSetAttribute(rp_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(RP_SMEM_WORDS * 4)));
         FFG_CUDA(cudaFuncSetAttribute(rp_slab_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        FFG_CUDA(cudaFuncSetAttribute(rp_slab_reg_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        FFG_CUDA(cudaFuncSetAttribute(rp_slab_reg_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     });
     const size_t rmax = std::min(m, n);
     DevBuf VB(rmax * n, b.st), PR(rmax, b.st), PC(rmax, b.st);
@@ -395,6 +684,9 @@ size_t rank_profile_dev(const Blas& b, DView W, std::vector<uint32_t>& prow, std
     rp.kk = kk;
     rp.w = w;
     rp.ncta = ncta;
+    // FFG_RP_SMEM=1: the shared-memory slab kernel at every width (diagnostics, parity tests)
+    const bool smem_only = getenv("FFG_RP_SMEM") && atoi(getenv("FFG_RP_SMEM")) != 0;  // per call: tests
+    rp.reg_path = !smem_only && w <= 2 * RP_THREADS;
     const int slot = b.ws.acquire_slot();
     if (slot < 0) throw Error(FFG_ERR_INTERNAL, "rank profile: no free mailbox");
     struct SlotGuard {
@@ -414,6 +706,17 @@ size_t rank_profile_dev(const Blas& b, DView W, std::vector<uint32_t>& prow, std
         FFG_CUDA(cudaMemcpyAsync(pcol.data(), PC.d, r * 4, cudaMemcpyDeviceToHost, b.st));
     }
     FFG_CUDA(cudaStreamSynchronize(b.st));
+#ifdef RP_TIMING
+    {
+        unsigned long long h[16];
+        FFG_CUDA(cudaMemcpyFromSymbol(h, rp_clk, sizeof(h)));
+        fprintf(stderr, "RP_TIMING slabs=%zu cycles/slab: load+offer %llu | publish %llu cluster_sync %llu winner %llu update %llu | dump %llu finish %llu exit %llu\n",
+                rp.leaves, h[0] / rp.leaves, h[1] / rp.leaves, h[2] / rp.leaves, h[3] / rp.leaves, h[4] / rp.leaves,
+                h[5] / rp.leaves, h[6] / rp.leaves, h[7] / rp.leaves);
+        memset(h, 0, sizeof(h));
+        FFG_CUDA(cudaMemcpyToSymbol(rp_clk, h, sizeof(h)));
+    }
+#endif
     static const bool log = getenv("FFG_PROFILE_LOG") != nullptr;
     if (log) fprintf(stderr, "RANK_PROFILE m=%zu n=%zu rank=%zu slabs=%zu kk=%u ctas=%u\n", m, n, r, rp.leaves, kk, ncta);
     return r;
@@ -487,9 +790,18 @@ size_t pluq_profile_first_dev(const Blas& b, DView a, size_t threshold, uint32_t
     const DView W{Wb.d, m, n, n};
     copy_block_dev(b, a, W);
     std::vector<uint32_t> prow, pcol;
+    static const bool log = getenv("FFG_PROFILE_LOG") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     const size_t r = rank_profile_dev(b, W, prow, pcol);  // phase 1 (reduces W)
+    const auto t1 = std::chrono::steady_clock::now();
     pluq_from_profile_dev(b, a, threshold, r, prow.data(), pcol.data(), P, Q, Wb.d);
     FFG_CUDA(cudaStreamSynchronize(b.st));  // like every exit of the device entry: outputs final on return
+    if (log) {
+        const auto t2 = std::chrono::steady_clock::now();
+        fprintf(stderr, "PROFILE_FIRST m=%zu n=%zu rank=%zu: rank profile %.2f ms, permutations + LU of the generic block %.2f ms\n",
+                m, n, r, std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
     return r;
 }
 

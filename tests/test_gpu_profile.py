@@ -37,9 +37,14 @@ def _to_dev(A):
     return torch.from_numpy(A.astype(np.int32)).cuda()
 
 
-def test_rank_profile_equals_rr_base_pivots(gpu, oracle_lib):
+@pytest.mark.parametrize("smem_kernel", [False, True])
+def test_rank_profile_equals_rr_base_pivots(gpu, oracle_lib, smem_kernel, monkeypatch):
+    """Both slab kernels: the register-resident one (<= 1024 columns per cluster CTA, the default)
+    and the shared-memory one (wider matrices; FFG_RP_SMEM=1 forces it at every width)."""
     G, ctx = gpu
     O = oracle_lib
+    if smem_kernel:
+        monkeypatch.setenv("FFG_RP_SMEM", "1")
     for name, p, A in _cases(O):
         _, Pb, Qb, rb = O.rr_base(p, A.copy())
         d = _to_dev(A)
