@@ -140,91 +140,108 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, TmemFn&& get_
     constexpr int D = 2 * L - 1;
     // warp (4 + e): TMEM lane quarter e & 3, column half e >> 2 (8-column chunks)
     constexpr int PER = NT / 16;                 // chunks per half
-    constexpr bool PREFETCH = PER * 8 <= 64;     // keep this thread's C values in registers
+    // This thread's C values are read ahead into a ring of GC 8-column chunks (<= 64 registers): the
+    // first GC before the accumulator is ready (overlapping the mainloop), chunk ch + GC as soon as
+    // chunk ch has been consumed -- a rank-k update with small K and one limb (GF(251), NT = 256) is
+    // bound by this read-modify-write of C, and loads issued one chunk at a time left it at the
+    // memory latency (~0.5 TB/s over all SMs).  The chunks run as a ROLLED loop over groups of GC:
+    // every instruction of an epilogue executes once per tile, so a fully unrolled one (17K SASS
+    // instructions for L = 1) spent 60 % of its issue slots waiting for instruction fetches.
+    constexpr int GC = L == 1 ? 8 : (PER % 4 == 0 ? 4 : PER);
+    constexpr int NG = PER / GC;
+    static_assert(PER % GC == 0 && GC * 8 <= 64, "chunk groups");
     const uint32_t e = warp - 4, q = e & 3, half = e >> 2;
     const uint32_t row = m_blk * BM + q * 32 + lane;
     const uint32_t col_first = n_blk * NT + half * PER * 8;
     const bool row_ok = row < ep.M;
     uint32_t* crow = ep.C + (uint64_t)(row_ok ? row : 0) * ep.ldc;
     const bool vec = ep.vec_ok && col_first + PER * 8 <= ep.N;
-    const bool need_c = ep.mode != EPI_PROD;
-    uint32_t cpre[PREFETCH ? PER * 8 : 1];
-    if (PREFETCH && need_c && row_ok) {  // overlap the C read with the mainloop
+    const uint32_t mode = ep.mode, p = ep.p;
+    const bool need_c = mode != EPI_PROD;
+    uint32_t cpre[GC * 8];
 #pragma unroll
-        for (int ch = 0; ch < (PREFETCH ? PER : 0); ++ch) {
-            const uint32_t col = col_first + ch * 8;
-            if (vec) {
-                const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
-                const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
-                cpre[ch * 8 + 0] = a.x, cpre[ch * 8 + 1] = a.y, cpre[ch * 8 + 2] = a.z, cpre[ch * 8 + 3] = a.w;
-                cpre[ch * 8 + 4] = b.x, cpre[ch * 8 + 5] = b.y, cpre[ch * 8 + 6] = b.z, cpre[ch * 8 + 7] = b.w;
-            } else {
+    for (int j = 0; j < GC * 8; ++j) cpre[j] = 0u;
+    auto load_chunk = [&](uint32_t ch, int slot) {  // chunk ch of this thread's row -> ring slot
+        const uint32_t col = col_first + ch * 8;
+        uint32_t* dst = cpre + slot * 8;
+        if (vec) {
+            const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
+            const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
+            dst[0] = a.x, dst[1] = a.y, dst[2] = a.z, dst[3] = a.w;
+            dst[4] = b.x, dst[5] = b.y, dst[6] = b.z, dst[7] = b.w;
+        } else {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) cpre[ch * 8 + j] = col + j < ep.N ? crow[col + j] : 0u;
-            }
+            for (int j = 0; j < 8; ++j) dst[j] = col + j < ep.N ? crow[col + j] : 0u;
         }
+    };
+    if (need_c && row_ok) {  // overlap the C read with the mainloop
+#pragma unroll
+        for (int c = 0; c < GC; ++c) load_chunk((uint32_t)c, c);
     }
     before_wait();
     ptx::mbar_wait(tmem_full, phase);
     ptx::tc_fence_after();
     const uint32_t tmem = get_tmem();
     const uint32_t t_lane = tmem + ((q * 32) << 16) + half * PER * 8;
+    const uint32_t mu32 = (uint32_t)(ep.mu >> 32);  // floor(2^32 / p)
+#pragma unroll 1
+    for (int g = 0; g < NG; ++g) {
 #pragma unroll
-    for (int ch = 0; ch < PER; ++ch) {
-        uint32_t r[D][8];
+        for (int c = 0; c < GC; ++c) {
+            const uint32_t ch = (uint32_t)(g * GC + c);
+            uint32_t r[D][8];
 #pragma unroll
-        for (int s2 = 0; s2 < D; ++s2) ptx::tmem_ld8(t_lane + s2 * NT + ch * 8, r[s2]);
-        ptx::tmem_ld_wait();
-        if (ch == PER - 1 && tmem_empty) {  // accumulators read: the next tile's MMAs may start
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tmem_empty);
-        }
-        if (!row_ok) continue;
-        const uint32_t col = col_first + ch * 8;
-        uint32_t cv[8];
-        if (need_c) {
-            if (PREFETCH) {
+            for (int s2 = 0; s2 < D; ++s2) ptx::tmem_ld8(t_lane + s2 * NT + ch * 8, r[s2]);
+            ptx::tmem_ld_wait();
+            if (c == GC - 1 && g == NG - 1 && tmem_empty) {  // accumulators read: the next tile's MMAs may start
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(tmem_empty);
+            }
+            if (!row_ok) continue;
+            const uint32_t col = col_first + ch * 8;
+            uint32_t cv[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) cv[j] = cpre[(PREFETCH ? ch * 8 : 0) + j];
-            } else if (vec) {
-                const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
-                const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
-                cv[0] = a.x, cv[1] = a.y, cv[2] = a.z, cv[3] = a.w, cv[4] = b.x, cv[5] = b.y, cv[6] = b.z, cv[7] = b.w;
+            for (int j = 0; j < 8; ++j) cv[j] = cpre[c * 8 + j];
+            if (need_c && g + 1 < NG) load_chunk(ch + GC, c);
+            uint32_t prod[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (L == 1) {  // one limb: the accumulator itself (< 2^31), 32-bit Barrett
+                    const uint32_t x = r[0][j];
+                    const uint32_t t = x - __umulhi(x, mu32) * p;  // < 2p
+                    prod[j] = min(t, t - p);
+                } else {
+                    uint64_t acc = 0;
+#pragma unroll
+                    for (int s2 = 0; s2 < D; ++s2) acc += (uint64_t)r[s2][j] * ep.w[s2];
+                    prod[j] = mod_u64(acc, p, ep.mu);
+                }
+            }
+            uint32_t out[8];
+            if (mode == EPI_GENERIC) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint64_t v = (uint64_t)ep.alpha * prod[j];
+                    if (ep.beta) v += (uint64_t)ep.beta * cv[j];
+                    out[j] = mod_u64(v, p, ep.mu);
+                }
+            } else {  // C - AB, AB (cv = 0), C + AB: one add and one conditional subtraction
+                const bool sub = mode == EPI_SUB;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t t = cv[j] + (sub ? p - prod[j] : prod[j]);  // < 2p (+1: p - 0)
+                    out[j] = min(t, t - p);
+                }
+            }
+            if (vec) {
+                *reinterpret_cast<uint4*>(crow + col) = make_uint4(out[0], out[1], out[2], out[3]);
+                *reinterpret_cast<uint4*>(crow + col + 4) = make_uint4(out[4], out[5], out[6], out[7]);
             } else {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) cv[j] = col + j < ep.N ? crow[col + j] : 0u;
+                for (int j = 0; j < 8; ++j)
+                    if (col + j < ep.N) crow[col + j] = out[j];
             }
-        }
-        uint32_t out[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            uint64_t acc = 0;
-#pragma unroll
-            for (int s2 = 0; s2 < D; ++s2) acc += (uint64_t)r[s2][j] * ep.w[s2];
-            const uint32_t prod = mod_u64(acc, ep.p, ep.mu);
-            switch (ep.mode) {
-                case EPI_SUB: out[j] = cv[j] >= prod ? cv[j] - prod : cv[j] + ep.p - prod; break;
-                case EPI_PROD: out[j] = prod; break;
-                case EPI_ADD: {
-                    const uint32_t t = cv[j] + prod;
-                    out[j] = t >= ep.p ? t - ep.p : t;
-                    break;
-                }
-                default: {
-                    uint64_t v = (uint64_t)ep.alpha * prod;
-                    if (ep.beta) v += (uint64_t)ep.beta * cv[j];
-                    out[j] = mod_u64(v, ep.p, ep.mu);
-                }
-            }
-        }
-        if (vec) {
-            *reinterpret_cast<uint4*>(crow + col) = make_uint4(out[0], out[1], out[2], out[3]);
-            *reinterpret_cast<uint4*>(crow + col + 4) = make_uint4(out[4], out[5], out[6], out[7]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (col + j < ep.N) crow[col + j] = out[j];
         }
     }
     ptx::tc_fence_before();

@@ -9,7 +9,7 @@ import paper_1402_3501_b200 as G  # noqa: E402
 
 m, n, k = (int(x) for x in sys.argv[1:4])
 compact = len(sys.argv) > 4 and sys.argv[4] == "compact"
-p = 131071
+p = int(os.environ.get("P", "131071"))
 ctx = G.Context(0)
 if compact:
     A = torch.empty((m, k), dtype=torch.int32, device="cuda")
@@ -18,7 +18,8 @@ if compact:
     for i, t in enumerate((A, B, C_)):
         G.random_mat_dev(p, t, i + 1, ctx=ctx)
 else:
-    big = torch.empty((16384, 16384), dtype=torch.int32, device="cuda")
+    NB = int(os.environ.get("BIG", "16384"))
+    big = torch.empty((NB, NB), dtype=torch.int32, device="cuda")
     G.random_mat_dev(p, big, 5, ctx=ctx)
     A, B, C_ = big[:m, :k], big[:k, 8192:8192 + n], big[8192:8192 + m, 4096:4096 + n]
 for _ in range(10):

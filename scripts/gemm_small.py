@@ -15,21 +15,25 @@ p = int(os.environ.get("P", "131071"))
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
 ctx = G.Context(0, stream=st.cuda_stream)
-big = torch.empty((16384, 16384), dtype=torch.int32, device="cuda")
+NB = int(os.environ.get("BIG", "16384"))
+H = NB // 2
+big = torch.empty((NB, NB), dtype=torch.int32, device="cuda")
 G.random_mat_dev(p, big, 5, ctx=ctx)
 shapes = [(64, 64, 64), (64, 64, 128), (128, 128, 128), (128, 128, 256), (128, 1024, 128), (1024, 128, 128),
           (128, 8192, 128), (8192, 128, 128), (256, 8192, 256), (8192, 256, 256), (512, 512, 1024),
           (1024, 1024, 2048), (2048, 2048, 4096)]
+if os.environ.get("SHAPES"):  # "m,n,k;m,n,k"
+    shapes = [tuple(int(x) for x in t.split(",")) for t in os.environ["SHAPES"].split(";")]
 for (m, n, k) in shapes:
     A = big[:m, :k]
-    B = big[:k, 8192:8192 + n] if n <= 8192 else big[:k, :n]
-    C_ = big[8192:8192 + m, 4096:4096 + n] if m <= 8192 else big[:m, 4096:4096 + n]
+    B = big[:k, H:H + n] if n <= H else big[:k, :n]
+    C_ = big[H:H + m, H // 2:H // 2 + n] if m <= H else big[:m, H // 2:H // 2 + n]
     inplace = os.environ.get("INPLACE") == "1" and m <= 128
     if inplace:
         if m != k:
             continue
-        C_ = B = big[:k, 8192:8192 + n]
-        A = big[8192:8192 + m, :k]
+        C_ = B = big[:k, H:H + n]
+        A = big[H:H + m, :k]
     for _ in range(3):
         G.fgemm(p, p - 1, A, B, 1, C_, ctx=ctx)
     reps = 20
