@@ -257,6 +257,9 @@ __global__ void __launch_bounds__(384, 1)
     constexpr int D = 2 * L - 1;
     constexpr uint32_t TMEM_COLS = 512;
     static_assert(D * NT <= 512, "accumulator diagonals exceed TMEM");
+    // two accumulator stages where they fit (one limb: 2 x 256 columns): the next tile's MMAs run
+    // while the epilogue drains this one
+    constexpr int ACC = 2 * D * NT <= 512 ? 2 : 1;
     static_assert(L * NT <= 256 && (L * NT) % 16 == 0 && NT % 16 == 0, "invalid UMMA N");
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -264,8 +267,8 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* tmem_empty = tmem_full + ACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + ACC);
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
     // Persistent over tiles (grid may be capped below the tile count so that a low-priority
@@ -285,8 +288,10 @@ __global__ void __launch_bounds__(384, 1)
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(tmem_full, 1);
-        ptx::mbar_init(tmem_empty, 8);  // one arrival per epilogue warp
+        for (int a = 0; a < ACC; ++a) {
+            ptx::mbar_init(&tmem_full[a], 1);
+            ptx::mbar_init(&tmem_empty[a], 8);  // one arrival per epilogue warp
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -341,7 +346,9 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t IDESC_TAIL = ptx::idesc_u8(BM, NT);
             uint32_t it = 0, t = 0;
             for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
-                ptx::mbar_wait(tmem_empty, (t & 1) ^ 1);  // previous tile's accumulators drained
+                const uint32_t as = t % ACC, aph = (t / ACC) & 1;
+                const uint32_t acc = tmem + as * (D * NT);
+                ptx::mbar_wait(&tmem_empty[as], aph ^ 1);  // this stage's previous accumulators drained
                 ptx::tc_fence_after();
                 for (uint32_t kb = 0; kb < ep.kblocks; ++kb, ++it) {
                     const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
@@ -356,21 +363,21 @@ __global__ void __launch_bounds__(384, 1)
                         for (int i = 0; i < L; ++i) {
                             const uint64_t adesc = ptx::desc_kmajor_sw128(a_base + i * BM * BK + kk * 32);
                             if (kb != 0 || kk != 0) {
-                                ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_FULL, 1);
+                                ptx::mma_i8(acc + i * NT, adesc, bdesc, IDESC_FULL, 1);
                             } else if (i == 0) {
-                                ptx::mma_i8(tmem, adesc, bdesc, IDESC_FULL, 0);
+                                ptx::mma_i8(acc, adesc, bdesc, IDESC_FULL, 0);
                             } else {
                                 // first K-step: diagonals i..i+L-2 already hold data, i+L-1 is fresh
-                                ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_HEAD, 1);
+                                ptx::mma_i8(acc + i * NT, adesc, bdesc, IDESC_HEAD, 1);
                                 const uint64_t btail =
                                     ptx::desc_kmajor_sw128(b_base + (L - 1) * NT * BK + kk * 32);
-                                ptx::mma_i8(tmem + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
+                                ptx::mma_i8(acc + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
                             }
                         }
                     }
                     ptx::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
                 }
-                ptx::mma_commit(tmem_full);
+                ptx::mma_commit(&tmem_full[as]);
             }
         }
         __syncwarp();
@@ -379,8 +386,9 @@ __global__ void __launch_bounds__(384, 1)
         for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
             uint32_t m_blk, n_blk;
             tile_coords(tile, m_blk, n_blk);
-            epilogue_tile<L>(ep, [&] { return tmem; }, tmem_full, m_blk, n_blk, warp, lane, [] {}, t & 1,
-                             tmem_empty);
+            const uint32_t as = t % ACC, aph = (t / ACC) & 1;
+            epilogue_tile<L>(ep, [&] { return tmem + as * (D * NT); }, &tmem_full[as], m_blk, n_blk, warp, lane,
+                             [] {}, aph, &tmem_empty[as]);
         }
     }
     ptx::tc_fence_before();
