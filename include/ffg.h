@@ -58,6 +58,11 @@ int ffg_synchronize(ffg_ctx *ctx);
 const char *ffg_last_error(void);     /* thread-local message of the last failure */
 size_t ffg_last_error_index(void);    /* SingularDiagonal::index (errors.hpp:33-38) */
 const char *ffg_version(void);
+/* The library snapshots its FFG_* environment switches (tuning values, test
+ * hooks, diagnostics) once, at first use, and never
+ * reads the environment on a call path.  This takes a fresh snapshot (tests
+ * that change a switch between calls; not needed otherwise). */
+void ffg_knobs_reload(void);
 
 /* ---- modular GEMM ------------------------------------------------------
  * C <- alpha*A*B + beta*C mod p, A m x k, B k x n, C m x n.

@@ -25,6 +25,7 @@ from .ffpluq import (  # noqa: F401
     pluq_from_profile_dev,
     pluq_tile_recursive,
     rank_profile_dev,
+    reload_knobs,
     rr_base,
     tile_rec_perms,
 )

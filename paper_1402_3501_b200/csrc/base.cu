@@ -988,19 +988,19 @@ __global__ void __launch_bounds__(SP_THREADS, 1)
 
 void base_dbg_init() {
     static bool done = false;
-    if (done || !getenv("FFG_BASE_DBG")) return;
+    if (done || !knob_set("FFG_BASE_DBG")) return;
     done = true;
     unsigned long long* buf = nullptr;
     FFG_CUDA(cudaMalloc(&buf, (4096 * 6 + 8 * 64) * 8));
     FFG_CUDA(cudaMemcpyToSymbol(g_base_dbg, &buf, sizeof(buf)));
-    if (getenv("FFG_BASE_SKIP")) {
+    if (knob_str("FFG_BASE_SKIP")) {
         int one = 1;
         FFG_CUDA(cudaMemcpyToSymbol(g_base_skip, &one, sizeof(one)));
     }
 }
 
 void base_dbg_dump() {
-    if (!getenv("FFG_BASE_DBG")) return;
+    if (!knob_set("FFG_BASE_DBG")) return;
     unsigned long long* buf = nullptr;
     unsigned int n = 0;
     FFG_CUDA(cudaDeviceSynchronize());
@@ -1047,7 +1047,7 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     BaseInfo* info = static_cast<BaseInfo*>(info_dev);
     // panel schedule: square speculative block with an inverse slot -> the fused base + inverses
     // kernel (baseinv.cu), which also writes inv(L) and inv(U) into inv_out
-    static const bool no_fused_inv = getenv("FFG_BASE_INV") && atoi(getenv("FFG_BASE_INV")) == 0;
+    static const bool no_fused_inv = (knob_int("FFG_BASE_INV", 1) == 0);
     if ((seq & SPEC_BIT) && inv_out && !no_fused_inv && lay.m == lay.n && lay.m <= 64 && lay.m > 0) {
         rr_base_inv_launch(b, a, Pd, Qd, info, inv_out, seq, allow_q);
         return true;
@@ -1058,12 +1058,12 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
     b.ws.prof.begin(b.st);
     // kernel choice (read per launch so tests can exercise every path): FFG_BASE_SMEM=1 forces the
     // shared-memory right-looking kernel, FFG_BASE_NO_SLAB=1 the register right-looking one
-    const char* e_smem = getenv("FFG_BASE_SMEM");
-    const char* e_slab = getenv("FFG_BASE_NO_SLAB");
+    const char* e_smem = knob_str("FFG_BASE_SMEM");
+    const char* e_slab = knob_str("FFG_BASE_NO_SLAB");
     const bool spec = (seq & SPEC_BIT) != 0;  // speculative launches need the slab kernel's check
     const bool no_reg = !spec && e_smem && atoi(e_smem) != 0;
     const bool no_slab = !spec && e_slab && atoi(e_slab) != 0;
-    const char* e_spec = getenv("FFG_SPEC_SLAB");  // diagnostics: speculative launches on the slab kernel
+    const char* e_spec = knob_str("FFG_SPEC_SLAB");  // diagnostics: speculative launches on the slab kernel
     if (spec && lay.m <= 64 && lay.n <= 64 && !(e_spec && atoi(e_spec) != 0)) {
         if (lay.m == 64 && lay.n == 64)
             launch_k(rr_base_spec_kernel<true>, dim3(1), dim3(SP_THREADS), 0, b.st, a.d, a.ld, lay.m, lay.n, Pd, Qd,

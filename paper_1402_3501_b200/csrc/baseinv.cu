@@ -461,7 +461,7 @@ void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    static const bool dbg = getenv("FFG_BI_DBG") != nullptr;
+    static const bool dbg = knob_set("FFG_BI_DBG");
     if (dbg) bi_dbg_dump(b.st);
     FFG_CUDA(cudaLaunchKernelEx(&cfg, rr_base_inv_kernel, a.d, (uint64_t)a.ld, t, Pd, Qd, info, inv, b.F.p, b.F.mu,
                                 seq, (uint32_t)allow_q));

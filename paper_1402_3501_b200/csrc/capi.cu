@@ -81,6 +81,8 @@ void check_mat(const char* what, const void* ptr, size_t rows, size_t cols, size
 
 extern "C" {
 
+void ffg_knobs_reload(void) { ffg::knobs_reload(); }
+
 const char* ffg_version(void) { return "ffg_b200 0.1 (sm_100a tcgen05 kind::i8 limb GEMM)"; }
 const char* ffg_last_error(void) { return g_err.c_str(); }
 size_t ffg_last_error_index(void) { return g_err_index; }
@@ -108,8 +110,8 @@ int ffg_create(ffg_ctx** out, int device) {
         return FFG_ERR_CUDA;
     }
     c->stream = c->own_stream;
-    if (const char* s = getenv("FFG_SIMT_MACS")) ffg::g_simt_macs = strtoull(s, nullptr, 10);
-    if (const char* s = getenv("FFG_SIMT_KMAX")) ffg::g_simt_kmax = strtoull(s, nullptr, 10);
+    if (const char* s = ffg::knob_str("FFG_SIMT_MACS")) ffg::g_simt_macs = strtoull(s, nullptr, 10);
+    if (const char* s = ffg::knob_str("FFG_SIMT_KMAX")) ffg::g_simt_kmax = strtoull(s, nullptr, 10);
     // keep freed stream-ordered allocations cached in the pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "../../include/ffg.h"
+#include "knobs.cuh"
 
 namespace ffg {
 
@@ -176,7 +177,7 @@ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 // predecessor on the stream finishes; every kernel launched this way calls ptx::pdl_wait()
 // before its first global-memory access.  FFG_NO_PDL=1 launches plainly.
 inline bool pdl_enabled() {
-    static const bool on = !(getenv("FFG_NO_PDL") && atoi(getenv("FFG_NO_PDL")) != 0);
+    static const bool on = !(knob_on("FFG_NO_PDL"));
     return on;
 }
 template <typename... KArgs, typename... Args>

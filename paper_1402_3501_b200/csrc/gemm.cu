@@ -1111,7 +1111,7 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
     ep.m_tiles = (uint32_t)(Mp / BM);
     ep.n_tiles = (uint32_t)(Np / S::NT);
     // L2 eviction hints once the limb planes no longer fit in L2 beside C (FFG_GEMM_L2_HINTS=0/1 forces)
-    static const int hints_env = getenv("FFG_GEMM_L2_HINTS") ? atoi(getenv("FFG_GEMM_L2_HINTS")) : -1;
+    static const int hints_env = (int)knob_int("FFG_GEMM_L2_HINTS", -1);
     ep.l2_hints = hints_env >= 0 ? (uint32_t)hints_env : ((uint64_t)L * (Mp + Np) * Kp > (64ull << 20) ? 1u : 0u);
     const uint32_t tiles = ep.m_tiles * ep.n_tiles;
     dim3 grid(sm_cap > 0 ? std::min<uint32_t>(tiles, (uint32_t)sm_cap) : tiles);
@@ -1187,7 +1187,7 @@ void launch_direct(const Field& F, uint32_t alpha, uint32_t beta, DView A, DView
     da.K = (uint32_t)A.cols;
     da.a_vec = ((reinterpret_cast<uintptr_t>(A.d) & 15) == 0 && (A.ld & 3) == 0) ? 1u : 0u;
     static unsigned long long* dbg_buf = nullptr;
-    static const bool dbg_on = getenv("FFG_DIRECT_DBG") != nullptr;
+    static const bool dbg_on = knob_set("FFG_DIRECT_DBG");
     if (dbg_on && !dbg_buf) FFG_CUDA(cudaMalloc(&dbg_buf, 64));
     da.dbg = dbg_on ? dbg_buf : nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1276,7 +1276,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     };
     // the CUDA-core kernel reads operands while other CTAs write C: only when C aliases nothing
     const bool simt = use_simt(M, N, K) && !overlap(C, A) && !overlap(C, B);
-    static const bool log = getenv("FFG_GEMM_LOG") != nullptr;
+    static const bool log = knob_set("FFG_GEMM_LOG");
     if (log) fprintf(stderr, "FFG_GEMM %zu %zu %zu %d\n", M, N, K, (int)simt);
     if (simt) {
         ws.prof.begin(st);
@@ -1289,10 +1289,10 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         return;
     }
     const int L = F.limbs, NT = tile_n(L);
-    static const int cap_env = getenv("FFG_GEMM_SM_CAP") ? atoi(getenv("FFG_GEMM_SM_CAP")) : 0;
+    static const int cap_env = (int)knob_int("FFG_GEMM_SM_CAP", 0);
     if (sm_cap <= 0) sm_cap = cap_env;  // test hook: force the persistent multi-tile path
     // small K, no aliasing: operands staged by the GEMM itself (one launch, no limb planes in HBM)
-    static const bool no_direct = getenv("FFG_NO_DIRECT") && atoi(getenv("FFG_NO_DIRECT")) != 0;
+    static const bool no_direct = knob_on("FFG_NO_DIRECT");
     // in place on B (the TRSM leaf X = inv(T) X) is race-free with one row tile: each CTA stages
     // its whole column strip of B before the CTA's own epilogue overwrites exactly that strip
     const bool c_is_b = C.d == B.d && C.ld == B.ld && C.rows == B.rows && C.cols == B.cols && M <= (size_t)BM;
@@ -1300,7 +1300,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     // 128 < K <= 256 takes the TMA pipeline: inside the PLUQ the direct kernel's two staged K
     // blocks cost more than the split (measured 29.9 -> 29.4 ms at n = 16384); FFG_DIRECT_KB2=1
     // restores the direct path for them
-    static const bool kb2 = getenv("FFG_DIRECT_KB2") && atoi(getenv("FFG_DIRECT_KB2")) != 0;
+    static const bool kb2 = knob_on("FFG_DIRECT_KB2");
     const bool fits = kb_need == 1 ? direct_fits(L, 1) : (kb2 && kb_need == 2 && direct_fits(L, 2));
     if (!no_direct && !no_direct_call && fits && !overlap(C, A) && (c_is_b || !overlap(C, B))) {
         ws.prof.begin(st);
@@ -1318,7 +1318,7 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
     // operands converted inside the GEMM (no limb planes in HBM; C must not alias an operand).
     // Opt-in (FFG_FUSED=1): the converter warps are bound by their global-load latency -- 4096^3
     // measured 2.37 ms against 0.52 ms for split + TMA kernel
-    static const bool fused = getenv("FFG_FUSED") && atoi(getenv("FFG_FUSED")) != 0;
+    static const bool fused = knob_on("FFG_FUSED");
     if (fused && !overlap(C, A) && !overlap(C, B)) {
         for (size_t k0 = 0; k0 < K; k0 += F.kmax) {  // delayed reduction: one fold per kmax chunk
             const size_t kc = std::min<size_t>(K - k0, F.kmax);

@@ -33,6 +33,25 @@
 
 namespace ffg {
 
+// Stream-ordered buffers of one call: freed on every exit path (an exception escaping a call --
+// out of memory in a workspace, a CUDA error -- must not leak a matrix-sized backup in a
+// long-lived context).  free_async frees early and disarms the guard.
+template <class T>
+struct AsyncFreeGuard {
+    T*& p;
+    cudaStream_t st;
+    ~AsyncFreeGuard() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+template <class T>
+static void free_async(T*& p, cudaStream_t st) {
+    if (!p) return;
+    T* q = p;
+    p = nullptr;
+    FFG_CUDA(cudaFreeAsync(q, st));
+}
+
 static bool panel_no_direct();
 
 namespace {
@@ -152,7 +171,7 @@ struct Driver {
         cudaEvent_t e = b.ws.event();  // critical stream starts after the caller's pending work
         FFG_CUDA(cudaEventRecord(e, user.st));
         FFG_CUDA(cudaStreamWaitEvent(b.st, e, 0));
-        static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
+        static const bool no_streams = knob_on("FFG_NO_STREAMS");
         // partitioned (multi-GPU) runs keep their side streams: every split operation (the only ones
         // with a collective) is moved onto the critical stream (pgemm_sub / ptrsm), so all ranks issue
         // their collectives in one stream and one order
@@ -165,10 +184,10 @@ struct Driver {
                 FFG_CUDA(cudaGetDevice(&dev));
                 FFG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             }
-            static const char* env = getenv("FFG_LOOKAHEAD_SMS");
+            static const char* env = knob_str("FFG_LOOKAHEAD_SMS");
             lookahead_sms = env ? atoi(env) : std::max(1, sms - 32);
-            static const char* ed = getenv("FFG_DEFER_SMS");
-            static const char* es = getenv("FFG_SIDE_SMS");
+            static const char* ed = knob_str("FFG_DEFER_SMS");
+            static const char* es = knob_str("FFG_SIDE_SMS");
             defer_sms = ed ? atoi(ed) : std::max(1, sms - 4);
             side_sms = es ? atoi(es) : std::max(1, sms - 4);
         }
@@ -179,7 +198,7 @@ struct Driver {
         info_dev = reinterpret_cast<BaseInfo*>(dev);
         ev = b.ws.event();
         // factor-tree TRSM (cached base-case inverses): opt-in, slower than blocked inverses today
-        static const bool on = getenv("FFG_FACTOR_TRSM") && atoi(getenv("FFG_FACTOR_TRSM")) != 0;
+        static const bool on = knob_on("FFG_FACTOR_TRSM");
         use_factors = on;
         if (use_factors) {
             // sum of r^2 over base cases <= min(m, n) * 64; two triangles each, plus one slot of slack
@@ -188,8 +207,8 @@ struct Driver {
         }
     }
     void alloc_panel_inv() {
-        static const bool off = getenv("FFG_PANEL_FUSED_TRSM") && atoi(getenv("FFG_PANEL_FUSED_TRSM")) != 0;
-        static const bool no_q = getenv("FFG_SPEC_NO_Q") && atoi(getenv("FFG_SPEC_NO_Q")) != 0;
+        static const bool off = knob_on("FFG_PANEL_FUSED_TRSM");
+        static const bool no_q = knob_on("FFG_SPEC_NO_Q");
         if (!off && !panel_inv) FFG_CUDA(cudaMallocAsync(&panel_inv, 2 * 2 * 64 * 64 * 4, b.st));
         // column pivots need the inverse-apply path (it gathers the bottom panel through Q)
         if (panel_inv && !no_q && !gq && pcols) {
@@ -262,10 +281,8 @@ struct Driver {
     bool can_fork(const DView& E, const DView& G) const {
         // each child thread spins on its mailbox: keep them within the host's cores
         const int max_threads =  // read per call (tests switch it)
-            getenv("FFG_SUBTREE_THREADS")
-                ? atoi(getenv("FFG_SUBTREE_THREADS"))
-                : std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2));
-        static const size_t gmin = getenv("FFG_FORK_MIN") ? (size_t)atoll(getenv("FFG_FORK_MIN")) : 0;
+            (int)knob_int("FFG_SUBTREE_THREADS", std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2)));
+        static const size_t gmin = (size_t)knob_int("FFG_FORK_MIN", 0);
         const size_t gm = gmin ? gmin : 2 * thr;  // smallest G worth a host thread
         return max_threads > 0 && !spec && use_streams && !b.ws.dist.active() && b.ws.prof.mode != 1 && !use_factors &&
                !E.empty() && !G.empty() &&
@@ -779,7 +796,7 @@ struct Driver {
         DView rmini = at(r0, beyond_c, t, mr), bmini = at(beyond_r, c0, mb, t);
         DView rrest = at(r0, beyond_c + mr, t, wr - mr), brest = at(beyond_r + mb, c0, hb - mb, t);
         const cudaEvent_t f = mark_event(b.st);
-        static const bool two = getenv("FFG_MINI_TWO") && atoi(getenv("FFG_MINI_TWO")) != 0;
+        static const bool two = knob_on("FFG_MINI_TWO");
         if (two) {  // diagnostics: the two strip applies on two streams
             const bool both = !rmini.empty() && !bmini.empty();
             const Blas side = both ? on(twin(depth)) : b;
@@ -825,7 +842,7 @@ struct Driver {
         leaves.push_back({c0, t1});
         if (!base_wrote_inv) panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
         flush_deferred();  // the node's rows / columns carry every earlier update
-        static const bool one_cta = getenv("FFG_CORNER_ONE") && atoi(getenv("FFG_CORNER_ONE")) != 0;
+        static const bool one_cta = knob_on("FFG_CORNER_ONE");
         if (one_cta) {  // diagnostics: the one-CTA corner kernel
             panel_corner_dev(b, a, t1, inv1, q1);
         } else {  // A1's panel blocks inside the node, then R's update, each in small CTAs
@@ -835,7 +852,7 @@ struct Driver {
         const cudaEvent_t f = mark_event(b.st);
         Blas sa = on(side_stream(0)), sb = on(side_stream(1));
         sa.sm_cap = sb.sm_cap = side_sms;
-        static const bool side_direct = getenv("FFG_SIDE_DIRECT") && atoi(getenv("FFG_SIDE_DIRECT")) != 0;
+        static const bool side_direct = knob_on("FFG_SIDE_DIRECT");
         if (side_direct) sa.no_direct = sb.no_direct = false;
         wait(sa.st, f);
         wait(sb.st, f);
@@ -916,7 +933,7 @@ struct Driver {
         }
         const size_t mark = arena.mark();
         const size_t m1 = (m + 1) / 2, n1 = (n + 1) / 2;
-        const bool no_corner = getenv("FFG_NO_CORNER") && atoi(getenv("FFG_NO_CORNER")) != 0;  // per call: tests
+        const bool no_corner = knob_on("FFG_NO_CORNER");  // per call: tests
         if (!no_corner && panel_inv && m == n && m1 <= thr && m1 <= 64 && m - m1 > 0) {
             two_leaf(a, depth, res);
             arena.reset(mark);
@@ -947,7 +964,7 @@ struct Driver {
             const size_t A = r0 + m1, f = first_leaf(m - m1), E = r0 + m;
             need(b.st, E);
             const cudaEvent_t forked = mark_event(b.st);
-            static const bool tc_corner = getenv("FFG_CORNER_TC") && atoi(getenv("FFG_CORNER_TC")) != 0;
+            static const bool tc_corner = knob_on("FFG_CORNER_TC");
             if (tc_corner)
                 gemm_sub(b, at(A, c0, f, n1), at(r0, A, m1, f), at(A, A, f, f));
             else  // f x f x m1 in small CUDA-core CTAs: shorter than a tensor-core launch at this size
@@ -956,7 +973,7 @@ struct Driver {
             sc.sm_cap = sd.sm_cap = defer_sms;  // leave SMs for the critical stream's small kernels
             // these GEMMs gate the next two-leaf node (flush_deferred): FFG_DEFER_DIRECT=1 lets the
             // single-launch direct kernel take the ones with K <= 128 (no limb split round trip)
-            static const bool defer_direct = getenv("FFG_DEFER_DIRECT") && atoi(getenv("FFG_DEFER_DIRECT")) != 0;
+            static const bool defer_direct = knob_on("FFG_DEFER_DIRECT");
             if (defer_direct) sc.no_direct = sd.no_direct = false;
             for (const Blas* sx : {&sc, &sd}) {
                 wait(sx->st, forked);
@@ -966,7 +983,7 @@ struct Driver {
             // (replicated when partitioned: only the critical stream issues collectives)
             // R's rows right of the corner in one GEMM (full row tiles), then the block below the
             // corner (rows A+f..E, columns A..A+f)
-            static const bool split_hr = getenv("FFG_SPLIT_HR") && atoi(getenv("FFG_SPLIT_HR")) != 0;
+            static const bool split_hr = knob_on("FFG_SPLIT_HR");
             if (split_hr) {
                 if (pcols > A + f) gemm_sub(sc, at(A, c0, f, n1), at(r0, A + f, m1, pcols - (A + f)), at(A, A + f, f, pcols - (A + f)));
                 if (E > A + f) gemm_sub(sc, at(A + f, c0, E - (A + f), n1), at(r0, A, m1, pcols - A), at(A + f, A, E - (A + f), pcols - A));
@@ -1039,9 +1056,10 @@ struct Driver {
     static inline size_t g_log_ld = 1;
     bool try_node_spec(DView a, int depth, NodeRes& res) {
         const size_t m = a.rows;
-        static const bool nlog = getenv("FFG_NODE_LOG") != nullptr;
+        static const bool nlog = knob_set("FFG_NODE_LOG");
         const double t0 = nlog ? host_ms() : 0.0;
         uint32_t* bk = nullptr;
+        AsyncFreeGuard<uint32_t> bk_guard{bk, b.st};
         FFG_CUDA(cudaMallocAsync(&bk, m * m * 4, b.st));
         copy_block_dev(b, a, DView{bk, m, m, m});
         std::vector<uint32_t> qh(m);
@@ -1087,19 +1105,19 @@ struct Driver {
             px.root = a.d;
             px.ld = a.ld;
             res = recover(a, depth, fail_off, bk, m, px);
-            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            free_async(bk, b.st);
             return true;
         }
         if (!ok) {
             // the node's first block is deficient: every node on its left spine would fail there
             // too, so the exact recursion descends that spine without guessing (spec_dead)
             copy_block_dev(b, DView{bk, m, m, m}, a);
-            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            free_async(bk, b.st);
             ++node_spec_fails;
             spec_dead = a.d;
             return false;
         }
-        FFG_CUDA(cudaFreeAsync(bk, b.st));
+        free_async(bk, b.st);
         node_spec_fails = 0;
         size_t lo = m, hi = 0;
         for (size_t j = 0; j < m; ++j)
@@ -1252,6 +1270,7 @@ struct Driver {
         if (r2 > 0 && !I.empty()) ptrsm(b, 1, r2s, U2, I);      // :144
         if (r2 > 0 && !K.empty()) ptrsm(b, 1, r2s, U2, K);      // :145
         uint32_t* jbuf = nullptr;
+        AsyncFreeGuard<uint32_t> jbuf_guard{jbuf, b.st};
         DView J = I;
         if (r3 > 0 && !I.empty()) {                              // :146, J = L3^-1 I into a temporary
             FFG_CUDA(cudaMallocAsync(&jbuf, I.rows * I.cols * 4, b.st));
@@ -1265,7 +1284,7 @@ struct Driver {
             if (!K.empty() && !V2.empty()) pgemm_sub(b, K, V2, R);
             if (!N.empty()) pgemm_sub(b, M3, N, R);
         }
-        if (jbuf) FFG_CUDA(cudaFreeAsync(jbuf, b.st));
+        free_async(jbuf, b.st);
 
         bool early_here = false;
         EarlyTop::Reg reg_top, reg_left;
@@ -1484,7 +1503,7 @@ void base_dbg_dump();
 // Speculation is tried unless disabled (FFG_NO_SPEC), partitioned, profiled, or recently failed in
 // this context (then it rests for a few calls: rank-deficient workloads pay one failed try).
 static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
-    static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
+    static const bool off = knob_str("FFG_NO_SPEC") || knob_str("FFG_FACTOR_TRSM") || knob_str("FFG_LEVEL_TIMING");
     if (off || a.rows == 0 || a.cols == 0) return false;
     // A base block of i.i.d. residues is rank deficient with probability ~1/p (config 5's GF(251)
     // at n = 32768: ~2 such blocks per matrix).  A failed guess costs little on square input: the
@@ -1505,36 +1524,36 @@ static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
 // off the critical path, throughput beats the direct kernel's latency (n = 16384: 29.4 -> 29.0
 // ms); the exact recursion (configs 4 / 5) keeps the direct kernel.  FFG_PANEL_DIRECT=1 reverts.
 static bool panel_no_direct() {
-    static const bool keep = getenv("FFG_PANEL_DIRECT") && atoi(getenv("FFG_PANEL_DIRECT")) != 0;
+    static const bool keep = knob_on("FFG_PANEL_DIRECT");
     return !keep;
 }
 
 // panel-mode nodes up to this size update only R's first block on the critical stream and defer
 // their wide GEMMs (FFG_CORNER_MAX, read per call; 0 = off)
 static size_t panel_corner_max() {
-    const char* e = getenv("FFG_CORNER_MAX");
+    const char* e = knob_str("FFG_CORNER_MAX");
     return e ? (size_t)atoll(e) : 4096;  // 1024 / 2048 / 4096 / 8192: 29.1 / 28.7 / 28.7 / 28.7 ms
 }
 // partitioned runs split the generic nodes' GEMMs over the ranks and keep the corner nodes'
 // deferred GEMMs replicated: keep more nodes generic there
 static size_t panel_corner_max(const Blas& b) {
     const size_t c = panel_corner_max();
-    return (b.ws.dist.active() && !getenv("FFG_CORNER_MAX")) ? std::min<size_t>(c, 1024) : c;
+    return (b.ws.dist.active() && !knob_set("FFG_CORNER_MAX")) ? std::min<size_t>(c, 1024) : c;
 }
 
 // panel-mode nodes of at least this size apply their trailing update progressively in K-chunks
 // (FFG_PROG_MIN, read per call; 0 = off); FFG_PROG_CHUNKS chunks per node, FFG_PROG_SMS SM cap
 static size_t panel_prog_min() {
-    const char* e = getenv("FFG_PROG_MIN");
+    const char* e = knob_str("FFG_PROG_MIN");
     return e ? (size_t)atoll(e) : 0;
 }
 static size_t prog_chunks() {
-    const char* e = getenv("FFG_PROG_CHUNKS");
+    const char* e = knob_str("FFG_PROG_CHUNKS");
     return e ? std::max<size_t>(1, (size_t)atoll(e)) : 4;
 }
 
 static size_t panel_lookahead_min() {
-    const char* e = getenv("FFG_PANEL_LA");
+    const char* e = knob_str("FFG_PANEL_LA");
     return e ? (size_t)atoll(e) : 0;
 }
 
@@ -1542,13 +1561,13 @@ static size_t panel_lookahead_min() {
 // where the whole-matrix guess was skipped for a small field, nodes whose guess holds with
 // probability >= ~90% (blocks per node <= p / 10), single stream drivers excluded.
 static size_t node_spec_max(const Blas& b, const DView& a, size_t thr, const Driver& drv) {
-    static const bool off = getenv("FFG_NO_SPEC") || getenv("FFG_FACTOR_TRSM") || getenv("FFG_LEVEL_TIMING");
-    const char* e = getenv("FFG_NODE_SPEC");
+    static const bool off = knob_str("FFG_NO_SPEC") || knob_str("FFG_FACTOR_TRSM") || knob_str("FFG_LEVEL_TIMING");
+    const char* e = knob_str("FFG_NODE_SPEC");
     size_t s = e ? (size_t)atoll(e) : 1024;
     if (off || s == 0 || !drv.use_streams || thr > 64) return 0;
     const double blocks_all = (double)std::min(a.rows, a.cols) / (double)std::max<size_t>(thr, 1);
     if (blocks_all <= 0.25 * (double)b.F.p) return 0;  // the whole-matrix guess was tried instead
-    static const double risk = getenv("FFG_NODE_SPEC_RISK") ? atof(getenv("FFG_NODE_SPEC_RISK")) : 0.1;
+    static const double risk = knob_num("FFG_NODE_SPEC_RISK", 0.1);
     while (s > thr && (double)s / (double)thr > risk * (double)b.F.p) s /= 2;
     return s > 2 * thr ? s : 0;
 }
@@ -1571,7 +1590,7 @@ static void band_bounds(size_t o, size_t s, size_t thr, size_t T, size_t Tmin, s
 // matrix is deficient throughout -- or was not tried, on single-GPU runs (partitioned runs keep
 // the recursion, whose large operations split over the ranks).
 static int profile_first_mode() {
-    const char* e = getenv("FFG_PROFILE_FIRST");
+    const char* e = knob_str("FFG_PROFILE_FIRST");
     return e ? atoi(e) : 1;
 }
 static bool profile_first_ok(const Blas& b, size_t m, size_t n) {
@@ -1598,6 +1617,7 @@ static bool profile_first_after_failure(const Blas& b, size_t fail_off, size_t m
 static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t lda, size_t thr, uint32_t* d,
                                uint32_t* P, uint32_t* Q, size_t& rank) {
     uint32_t* bk = nullptr;
+    AsyncFreeGuard<uint32_t> bk_guard{bk, b.st};
     FFG_CUDA(cudaMallocAsync(&bk, n * n * 4, b.st));
     bool ok = false, resumable = false;
     size_t fail_off = 0;
@@ -1614,8 +1634,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             // the bands still crossing PCIe: R's first band starts as soon as it has arrived
             // (n = 16384: e2e 42.4 -> 39.6 ms with nodes >= n/4 ending in the first half; the root
             // included: 40.3 ms)
-            const char* e = getenv("FFG_HOST_LA");
-            const char* ee = getenv("FFG_HOST_LA_END");
+            const char* e = knob_str("FFG_HOST_LA");
+            const char* ee = knob_str("FFG_HOST_LA_END");
             const size_t hl = e ? (size_t)atoll(e) : (n / 4 >= 2048 ? n / 4 : 0);
             if (hl && !drv.la_min) {  // an explicit FFG_PANEL_LA wins
                 drv.la_min = hl;
@@ -1625,7 +1645,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         drv.corner_max = panel_corner_max(b);
         drv.prog_min = panel_prog_min();
         drv.prog_nchunks = prog_chunks();
-        drv.prog_sms = getenv("FFG_PROG_SMS") ? atoi(getenv("FFG_PROG_SMS")) : drv.lookahead_sms;
+        drv.prog_sms = (int)knob_int("FFG_PROG_SMS", drv.lookahead_sms);
         drv.proot = d;
         drv.pld = n;
         drv.prows = n;
@@ -1635,8 +1655,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
         cudaEvent_t start = drv.b.ws.event();  // d and bk are allocated on the caller's stream
         FFG_CUDA(cudaEventRecord(start, b.st));
         for (cudaStream_t st : {up, down, bks}) drv.wait(st, start);
-        const size_t T_env = getenv("FFG_BAND_MAX") ? (size_t)atoll(getenv("FFG_BAND_MAX")) : 0;
-        const size_t Tmin_env = getenv("FFG_BAND_MIN") ? (size_t)atoll(getenv("FFG_BAND_MIN")) : 256;
+        const size_t T_env = (size_t)knob_int("FFG_BAND_MAX", 0);
+        const size_t Tmin_env = (size_t)knob_int("FFG_BAND_MIN", 256);
         const size_t T = T_env ? T_env : std::max<size_t>(256, n / 16);
         // bands of 256 rows first (a narrower band's column strip is a 2-D copy of short rows,
         // which the copy engines move slowly: 128-row bands measured slower)
@@ -1696,7 +1716,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             b.ws.spec_failed();
         else
             b.ws.spec_fails = 0;
-        FFG_CUDA(cudaFreeAsync(bk, b.st));
+        free_async(bk, b.st);
         return true;
     }
     if (!ok) {
@@ -1705,7 +1725,7 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
     } else {
         b.ws.spec_fails = 0;
     }
-    FFG_CUDA(cudaFreeAsync(bk, b.st));
+    free_async(bk, b.st);
     return ok;
 }
 
@@ -1714,12 +1734,13 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
         return pluq_profile_first_dev(b, a, threshold, P, Q);
     if (threshold <= 64 && spec_allowed(b, a, threshold)) {
         const size_t m = a.rows, n = a.cols;
-        const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
+        const bool no_panel = knob_on("FFG_NO_PANEL");
         const bool panel = !no_panel && m == n;
         // backup of the input for a failed guess: the panel schedule backs each band up lazily
         // on a side stream right before its first use (bands, as the host entry); otherwise
         // one copy up front
         uint32_t* bk = nullptr;
+        AsyncFreeGuard<uint32_t> bk_guard{bk, b.st};
         const size_t ldb = panel ? a.ld : n;
         FFG_CUDA(cudaMallocAsync(&bk, m * ldb * 4, b.st));
         if (!panel) copy_block_dev(b, a, DView{bk, m, n, ldb});
@@ -1735,7 +1756,7 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             drv.corner_max = panel_corner_max(b);
             drv.prog_min = panel_prog_min();
             drv.prog_nchunks = prog_chunks();
-            drv.prog_sms = getenv("FFG_PROG_SMS") ? atoi(getenv("FFG_PROG_SMS")) : drv.lookahead_sms;
+            drv.prog_sms = (int)knob_int("FFG_PROG_SMS", drv.lookahead_sms);
             drv.proot = a.d;
             drv.pld = a.ld;
             drv.prows = m;
@@ -1771,17 +1792,17 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
                 resumable = true;
             }
         }
-        static const bool log = getenv("FFG_SPEC_LOG") != nullptr;
+        static const bool log = knob_set("FFG_SPEC_LOG");
         if (log) fprintf(stderr, "SPEC %s (panel %d, %zu base cases enqueued)\n", ok ? "ok" : "failed", (int)(m == n), (size_t)b.ws.base_seq.load());
         if (ok) {
             b.ws.spec_fails = 0;
-            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            free_async(bk, b.st);
             return rank;
         }
         if (resumable && profile_first_after_failure(b, fail_off, m, n, threshold)) {
             // deficient from the start: the profile-first path on the restored input
             copy_block_dev(b, DView{bk, m, n, ldb}, a);
-            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            free_async(bk, b.st);
             if (fail_off == 0) b.ws.spec_failed();
             return pluq_profile_first_dev(b, a, threshold, P, Q);
         }
@@ -1798,22 +1819,22 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
             NodeRes res = rdrv.recover(a, 0, fail_off, bk, ldb, rx);
             rdrv.finish();
             rdrv.download(res, m, n, P, Q);
-            FFG_CUDA(cudaFreeAsync(bk, b.st));
+            free_async(bk, b.st);
             if (fail_off == 0)
                 b.ws.spec_failed();  // the very first block: likely deficient everywhere, rest a few calls
             else
                 b.ws.spec_fails = 0;
-            static const bool log2 = getenv("FFG_SPEC_LOG") != nullptr;
+            static const bool log2 = knob_set("FFG_SPEC_LOG");
             if (log2) fprintf(stderr, "SPEC resumed at offset %zu of %zu\n", fail_off, m);
             return res.rank;
         }
         copy_block_dev(b, DView{bk, m, n, ldb}, a);  // a copy kernel: the DMA engines are far slower HBM to HBM
-        FFG_CUDA(cudaFreeAsync(bk, b.st));
+        free_async(bk, b.st);
         b.ws.spec_failed();
     }
     if (profile_first_ok(b, a.rows, a.cols)) return pluq_profile_first_dev(b, a, threshold, P, Q);
     Driver drv(b, threshold, a.rows, a.cols);
-    drv.level_timing = getenv("FFG_LEVEL_TIMING") != nullptr;
+    drv.level_timing = knob_set("FFG_LEVEL_TIMING");
     drv.node_spec_max = node_spec_max(b, a, threshold, drv);
     NodeRes res = drv.rec(a);
     drv.level_report();
@@ -1835,15 +1856,16 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     const size_t thr = std::max<size_t>(1, threshold);
     cudaStream_t cs = b.ws.stream(300, 0);  // copy stream
     uint32_t* d = nullptr;
+    AsyncFreeGuard<uint32_t> d_guard{d, b.st};
     FFG_CUDA(cudaMallocAsync(&d, m * n * 4, b.st));
-    static const bool no_stream_spec = getenv("FFG_NO_HOST_SPEC") != nullptr;
-    static const bool no_streams = getenv("FFG_NO_STREAMS") && atoi(getenv("FFG_NO_STREAMS")) != 0;
-    static const bool no_panel = getenv("FFG_NO_PANEL") && atoi(getenv("FFG_NO_PANEL")) != 0;
+    static const bool no_stream_spec = knob_set("FFG_NO_HOST_SPEC");
+    static const bool no_streams = knob_on("FFG_NO_STREAMS");
+    static const bool no_panel = knob_on("FFG_NO_PANEL");
     bool restored = false;  // d already holds the input (a failed speculative attempt restored it)
     if (m == n && thr <= 64 && !no_stream_spec && !no_streams && !no_panel && spec_allowed(b, DView{host, m, n, lda}, thr)) {
         size_t rank = 0;
         if (host_streamed_spec(b, host, n, lda, thr, d, P, Q, rank)) {
-            FFG_CUDA(cudaFreeAsync(d, b.st));
+            free_async(d, b.st);
             FFG_CUDA(cudaStreamSynchronize(b.st));
             return rank;
         }
@@ -1854,7 +1876,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
             FFG_CUDA(cudaMemcpy2DAsync(d, n * 4, host, lda * 4, n * 4, m, cudaMemcpyHostToDevice, b.st));
         const size_t rank = pluq_profile_first_dev(b, DView{d, m, n, n}, thr, P, Q);
         FFG_CUDA(cudaMemcpy2DAsync(host, lda * 4, d, n * 4, n * 4, m, cudaMemcpyDeviceToHost, b.st));
-        FFG_CUDA(cudaFreeAsync(d, b.st));
+        free_async(d, b.st);
         FFG_CUDA(cudaStreamSynchronize(b.st));
         return rank;
     }
@@ -1863,6 +1885,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     // (measured: e2e 75 ms with, 63 ms without).  The machinery below stays ready for it.
     const bool spec = false;
     uint32_t* bk = nullptr;
+    AsyncFreeGuard<uint32_t> bk_guard{bk, b.st};
     if (spec) FFG_CUDA(cudaMallocAsync(&bk, m * n * 4, b.st));
     b.ws.reset_events();
     auto record = [&](cudaStream_t st) {
@@ -1881,7 +1904,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
     };
     // spine blocks S_0 = whole matrix, S_{d+1} = top-left ceil-halves, down to ~16 MB or a leaf
     std::vector<std::pair<size_t, size_t>> sp{{m, n}};
-    static const bool no_spine = getenv("FFG_NO_SPINE") != nullptr;  // diagnostics: upload all first
+    static const bool no_spine = knob_set("FFG_NO_SPINE");  // diagnostics: upload all first
     while (!restored && !no_spine && std::min(sp.back().first, sp.back().second) > thr &&
            sp.back().first * sp.back().second > (size_t(1) << 22))
         sp.push_back({(sp.back().first + 1) / 2, (sp.back().second + 1) / 2});
@@ -1904,7 +1927,7 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
             drv.spine_root = d;
             drv.spine = spine;
         }
-        drv.early.armed = getenv("FFG_NO_EARLY") == nullptr;  // diagnostics: download all at the end
+        drv.early.armed = !knob_set("FFG_NO_EARLY");  // diagnostics: download all at the end
         drv.early.cs = cs;
         drv.early.host = host;
         drv.early.ldh = lda;
@@ -1939,8 +1962,8 @@ size_t pluq_tile_recursive_host(const Blas& b, uint32_t* host, size_t m, size_t 
         b.ws.spec_failed();
         run(false, false, rank);
     }
-    if (bk) FFG_CUDA(cudaFreeAsync(bk, b.st));
-    FFG_CUDA(cudaFreeAsync(d, b.st));
+    free_async(bk, b.st);
+    free_async(d, b.st);
     return rank;
 }
 
@@ -1951,6 +1974,8 @@ size_t pluq_tile_recursive_host_u8(const Blas& b, uint8_t* host, size_t m, size_
     cudaStream_t cs = b.ws.stream(300, 0);  // copy stream
     uint32_t* d = nullptr;
     uint8_t* s8 = nullptr;
+    AsyncFreeGuard<uint32_t> d_guard{d, b.st};
+    AsyncFreeGuard<uint8_t> s8_guard{s8, b.st};
     FFG_CUDA(cudaMallocAsync(&d, m * n * 4, b.st));
     FFG_CUDA(cudaMallocAsync(&s8, m * n, b.st));
     b.ws.reset_events();
@@ -1975,8 +2000,8 @@ size_t pluq_tile_recursive_host_u8(const Blas& b, uint8_t* host, size_t m, size_
         FFG_CUDA(cudaMemcpy2DAsync(host + r0 * lda, lda, s8 + r0 * n, n, n, rows, cudaMemcpyDeviceToHost, cs));
     }
     FFG_CUDA(cudaStreamWaitEvent(b.st, mark(cs), 0));
-    FFG_CUDA(cudaFreeAsync(s8, b.st));
-    FFG_CUDA(cudaFreeAsync(d, b.st));
+    free_async(s8, b.st);
+    free_async(d, b.st);
     FFG_CUDA(cudaStreamSynchronize(b.st));
     return rank;
 }

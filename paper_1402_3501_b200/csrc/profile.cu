@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(512) gather_pq_kernel(const uint32_t* __restri
 }
 
 int rp_cluster_ctas() {
-    static const int c = getenv("FFG_RP_CLUSTER") ? atoi(getenv("FFG_RP_CLUSTER")) : 16;
+    static const int c = (int)knob_int("FFG_RP_CLUSTER", 16);
     return std::max(1, std::min(16, c));
 }
 
@@ -685,7 +685,7 @@ size_t rank_profile_dev(const Blas& b, DView W, std::vector<uint32_t>& prow, std
     rp.w = w;
     rp.ncta = ncta;
     // FFG_RP_SMEM=1: the shared-memory slab kernel at every width (diagnostics, parity tests)
-    const bool smem_only = getenv("FFG_RP_SMEM") && atoi(getenv("FFG_RP_SMEM")) != 0;  // per call: tests
+    const bool smem_only = knob_on("FFG_RP_SMEM");  // per call: tests
     rp.reg_path = !smem_only && w <= 2 * RP_THREADS;
     const int slot = b.ws.acquire_slot();
     if (slot < 0) throw Error(FFG_ERR_INTERNAL, "rank profile: no free mailbox");
@@ -717,7 +717,7 @@ size_t rank_profile_dev(const Blas& b, DView W, std::vector<uint32_t>& prow, std
         FFG_CUDA(cudaMemcpyToSymbol(rp_clk, h, sizeof(h)));
     }
 #endif
-    static const bool log = getenv("FFG_PROFILE_LOG") != nullptr;
+    static const bool log = knob_set("FFG_PROFILE_LOG");
     if (log) fprintf(stderr, "RANK_PROFILE m=%zu n=%zu rank=%zu slabs=%zu kk=%u ctas=%u\n", m, n, r, rp.leaves, kk, ncta);
     return r;
 }
@@ -790,7 +790,7 @@ size_t pluq_profile_first_dev(const Blas& b, DView a, size_t threshold, uint32_t
     const DView W{Wb.d, m, n, n};
     copy_block_dev(b, a, W);
     std::vector<uint32_t> prow, pcol;
-    static const bool log = getenv("FFG_PROFILE_LOG") != nullptr;
+    static const bool log = knob_set("FFG_PROFILE_LOG");
     const auto t0 = std::chrono::steady_clock::now();
     const size_t r = rank_profile_dev(b, W, prow, pcol);  // phase 1 (reduces W)
     const auto t1 = std::chrono::steady_clock::now();

@@ -584,7 +584,7 @@ void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
         FFG_CUDA(cudaFuncSetAttribute(panel_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     b.ws.prof.begin(b.st);
-    static const bool one = getenv("FFG_INV_ONE_CTA") && atoi(getenv("FFG_INV_ONE_CTA")) != 0;
+    static const bool one = knob_on("FFG_INV_ONE_CTA");
     launch_k(panel_inv_kernel, dim3(one ? 1 : 2), dim3(512), smem, b.st, T.d, T.ld, t, inv, b.F.p, b.F.mu);
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_TRINV, 8.0 * t * t);
@@ -594,7 +594,7 @@ void panel_inverses_dev(const Blas& b, DView T, uint32_t* inv) {
 // CTAs of a panel apply: one per strip up to FFG_APPLY_CTAS (default: no cap); fewer CTAs loop
 // over strips and leave SMs to concurrent work
 static unsigned apply_grid(size_t nvec) {
-    const char* e = getenv("FFG_APPLY_CTAS");
+    const char* e = knob_str("FFG_APPLY_CTAS");
     const size_t cap = e ? (size_t)std::max(1, atoi(e)) : (size_t)1 << 30;
     return (unsigned)std::min(ceil_div(nvec, (size_t)LA), cap);
 }
@@ -861,7 +861,7 @@ void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv,
 
 // true when the fused kernel handled the solve
 bool trsm_fused(const Blas& b, int side, int upper, int unit, DView T, DView B) {
-    static const bool off = getenv("FFG_NO_FUSED_TRSM") && atoi(getenv("FFG_NO_FUSED_TRSM")) != 0;
+    static const bool off = knob_on("FFG_NO_FUSED_TRSM");
     if (off) return false;
     const bool pair = (side == 0 && !upper && unit) || (side == 1 && upper && !unit);
     if (!pair || T.rows > 128 || T.rows == 0) return false;
@@ -1032,7 +1032,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     }
     const int upper = uplo == 1, unit = diag == 0;
     if (trsm_fused(b, side, upper, unit, A, B)) return;
-    static const bool inverse_leaves = !(getenv("FFG_TRSM_DIRECT") && atoi(getenv("FFG_TRSM_DIRECT")) != 0);
+    static const bool inverse_leaves = !(knob_on("FFG_TRSM_DIRECT"));
     if (!inverse_leaves) {  // default: direct CUDA-core leaves, tensor-core Schur updates between them
         TrsmCtx c{b, side, upper, unit, A, nullptr};
         trsm_rec(c, 0, t, B);
@@ -1041,7 +1041,7 @@ void ftrsm_dev(const Blas& b, int side, int uplo, int diag, DView A, DView B, bo
     const size_t nblk = ceil_div(t, TB);
     uint32_t* Tinv = nullptr;
     FFG_CUDA(cudaMallocAsync(&Tinv, nblk * TB * TB * sizeof(uint32_t), b.st));
-    static const bool column_inverse = getenv("FFG_TRI_COLUMN") && atoi(getenv("FFG_TRI_COLUMN")) != 0;
+    static const bool column_inverse = knob_on("FFG_TRI_COLUMN");
     b.ws.prof.begin(b.st);
     if (column_inverse) {  // per-column substitution (kept for A/B comparison)
         const size_t smem = (TB * TSTR + 2 * TB) * sizeof(uint32_t);

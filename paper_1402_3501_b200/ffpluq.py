@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         L.ffg_last_error.restype = C.c_char_p
         L.ffg_last_error_index.restype = sz
         L.ffg_version.restype = C.c_char_p
+        L.ffg_knobs_reload.restype = None
         L.ffg_set_stream.argtypes = [vp, vp]
         L.ffg_get_stream.argtypes = [vp]
         L.ffg_get_stream.restype = vp
@@ -242,6 +243,11 @@ def tile_rec_perms(m: int, n: int, threshold: int, prow, pcol) -> tuple[np.ndarr
     _check(lib().ffg_tile_rec_perms(m, n, threshold, prow.size, prow.ctypes.data, pcol.ctypes.data,
                                     P.ctypes.data, Q.ctypes.data))
     return P[:m], Q[:n], int(prow.size)
+
+
+def reload_knobs() -> None:
+    """Re-snapshot the FFG_* environment switches (the library reads them once, at first use)."""
+    lib().ffg_knobs_reload()
 
 
 def _nccl_hint() -> None:

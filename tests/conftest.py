@@ -28,3 +28,27 @@ def gpu():
     ctx = G.Context(0)
     yield G, ctx
     ctx.close()
+
+
+# The library snapshots its FFG_* switches once (csrc/knobs.cuh); tests that flip one with
+# monkeypatch get a fresh snapshot after every change, including the teardown's restore.
+def _reload_knobs():
+    mod = sys.modules.get("paper_1402_3501_b200")
+    if mod is not None and getattr(mod.ffpluq, "_lib", None) is not None:
+        mod.reload_knobs()
+
+
+def _wrap(name):
+    orig = getattr(pytest.MonkeyPatch, name)
+
+    def wrapped(self, *args, **kwargs):
+        out = orig(self, *args, **kwargs)
+        if name == "undo" or (args and str(args[0]).startswith("FFG_")):
+            _reload_knobs()
+        return out
+
+    setattr(pytest.MonkeyPatch, name, wrapped)
+
+
+for _name in ("setenv", "delenv", "undo"):
+    _wrap(_name)
