@@ -661,223 +661,6 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 2) ptx::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-// --------------------------------------------------------------------------- fused pipelined kernel
-// The persistent TMA kernel above reads limb planes that split_kernel wrote to HBM first (a
-// separate launch and a write + read of L bytes per operand element).  This kernel cuts the limbs
-// itself: 7 converter warps read the u32 operand tiles straight from global memory (L2), split
-// them into the SW128 K-major limb planes of a pipeline stage and release the stage to the MMA
-// thread; 8 epilogue warps drain TMEM as in modgemm_kernel (7 converter warps + 1 MMA warp + 8).  One launch per GEMM (per kmax chunk),
-// no limb planes in HBM.  C must not alias A or B (other CTAs write C while this one reads).
-constexpr int FZ_CONV = 7;                  // converter warps 0..6
-constexpr int FZ_MMA = 7;                   // MMA issuer + TMEM allocation
-constexpr int FZ_EPI0 = 8;                  // epilogue warps 8..15 (TMEM lane quarter = warp % 4)
-constexpr int FZ_THREADS = 16 * 32;
-constexpr int FZ_CT = FZ_CONV * 32;         // converter threads
-
-struct FusedArgs {
-    const uint32_t* A;
-    uint64_t lda;
-    const uint32_t* B;
-    uint64_t ldb;
-    uint32_t K;
-    uint32_t a_vec;  // A rows 16-byte aligned (A and lda multiples of 4 words)
-};
-
-template <int L>
-__global__ void __launch_bounds__(FZ_THREADS, 1)
-    modgemm_fused_kernel(const FusedArgs fa, const EpiParams ep) {
-    using S = Smem<L>;
-    constexpr int NT = S::NT, STAGES = S::STAGES;
-    constexpr uint32_t TMEM_COLS = 512;
-    static_assert((2 * L - 1) * NT <= 512, "accumulator diagonals exceed TMEM");
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-    const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-
-    const uint32_t tiles = ep.m_tiles * ep.n_tiles;
-    auto tile_coords = [&](uint32_t pid, uint32_t& m_blk, uint32_t& n_blk) {
-        const uint32_t in_group = GROUP_M * ep.n_tiles;
-        const uint32_t first_m = (pid / in_group) * GROUP_M;
-        const uint32_t gsize = min((uint32_t)GROUP_M, ep.m_tiles - first_m);
-        m_blk = first_m + (pid % in_group) % gsize;
-        n_blk = (pid % in_group) / gsize;
-    };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(&full[s], FZ_CONV);  // one arrival per converter warp
-            ptx::mbar_init(&empty[s], 1);
-        }
-        ptx::mbar_init(tmem_full, 1);
-        ptx::mbar_init(tmem_empty, 8);
-        ptx::fence_mbar_init();
-    }
-    ptx::pdl_enter();
-    if (warp == FZ_MMA) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp < FZ_CONV) {
-        // ---------------- converters: u32 tiles -> limb planes of stage s
-        const uint32_t tid = threadIdx.x;
-        uint32_t it = 0;
-#pragma unroll 1
-        for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            uint32_t m_blk, n_blk;
-            tile_coords(tile, m_blk, n_blk);
-            const uint32_t a_rows = min((uint32_t)BM, ep.M - m_blk * BM);
-            const uint32_t b_cols = min((uint32_t)NT, ep.N - n_blk * NT);
-            const uint32_t* Arow0 = fa.A + (uint64_t)m_blk * BM * fa.lda;
-            const uint32_t* Bcol0 = fa.B + (uint64_t)n_blk * NT;
-#pragma unroll 1
-            for (uint32_t kb = 0; kb < ep.kblocks; ++kb, ++it) {
-                const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-                ptx::mbar_wait(&empty[s], ph ^ 1);
-                const uint32_t sa = ptx::smem_u32(smem + s * S::STAGE_BYTES), sb = sa + S::A_BYTES;
-                const uint32_t k0 = kb * BK;
-                // A: row r, k = k0 + 4 (i & 31) .. + 3 (one 16-byte load); B: a 4 (k) x 4 (n) block
-                // (four 16-byte loads, transposed in registers).  Rows >= M / columns >= N are left
-                // stale (their outputs are never written); k >= K is zero in A, which neutralises B.
-                // Up to FZ_B items in flight per thread: an L2 round trip per batch is the bound.
-                constexpr int FZ_B = 4;
-                const uint32_t a_items = a_rows * 32;
-                const uint32_t kq_n = fa.K > k0 ? min(32u, (fa.K - k0 + 3) / 4) : 0u;
-                const uint32_t nq = (b_cols + 3) / 4, b_items = nq * kq_n;
-                const bool b_vec = (reinterpret_cast<uintptr_t>(Bcol0) & 15) == 0 && (fa.ldb & 3) == 0 && (b_cols & 3) == 0;
-#pragma unroll 1
-                for (uint32_t base = tid; base < a_items + b_items; base += FZ_B * FZ_CT) {
-                    uint4 v[FZ_B][4];
-#pragma unroll
-                    for (int u = 0; u < FZ_B; ++u) {
-                        const uint32_t i = base + u * FZ_CT;
-                        v[u][0] = v[u][1] = v[u][2] = v[u][3] = make_uint4(0, 0, 0, 0);
-                        if (i < a_items) {
-                            const uint32_t r = i >> 5, k = k0 + (i & 31) * 4;
-                            const uint32_t* src = Arow0 + (uint64_t)r * fa.lda + k;
-                            if (fa.a_vec && k + 3 < fa.K) {
-                                v[u][0] = __ldg(reinterpret_cast<const uint4*>(src));
-                            } else {
-                                v[u][0].x = k < fa.K ? src[0] : 0u;
-                                v[u][0].y = k + 1 < fa.K ? src[1] : 0u;
-                                v[u][0].z = k + 2 < fa.K ? src[2] : 0u;
-                                v[u][0].w = k + 3 < fa.K ? src[3] : 0u;
-                            }
-                        } else if (i < a_items + b_items) {
-                            const uint32_t j = i - a_items, n4 = (j / kq_n) * 4, k = k0 + (j % kq_n) * 4;
-                            const uint32_t* src = Bcol0 + (uint64_t)k * fa.ldb + n4;
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                if (k + t >= fa.K) continue;
-                                const uint32_t* rw = src + (uint64_t)t * fa.ldb;
-                                if (b_vec) {
-                                    v[u][t] = __ldg(reinterpret_cast<const uint4*>(rw));
-                                } else {
-                                    v[u][t].x = n4 < b_cols ? rw[0] : 0u;
-                                    v[u][t].y = n4 + 1 < b_cols ? rw[1] : 0u;
-                                    v[u][t].z = n4 + 2 < b_cols ? rw[2] : 0u;
-                                    v[u][t].w = n4 + 3 < b_cols ? rw[3] : 0u;
-                                }
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < FZ_B; ++u) {
-                        const uint32_t i = base + u * FZ_CT;
-                        if (i < a_items) {
-                            const uint4 x = v[u][0];
-                            const uint32_t off = sa + sw128(i >> 5, i & 31);
-                            ptx::st_shared_u32(off, limb_bytes<0>(x.x, x.y, x.z, x.w));
-                            if (L > 1) ptx::st_shared_u32(off + BM * BK, limb_bytes<1>(x.x, x.y, x.z, x.w));
-                            if (L > 2) ptx::st_shared_u32(off + 2 * BM * BK, limb_bytes<2>(x.x, x.y, x.z, x.w));
-                            if (L > 3) ptx::st_shared_u32(off + 3 * BM * BK, limb_bytes<3>(x.x, x.y, x.z, x.w));
-                        } else if (i < a_items + b_items) {
-                            // lanes walk k within a 4-column group: the shared stores of a warp hit
-                            // one 128-byte row each, conflict-free under the swizzle
-                            const uint32_t j = i - a_items, n4 = (j / kq_n) * 4, kq = j % kq_n;
-                            const uint32_t c0[4] = {v[u][0].x, v[u][1].x, v[u][2].x, v[u][3].x};
-                            const uint32_t c1[4] = {v[u][0].y, v[u][1].y, v[u][2].y, v[u][3].y};
-                            const uint32_t c2[4] = {v[u][0].z, v[u][1].z, v[u][2].z, v[u][3].z};
-                            const uint32_t c3[4] = {v[u][0].w, v[u][1].w, v[u][2].w, v[u][3].w};
-                            const uint32_t* cc[4] = {c0, c1, c2, c3};
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                if (n4 + q >= b_cols) break;
-                                const uint32_t* c = cc[q];
-                                const uint32_t off = sb + sw128(n4 + q, kq);
-                                ptx::st_shared_u32(off, limb_bytes<0>(c[0], c[1], c[2], c[3]));
-                                if (L > 1) ptx::st_shared_u32(off + NT * BK, limb_bytes<1>(c[0], c[1], c[2], c[3]));
-                                if (L > 2) ptx::st_shared_u32(off + 2 * NT * BK, limb_bytes<2>(c[0], c[1], c[2], c[3]));
-                                if (L > 3) ptx::st_shared_u32(off + 3 * NT * BK, limb_bytes<3>(c[0], c[1], c[2], c[3]));
-                            }
-                        }
-                    }
-                }
-                ptx::fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full[s]);
-            }
-        }
-    } else if (warp == FZ_MMA) {
-        // ---------------- MMA issuer (single thread), the diagonal scheme of modgemm_kernel
-        if (lane == 0) {
-            constexpr uint32_t IDESC_FULL = ptx::idesc_u8(BM, L * NT);
-            constexpr uint32_t IDESC_HEAD = ptx::idesc_u8(BM, (L > 1 ? (L - 1) : 1) * NT);
-            constexpr uint32_t IDESC_TAIL = ptx::idesc_u8(BM, NT);
-            uint32_t it = 0, t = 0;
-            for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
-                ptx::mbar_wait(tmem_empty, (t & 1) ^ 1);
-                ptx::tc_fence_after();
-                for (uint32_t kb = 0; kb < ep.kblocks; ++kb, ++it) {
-                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-                    ptx::mbar_wait(&full[s], ph);
-                    ptx::tc_fence_after();
-                    const uint32_t a_base = ptx::smem_u32(smem + s * S::STAGE_BYTES);
-                    const uint32_t b_base = a_base + S::A_BYTES;
-#pragma unroll
-                    for (int kk = 0; kk < BK / 32; ++kk) {
-                        const uint64_t bdesc = ptx::desc_kmajor_sw128(b_base + kk * 32);
-#pragma unroll
-                        for (int i = 0; i < L; ++i) {
-                            const uint64_t adesc = ptx::desc_kmajor_sw128(a_base + i * BM * BK + kk * 32);
-                            if (kb != 0 || kk != 0) {
-                                ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_FULL, 1);
-                            } else if (i == 0) {
-                                ptx::mma_i8(tmem, adesc, bdesc, IDESC_FULL, 0);
-                            } else {
-                                ptx::mma_i8(tmem + i * NT, adesc, bdesc, IDESC_HEAD, 1);
-                                const uint64_t btail =
-                                    ptx::desc_kmajor_sw128(b_base + (L - 1) * NT * BK + kk * 32);
-                                ptx::mma_i8(tmem + (i + L - 1) * NT, adesc, btail, IDESC_TAIL, 0);
-                            }
-                        }
-                    }
-                    ptx::mma_commit(&empty[s]);
-                }
-                ptx::mma_commit(tmem_full);
-            }
-        }
-        __syncwarp();
-    } else {
-        // ---------------- epilogue warps 8..15
-        uint32_t t = 0;
-        for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
-            uint32_t m_blk, n_blk;
-            tile_coords(tile, m_blk, n_blk);
-            epilogue_tile<L>(ep, [&] { return tmem; }, tmem_full, m_blk, n_blk, warp - (FZ_EPI0 - 4), lane, [] {},
-                             t & 1, tmem_empty);
-        }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == FZ_MMA) ptx::tmem_dealloc<TMEM_COLS>(tmem);
-}
-
 // --------------------------------------------------------------------------- limb split (one launch)
 // Blocks [0, a_blocks): A (M x K view) -> planes[l][Mp][Kp] (K-major, no transpose), one
 //   thread = 4 consecutive k of one row, 1024 (row, k-quad) items per block.
@@ -1119,37 +902,6 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
     FFG_CUDA(cudaGetLastError());
 }
 
-template <int L>
-void launch_fused(const Field& F, uint32_t alpha, uint32_t beta, DView A, DView B, DView C, size_t K,
-                  cudaStream_t st, int sm_cap) {
-    using S = Smem<L>;
-    static PerDeviceOnce once;
-    once([] {
-        FFG_CUDA(cudaFuncSetAttribute(modgemm_fused_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL));
-    });
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        FFG_CUDA(cudaGetDevice(&dev));
-        FFG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    EpiParams ep = make_ep(F, alpha, beta, C);
-    ep.kblocks = (uint32_t)ceil_div(K, (size_t)BK);
-    ep.m_tiles = (uint32_t)ceil_div(C.rows, BM);
-    ep.n_tiles = (uint32_t)ceil_div(C.cols, S::NT);
-    FusedArgs fa;
-    fa.A = A.d;
-    fa.lda = A.ld;
-    fa.B = B.d;
-    fa.ldb = B.ld;
-    fa.K = (uint32_t)K;
-    fa.a_vec = ((reinterpret_cast<uintptr_t>(A.d) & 15) == 0 && (A.ld & 3) == 0) ? 1u : 0u;
-    const uint32_t tiles = ep.m_tiles * ep.n_tiles;
-    const uint32_t cap = sm_cap > 0 ? (uint32_t)sm_cap : (uint32_t)sms;
-    launch_k(modgemm_fused_kernel<L>, dim3(std::min(tiles, cap)), dim3(FZ_THREADS), S::TOTAL, st, fa, ep);
-    FFG_CUDA(cudaGetLastError());
-}
-
 bool direct_fits(int L, int KB) {
     switch (L * 4 + KB) {
         case 1 * 4 + 1: return DirectSmem<1, 1>::FITS;
@@ -1313,27 +1065,6 @@ void fgemm_dev(const Field& F, uint32_t alpha, DView A, DView B, uint32_t beta, 
         }
         ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * K, 2.0 * (double)M * N * K);
         if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
-        return;
-    }
-    // operands converted inside the GEMM (no limb planes in HBM; C must not alias an operand).
-    // Opt-in (FFG_FUSED=1): the converter warps are bound by their global-load latency -- 4096^3
-    // measured 2.37 ms against 0.52 ms for split + TMA kernel
-    static const bool fused = knob_on("FFG_FUSED");
-    if (fused && !overlap(C, A) && !overlap(C, B)) {
-        for (size_t k0 = 0; k0 < K; k0 += F.kmax) {  // delayed reduction: one fold per kmax chunk
-            const size_t kc = std::min<size_t>(K - k0, F.kmax);
-            const uint32_t b = (k0 == 0) ? beta : 1u;
-            const DView Ak{A.d + k0, A.rows, kc, A.ld}, Bk{B.d + k0 * B.ld, kc, B.cols, B.ld};
-            ws.prof.begin(st);
-            switch (L) {
-                case 1: launch_fused<1>(F, alpha, b, Ak, Bk, C, kc, st, sm_cap); break;
-                case 2: launch_fused<2>(F, alpha, b, Ak, Bk, C, kc, st, sm_cap); break;
-                case 3: launch_fused<3>(F, alpha, b, Ak, Bk, C, kc, st, sm_cap); break;
-                default: launch_fused<4>(F, alpha, b, Ak, Bk, C, kc, st, sm_cap); break;
-            }
-            ws.prof.end(st, PROF_GEMM, 2.0 * L * L * (double)M * N * kc, 2.0 * (double)M * N * kc);
-            if (launches) __atomic_add_fetch(launches, 1, __ATOMIC_RELAXED);
-        }
         return;
     }
     const size_t Mp = round_up(M, BM), Np = round_up(N, NT);

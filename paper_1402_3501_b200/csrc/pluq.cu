@@ -76,7 +76,6 @@ struct NodeRes {
     uint32_t* P = nullptr;  // device index arrays (valid inside pr / qr)
     uint32_t* Q = nullptr;
     Range pr, qr;
-    Factor* fac = nullptr;  // structure of the leading r x r factor (for TRSMs that use it)
 };
 
 // device LIFO arena for permutation index arrays
@@ -113,12 +112,6 @@ struct Driver {
     BaseInfo* info_host = nullptr;
     cudaEvent_t ev = nullptr;
     uint64_t base_cases = 0;
-    // factor tree + the base cases' cached factor inverses (live for the whole call)
-    std::deque<Factor> factors;
-    uint32_t* inv_arena = nullptr;
-    size_t inv_cap = 0, inv_top = 0;
-    bool use_factors = true;
-
     bool use_streams = true;     // exact recursion: side streams (off when partitioned)
     bool panel_streams = true;   // panel schedule: side streams (collectives stay on the critical one)
     int lookahead_sms = 0;  // SM cap of the look-ahead GEMMs (FFG_LOOKAHEAD_SMS, default SMs - 32)
@@ -197,14 +190,6 @@ struct Driver {
         info_host = reinterpret_cast<BaseInfo*>(b.ws.mailbox(slot, &dev));
         info_dev = reinterpret_cast<BaseInfo*>(dev);
         ev = b.ws.event();
-        // factor-tree TRSM (cached base-case inverses): opt-in, slower than blocked inverses today
-        static const bool on = knob_on("FFG_FACTOR_TRSM");
-        use_factors = on;
-        if (use_factors) {
-            // sum of r^2 over base cases <= min(m, n) * 64; two triangles each, plus one slot of slack
-            inv_cap = 2 * (std::min(m, n) * 64 + 64 * 64) + 64;
-            FFG_CUDA(cudaMallocAsync(&inv_arena, inv_cap * 4, b.st));
-        }
     }
     void alloc_panel_inv() {
         static const bool off = knob_on("FFG_PANEL_FUSED_TRSM");
@@ -248,7 +233,6 @@ struct Driver {
     ~Driver() {
         if (gq) cudaFreeAsync(gq, b.st);
         if (panel_inv) cudaFreeAsync(panel_inv, b.st);
-        if (inv_arena) cudaFreeAsync(inv_arena, b.st);
         if (owns_slot) b.ws.release_slot(slot);
     }
     // join the critical stream back into the caller's stream
@@ -284,7 +268,7 @@ struct Driver {
             (int)knob_int("FFG_SUBTREE_THREADS", std::max(0, std::min(15, (int)std::thread::hardware_concurrency() - 2)));
         static const size_t gmin = (size_t)knob_int("FFG_FORK_MIN", 0);
         const size_t gm = gmin ? gmin : 2 * thr;  // smallest G worth a host thread
-        return max_threads > 0 && !spec && use_streams && !b.ws.dist.active() && b.ws.prof.mode != 1 && !use_factors &&
+        return max_threads > 0 && !spec && use_streams && !b.ws.dist.active() && b.ws.prof.mode != 1 &&
                !E.empty() && !G.empty() &&
                std::min(G.rows, G.cols) > gm && std::min(E.rows, E.cols) > thr &&
                active_children().load() < max_threads;
@@ -296,12 +280,6 @@ struct Driver {
     }
     void wait(cudaStream_t st, cudaEvent_t e) {
         if (e) FFG_CUDA(cudaStreamWaitEvent(st, e, 0));
-    }
-
-    Factor* new_factor(size_t rank) {
-        factors.emplace_back();
-        factors.back().rank = rank;
-        return &factors.back();
     }
 
     // The base kernel writes its result into host-mapped memory and then the launch's sequence
@@ -431,42 +409,21 @@ struct Driver {
             res.rank = std::min(a.rows, a.cols);
             res.pr = Range{};
             res.qr = Range{};
-            res.fac = nullptr;
             return res;
         }
-        const size_t rmax = std::min(a.rows, a.cols);
-        uint32_t* slot = nullptr;
-        if (use_factors && rmax <= 64 && inv_top + 2 * rmax * rmax <= inv_cap) slot = inv_arena + inv_top;
         const uint32_t seq = (b.ws.base_seq.fetch_add(1) + 1) & ~SPEC_BIT;
-        const bool asked = rr_base_launch(b, a, res.P, res.Q, info_dev, slot, seq);
+        rr_base_launch(b, a, res.P, res.Q, info_dev, nullptr, seq);
         wait_mailbox(seq);  // the rank decides every later shape
         ++base_cases;
         res.rank = info_host->rank;
         res.pr = Range{info_host->plo, info_host->phi};
         res.qr = Range{info_host->qlo, info_host->qhi};
-        res.fac = use_factors ? new_factor(res.rank) : nullptr;  // factor trees: opt-in TRSM path only
-        if (res.fac && asked && info_host->cached && res.rank > 0) {
-            res.fac->invL = slot;
-            res.fac->invU = slot + res.rank * res.rank;
-            inv_top += 2 * res.rank * res.rank;
-        }
         return res;
     }
 
-    // TRSMs of tile_rec always use a child's leading factor: walk its factor tree when every
-    // leaf has cached inverses, else the generic blocked-inverse TRSM
-    void trsm_lower_unit(const Blas& bb, const NodeRes& c, DView L, DView B) {
-        if (c.fac && c.fac->complete())
-            trsm_factor(bb, 0, *c.fac, L, B);
-        else
-            ftrsm_dev(bb, 0, 0, 0, L, B, false);
-    }
-    void trsm_upper_nonunit(const Blas& bb, const NodeRes& c, DView U, DView B) {
-        if (c.fac && c.fac->complete())
-            trsm_factor(bb, 1, *c.fac, U, B);
-        else
-            ftrsm_dev(bb, 1, 1, 1, U, B, false);
-    }
+    // TRSMs of tile_rec against a child's leading factor: the blocked-inverse TRSM
+    void trsm_lower_unit(const Blas& bb, const NodeRes&, DView L, DView B) { ftrsm_dev(bb, 0, 0, 0, L, B, false); }
+    void trsm_upper_nonunit(const Blas& bb, const NodeRes&, DView U, DView B) { ftrsm_dev(bb, 1, 1, 1, U, B, false); }
 
     void apply(const NodeRes& c, int axis, DView v) {
         const Range& r = axis == 0 ? c.pr : c.qr;
@@ -796,17 +753,7 @@ struct Driver {
         DView rmini = at(r0, beyond_c, t, mr), bmini = at(beyond_r, c0, mb, t);
         DView rrest = at(r0, beyond_c + mr, t, wr - mr), brest = at(beyond_r + mb, c0, hb - mb, t);
         const cudaEvent_t f = mark_event(b.st);
-        static const bool two = knob_on("FFG_MINI_TWO");
-        if (two) {  // diagnostics: the two strip applies on two streams
-            const bool both = !rmini.empty() && !bmini.empty();
-            const Blas side = both ? on(twin(depth)) : b;
-            if (both) wait(side.st, f);
-            panel_apply_dev(b, 0, inv, t, rmini);
-            panel_apply_dev(side, 1, inv, t, bmini, q);
-            if (both) wait(b.st, mark_event(side.st));
-        } else {
-            panel_mini_dev(b, inv, t, rmini, bmini, q);  // one launch of small CTAs
-        }
+        panel_mini_dev(b, inv, t, rmini, bmini, q);  // one launch of small CTAs
         if (!rrest.empty()) {
             wait(sa.st, f);
             panel_apply_dev(sa, 0, inv, t, rrest);
@@ -842,13 +789,9 @@ struct Driver {
         leaves.push_back({c0, t1});
         if (!base_wrote_inv) panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
         flush_deferred();  // the node's rows / columns carry every earlier update
-        static const bool one_cta = knob_on("FFG_CORNER_ONE");
-        if (one_cta) {  // diagnostics: the one-CTA corner kernel
-            panel_corner_dev(b, a, t1, inv1, q1);
-        } else {  // A1's panel blocks inside the node, then R's update, each in small CTAs
-            panel_mini_dev(b, inv1, t1, a.sub(0, t1, t1, t2), a.sub(t1, 0, t2, t1), q1);
-            panel_update_dev(b, a.sub(t1, 0, t2, t1), a.sub(0, t1, t1, t2), a.sub(t1, t1, t2, t2));
-        }
+        // A1's panel blocks inside the node, then R's update, each in small CTAs
+        panel_mini_dev(b, inv1, t1, a.sub(0, t1, t1, t2), a.sub(t1, 0, t2, t1), q1);
+        panel_update_dev(b, a.sub(t1, 0, t2, t1), a.sub(0, t1, t1, t2), a.sub(t1, t1, t2, t2));
         const cudaEvent_t f = mark_event(b.st);
         Blas sa = on(side_stream(0)), sb = on(side_stream(1));
         sa.sm_cap = sb.sm_cap = side_sms;
@@ -1338,11 +1281,6 @@ struct Driver {
         rotate_block_dev(b, a, 1, r1 + r2 + r3, n1 + r2, r4);
 
         res.rank = r1 + r2 + r3 + r4;
-        if (use_factors) {  // leading factor = children's factors in gather order
-            res.fac = new_factor(res.rank);
-            for (const NodeRes* c : std::initializer_list<const NodeRes*>{&r1s, &r2s, &r3s, &r4s})
-                if (c->rank > 0) res.fac->kids.push_back(c->fac);
-        }
         arena.reset(mark);  // children consumed (stream order protects the pending kernels)
         if (level_timing) {
             LR.e[3] = tev();
@@ -1503,7 +1441,7 @@ void base_dbg_dump();
 // Speculation is tried unless disabled (FFG_NO_SPEC), partitioned, profiled, or recently failed in
 // this context (then it rests for a few calls: rank-deficient workloads pay one failed try).
 static bool spec_allowed(const Blas& b, const DView& a, size_t thr) {
-    static const bool off = knob_str("FFG_NO_SPEC") || knob_str("FFG_FACTOR_TRSM") || knob_str("FFG_LEVEL_TIMING");
+    static const bool off = knob_set("FFG_NO_SPEC") || knob_set("FFG_LEVEL_TIMING");
     if (off || a.rows == 0 || a.cols == 0) return false;
     // A base block of i.i.d. residues is rank deficient with probability ~1/p (config 5's GF(251)
     // at n = 32768: ~2 such blocks per matrix).  A failed guess costs little on square input: the
@@ -1561,7 +1499,7 @@ static size_t panel_lookahead_min() {
 // where the whole-matrix guess was skipped for a small field, nodes whose guess holds with
 // probability >= ~90% (blocks per node <= p / 10), single stream drivers excluded.
 static size_t node_spec_max(const Blas& b, const DView& a, size_t thr, const Driver& drv) {
-    static const bool off = knob_str("FFG_NO_SPEC") || knob_str("FFG_FACTOR_TRSM") || knob_str("FFG_LEVEL_TIMING");
+    static const bool off = knob_set("FFG_NO_SPEC") || knob_set("FFG_LEVEL_TIMING");
     const char* e = knob_str("FFG_NODE_SPEC");
     size_t s = e ? (size_t)atoll(e) : 1024;
     if (off || s == 0 || !drv.use_streams || thr > 64) return 0;

@@ -43,8 +43,6 @@ void panel_mini_dev(const Blas& b, const uint32_t* inv, size_t t, DView X, DView
 // C -= Y X for blocks <= 64 (small CTAs, 16 columns each)
 void panel_update_dev(const Blas& b, DView Y, DView X, DView C);
 
-// two-leaf node of the panel schedule: A1's panel blocks inside the node and R's update (see trsm.cu)
-void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv, const uint32_t* q);
 
 // pluq_tile_recursive on a HOST matrix (ld lda), pipelined: the recursion's top-left spine
 // starts while the rest uploads, the root's finished top rows download while its trailing
@@ -87,20 +85,6 @@ bool rr_base_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* in
 void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void* info_dev, uint32_t* inv,
                         uint32_t seq, bool allow_q);
 
-// Structure of a node's leading r x r factor (tile_rec pivot gather order A1, E, G, R):
-// block triangular with the children's leading factors on the diagonal.  Leaves are base
-// cases whose inverses were cached by the base kernel.
-struct Factor {
-    size_t rank = 0;
-    const uint32_t* invL = nullptr;  // base case: inv(L) (unit lower), r x r, ld r
-    const uint32_t* invU = nullptr;  // base case: inv(U) (upper), r x r, ld r
-    std::vector<const Factor*> kids;  // internal node: children with rank > 0, in gather order
-    bool complete() const;           // every leaf carries cached inverses
-};
-
-// TRSM against a node's factor (T = its r x r leading packed block):
-// side 0: B <- L^-1 B (unit lower);  side 1: B <- B U^-1 (upper, non-unit)
-void trsm_factor(const Blas& b, int side, const Factor& f, DView T, DView B);
 
 // permutation kernels (perm.cu)
 void perm_apply_range(const Blas& b, DView a, int axis, const uint32_t* perm, size_t lo, size_t hi);

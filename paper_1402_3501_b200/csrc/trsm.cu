@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256) trsm_small_kernel(const uint32_t* __restr
     }
 }
 
-// Leaf of a factor-tree TRSM: X = inv(L) B (left) or X = B inv(U) (right), in place, with the
+// Leaf of a panel solve: X = inv(L) B (left) or X = B inv(U) (right), in place, with the
 // inverse cached by the base case (d <= 64).  A CTA owns 64 vectors (columns of B for left,
 // rows for right) and stages them in shared memory before writing, so in place is safe.
 // 256 threads x (4 x 4) register tiles fed by two 16-byte shared loads per k (coefficients
@@ -766,99 +766,6 @@ void panel_update_dev(const Blas& b, DView Y, DView X, DView C) {
     b.count();
 }
 
-// Corner of a two-leaf node of the panel schedule (A1 = rows/cols [0, t1), R = [t1, t1 + t2),
-// t1, t2 <= 64, A1 factored, its inverses in inv): X = inv(L1) A(A1, R) and Y = A(R, A1) inv(U1)
-// (A(R, A1) read through A1's column pivots q, may be null) are written back, and A(R, R) -= Y X,
-// so R's base case can start before the wide panels of A1 and their updates are done.
-// One CTA, 512 threads, each owning a 2 x 4 tile of every 64 x 64 product (exact u64 sums).
-constexpr int CS = 68;
-__device__ __forceinline__ void mm64_tile(const uint32_t* Am, const uint32_t* Bm, uint32_t k0, uint32_t kn,
-                                          uint32_t i0, uint32_t v0, uint64_t acc[2][4]) {
-    // acc[a][q] += sum_{k0 <= k < kn} Am[(i0+a)][k] * Bm[k][v0+q]   (row-major, stride CS)
-#pragma unroll 4
-    for (uint32_t k = k0; k < kn; ++k) {
-        const uint4 x = *reinterpret_cast<const uint4*>(&Bm[k * CS + v0]);
-        const uint32_t a0 = Am[i0 * CS + k], a1 = Am[(i0 + 1) * CS + k];
-        const uint32_t xx[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            acc[0][q] += (uint64_t)a0 * xx[q];
-            acc[1][q] += (uint64_t)a1 * xx[q];
-        }
-    }
-}
-
-__global__ void __launch_bounds__(512) panel_corner_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t t1,
-                                                           uint32_t t2, const uint32_t* __restrict__ inv,
-                                                           const uint32_t* __restrict__ q, uint32_t p, uint64_t mu) {
-    extern __shared__ __align__(16) uint32_t sm[];
-    uint32_t* Li = sm;            // inv(L1)      t1 x t1
-    uint32_t* Ui = Li + 64 * CS;  // inv(U1)      t1 x t1
-    uint32_t* B1 = Ui + 64 * CS;  // A(A1, R)     t1 x t2  -> X
-    uint32_t* B2 = B1 + 64 * CS;  // A(R, A1)     t2 x t1  -> Y
-    uint32_t* Cc = B2 + 64 * CS;  // A(R, R)      t2 x t2
-    const uint32_t tid = threadIdx.x;
-    ptx::pdl_enter();
-#pragma unroll
-    for (int rr = 0; rr < 8; ++rr) {
-        const uint32_t idx = tid + 512 * rr, i = idx / 64, j = idx % 64;
-        Li[i * CS + j] = (i < t1 && j < t1) ? inv[i * t1 + j] : 0u;
-        Ui[i * CS + j] = (i < t1 && j < t1) ? inv[t1 * t1 + i * t1 + j] : 0u;
-        B1[i * CS + j] = (i < t1 && j < t2) ? A[(uint64_t)i * lda + t1 + j] : 0u;
-        B2[i * CS + j] = (i < t2 && j < t1) ? A[(uint64_t)(t1 + i) * lda + (q ? q[j] : j)] : 0u;
-        Cc[i * CS + j] = (i < t2 && j < t2) ? A[(uint64_t)(t1 + i) * lda + t1 + j] : 0u;
-    }
-    __syncthreads();
-    const uint32_t i0 = (tid / 16) * 2, v0 = (tid % 16) * 4;
-    uint64_t ax[2][4] = {}, ay[2][4] = {};
-    mm64_tile(Li, B1, 0, min(t1, i0 + 2), i0, v0, ax);  // X = inv(L1) B1 (inv(L1) lower: k <= i)
-    mm64_tile(B2, Ui, 0, min(t1, v0 + 4), i0, v0, ay);  // Y = B2 inv(U1) (inv(U1) upper: k <= v)
-    __syncthreads();  // B1 / B2 fully read
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            B1[(i0 + a) * CS + v0 + c] = mod_u64(ax[a][c], p, mu);
-            B2[(i0 + a) * CS + v0 + c] = mod_u64(ay[a][c], p, mu);
-        }
-    __syncthreads();
-    uint64_t ac[2][4] = {};
-    mm64_tile(B2, B1, 0, t1, i0, v0, ac);  // Y X
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const uint32_t yx = mod_u64(ac[a][c], p, mu), cv = Cc[(i0 + a) * CS + v0 + c];
-            Cc[(i0 + a) * CS + v0 + c] = cv >= yx ? cv - yx : cv + p - yx;
-        }
-    __syncthreads();
-#pragma unroll
-    for (int rr = 0; rr < 8; ++rr) {
-        const uint32_t idx = tid + 512 * rr, i = idx / 64, j = idx % 64;
-        if (i < t1 && j < t2) A[(uint64_t)i * lda + t1 + j] = B1[i * CS + j];
-        if (i < t2 && j < t1) A[(uint64_t)(t1 + i) * lda + j] = B2[i * CS + j];
-        if (i < t2 && j < t2) A[(uint64_t)(t1 + i) * lda + t1 + j] = Cc[i * CS + j];
-    }
-}
-
-void panel_corner_dev(const Blas& b, DView node, size_t t1, const uint32_t* inv, const uint32_t* q) {
-    const size_t t2 = node.rows - t1;
-    if (t1 == 0 || t1 > 64 || t2 > 64 || node.rows != node.cols)
-        throw Error(FFG_ERR_INTERNAL, "panel_corner: node must be square with two leaves <= 64");
-    if (t2 == 0) return;
-    const size_t smem = 5 * 64 * CS * 4;
-    static PerDeviceOnce once;
-    once([smem] {
-        FFG_CUDA(cudaFuncSetAttribute(panel_corner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    });
-    b.ws.prof.begin(b.st);
-    launch_k(panel_corner_kernel, dim3(1), dim3(512), smem, b.st, node.d, node.ld, (uint32_t)t1, (uint32_t)t2, inv, q,
-             b.F.p, b.F.mu);
-    FFG_CUDA(cudaGetLastError());
-    b.ws.prof.end(b.st, PROF_TRINV, 8.0 * 64 * 64 * 5);
-    b.count();
-}
-
 // true when the fused kernel handled the solve
 bool trsm_fused(const Blas& b, int side, int upper, int unit, DView T, DView B) {
     static const bool off = knob_on("FFG_NO_FUSED_TRSM");
@@ -870,49 +777,6 @@ bool trsm_fused(const Blas& b, int side, int upper, int unit, DView T, DView B) 
     else
         trsm_fused_launch<128>(b, side, upper, unit, T, B);
     return true;
-}
-
-bool Factor::complete() const {
-    if (invL) return true;
-    if (kids.empty()) return rank == 0;
-    for (const Factor* k : kids)
-        if (!k->complete()) return false;
-    return true;
-}
-
-void trsm_factor(const Blas& b, int side, const Factor& f, DView T, DView B) {
-    const size_t r = f.rank;
-    if (r == 0 || B.empty()) return;
-    if (f.invL) {
-        const size_t nvec = side == 0 ? B.cols : B.rows;
-        b.ws.prof.begin(b.st);
-        if (side == 0)
-            leaf_apply_kernel<0><<<(unsigned)ceil_div(nvec, LA), 256, 0, b.st>>>(f.invL, (uint32_t)r, B.d, B.ld,
-                                                                               (uint32_t)nvec, b.F.p, b.F.mu, nullptr);
-        else
-            leaf_apply_kernel<1><<<(unsigned)ceil_div(nvec, LA), 256, 0, b.st>>>(f.invU, (uint32_t)r, B.d, B.ld,
-                                                                               (uint32_t)nvec, b.F.p, b.F.mu, nullptr);
-        FFG_CUDA(cudaGetLastError());
-        b.ws.prof.end(b.st, PROF_TRINV, 8.0 * (double)r * nvec);
-        b.count();
-        return;
-    }
-    // block substitution over the children's factors (block triangular, gather order)
-    const uint32_t pm1 = b.F.p - 1;
-    size_t o = 0;
-    for (const Factor* k : f.kids) {
-        const size_t d = k->rank;
-        if (side == 0) {  // L X = B, row blocks
-            DView Bi = B.sub(o, 0, d, B.cols);
-            if (o > 0) b.gemm(pm1, T.sub(o, 0, d, o), B.sub(0, 0, o, B.cols), 1, Bi);
-            trsm_factor(b, 0, *k, T.sub(o, o, d, d), Bi);
-        } else {  // X U = B, column blocks
-            DView Bi = B.sub(0, o, B.rows, d);
-            if (o > 0) b.gemm(pm1, B.sub(0, 0, B.rows, o), T.sub(0, o, o, d), 1, Bi);
-            trsm_factor(b, 1, *k, T.sub(o, o, d, d), Bi);
-        }
-        o += d;
-    }
 }
 
 // smallest i with T[i][i] == 0 (blas.hpp:291-297 / 347-353)
