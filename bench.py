@@ -379,6 +379,7 @@ def our_arm(a, rank, world, local_rank):
 
     # ---- timed region: exactly K steps
     launches0 = ctx.launches
+    spec0 = ctx.spec_stats()
     with ClockSampler(local_rank) as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -389,6 +390,8 @@ def our_arm(a, rank, world, local_rank):
         e1.record(stream)
         barrier()
     launches = ctx.launches - launches0
+    spec1 = ctx.spec_stats()
+    speculation = {k: spec1[k] - spec0[k] for k in spec1}  # full-rank guesses inside the timed region
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -439,6 +442,8 @@ def our_arm(a, rank, world, local_rank):
             "data": "synthetic (seeded SplitMix64 random_mat / L*R*U, generated in HBM)",
             "config": workload_config(a, world), "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
             "roofline": roof, "cpu_baseline": cpu}
+    if not is_fgemm:
+        line["speculation"] = speculation
     if fg:
         line["fgemm"] = fg
     print(json.dumps(line), flush=True)

@@ -160,6 +160,12 @@ int ffg_lru_matrix_dev(ffg_ctx *ctx, uint64_t p, uint64_t seed, uint32_t *M, siz
  * Kernel launches issued by this context since creation (all kernels of this
  * library; used for the bench's gpu_launches claim). */
 uint64_t ffg_launch_count(ffg_ctx *ctx);
+/* Outcomes of the speculative full-rank guesses since the context was created
+ * (the GPU schedule's own bookkeeping, no reference counterpart): out[0..4] =
+ * whole-matrix guesses tried, of those failed (resumed at the failed block or
+ * rerun profile-first), node-level guesses tried, of those failed, profile-first
+ * factorisations run. */
+int ffg_spec_stats(ffg_ctx *ctx, uint64_t *out);
 /* Per-kernel-class timing with CUDA events on the launching stream (off by
  * default).  Classes: 0 tensor-core GEMM, 1 limb split, 2 base case,
  * 3 triangle inverse, 4 permutation gathers, 5 CUDA-core small GEMM.  ffg_profile_read fills

@@ -137,6 +137,17 @@ void* ffg_get_stream(ffg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 int ffg_synchronize(ffg_ctx* ctx) { return guarded(ctx, [&] { FFG_CUDA(cudaStreamSynchronize(ctx->stream)); }); }
 uint64_t ffg_launch_count(ffg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int ffg_spec_stats(ffg_ctx* ctx, uint64_t* out) {
+    return guarded(ctx, [&] {
+        if (!out) throw ffg::Error(FFG_ERR_INVALID_DIM, "spec_stats: null output");
+        out[0] = ctx->ws.st_guess;
+        out[1] = ctx->ws.st_guess_failed;
+        out[2] = ctx->ws.st_node;
+        out[3] = ctx->ws.st_node_failed;
+        out[4] = ctx->ws.st_profile_first;
+    });
+}
+
 int ffg_profile_enable(ffg_ctx* ctx, int on) {
     return guarded(ctx, [&] { ctx->ws.prof.mode = on < 0 || on > 2 ? 1 : on; });
 }

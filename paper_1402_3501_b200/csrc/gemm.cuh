@@ -111,6 +111,9 @@ class Workspace {
 public:
     Profiler prof;
     std::atomic<uint32_t> base_seq{0};  // sequence numbers of base-case completion mailboxes
+    // outcomes of the full-rank guesses since the context was created (ffg_spec_stats):
+    // whole-matrix guesses tried / failed, node-level guesses tried / failed, profile-first runs
+    std::atomic<uint64_t> st_guess{0}, st_guess_failed{0}, st_node{0}, st_node_failed{0}, st_profile_first{0};
     int spec_rest = 0;                   // calls left before speculative full rank is tried again
     int spec_fails = 0;                  // consecutive failed guesses (the rest doubles with them)
     void spec_failed() {

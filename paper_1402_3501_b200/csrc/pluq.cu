@@ -789,6 +789,11 @@ struct Driver {
         leaves.push_back({c0, t1});
         if (!base_wrote_inv) panel_inverses_dev(b, a.sub(0, 0, t1, t1), inv1);
         flush_deferred();  // the node's rows / columns carry every earlier update
+        // A1's wide panels beyond the node need only A1's inverses: they fork here, before the
+        // corner kernels (disjoint regions); their GEMMs read the corner's L(R, A1) / U(A1, R)
+        // blocks and wait for the second event
+        static const bool early_apply = knob_int("FFG_EARLY_APPLY", 1) != 0;
+        const cudaEvent_t f0 = early_apply ? mark_event(b.st) : nullptr;
         // A1's panel blocks inside the node, then R's update, each in small CTAs
         panel_mini_dev(b, inv1, t1, a.sub(0, t1, t1, t2), a.sub(t1, 0, t2, t1), q1);
         panel_update_dev(b, a.sub(t1, 0, t2, t1), a.sub(0, t1, t1, t2), a.sub(t1, t1, t2, t2));
@@ -797,12 +802,16 @@ struct Driver {
         sa.sm_cap = sb.sm_cap = side_sms;
         static const bool side_direct = knob_on("FFG_SIDE_DIRECT");
         if (side_direct) sa.no_direct = sb.no_direct = false;
-        wait(sa.st, f);
-        wait(sb.st, f);
+        wait(sa.st, early_apply ? f0 : f);
+        wait(sb.st, early_apply ? f0 : f);
         DView rightA{a.d + m, t1, pcols - (c0 + m), pld};       // A1 rows, columns beyond the node
         DView bottomA{a.d + m * pld, prows - (r0 + m), t1, pld};  // rows beyond the node, A1 columns
         panel_apply_dev(sa, 0, inv1, t1, rightA);
         panel_apply_dev(sb, 1, inv1, t1, bottomA, q1);
+        if (early_apply) {
+            wait(sa.st, f);
+            wait(sb.st, f);
+        }
         DView HRp{a.d + t1 * pld + m, t2, pcols - (c0 + m), pld};  // R rows beyond the node
         DView BPp{a.d + m * pld + t1, prows - (r0 + m), t2, pld};  // beyond the node, R columns
         if (!HRp.empty()) gemm_sub(sa, a.sub(t1, 0, t2, t1), rightA, HRp);
@@ -1039,6 +1048,8 @@ struct Driver {
                 }
             }
         }
+        ++b.ws.st_node;
+        if (!ok) ++b.ws.st_node_failed;
         if (nlog)
             fprintf(stderr, "[node] depth %d m %zu at %td: %s fail_off %zu, %.2f ms host\n", depth, m,
                     g_log_root ? (a.d - g_log_root) / (ptrdiff_t)g_log_ld : -1, ok ? "ok" : (resumable ? "resume" : "fail"), fail_off, host_ms() - t0);
@@ -1637,6 +1648,8 @@ static bool host_streamed_spec(const Blas& b, uint32_t* host, size_t n, size_t l
             }
         }
     }
+    ++b.ws.st_guess;
+    if (!ok) ++b.ws.st_guess_failed;
     if (!ok && resumable && profile_first_after_failure(b, fail_off, n, n, thr)) resumable = false;  // profile-first
     if (!ok && resumable) {
         // resume tile_rec at the failed block on the device copy (every band is uploaded and backed
@@ -1730,6 +1743,8 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
                 resumable = true;
             }
         }
+        ++b.ws.st_guess;
+        if (!ok) ++b.ws.st_guess_failed;
         static const bool log = knob_set("FFG_SPEC_LOG");
         if (log) fprintf(stderr, "SPEC %s (panel %d, %zu base cases enqueued)\n", ok ? "ok" : "failed", (int)(m == n), (size_t)b.ws.base_seq.load());
         if (ok) {

@@ -782,6 +782,7 @@ void pluq_from_profile_dev(const Blas& b, DView a, size_t threshold, size_t rank
 
 size_t pluq_profile_first_dev(const Blas& b, DView a, size_t threshold, uint32_t* P, uint32_t* Q) {
     const size_t m = a.rows, n = a.cols;
+    ++b.ws.st_profile_first;
     if (m == 0 || n == 0) {
         tile_rec_perms(m, n, threshold, 0, nullptr, nullptr, P, Q);
         return 0;

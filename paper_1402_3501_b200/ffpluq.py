@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
         L.ffg_last_error_index.restype = sz
         L.ffg_version.restype = C.c_char_p
         L.ffg_knobs_reload.restype = None
+        L.ffg_spec_stats.argtypes = [vp, C.POINTER(C.c_uint64)]
         L.ffg_set_stream.argtypes = [vp, vp]
         L.ffg_get_stream.argtypes = [vp]
         L.ffg_get_stream.restype = vp
@@ -160,6 +161,13 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().ffg_launch_count(self._h))
+
+    def spec_stats(self) -> dict:
+        """Outcomes of the full-rank guesses since the context was created (ffg_spec_stats)."""
+        out = (C.c_uint64 * 5)()
+        _check(lib().ffg_spec_stats(self._h, out))
+        keys = ("guesses", "guesses_failed", "node_guesses", "node_guesses_failed", "profile_first_runs")
+        return {k: int(v) for k, v in zip(keys, out)}
 
     PROFILE_CLASSES = ("gemm", "split", "base", "trinv", "perm", "simt")
 

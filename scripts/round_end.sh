@@ -8,6 +8,13 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; 
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 python bench.py --workload lru --steps 2 --warmup 3 --no-cpu --no-fgemm > gpurun_out/bench_config4.json 2> gpurun_out/bench_config4.err
 python bench.py --p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-fgemm > gpurun_out/bench_config5.json 2> gpurun_out/bench_config5.err
+# config 5 again, three consecutive runs (each line carries the guesses tried / failed in its timed region)
+for i in 1 2 3; do
+  python bench.py --p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof >> gpurun_out/bench_config5_x3.json 2>/dev/null
+done
+python scripts/trace_pluq.py --n 32768 --p 251 > gpurun_out/trace_c5.txt 2>&1
+python scripts/trace_pluq.py --lru --n 16384 > gpurun_out/trace_c4.txt 2>&1
+python scripts/trace_e2e.py > gpurun_out/trace_e2e.txt 2>&1
 python scripts/trace_pluq.py --n 16384 --json gpurun_out/trace_n16384.json > gpurun_out/trace_n16384.txt 2>&1
 # launch list of one bench step (durations only)
 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/bench_small.log 2>&1 && \

@@ -174,3 +174,47 @@ def test_device_entries_reject_bad_leading_dimension(gpu):
     with pytest.raises(ValueError):
         G.pluq_tile_recursive(131071, torch.zeros((8, 8), dtype=torch.int32, device="cuda").t(), 8, ctx=ctx)
     ctx.synchronize()
+
+
+def test_spec_stats_and_knob_snapshot(oracle_lib, monkeypatch):
+    """ffg_spec_stats counts the full-rank guesses of a context; the FFG_* switches are a snapshot
+    that ffg_knobs_reload() refreshes (conftest reloads after every monkeypatch change)."""
+    import paper_1402_3501_b200 as G
+    O = oracle_lib
+    p = 131071
+    ctx = G.Context(0)
+    try:
+        s0 = ctx.spec_stats()
+        assert set(s0) == {"guesses", "guesses_failed", "node_guesses", "node_guesses_failed", "profile_first_runs"}
+        A = O.random_mat(p, 640, 640, 5)  # full rank: the guess holds
+        want = O.pluq_tile_recursive(p, A, 64)
+        got = A.copy()
+        r = G.pluq_tile_recursive(p, got, 64, ctx=ctx)
+        assert r.rank == want[3] and np.array_equal(got, want[0])
+        s1 = ctx.spec_stats()
+        assert s1["guesses"] == s0["guesses"] + 1 and s1["guesses_failed"] == s0["guesses_failed"]
+        B, _, _ = O.lru_matrix(640, 300, p, 9)  # deficient from the first block: the guess fails
+        want = O.pluq_tile_recursive(p, B, 64)
+        got = B.copy()
+        r = G.pluq_tile_recursive(p, got, 64, ctx=ctx)
+        assert r.rank == want[3] == 300 and np.array_equal(got, want[0])
+        assert np.array_equal(r.P, want[1]) and np.array_equal(r.Q, want[2])
+        s2 = ctx.spec_stats()
+        # the failed whole-matrix guess, then the profile-first path's own (holding) guess on the
+        # generic leading block
+        assert s2["guesses"] == s1["guesses"] + 2 and s2["guesses_failed"] == s1["guesses_failed"] + 1
+        assert s2["profile_first_runs"] == s1["profile_first_runs"] + 1
+    finally:
+        ctx.close()
+    # a switch set after the first snapshot is seen once the snapshot is refreshed
+    ctx = G.Context(0)
+    try:
+        monkeypatch.setenv("FFG_NO_SPEC", "1")
+        s0 = ctx.spec_stats()
+        got = A.copy()
+        r = G.pluq_tile_recursive(p, got, 64, ctx=ctx)
+        want = O.pluq_tile_recursive(p, A, 64)
+        assert r.rank == want[3] and np.array_equal(got, want[0])
+        assert ctx.spec_stats()["guesses"] == s0["guesses"]  # no guess was tried
+    finally:
+        ctx.close()
