@@ -115,6 +115,7 @@ enum EpiMode : uint32_t { EPI_GENERIC = 0, EPI_SUB = 1, EPI_PROD = 2, EPI_ADD = 
 struct EpiParams {
     uint32_t mode;     // EPI_SUB: C - AB (alpha = p-1, beta = 1); EPI_PROD: AB (alpha 1, beta 0); EPI_ADD: C + AB
     uint32_t vec_ok;   // C rows 16-byte aligned (C and ldc multiples of 4 words)
+    uint32_t vec8_ok;  // C rows 32-byte aligned (C and ldc multiples of 8 words): 256-bit accesses
     uint32_t* C;
     uint64_t ldc;
     uint32_t M, N;
@@ -156,6 +157,9 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, TmemFn&& get_
     const bool row_ok = row < ep.M;
     uint32_t* crow = ep.C + (uint64_t)(row_ok ? row : 0) * ep.ldc;
     const bool vec = ep.vec_ok && col_first + PER * 8 <= ep.N;
+    // one 256-bit access per 8-column chunk: a warp's 32 rows are 32 different lines either way,
+    // and the tag stage of the L1 takes one line per cycle -- half the instructions, half the time
+    const bool vec8 = vec && ep.vec8_ok;
     const uint32_t mode = ep.mode, p = ep.p;
     const bool need_c = mode != EPI_PROD;
     uint32_t cpre[GC * 8];
@@ -164,7 +168,12 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, TmemFn&& get_
     auto load_chunk = [&](uint32_t ch, int slot) {  // chunk ch of this thread's row -> ring slot
         const uint32_t col = col_first + ch * 8;
         uint32_t* dst = cpre + slot * 8;
-        if (vec) {
+        if (vec8) {
+            uint32_t v[8];
+            ptx::ld_global_v8(crow + col, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dst[j] = v[j];
+        } else if (vec) {
             const uint4 a = *reinterpret_cast<const uint4*>(crow + col);
             const uint4 b = *reinterpret_cast<const uint4*>(crow + col + 4);
             dst[0] = a.x, dst[1] = a.y, dst[2] = a.z, dst[3] = a.w;
@@ -234,7 +243,9 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, TmemFn&& get_
                     out[j] = min(t, t - p);
                 }
             }
-            if (vec) {
+            if (vec8) {
+                ptx::st_global_v8(crow + col, out);
+            } else if (vec) {
                 *reinterpret_cast<uint4*>(crow + col) = make_uint4(out[0], out[1], out[2], out[3]);
                 *reinterpret_cast<uint4*>(crow + col + 4) = make_uint4(out[4], out[5], out[6], out[7]);
             } else {
@@ -877,6 +888,7 @@ EpiParams make_ep(const Field& F, uint32_t alpha, uint32_t beta, DView C) {
               : (alpha == 1 && beta == 1)                ? EPI_ADD
                                                          : EPI_GENERIC;
     ep.vec_ok = ((reinterpret_cast<uintptr_t>(C.d) & 15) == 0 && (C.ld & 3) == 0) ? 1u : 0u;
+    ep.vec8_ok = ((reinterpret_cast<uintptr_t>(C.d) & 31) == 0 && (C.ld & 7) == 0) ? 1u : 0u;
     for (int s = 0; s < 8; ++s) ep.w[s] = F.w[s];
     return ep;
 }

@@ -206,15 +206,17 @@ def test_spec_stats_and_knob_snapshot(oracle_lib, monkeypatch):
         assert s2["profile_first_runs"] == s1["profile_first_runs"] + 1
     finally:
         ctx.close()
-    # a switch set after the first snapshot is seen once the snapshot is refreshed
+    # a switch set after the first snapshot is seen once the snapshot is refreshed (conftest reloads
+    # on monkeypatch): without the profile-first path the same input takes the exact recursion
     ctx = G.Context(0)
     try:
-        monkeypatch.setenv("FFG_NO_SPEC", "1")
+        monkeypatch.setenv("FFG_PROFILE_FIRST", "0")
         s0 = ctx.spec_stats()
-        got = A.copy()
+        got = B.copy()
         r = G.pluq_tile_recursive(p, got, 64, ctx=ctx)
-        want = O.pluq_tile_recursive(p, A, 64)
+        want = O.pluq_tile_recursive(p, B, 64)
         assert r.rank == want[3] and np.array_equal(got, want[0])
-        assert ctx.spec_stats()["guesses"] == s0["guesses"]  # no guess was tried
+        assert np.array_equal(r.P, want[1]) and np.array_equal(r.Q, want[2])
+        assert ctx.spec_stats()["profile_first_runs"] == s0["profile_first_runs"]
     finally:
         ctx.close()
