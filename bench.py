@@ -104,17 +104,26 @@ METRIC_FGEMM = "fgemm effective field Gop/s (2mnk / time) mod p"
 
 # ---------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    nvidia-smi is started BEFORE the warm-up (start()): its start-up initialises NVML, which holds
+    driver locks for a few hundred ms and, when it fell inside the timed region, stalled the
+    factorisation's own launches (config 5, whose host is on the critical path, read 90-160 ms
+    instead of 72 in one run out of four).  The `with` block only marks the timed window; the
+    summary uses the samples whose timestamps fall inside it."""
+
+    FMT = "%Y/%m/%d %H:%M:%S.%f"
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+    def start(self):
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
                                           "-lms", "50", "-i", str(self.idx)], stdout=subprocess.PIPE,
@@ -125,11 +134,20 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def __enter__(self):
+        if self.proc is None and not self.lines:
+            self.start()
+        self.t0 = time.time()
+        return self
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -137,20 +155,30 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
             self.t.join(timeout=2)
+            self.proc = None
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
+        self.stop()
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
+                ts = datetime.datetime.strptime(f[0], self.FMT).timestamp()
+                rows.append((ts, float(f[1]), float(f[2]), f[5:9]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[4:8]):
+        inside = [r for r in rows if self.t0 is not None and self.t0 - 0.03 <= r[0] <= (self.t1 or self.t0) + 0.03]
+        if not inside and rows and self.t0 is not None:  # a window shorter than the sampling period
+            inside = [min(rows, key=lambda r: abs(r[0] - 0.5 * (self.t0 + (self.t1 or self.t0))))]
+        sm = [r[1] for r in inside]
+        mx = max([r[2] for r in inside], default=0.0)
+        reasons = set()
+        for r in inside:
+            for nm, v in zip(names, r[3]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
@@ -372,7 +400,9 @@ def our_arm(a, rank, world, local_rank):
         mats = [make(seed0 + i) for i in range(a.warmup + a.steps)]
     ctx.synchronize()
 
-    # ---- warmup (untimed)
+    # ---- warmup (untimed); the clock sampler starts here so that nvidia-smi's own start-up is over
+    # before the timed region
+    sampler = ClockSampler(local_rank).start()
     for i in range(a.warmup):
         run_once(mats, i)
     ctx.synchronize()
@@ -380,7 +410,7 @@ def our_arm(a, rank, world, local_rank):
     # ---- timed region: exactly K steps
     launches0 = ctx.launches
     spec0 = ctx.spec_stats()
-    with ClockSampler(local_rank) as clk:
+    with sampler as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)

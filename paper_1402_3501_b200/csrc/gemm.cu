@@ -89,7 +89,7 @@ struct TileCfg<4> {
 
 constexpr int BM = 128;  // rows per CTA tile (UMMA M)
 constexpr int BK = 128;  // K bytes per stage (one 128-byte swizzle row)
-constexpr int GROUP_M = 16;
+constexpr int GROUP_M = 12;  // 8192^3, L = 3: DRAM reads 2.30 / 2.02 / 2.32 / 3.37 / 5.41 GB at 8 / 12 / 16 / 20 / 32 (the row group's A panel must stay in L2)
 
 int tile_n(int limbs) {
     switch (limbs) {
@@ -126,6 +126,7 @@ struct EpiParams {
     uint32_t kblocks;
     uint32_t m_tiles, n_tiles;
     uint32_t l2_hints;  // TMA loads carry L2 eviction policies (large problems: keep the A panel of a row group)
+    uint32_t group_m;   // row blocks per rasterization group
 };
 
 // --------------------------------------------------------------------------- epilogue
@@ -287,9 +288,9 @@ __global__ void __launch_bounds__(384, 1)
     // GROUP_M row-blocks x a few column-blocks.
     const uint32_t tiles = ep.m_tiles * ep.n_tiles;
     auto tile_coords = [&](uint32_t pid, uint32_t& m_blk, uint32_t& n_blk) {
-        const uint32_t in_group = GROUP_M * ep.n_tiles;
-        const uint32_t first_m = (pid / in_group) * GROUP_M;
-        const uint32_t gsize = min((uint32_t)GROUP_M, ep.m_tiles - first_m);
+        const uint32_t in_group = ep.group_m * ep.n_tiles;
+        const uint32_t first_m = (pid / in_group) * ep.group_m;
+        const uint32_t gsize = min(ep.group_m, ep.m_tiles - first_m);
         m_blk = first_m + (pid % in_group) % gsize;
         n_blk = (pid % in_group) / gsize;
     };
@@ -908,6 +909,8 @@ void launch_modgemm(const Field& F, uint32_t alpha, uint32_t beta, const uint8_t
     // L2 eviction hints once the limb planes no longer fit in L2 beside C (FFG_GEMM_L2_HINTS=0/1 forces)
     static const int hints_env = (int)knob_int("FFG_GEMM_L2_HINTS", -1);
     ep.l2_hints = hints_env >= 0 ? (uint32_t)hints_env : ((uint64_t)L * (Mp + Np) * Kp > (64ull << 20) ? 1u : 0u);
+    static const int group_env = (int)knob_int("FFG_GEMM_GROUP_M", GROUP_M);
+    ep.group_m = (uint32_t)std::max(1, group_env);
     const uint32_t tiles = ep.m_tiles * ep.n_tiles;
     dim3 grid(sm_cap > 0 ? std::min<uint32_t>(tiles, (uint32_t)sm_cap) : tiles);
     launch_k(modgemm_kernel<L>, grid, dim3(384), S::TOTAL, st, ma, mb, ep);

@@ -1,3 +1,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-bash scripts/sweep.sh "FFG_SIDE_PRIO=0" "FFG_SIDE_PRIO=2" "FFG_SIDE_PRIO=1" "FFG_SIDE_PRIO=0" "FFG_SIDE_PRIO=2"
-ARGS="--p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof" bash scripts/sweep.sh "FFG_SIDE_PRIO=0" "FFG_SIDE_PRIO=2" "FFG_SIDE_PRIO=1" "FFG_SIDE_PRIO=0" "FFG_SIDE_PRIO=2"
+for i in 1 2 3 4 5 6; do
+python bench.py --p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c5', round(d['ms_per_step'],2), d['clocks'])"
+done
+for i in 1 2 3; do
+python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c3', round(d['ms_per_step'],2), d['clocks'])"
+done
