@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fgemm", action="store_true")
     ap.add_argument("--no-prof", action="store_true", help="skip the extra CUPTI-profiled step (roofline)")
+    ap.add_argument("--no-clocks", action="store_true",
+                    help="no nvidia-smi clock sampling (for runs under ncu: the polling slows its replays)")
     # under the self-relaunch (--gpus N outside torchrun) the arguments travel in the environment:
     # torchrun's own parser would otherwise claim abbreviations such as --n
     argv = json.loads(os.environ["FFG_BENCH_ARGV"]) if "FFG_BENCH_ARGV" in os.environ else None
@@ -135,8 +137,6 @@ class ClockSampler:
         return self
 
     def __enter__(self):
-        if self.proc is None and not self.lines:
-            self.start()
         self.t0 = time.time()
         return self
 
@@ -402,7 +402,9 @@ def our_arm(a, rank, world, local_rank):
 
     # ---- warmup (untimed); the clock sampler starts here so that nvidia-smi's own start-up is over
     # before the timed region
-    sampler = ClockSampler(local_rank).start()
+    sampler = ClockSampler(local_rank)
+    if not a.no_clocks:
+        sampler.start()
     for i in range(a.warmup):
         run_once(mats, i)
     ctx.synchronize()

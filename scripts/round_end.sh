@@ -19,7 +19,7 @@ python scripts/trace_pluq.py --n 16384 --json gpurun_out/trace_n16384.json > gpu
 # launch list of one bench step (durations only)
 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/bench_small.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv --log-file gpurun_out/launches_bench.csv \
-    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof > gpurun_out/ncu_bench.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-fgemm --no-prof --no-clocks > gpurun_out/ncu_bench.log 2>&1
 # the fused base case + inverses inside an n = 16384 PLUQ (full set, with source)
 python scripts/prof_pluq.py --n 16384 > gpurun_out/prof_pluq_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"rr_base_inv|leaf_apply|panel_update|panel_mini" \
@@ -39,3 +39,12 @@ FFG_GEMM_LOG=1 python scripts/gemm_shapes.py --run --n 16384 2> gpurun_out/shape
 python scripts/pluq_traffic.py gpurun_out/gemm_dram.csv gpurun_out/shapes.log --n 16384 --p 131071 --thr 64 \
   > gpurun_out/pluq_gemm_traffic.json 2> gpurun_out/pluq_traffic.err
 echo done
+# fgemm DRAM traffic per launch (bench.py reads profiles/gemm_traffic.json)
+python - <<'PY' > gpurun_out/gemm_traffic.json
+import json
+d = json.load(open("gpurun_out/ncu_gemm_summary.json"))["launches"][0]
+print(json.dumps({"dram_bytes_per_launch": d["dram_bytes"], "algorithmic_bytes_per_launch": 939524096,
+                  "algorithmic_note": "L=3 limb planes of A and B (2*3*8192^2) + C read and written (2*4*8192^2)",
+                  "source": "profiles/r02_ncu_gemm_8192_summary.json", "shape": "8192^3 L=3"}, indent=1))
+PY
+echo collected
