@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-python bench.py --workload lru --steps 2 --warmup 3 --no-cpu --no-fgemm > gpurun_out/bench_config4.json 2> gpurun_out/bench_config4.err
-python bench.py --p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-fgemm > gpurun_out/bench_config5.json 2> gpurun_out/bench_config5.err
-python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "ref rc=$?"
+timeout 1200 python -m pytest tests -q -m "gpu and not slow" -x -k "panel or resume or pluq or host or trsm" > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_quick.log
+bash scripts/sweep.sh "FFG_X=0" "FFG_X=1"
+ARGS="--p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof --no-clocks" bash scripts/sweep.sh "FFG_X=0" "FFG_X=1"
