@@ -362,13 +362,16 @@ __global__ void __launch_bounds__(256) leaf_apply_kernel(const uint32_t* __restr
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
             const uint32_t idx = tid + 256 * r, hi = idx / LA, lo = idx % LA;
-            rc[r] = (lo < d && hi < d) ? (SIDE == 0 ? inv[lo * d + hi] : inv[hi * d + lo]) : 0u;
+            rc[r] = (lo < d && hi < d) ? inv[hi * d + lo] : 0u;  // coalesced rows of the inverse
         }
         if (blockIdx.x * LA < nvec) load(blockIdx.x * LA);
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
             const uint32_t idx = tid + 256 * r;
-            Ct[idx / LA][idx % LA] = rc[r];
+            if (SIDE == 0)  // Ct[k][i] = inv(L)[i][k]: transposed on the shared-memory store (a
+                Ct[idx % LA][idx / LA] = rc[r];  // strided global read cost 32 lines per warp load)
+            else
+                Ct[idx / LA][idx % LA] = rc[r];
         }
     }
     // strips blockIdx.x, blockIdx.x + gridDim.x, ...: the next strip's loads fly during this one's math
@@ -636,7 +639,7 @@ __global__ void __launch_bounds__(256) panel_mini_kernel(const uint32_t* __restr
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
         const uint32_t idx = tid + 256 * r, k = idx / 64, i = idx % 64;
-        rc[r] = (i < d && k < d) ? (right ? invp[i * d + k] : invp[k * d + i]) : 0u;
+        rc[r] = (i < d && k < d) ? invp[k * d + i] : 0u;  // row k of the inverse, coalesced
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -648,7 +651,10 @@ __global__ void __launch_bounds__(256) panel_mini_kernel(const uint32_t* __restr
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
         const uint32_t idx = tid + 256 * r;
-        Ct[idx / 64][idx % 64] = rc[r];
+        if (right)  // Ct[k][i] = inv(L)[i][k]: transposed on the shared-memory store
+            Ct[idx % 64][idx / 64] = rc[r];
+        else
+            Ct[idx / 64][idx % 64] = rc[r];
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
