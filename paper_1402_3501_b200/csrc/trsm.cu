@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(256) panel_mini_kernel(const uint32_t* __restr
                                                          uint32_t* __restrict__ Y, uint64_t ldy, uint32_t h,
                                                          const uint32_t* __restrict__ qp, uint32_t p, uint64_t mu) {
     __shared__ __align__(16) uint32_t Ct[64][68];  // Ct[k][i] = coefficient of x_k in output i
-    __shared__ __align__(16) uint32_t Bs[64][MV];  // Bs[k][v]
+    __shared__ __align__(16) uint32_t Bs[64][MV + 4];  // Bs[k][v]
     const uint32_t tid = threadIdx.x, nr = (w + MV - 1) / MV;
     const bool right = blockIdx.x < nr;
     const uint32_t v0 = (right ? blockIdx.x : blockIdx.x - nr) * MV, nvec = right ? w : h;
@@ -643,7 +643,8 @@ __global__ void __launch_bounds__(256) panel_mini_kernel(const uint32_t* __restr
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        const uint32_t idx = tid + 256 * r, k = idx / MV, v = idx % MV;
+        // right: 16 consecutive columns of row k; bottom: 64 consecutive columns of row v
+        const uint32_t idx = tid + 256 * r, k = right ? idx / MV : idx % 64, v = right ? idx % MV : idx / 64;
         rb[r] = 0u;
         if (k < d && v < nv)
             rb[r] = right ? X[(uint64_t)k * ldx + v0 + v] : Y[(uint64_t)(v0 + v) * ldy + (qp ? qp[k] : k)];
@@ -659,7 +660,10 @@ __global__ void __launch_bounds__(256) panel_mini_kernel(const uint32_t* __restr
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const uint32_t idx = tid + 256 * r;
-        Bs[idx / MV][idx % MV] = rb[r];
+        if (right)
+            Bs[idx / MV][idx % MV] = rb[r];
+        else
+            Bs[idx % 64][idx / 64] = rb[r];
     }
     __syncthreads();
     const uint32_t i = tid >> 2, vg = (tid & 3) * 4;
