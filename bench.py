@@ -122,16 +122,19 @@ class ClockSampler:
         self.lines = []
         self.t0 = self.t1 = None
 
-    def start(self):
+    def start(self, period_ms: int = 25, wait_first: float = 3.0):
         q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "25", "-i", str(self.idx)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", str(int(period_ms)), "-i", str(self.idx)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + wait_first  # its first line = NVML is up: nothing of that start-up is left
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.005)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -400,13 +403,22 @@ def our_arm(a, rank, world, local_rank):
         mats = [make(seed0 + i) for i in range(a.warmup + a.steps)]
     ctx.synchronize()
 
-    # ---- warmup (untimed); the clock sampler starts here so that nvidia-smi's own start-up is over
-    # before the timed region
+    # ---- warmup (untimed); the clock sampler starts after the first warm-up step -- which tells the
+    # step time, hence a polling period of about five samples per timed region -- and its start-up
+    # (NVML initialisation) is waited for here, before the remaining warm-up steps
     sampler = ClockSampler(local_rank)
-    if not a.no_clocks:
-        sampler.start()
+    probe = min(1, a.warmup - 1)  # the second warm-up step is already warm
     for i in range(a.warmup):
+        if i == probe:
+            ctx.synchronize()
+        t_w = time.time()
         run_once(mats, i)
+        if i == probe and not a.no_clocks:
+            ctx.synchronize()
+            step_ms = (time.time() - t_w) * 1e3
+            sampler.start(period_ms=int(min(500, max(25, step_ms * a.steps / 5))))
+    if a.warmup == 0 and not a.no_clocks:
+        sampler.start()
     ctx.synchronize()
 
     # ---- timed region: exactly K steps
