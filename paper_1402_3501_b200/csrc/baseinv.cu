@@ -148,17 +148,16 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     ptx::pdl_enter();
     BI_STAMP(1);
     // stage the block (coalesced), zero-padded to 64 x 64
-#pragma unroll 1
-    for (uint32_t idx = tid; idx < 64 * 64; idx += 4 * BI_THREADS) {
-        uint32_t r[4];
+    {   // all eight loads of a thread in flight at once: one global-memory latency, not two
+        uint32_t r[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t x = idx + q * BI_THREADS, i = x >> 6, j = x & 63;
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t x = tid + q * BI_THREADS, i = x >> 6, j = x & 63;
             r[q] = (i < t && j < t) ? A[(uint64_t)i * lda + j] : 0u;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t x = idx + q * BI_THREADS;
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t x = tid + q * BI_THREADS;
             sm.S[x >> 6][x & 63] = r[q];
         }
     }

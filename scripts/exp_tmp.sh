@@ -1,9 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for i in 1 2 3 4; do
-python bench.py --p 251 --n 32768 --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c5', round(d['ms_per_step'],2), d['clocks'])"
-done
-for i in 1 2; do
-python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c3', round(d['ms_per_step'],2), d['clocks'])"
-done
-python bench.py --workload lru --steps 2 --warmup 3 --no-cpu --no-e2e --no-fgemm --no-prof 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c4', round(d['ms_per_step'],2), d['clocks'])"
-python bench.py --workload fgemm --steps 5 --warmup 3 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('fgemm', round(d['ms_per_step'],2), d['clocks'])"
+timeout 1500 python -m pytest tests -q -m "gpu and not slow" -x -k "panel or pluq or resume or base" > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_quick.log
+bash scripts/sweep.sh "FFG_X=0" "FFG_X=1" "FFG_X=2"
