@@ -341,14 +341,19 @@ struct Driver {
                 for (size_t i = 0; i < lf.second; ++i) gqh[lf.first + i] = (uint32_t)i;  // no column pivots
         }
     }
+    // diagnostics (FFG_SPEC_LOG): throttle calls, and those that found the device behind (the host
+    // had to wait: the device, not the host's enqueue rate, bounds the run)
+    uint64_t throttle_calls = 0, throttle_waits = 0;
     void spec_throttle() {
         if (spec_seqs.size() < spec_window) return;
         const uint32_t target = spec_seqs[spec_seqs.size() - spec_window] & ~SPEC_BIT;
         volatile uint32_t* sq = &info_host->seq;
         volatile uint32_t* sf = &info_host->spec_fail;
+        ++throttle_calls;
         for (uint64_t it = 0;; ++it) {
             if (*sf) throw SpecAbort{};
             const uint32_t cur = *sq & ~SPEC_BIT;
+            if (it == 1) ++throttle_waits;
             if (((cur - target) & ~SPEC_BIT) < 0x40000000u) return;  // cur at or after target (mod 2^31)
             if (it > (1u << 24)) {  // slow or failed kernel: block on the stream (reports errors)
                 FFG_CUDA(cudaStreamSynchronize(b.st));
@@ -1742,6 +1747,10 @@ size_t pluq_tile_recursive_dev(const Blas& b, DView a, size_t threshold, uint32_
                 drv.prefix_of(fail_off, px.gq, px.leaves);
                 resumable = true;
             }
+            static const bool tlog = knob_set("FFG_SPEC_LOG");
+            if (tlog)
+                fprintf(stderr, "SPEC host run-ahead: %llu throttle points, the host waited for the device at %llu\n",
+                        (unsigned long long)drv.throttle_calls, (unsigned long long)drv.throttle_waits);
         }
         ++b.ws.st_guess;
         if (!ok) ++b.ws.st_guess_failed;
