@@ -91,14 +91,31 @@ __device__ __forceinline__ uint32_t bi_shoup_lazy(uint32_t x, uint32_t w, uint32
 // per-step values every row update of step k uses
 struct BiStep {
     uint32_t kh, kl, pv, pvp, b0, b1, f0, f1, p;
+    uint32_t k4p2, mu32;  // small fields: 4 p^2 and floor(2^32 / p)
     bool dk0, dk1;
 };
 
 // one row's step-k update (fast path): numer = its live value in column k (frozen as the L
 // numerator there), every lane column then takes new = pv * live - numer * b  (lazy, [0, 4p));
 // in column k the I part starts from zero
+//
+// SMALLP (p < 2^14): pv * live - numer * b + 4 p^2 lies in (0, 8 p^2) < 2^31, so the update is two
+// 32-bit multiply-adds and one 32-bit Barrett step (result in [0, 2p)) -- four IMADs per entry
+// instead of six, and the published rows need no Shoup factors (three shoup_pre less on the
+// owner's serial path per pivot).
+template <bool SMALLP>
 __device__ __forceinline__ void bi_row(uint32_t (&lv)[2], uint32_t (&fz)[2], const BiStep& q) {
     const uint32_t numer = __shfl_sync(BI_FULL, q.kh ? lv[1] : lv[0], q.kl);
+    if (SMALLP) {
+        const uint32_t nn = 0u - numer;
+        const uint32_t u0 = (q.dk0 ? 0u : lv[0]) * q.pv + q.k4p2 + nn * q.b0;
+        const uint32_t u1 = (q.dk1 ? 0u : lv[1]) * q.pv + q.k4p2 + nn * q.b1;
+        lv[0] = u0 - __umulhi(u0, q.mu32) * q.p;
+        lv[1] = u1 - __umulhi(u1, q.mu32) * q.p;
+        fz[0] = q.dk0 ? numer : fz[0];
+        fz[1] = q.dk1 ? numer : fz[1];
+        return;
+    }
     const uint32_t t10 = bi_shoup_lazy(lv[0], q.pv, q.pvp, q.p), t11 = bi_shoup_lazy(lv[1], q.pv, q.pvp, q.p);
     const uint32_t t20 = bi_shoup_lazy(numer, q.b0, q.f0, q.p), t21 = bi_shoup_lazy(numer, q.b1, q.f1, q.p);
     lv[0] = (q.dk0 ? 0u : t10) + 2 * q.p - t20;
@@ -126,6 +143,7 @@ __device__ long long* g_bi_dbg = nullptr;
 // shared memory.  Outputs (CTA 0): the packed block (logical column order), Pd = identity, Qd =
 // column pivots, inv[0, t^2) = inv(L); (CTA 1): inv[t^2, 2 t^2) = inv(U), both row-major with ld t;
 // info as rr_base_spec_kernel.  allow_q = 0: any column pivot fails the guess.
+template <bool SMALLP>
 __global__ void __launch_bounds__(BI_THREADS, 1)
     rr_base_inv_kernel(uint32_t* __restrict__ A, uint64_t lda, uint32_t t, uint32_t* __restrict__ Pd,
                        uint32_t* __restrict__ Qd, BaseInfo* __restrict__ info, uint32_t* __restrict__ inv, uint32_t p,
@@ -198,14 +216,21 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
         const uint32_t a0 = bi_red4p(lv[0][0], p), a1 = bi_red4p(lv[0][1], p);
         const uint32_t pvn = __shfl_sync(BI_FULL, kn >= 32 ? a1 : a0, kn & 31);
         const uint32_t v0 = lane == kn ? 1u : a0, v1 = lane + 32 == kn ? 1u : a1;
-        const uint32_t g0 = shoup_pre(v0, p, mu), g1 = shoup_pre(v1, p, mu), pvnf = shoup_pre(pvn, p, mu);
+        uint32_t g0 = 0, g1 = 0, pvnf = 0;
+        if (!SMALLP) {
+            g0 = shoup_pre(v0, p, mu);
+            g1 = shoup_pre(v1, p, mu);
+            pvnf = shoup_pre(pvn, p, mu);
+        }
         sm.pub[kn][lane] = v0;
         sm.pub[kn][lane + 32] = v1;
-        sm.pf[kn][lane] = g0;
-        sm.pf[kn][lane + 32] = g1;
+        if (!SMALLP) {
+            sm.pf[kn][lane] = g0;
+            sm.pf[kn][lane + 32] = g1;
+        }
         if (lane == 0) {
             sm.pv[kn] = pvn;
-            sm.pvf[kn] = pvnf;
+            if (!SMALLP) sm.pvf[kn] = pvnf;
         }
         ptx::mbar_arrive(&sm.full[kn]);
         fwd = true;
@@ -252,11 +277,15 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
             ptx::mbar_wait(&sm.full[k], (uint32_t)(ph >> k) & 1u);
 #endif
             q.pv = sm.pv[k];
-            q.pvp = sm.pvf[k];
             q.b0 = sm.pub[k][lane];
             q.b1 = sm.pub[k][lane + 32];
-            q.f0 = sm.pf[k][lane];
-            q.f1 = sm.pf[k][lane + 32];
+            if (!SMALLP) {
+                q.pvp = sm.pvf[k];
+                q.f0 = sm.pf[k][lane];
+                q.f1 = sm.pf[k][lane + 32];
+            } else {
+                q.pvp = q.f0 = q.f1 = 0u;
+            }
         }
         fwd = false;
         if (q.pv == 0u) {  // zero Schur diagonal: every warp still holding rows leaves at this step
@@ -264,24 +293,26 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
             break;
         }
         q.p = p;
+        q.k4p2 = 4u * p * p;                // (used by SMALLP only: p < 2^14)
+        q.mu32 = (uint32_t)(mu >> 32);
         q.kh = k >> 5;
         q.kl = k & 31;
         q.dk0 = lane == k;
         q.dk1 = lane + 32 == k;
         const bool owner = nxt == k + 1;  // slot 0 is the next pivot row
         if (owner) {
-            bi_row(lv[0], fz[0], q);
+            bi_row<SMALLP>(lv[0], fz[0], q);
             publish(k + 1);  // shifts: the rows after it move down one slot
 #ifndef BI_CHAIN_ONLY
-            bi_row(lv[0], fz[0], q);  // (rows past the block's last are stale copies: updating them
-            bi_row(lv[1], fz[1], q);  //  unconditionally measured faster than branching around them)
-            bi_row(lv[2], fz[2], q);
+            bi_row<SMALLP>(lv[0], fz[0], q);  // (rows past the block's last are stale copies: updating them
+            bi_row<SMALLP>(lv[1], fz[1], q);  //  unconditionally measured faster than branching around them)
+            bi_row<SMALLP>(lv[2], fz[2], q);
 #endif
         } else {
-            bi_row(lv[0], fz[0], q);
-            bi_row(lv[1], fz[1], q);
-            bi_row(lv[2], fz[2], q);
-            bi_row(lv[3], fz[3], q);
+            bi_row<SMALLP>(lv[0], fz[0], q);
+            bi_row<SMALLP>(lv[1], fz[1], q);
+            bi_row<SMALLP>(lv[2], fz[2], q);
+            bi_row<SMALLP>(lv[3], fz[3], q);
         }
     }
     __syncthreads();
@@ -442,7 +473,8 @@ void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void
     const size_t smem = sizeof(BiSmem);
     static PerDeviceOnce once;
     once([smem] {
-        FFG_CUDA(cudaFuncSetAttribute(rr_base_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FFG_CUDA(cudaFuncSetAttribute(rr_base_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FFG_CUDA(cudaFuncSetAttribute(rr_base_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     });
     BaseInfo* info = static_cast<BaseInfo*>(info_dev);
     b.ws.prof.begin(b.st);
@@ -462,7 +494,10 @@ void rr_base_inv_launch(const Blas& b, DView a, uint32_t* Pd, uint32_t* Qd, void
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     static const bool dbg = knob_set("FFG_BI_DBG");
     if (dbg) bi_dbg_dump(b.st);
-    FFG_CUDA(cudaLaunchKernelEx(&cfg, rr_base_inv_kernel, a.d, (uint64_t)a.ld, t, Pd, Qd, info, inv, b.F.p, b.F.mu,
+    // fields below 2^14 take the 32-bit update (FFG_BASE_SMALLP=0: the general kernel everywhere)
+    static const bool smallp_on = knob_int("FFG_BASE_SMALLP", 1) != 0;
+    const auto kern = (smallp_on && b.F.p < (1u << 14)) ? rr_base_inv_kernel<true> : rr_base_inv_kernel<false>;
+    FFG_CUDA(cudaLaunchKernelEx(&cfg, kern, a.d, (uint64_t)a.ld, t, Pd, Qd, info, inv, b.F.p, b.F.mu,
                                 seq, (uint32_t)allow_q));
     FFG_CUDA(cudaGetLastError());
     b.ws.prof.end(b.st, PROF_BASE, 2.0 * t * t * 4, 2.0 * t * (double)t * t);
